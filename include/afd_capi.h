@@ -1,0 +1,164 @@
+/*
+ * afd_capi.h — C ABI of the B200-native FFT-AFD selection hot path.
+ *
+ * The reference (arXiv 1711.08604, package `fastafd`) is pure Python/numpy
+ * with no FFI; its seam is the Python API.  Each entry point below replaces
+ * one reference function (file:line under /root/reference/pkg/src/fastafd)
+ * and reproduces its results bit for bit (numpy/CPython arithmetic is
+ * emulated on the device; see paper_1711_08604_b200/csrc/afd_common.cuh).
+ * The Python package `paper_1711_08604_b200` binds these with ctypes
+ * (paper_1711_08604_b200/_capi.py); INTEGRATION.md shows the binding a
+ * `fastafd` maintainer would add.
+ *
+ * Conventions
+ *  - Every function returns 0 on success or a negative AFD_E* code; the
+ *    message is available from afd_last_error() (thread-local).  Nothing
+ *    throws across the ABI.
+ *  - Complex numbers are interleaved (re, im) doubles (numpy complex128).
+ *  - Pointers are DEVICE pointers owned by the caller unless named *_host.
+ *    All work is stream-ordered on the caller's `stream` (a cudaStream_t;
+ *    NULL = legacy default stream).
+ *  - A plan binds one device, one transform length N = 2^K (8 <= N), the
+ *    radius grid (M radii, of which this plan evaluates rows [m0, m1)) and
+ *    a maximum batch of independent signals.  Plans are not thread-safe;
+ *    use one plan per host thread.
+ *  - Host tables are taken from the caller so both sides start from the
+ *    same bits: twiddles exp(-2 pi i k/N), k < N/2 (transform.py:65),
+ *    circle exp(2 pi i m/N) (core.py:87), scales
+ *    sqrt(1-r^2)/(N(1-r^N)) (transform.py:153).
+ */
+#ifndef AFD_CAPI_H
+#define AFD_CAPI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AFD_OK 0
+#define AFD_E_INVALID -1     /* bad argument (the reference raises ValueError)  */
+#define AFD_E_CUDA -2        /* CUDA runtime error                              */
+#define AFD_E_UNSUPPORTED -3 /* size not supported by this build                */
+#define AFD_E_NOMEM -4       /* device allocation failed                        */
+
+/* Step record of one AFD step (core.DecompositionStep, core.py:170-175).
+ * s, j: grid indices of the selected pole a = r_s exp(2 pi i j/N)
+ * (core.ParameterGrid.point, core.py:163-167); coefficient <G_k, e_a>;
+ * residual = discrete_energy(G_{k+1}).  flags bit 0: CPython's pow(|a|, 2)
+ * is not provably equal to the device's |a|*|a| for this pole (see
+ * afd_common.cuh kernel_norm). */
+typedef struct afd_step {
+  int64_t s, j;
+  double radius, a_re, a_im, c_re, c_im, residual;
+  int32_t flags;
+  int32_t pad;
+} afd_step;
+
+/* Grid candidate: |F|^2, flat index s*N + j (global s), F.  32 bytes.
+ * Ordering: larger mag2 wins, ties go to the lower flat index (np.argmax
+ * first-maximum, core.py:299). */
+typedef struct afd_candidate {
+  double mag2;
+  int64_t flat;
+  double re, im;
+} afd_candidate;
+
+typedef struct afd_plan afd_plan;
+
+const char *afd_last_error(void);
+int afd_version(void);
+
+/* Create a plan.  radii_host/scales_host hold all M radii/scales
+ * (core.ParameterGrid.radii, core.py:115-145); the plan evaluates global
+ * rows [m0, m1) (radius sharding across GPUs).
+ * Replaces transform._plan + transform._radius_tables
+ * (transform.py:56-70, 137-156). */
+int afd_plan_create(afd_plan **out, int device, int64_t n, int64_t m, int64_t m0, int64_t m1,
+                    int64_t max_batch, const double *radii_host, const double *scales_host,
+                    const double *twiddle_host /* N/2 complex */,
+                    const double *circle_host /* N complex */);
+int afd_plan_destroy(afd_plan *plan);
+
+/* transform.dft_forward / dft_inverse (transform.py:106-134), batch rows. */
+int afd_dft_forward(afd_plan *plan, const double *x, double *out, int64_t batch, void *stream);
+int afd_dft_inverse(afd_plan *plan, const double *c, double *out, int64_t batch, void *stream);
+
+/* core.analytic_projection (core.py:201-231) of `batch` real rows given as
+ * complex with zero imaginary part. */
+int afd_analytic_projection(afd_plan *plan, const double *x, double *out, int64_t batch,
+                            void *stream);
+
+/* core.inner_product_field restricted to global rows [r0, r1) of ONE
+ * signal's spectrum (transform.weighted_inverse_grid, transform.py:185-201):
+ * field is (r1-r0) x N complex. */
+int afd_field(afd_plan *plan, const double *ghat, double *field, int64_t r0, int64_t r1,
+              void *stream);
+
+/* Fused field + maximal_selection over the plan's rows for `batch` spectra
+ * (core.inner_product_field + core.maximal_selection, core.py:259-300):
+ * writes one candidate per signal to out[batch]. */
+int afd_field_argmax(afd_plan *plan, const double *ghat, afd_candidate *out, int64_t batch,
+                     void *stream);
+
+/* core.maximal_selection on a materialised (rows x N) field (core.py:285-300):
+ * out receives the first maximum, flat index relative to the field. */
+int afd_argmax(afd_plan *plan, const double *field, int64_t rows, afd_candidate *out,
+               void *stream);
+
+/* Pointwise atoms over the circle (core.py:234-245, 303-314), N points:
+ *   kind 0 kernel_samples(a)      kind 1 blaschke_samples(a)
+ *   kind 2 remainder_update(g, a, c)
+ *   kind 3 g * blaschke_samples(a)  (core.tm_basis_samples step, core.py:406-407)
+ * g is used by kinds 2 and 3 only. */
+int afd_atom(afd_plan *plan, int kind, const double *g, double a_re, double a_im, double c_re,
+             double c_im, double *out, void *stream);
+
+/* core.discrete_energy (core.py:195-198) of `batch` signals -> energies[batch].
+ * With s != NULL the energy of g - s (core.relative_error, core.py:430-439). */
+int afd_energy(afd_plan *plan, const double *g, double *energies, int64_t batch, void *stream);
+int afd_energy_diff(afd_plan *plan, const double *g, const double *s, double *energies,
+                    int64_t batch, void *stream);
+
+/* core.decompose (core.py:317-391), engine "fft", for `batch` independent
+ * signals g0 (batch x N).  threshold <= 0 means None.  Outputs (device):
+ * steps[batch][max_terms], n_steps[batch], initial[batch] (initial energy),
+ * remainder[batch][N] (final G_{n+1}; a copy of g0 for zero-energy input).
+ * The loop runs device-resident (captured once into a CUDA graph per
+ * (max_terms, threshold, dc_first, batch)).  Requires m0 == 0 && m1 == M
+ * (single-shard plan); sharded plans use afd_select_local/afd_apply_step. */
+int afd_decompose(afd_plan *plan, const double *g0, int64_t batch, int max_terms,
+                  double threshold, int dc_first, afd_step *steps, int32_t *n_steps,
+                  double *initial, double *remainder, void *stream);
+
+/* Radius-sharded decomposition, one step at a time:
+ *   afd_sharded_begin        copy g0, initial energy, first spectrum
+ *   afd_select_local         field + argmax over the plan's rows -> cand[batch]
+ *   (caller all-gathers the candidates of all ranks, rank-major)
+ *   afd_apply_step           reduce cands[batch][ncand], update, energy, record,
+ *                            next spectrum; identical on every rank
+ *   afd_sharded_state        n_steps / stopped flags / initial energies   */
+int afd_sharded_begin(afd_plan *plan, const double *g0, int64_t batch, void *stream);
+int afd_select_local(afd_plan *plan, int k, int dc_first, afd_candidate *cand, int64_t batch,
+                     void *stream);
+int afd_apply_step(afd_plan *plan, int k, int max_terms, double threshold, int dc_first,
+                   const afd_candidate *cands, int ncand, int64_t batch, afd_step *steps,
+                   void *stream);
+int afd_sharded_finish(afd_plan *plan, int64_t batch, int32_t *n_steps, double *initial,
+                       double *remainder, int32_t *stopped, void *stream);
+
+/* core.error_trace + core.reconstruct (core.py:411-460) for `batch` signals:
+ * errors[batch][max_terms] (entry k = relative error of the (k+1)-term
+ * partial sum), recon[batch][N] = S_{n_steps} (may be NULL). */
+int afd_error_trace(afd_plan *plan, const double *g, const afd_step *steps, int max_terms,
+                    const int32_t *n_steps, int64_t batch, double *errors, double *recon,
+                    void *stream);
+
+/* Number of this library's kernels launched since plan creation (counts
+ * launches issued, including those replayed inside CUDA graphs). */
+int64_t afd_launch_count(afd_plan *plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AFD_CAPI_H */

@@ -1,0 +1,635 @@
+// afd_capi.cu — host runtime behind include/afd_capi.h: plans (device
+// tables), kernel dispatch by transform length, the device-resident
+// decomposition loop captured as a CUDA graph, and the sharded step API.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/afd_capi.h"
+#include "afd_kernels.cuh"
+#include "afd_aux.cuh"
+
+using namespace afd;
+
+static_assert(sizeof(afd_step) == sizeof(Step), "afd_step layout");
+static_assert(sizeof(afd_candidate) == sizeof(Cand), "afd_candidate layout");
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(call)                                                                  \
+  do {                                                                            \
+    cudaError_t e_ = (call);                                                      \
+    if (e_ != cudaSuccess)                                                        \
+      return fail(AFD_E_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_),    \
+                  __FILE__, __LINE__);                                            \
+  } while (0)
+
+constexpr int kMinK = 3;
+constexpr int kMaxOnChipK = 13;
+
+}  // namespace
+
+struct afd_plan {
+  int device = 0;
+  int K = 0;
+  int64_t n = 0, m = 0, m0 = 0, m1 = 0, max_batch = 0;
+  int sms = 148;
+  // device tables
+  double* radii = nullptr;    // [M]
+  double* scales = nullptr;   // [M]
+  double2* twst = nullptr;    // stage tables [N-1]
+  double2* circle = nullptr;  // [N]
+  double* pw = nullptr;       // [m1-m0][N] cumprod r^l
+  // per-signal working buffers
+  double2* ghat = nullptr;    // [max_batch][N]
+  double2* rem = nullptr;     // [max_batch][N]
+  double2* gin = nullptr;     // [max_batch][N] staged input
+  State* state = nullptr;     // [max_batch]
+  Cand* cand = nullptr;       // [max_batch][ncand_cap]
+  int ncand_cap = 0;
+  Step* steps = nullptr;      // [max_batch][steps_cap]
+  int steps_cap = 0;
+  double* scratch = nullptr;  // generic scratch (bookkeeping kernels)
+  size_t scratch_bytes = 0;
+  // field launch geometry
+  int field_occ = 1;
+  // graph cache
+  cudaGraphExec_t gexec = nullptr;
+  int g_max_terms = -1, g_dc_first = -1;
+  double g_threshold = -2;
+  int64_t g_batch = -1;
+  cudaStream_t g_stream = nullptr;
+  int64_t launches = 0;
+  int64_t graph_launches_per_replay = 0;
+};
+
+// ---------------------------------------------------------------------------
+// Templated launchers, dispatched on K.
+// ---------------------------------------------------------------------------
+namespace {
+
+template <int K>
+constexpr int groups_for() {
+  return Geo<K>::T >= 256 ? 1 : 256 / Geo<K>::T;
+}
+
+template <int K>
+int field_block() {
+  return Geo<K>::T * groups_for<K>();
+}
+
+template <int K>
+size_t field_smem() {
+  return sizeof(double2) * Geo<K>::N * groups_for<K>();
+}
+
+template <int K>
+int row_block() {
+  return Geo<K>::T < 64 ? 64 : Geo<K>::T;
+}
+
+template <int K, bool MAT>
+int setup_field_kernel(int* occ) {
+  auto kern = field_kernel<K, groups_for<K>(), MAT>;
+  CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem<K>()));
+  if (occ) CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, field_block<K>(), field_smem<K>()));
+  return 0;
+}
+
+template <int K>
+int setup_kernels(afd_plan* p) {
+  int rc;
+  if ((rc = setup_field_kernel<K, false>(&p->field_occ))) return rc;
+  if ((rc = setup_field_kernel<K, true>(nullptr))) return rc;
+  CU(cudaFuncSetAttribute(step_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)RowSmem<K>::bytes));
+  CU(cudaFuncSetAttribute(fft_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)RowSmem<K>::bytes));
+  if (p->field_occ < 1) p->field_occ = 1;
+  return 0;
+}
+
+// Number of CTAs per signal for `rows` rows: minimise waves x rows-per-CTA.
+int field_ctas(const afd_plan* p, int64_t rows, int G, int64_t batch) {
+  const int64_t units = (rows + G - 1) / G;
+  const int64_t slots = (int64_t)p->sms * p->field_occ;
+  int64_t best_x = 1;
+  double best_t = 1e300;
+  for (int64_t x = 1; x <= units && x <= 65535; ++x) {
+    const int64_t per = (units + x - 1) / x;
+    if (x > 1 && (units + x - 2) / (x - 1) == per) continue;  // same per-CTA load, more CTAs
+    const int64_t ctas = x * batch;
+    const int64_t waves = (ctas + slots - 1) / slots;
+    const double t = (double)waves * (double)per + 1e-3 * (double)ctas / (double)slots;
+    if (t < best_t) {
+      best_t = t;
+      best_x = x;
+    }
+  }
+  return (int)best_x;
+}
+
+template <int K>
+int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64_t batch,
+                 Cand* cand, int ncta, double2* field_out, const State* state, cudaStream_t st) {
+  constexpr int G = groups_for<K>();
+  dim3 grid(ncta, (unsigned)batch);
+  if (field_out) {
+    field_kernel<K, G, true><<<grid, field_block<K>(), field_smem<K>(), st>>>(
+        ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, nullptr, field_out, nullptr);
+  } else {
+    field_kernel<K, G, false><<<grid, field_block<K>(), field_smem<K>(), st>>>(
+        ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, cand, nullptr, state);
+  }
+  p->launches++;
+  CU(cudaGetLastError());
+  return 0;
+}
+
+template <int K>
+int launch_step(afd_plan* p, int k, int max_terms, double thr, int dc_first, const double2* g0,
+                const Cand* cand, int ncand, int64_t batch, Step* steps, cudaStream_t st) {
+  step_kernel<K><<<(unsigned)batch, row_block<K>(), RowSmem<K>::bytes, st>>>(
+      k, max_terms, thr, dc_first, g0, p->rem, p->ghat, cand, ncand, p->radii, p->circle,
+      p->twst, p->state, steps);
+  p->launches++;
+  CU(cudaGetLastError());
+  return 0;
+}
+
+template <int K>
+int launch_fft(afd_plan* p, int mode, const double2* x, double2* y, int64_t batch,
+               cudaStream_t st) {
+  fft_kernel<K><<<(unsigned)batch, row_block<K>(), RowSmem<K>::bytes, st>>>(mode, x, y, p->twst);
+  p->launches++;
+  CU(cudaGetLastError());
+  return 0;
+}
+
+// Dispatch helper: calls F<K>::run(args...) for the plan's K.
+#define AFD_DISPATCH(KV, EXPR)                 \
+  switch (KV) {                                \
+    case 3: { constexpr int KK = 3; EXPR; }    \
+    case 4: { constexpr int KK = 4; EXPR; }    \
+    case 5: { constexpr int KK = 5; EXPR; }    \
+    case 6: { constexpr int KK = 6; EXPR; }    \
+    case 7: { constexpr int KK = 7; EXPR; }    \
+    case 8: { constexpr int KK = 8; EXPR; }    \
+    case 9: { constexpr int KK = 9; EXPR; }    \
+    case 10: { constexpr int KK = 10; EXPR; }  \
+    case 11: { constexpr int KK = 11; EXPR; }  \
+    case 12: { constexpr int KK = 12; EXPR; }  \
+    case 13: { constexpr int KK = 13; EXPR; }  \
+    default:                                   \
+      return fail(AFD_E_UNSUPPORTED, "transform length 2^%d not supported yet", KV); \
+  }
+
+int groups_of(int K) {
+  AFD_DISPATCH(K, return groups_for<KK>());
+}
+
+int ensure_cand(afd_plan* p, int64_t batch, int ncta) {
+  if (ncta > p->ncand_cap) {
+    if (p->cand) cudaFree(p->cand);
+    p->cand = nullptr;
+    p->ncand_cap = 0;
+    CU(cudaMalloc(&p->cand, sizeof(Cand) * (size_t)p->max_batch * ncta));
+    p->ncand_cap = ncta;
+  }
+  (void)batch;
+  return 0;
+}
+
+int ensure_steps(afd_plan* p, int max_terms) {
+  if (max_terms > p->steps_cap) {
+    if (p->steps) cudaFree(p->steps);
+    p->steps = nullptr;
+    p->steps_cap = 0;
+    CU(cudaMalloc(&p->steps, sizeof(Step) * (size_t)p->max_batch * max_terms));
+    p->steps_cap = max_terms;
+  }
+  return 0;
+}
+
+int ensure_scratch(afd_plan* p, size_t bytes) {
+  if (bytes > p->scratch_bytes) {
+    if (p->scratch) cudaFree(p->scratch);
+    p->scratch = nullptr;
+    p->scratch_bytes = 0;
+    CU(cudaMalloc(&p->scratch, bytes));
+    p->scratch_bytes = bytes;
+  }
+  return 0;
+}
+
+int check_batch(const afd_plan* p, int64_t batch) {
+  if (batch < 1 || batch > p->max_batch)
+    return fail(AFD_E_INVALID, "batch %lld outside 1..%lld", (long long)batch,
+                (long long)p->max_batch);
+  return 0;
+}
+
+int set_device(const afd_plan* p) {
+  CU(cudaSetDevice(p->device));
+  return 0;
+}
+
+// Enqueue the whole decomposition (init + max_terms steps) on `st`.
+int enqueue_decompose(afd_plan* p, int64_t batch, int max_terms, double thr, int dc_first,
+                      cudaStream_t st) {
+  const int64_t rows = p->m1 - p->m0;
+  const int G = groups_of(p->K);
+  const int ncta = field_ctas(p, rows, G, batch);
+  int rc;
+  if ((rc = ensure_cand(p, batch, ncta))) return rc;
+  AFD_DISPATCH(p->K, {
+    if ((rc = launch_step<KK>(p, -1, max_terms, thr, dc_first, p->gin, nullptr, 0, batch,
+                              p->steps, st)))
+      return rc;
+    for (int k = 0; k < max_terms; ++k) {
+      if (!(k == 0 && dc_first)) {
+        if ((rc = launch_field<KK>(p, p->ghat, p->m0, p->m1, batch, p->cand, ncta, nullptr,
+                                   p->state, st)))
+          return rc;
+      }
+      if ((rc = launch_step<KK>(p, k, max_terms, thr, dc_first, nullptr, p->cand, ncta, batch,
+                                p->steps, st)))
+        return rc;
+    }
+    return 0;
+  });
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* afd_last_error(void) { return g_err.c_str(); }
+
+int afd_version(void) { return 1; }
+
+int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0, int64_t m1,
+                    int64_t max_batch, const double* radii_host, const double* scales_host,
+                    const double* twiddle_host, const double* circle_host) {
+  if (!out) return fail(AFD_E_INVALID, "out is NULL");
+  *out = nullptr;
+  if (n < 8 || (n & (n - 1)))
+    return fail(AFD_E_INVALID, "signal length must be a power of two >= 8, got %lld",
+                (long long)n);
+  int K = 0;
+  while ((1LL << K) < n) ++K;
+  if (K < kMinK || K > kMaxOnChipK)
+    return fail(AFD_E_UNSUPPORTED, "transform length 2^%d not supported yet", K);
+  if (m < 1) return fail(AFD_E_INVALID, "grid needs at least one radius");
+  if (m0 < 0 || m1 > m || m0 >= m1) return fail(AFD_E_INVALID, "bad radius shard [%lld, %lld)",
+                                                (long long)m0, (long long)m1);
+  if (max_batch < 1) return fail(AFD_E_INVALID, "max_batch must be >= 1");
+  if (!radii_host || !scales_host || !twiddle_host || !circle_host)
+    return fail(AFD_E_INVALID, "NULL host table");
+  for (int64_t i = 0; i < m; ++i) {
+    if (!(radii_host[i] >= 0.0 && radii_host[i] < 1.0))
+      return fail(AFD_E_INVALID, "grid radii must lie in [0, 1), got %g", radii_host[i]);
+  }
+  afd_plan* p = new afd_plan();
+  p->device = device;
+  p->K = K;
+  p->n = n;
+  p->m = m;
+  p->m0 = m0;
+  p->m1 = m1;
+  p->max_batch = max_batch;
+  auto cleanup = [&](int rc) {
+    afd_plan_destroy(p);
+    return rc;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) return cleanup(fail(AFD_E_CUDA, "cudaSetDevice(%d)", device));
+  cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
+  const size_t N = (size_t)n;
+  // stage twiddle tables S_b[k] = w[k << (K-1-b)], offset 2^b - 1
+  std::vector<double2> st(N - 1);
+  for (int b = 0; b < K; ++b)
+    for (int64_t k = 0; k < (1LL << b); ++k) {
+      const int64_t idx = k << (K - 1 - b);
+      st[(1LL << b) - 1 + k] = make_double2(twiddle_host[2 * idx], twiddle_host[2 * idx + 1]);
+    }
+#define ALLOC(ptr, bytes)                                                          \
+  do {                                                                             \
+    if (cudaMalloc(&(ptr), (bytes)) != cudaSuccess)                                \
+      return cleanup(fail(AFD_E_NOMEM, "cudaMalloc(%zu) failed", (size_t)(bytes))); \
+  } while (0)
+  ALLOC(p->radii, sizeof(double) * m);
+  ALLOC(p->scales, sizeof(double) * m);
+  ALLOC(p->twst, sizeof(double2) * (N - 1));
+  ALLOC(p->circle, sizeof(double2) * N);
+  ALLOC(p->pw, sizeof(double) * N * (size_t)(m1 - m0));
+  ALLOC(p->ghat, sizeof(double2) * N * max_batch);
+  ALLOC(p->rem, sizeof(double2) * N * max_batch);
+  ALLOC(p->gin, sizeof(double2) * N * max_batch);
+  ALLOC(p->state, sizeof(State) * max_batch);
+#undef ALLOC
+  if (cudaMemcpy(p->radii, radii_host, sizeof(double) * m, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p->scales, scales_host, sizeof(double) * m, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p->twst, st.data(), sizeof(double2) * (N - 1), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p->circle, circle_host, sizeof(double2) * N, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemset(p->state, 0, sizeof(State) * max_batch) != cudaSuccess)
+    return cleanup(fail(AFD_E_CUDA, "table upload failed"));
+  // r^l power rows (np.cumprod, transform.py:147-150), once per plan
+  {
+    const int64_t rows = m1 - m0;
+    power_table_kernel<<<(unsigned)((rows + 31) / 32), 32>>>(p->radii, m0, m1, n, p->pw);
+    p->launches++;
+    if (cudaGetLastError() != cudaSuccess) return cleanup(fail(AFD_E_CUDA, "power table launch"));
+  }
+  int rc;
+  AFD_DISPATCH(K, { rc = setup_kernels<KK>(p); break; });
+  if (rc) return cleanup(rc);
+  if (cudaDeviceSynchronize() != cudaSuccess) return cleanup(fail(AFD_E_CUDA, "plan init: %s",
+                                                                  cudaGetErrorString(cudaGetLastError())));
+  *out = p;
+  return AFD_OK;
+}
+
+int afd_plan_destroy(afd_plan* p) {
+  if (!p) return AFD_OK;
+  cudaSetDevice(p->device);
+  if (p->gexec) cudaGraphExecDestroy(p->gexec);
+  cudaFree(p->radii);
+  cudaFree(p->scales);
+  cudaFree(p->twst);
+  cudaFree(p->circle);
+  cudaFree(p->pw);
+  cudaFree(p->ghat);
+  cudaFree(p->rem);
+  cudaFree(p->gin);
+  cudaFree(p->state);
+  cudaFree(p->cand);
+  cudaFree(p->steps);
+  cudaFree(p->scratch);
+  delete p;
+  return AFD_OK;
+}
+
+static int fft_entry(afd_plan* p, int mode, const double* x, double* out, int64_t batch,
+                     void* stream) {
+  if (!p || !x || !out) return fail(AFD_E_INVALID, "NULL argument");
+  int rc;
+  if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  AFD_DISPATCH(p->K, return launch_fft<KK>(p, mode, (const double2*)x, (double2*)out, batch, st));
+}
+
+int afd_dft_forward(afd_plan* p, const double* x, double* out, int64_t batch, void* stream) {
+  return fft_entry(p, 0, x, out, batch, stream);
+}
+int afd_dft_inverse(afd_plan* p, const double* c, double* out, int64_t batch, void* stream) {
+  return fft_entry(p, 1, c, out, batch, stream);
+}
+int afd_analytic_projection(afd_plan* p, const double* x, double* out, int64_t batch,
+                            void* stream) {
+  return fft_entry(p, 2, x, out, batch, stream);
+}
+
+int afd_field(afd_plan* p, const double* ghat, double* field, int64_t r0, int64_t r1,
+              void* stream) {
+  if (!p || !ghat || !field) return fail(AFD_E_INVALID, "NULL argument");
+  if (r0 < p->m0 || r1 > p->m1 || r0 >= r1)
+    return fail(AFD_E_INVALID, "rows [%lld, %lld) outside the plan's [%lld, %lld)",
+                (long long)r0, (long long)r1, (long long)p->m0, (long long)p->m1);
+  int rc;
+  if ((rc = set_device(p))) return rc;
+  const int ncta = field_ctas(p, r1 - r0, groups_of(p->K), 1);
+  AFD_DISPATCH(p->K, return launch_field<KK>(p, (const double2*)ghat, r0, r1, 1, nullptr, ncta,
+                                             (double2*)field, nullptr, (cudaStream_t)stream));
+}
+
+int afd_field_argmax(afd_plan* p, const double* ghat, afd_candidate* out, int64_t batch,
+                     void* stream) {
+  if (!p || !ghat || !out) return fail(AFD_E_INVALID, "NULL argument");
+  int rc;
+  if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int ncta = field_ctas(p, p->m1 - p->m0, groups_of(p->K), batch);
+  if ((rc = ensure_cand(p, batch, ncta))) return rc;
+  AFD_DISPATCH(p->K, {
+    if ((rc = launch_field<KK>(p, (const double2*)ghat, p->m0, p->m1, batch, p->cand, ncta,
+                               nullptr, nullptr, st)))
+      return rc;
+    break;
+  });
+  cand_reduce_kernel<<<(unsigned)batch, 128, 0, st>>>(p->cand, ncta, (Cand*)out);
+  p->launches++;
+  CU(cudaGetLastError());
+  return 0;
+}
+
+int afd_argmax(afd_plan* p, const double* field, int64_t rows, afd_candidate* out, void* stream) {
+  if (!p || !field || !out) return fail(AFD_E_INVALID, "NULL argument");
+  if (rows < 1) return fail(AFD_E_INVALID, "empty field");
+  int rc;
+  if ((rc = set_device(p))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long total = rows * p->n;
+  int nblk = (int)std::min<long long>((total + 255) / 256, (long long)p->sms * 8);
+  if ((rc = ensure_scratch(p, sizeof(Cand) * nblk))) return rc;
+  argmax_kernel<<<nblk, 256, 0, st>>>((const double2*)field, total, (Cand*)p->scratch);
+  cand_reduce_kernel<<<1, 256, 0, st>>>((const Cand*)p->scratch, nblk, (Cand*)out);
+  p->launches += 2;
+  CU(cudaGetLastError());
+  return 0;
+}
+
+int afd_atom(afd_plan* p, int kind, const double* g, double a_re, double a_im, double c_re,
+             double c_im, double* out, void* stream) {
+  if (!p || !out || (kind == 2 && !g)) return fail(AFD_E_INVALID, "NULL argument");
+  if (kind < 0 || kind > 3) return fail(AFD_E_INVALID, "bad atom kind %d", kind);
+  if (kind == 3 && !g) return fail(AFD_E_INVALID, "NULL argument");
+  if (!(a_re * a_re + a_im * a_im < 1.0))
+    return fail(AFD_E_INVALID, "pole must lie strictly inside the unit disc");
+  int rc;
+  if ((rc = set_device(p))) return rc;
+  const int n = (int)p->n;
+  atom_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+      kind, n, (const double2*)g, make_double2(a_re, a_im), make_double2(c_re, c_im), p->circle,
+      (double2*)out);
+  p->launches++;
+  CU(cudaGetLastError());
+  return 0;
+}
+
+int afd_energy(afd_plan* p, const double* g, double* energies, int64_t batch, void* stream) {
+  return afd_energy_diff(p, g, nullptr, energies, batch, stream);
+}
+
+int afd_energy_diff(afd_plan* p, const double* g, const double* s, double* energies,
+                    int64_t batch, void* stream) {
+  if (!p || !g || !energies) return fail(AFD_E_INVALID, "NULL argument");
+  int rc;
+  if ((rc = set_device(p))) return rc;
+  const size_t per = (size_t)p->n + 2 * ((size_t)p->n / 8 + 16);
+  if ((rc = ensure_scratch(p, sizeof(double) * per * batch))) return rc;
+  energy_kernel<<<(unsigned)batch, 256, 0, (cudaStream_t)stream>>>(
+      (int)p->n, (const double2*)g, (const double2*)s, p->scratch, energies);
+  p->launches++;
+  CU(cudaGetLastError());
+  return 0;
+}
+
+int afd_decompose(afd_plan* p, const double* g0, int64_t batch, int max_terms, double threshold,
+                  int dc_first, afd_step* steps, int32_t* n_steps, double* initial,
+                  double* remainder, void* stream) {
+  if (!p || !g0 || !steps || !n_steps || !initial || !remainder)
+    return fail(AFD_E_INVALID, "NULL argument");
+  if (max_terms < 1) return fail(AFD_E_INVALID, "max_terms must be >= 1");
+  if (p->m0 != 0 || p->m1 != p->m)
+    return fail(AFD_E_INVALID, "afd_decompose needs an unsharded plan (use the step API)");
+  int rc;
+  if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
+  if ((rc = ensure_steps(p, max_terms))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const double thr = threshold > 0.0 ? threshold : 0.0;
+  const size_t sig_bytes = sizeof(double2) * (size_t)p->n * batch;
+  CU(cudaMemcpyAsync(p->gin, g0, sig_bytes, cudaMemcpyDeviceToDevice, st));
+  const bool reuse = p->gexec && p->g_max_terms == max_terms && p->g_dc_first == dc_first &&
+                     p->g_threshold == thr && p->g_batch == batch && p->g_stream == st;
+  if (!reuse) {
+    if (p->gexec) cudaGraphExecDestroy(p->gexec);
+    p->gexec = nullptr;
+    // make sure buffers exist before capture (allocation is not capturable)
+    const int ncta = field_ctas(p, p->m1 - p->m0, groups_of(p->K), batch);
+    if ((rc = ensure_cand(p, batch, ncta))) return rc;
+    cudaStream_t cap;
+    CU(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    cudaGraph_t graph;
+    const int64_t before = p->launches;
+    CU(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    rc = enqueue_decompose(p, batch, max_terms, thr, dc_first, cap);
+    cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+    cudaStreamDestroy(cap);
+    if (rc) return rc;
+    if (ce != cudaSuccess) return fail(AFD_E_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+    p->graph_launches_per_replay = p->launches - before;
+    p->launches = before;
+    ce = cudaGraphInstantiate(&p->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) return fail(AFD_E_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+    p->g_max_terms = max_terms;
+    p->g_dc_first = dc_first;
+    p->g_threshold = thr;
+    p->g_batch = batch;
+    p->g_stream = st;
+  }
+  CU(cudaGraphLaunch(p->gexec, st));
+  p->launches += p->graph_launches_per_replay;
+  // outputs
+  gather_outputs_kernel<<<(unsigned)batch, 256, 0, st>>>(
+      (int)p->n, max_terms, p->steps, p->state, p->rem, (Step*)steps, n_steps, initial,
+      (double2*)remainder, nullptr);
+  p->launches++;
+  CU(cudaGetLastError());
+  return 0;
+}
+
+int afd_sharded_begin(afd_plan* p, const double* g0, int64_t batch, void* stream) {
+  if (!p || !g0) return fail(AFD_E_INVALID, "NULL argument");
+  int rc;
+  if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  CU(cudaMemcpyAsync(p->gin, g0, sizeof(double2) * (size_t)p->n * batch,
+                     cudaMemcpyDeviceToDevice, st));
+  AFD_DISPATCH(p->K, return launch_step<KK>(p, -1, 1, 0.0, 0, p->gin, nullptr, 0, batch, p->steps,
+                                            st));
+}
+
+int afd_select_local(afd_plan* p, int k, int dc_first, afd_candidate* cand, int64_t batch,
+                     void* stream) {
+  if (!p || !cand) return fail(AFD_E_INVALID, "NULL argument");
+  int rc;
+  if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k == 0 && dc_first) {
+    // the pinned mean atom needs no field; emit a neutral candidate
+    neutral_cand_kernel<<<1, 128, 0, st>>>((Cand*)cand, (int)batch);
+    p->launches++;
+    CU(cudaGetLastError());
+    return 0;
+  }
+  const int ncta = field_ctas(p, p->m1 - p->m0, groups_of(p->K), batch);
+  if ((rc = ensure_cand(p, batch, ncta))) return rc;
+  AFD_DISPATCH(p->K, {
+    if ((rc = launch_field<KK>(p, p->ghat, p->m0, p->m1, batch, p->cand, ncta, nullptr, p->state,
+                               st)))
+      return rc;
+    break;
+  });
+  cand_reduce_kernel<<<(unsigned)batch, 128, 0, st>>>(p->cand, ncta, (Cand*)cand);
+  p->launches++;
+  CU(cudaGetLastError());
+  return 0;
+}
+
+int afd_apply_step(afd_plan* p, int k, int max_terms, double threshold, int dc_first,
+                   const afd_candidate* cands, int ncand, int64_t batch, afd_step* steps,
+                   void* stream) {
+  if (!p || !cands || !steps) return fail(AFD_E_INVALID, "NULL argument");
+  if (k < 0 || k >= max_terms) return fail(AFD_E_INVALID, "step %d outside 0..%d", k, max_terms - 1);
+  int rc;
+  if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
+  const double thr = threshold > 0.0 ? threshold : 0.0;
+  AFD_DISPATCH(p->K, return launch_step<KK>(p, k, max_terms, thr, dc_first, nullptr,
+                                            (const Cand*)cands, ncand, batch, (Step*)steps,
+                                            (cudaStream_t)stream));
+}
+
+int afd_sharded_finish(afd_plan* p, int64_t batch, int32_t* n_steps, double* initial,
+                       double* remainder, int32_t* stopped, void* stream) {
+  if (!p || !n_steps || !initial || !remainder) return fail(AFD_E_INVALID, "NULL argument");
+  int rc;
+  if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
+  gather_outputs_kernel<<<(unsigned)batch, 256, 0, (cudaStream_t)stream>>>(
+      (int)p->n, 0, nullptr, p->state, p->rem, nullptr, n_steps, initial, (double2*)remainder,
+      stopped);
+  p->launches++;
+  CU(cudaGetLastError());
+  return 0;
+}
+
+int afd_error_trace(afd_plan* p, const double* g, const afd_step* steps, int max_terms,
+                    const int32_t* n_steps, int64_t batch, double* errors, double* recon,
+                    void* stream) {
+  if (!p || !g || !steps || !n_steps || !errors) return fail(AFD_E_INVALID, "NULL argument");
+  int rc;
+  if ((rc = set_device(p))) return rc;
+  const size_t n = (size_t)p->n;
+  const size_t per = 2 * n * 2 + n + 2 * (n / 8 + 16);  // total, bp (complex), mag, scratch
+  if ((rc = ensure_scratch(p, sizeof(double) * per * batch))) return rc;
+  error_trace_kernel<<<(unsigned)batch, 256, 0, (cudaStream_t)stream>>>(
+      (int)n, (const double2*)g, (const Step*)steps, max_terms, n_steps, p->circle, p->scratch,
+      errors, (double2*)recon);
+  p->launches++;
+  CU(cudaGetLastError());
+  return 0;
+}
+
+int64_t afd_launch_count(afd_plan* p) { return p ? p->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,362 @@
+// afd_kernels.cuh — the sm_100a kernels of the AFD selection hot path for
+// on-chip transform lengths N = 2^K <= 8192.
+//
+//   field_kernel   ★ K2 of SURVEY.md §2.2: per (signal, radius row) the
+//                  prologue r^l * Ghat[l], the inverse butterflies, the
+//                  sqrt(1-r^2)/(N(1-r^N)) scale, |.|^2 and the running
+//                  first-maximum; one 32-byte candidate per CTA (or the
+//                  materialised rows, for parity tests).
+//                  Reference: transform.weighted_inverse_grid + maximal_selection
+//                  (transform.py:185-201, core.py:285-300).
+//   step_kernel    K3+K4+K1: reduce the candidates (first max), form the
+//                  pole a = r_s z_j, update the remainder
+//                  (core.py:303-314), its energy (core.py:195-198), record
+//                  the step, test the stop rules (core.py:386-389) and
+//                  forward-transform the new remainder for the next step
+//                  (core.py:248-250).  One CTA per signal.
+//   fft_kernel     dft_forward / dft_inverse (transform.py:106-134) and the
+//                  analytic projection (core.py:201-231).
+//
+// All kernels reproduce the reference's arithmetic bit for bit (see
+// afd_common.cuh); the library is compiled with -fmad=false.
+#pragma once
+
+#include "afd_fft.cuh"
+
+namespace afd {
+
+struct State {
+  int stopped;   // no further steps for this signal
+  int nsteps;    // recorded steps
+  int flags;     // OR of step flags
+  int pad;
+  double initial;
+};
+
+// Must match afd_step in include/afd_capi.h.
+struct Step {
+  long long s, j;
+  double radius, a_re, a_im, c_re, c_im, residual;
+  int flags;
+  int pad;
+};
+
+enum : int { kStepPowAmbiguous = 1 };
+
+// ---------------------------------------------------------------------------
+// Field + argmax (or materialised field).  Block = G row-groups of T threads;
+// each group evaluates one radius row per round; rows are strided over the
+// CTAs of a signal (blockIdx.y).
+// ---------------------------------------------------------------------------
+template <int K, int G, bool MATERIALIZE>
+__global__ void __launch_bounds__(Geo<K>::T * G, (Geo<K>::T * G <= 256) ? 2 : 1)
+field_kernel(const double2* __restrict__ ghat,     // [batch][N]
+             const double* __restrict__ pw,        // [rows of plan][N], r^l natural l
+             const double* __restrict__ scales,    // [M] (global radius index)
+             const double2* __restrict__ twst,     // stage twiddle tables (N-1)
+             long long row0, long long row1,       // global rows to evaluate
+             long long pw_row0,                    // global row of pw[0]
+             Cand* __restrict__ cand_out,          // [batch][gridDim.x]
+             double2* __restrict__ field_out,      // [row1-row0][N] (MATERIALIZE)
+             const State* __restrict__ state) {    // per-signal stop flags or null
+  using Gm = Geo<K>;
+  constexpr int N = Gm::N, T = Gm::T, P = Gm::P;
+  extern __shared__ double2 smem[];
+  const int sig = blockIdx.y;
+  if (state != nullptr && state[sig].stopped) return;
+  const int g = threadIdx.x / T;
+  const int tp = threadIdx.x % T;
+  double2* sm = smem + g * N;
+  const double2* __restrict__ gh = ghat + (size_t)sig * N;
+
+  Cand best;
+  best.mag = -1.0;
+  best.flat = 0x7fffffffffffffffLL;
+  best.re = 0.0;
+  best.im = 0.0;
+
+  const long long rows = row1 - row0;
+  const long long per_round = (long long)gridDim.x * G;
+  const long long rounds = (rows + per_round - 1) / per_round;
+  for (long long rd = 0; rd < rounds; ++rd) {
+    const long long s = row0 + rd * per_round + (long long)blockIdx.x * G + g;
+    const bool active = s < row1;
+    double2 v[P];
+    if (active) {
+      // prologue: y = powers * c[rev] (transform.py:198), per component
+      const double* __restrict__ pr = pw + (size_t)(s - pw_row0) * N;
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const int l = Gm::l0(tp, i);
+        const double p = __ldg(pr + l);
+        const double2 c = __ldg(gh + l);
+        v[i] = make_double2(p * c.x, p * c.y);
+      }
+    }
+    fft_passes<K, true>(v, tp, active, sm, twst);
+    if (active) {
+      const double sc = __ldg(scales + s);
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const int j = out_pos<K>(tp, i);
+        // y *= scales[:, None] (transform.py:200)
+        const double2 f = make_double2(v[i].x * sc, v[i].y * sc);
+        if (MATERIALIZE) {
+          field_out[(size_t)(s - row0) * N + j] = f;
+        } else {
+          const double mg = np_mag2(f);
+          const long long flat = s * (long long)N + j;
+          if (cand_better(mg, flat, best.mag, best.flat)) {
+            best.mag = mg;
+            best.flat = flat;
+            best.re = f.x;
+            best.im = f.y;
+          }
+        }
+      }
+    }
+  }
+  if (MATERIALIZE) return;
+  // CTA reduction of the candidates (first maximum).
+  __shared__ Cand red[32];
+  best = warp_argmax(best);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red[wid] = best;
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    Cand c = lane < nw ? red[lane] : best;
+    c = warp_argmax(c);
+    if (lane == 0) cand_out[(size_t)sig * gridDim.x + blockIdx.x] = c;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Shared helpers for the one-CTA-per-signal kernels.
+// ---------------------------------------------------------------------------
+
+// Forward (INV=false) or inverse transform of the row held in `buf`
+// (natural order, swizzled), result written to `out` (natural order,
+// global).  For the inverse, SCALE_N applies `y /= n` (transform.py:133).
+template <int K, bool INV, bool SCALE_N>
+__device__ void row_transform(double2* buf, const double2* __restrict__ twst,
+                              double2* __restrict__ out) {
+  using Gm = Geo<K>;
+  constexpr int T = Gm::T, P = Gm::P;
+  const int tp = threadIdx.x;
+  const bool active = tp < T;
+  double2 v[P];
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < P; ++i) v[i] = buf[Gm::sw(Gm::l0(tp, i))];
+  }
+  __syncthreads();
+  fft_passes<K, INV>(v, tp, active, buf, twst);
+  if (active) {
+    const double2 dn = make_double2((double)Gm::N, 0.0);
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      double2 y = v[i];
+      if (SCALE_N) y = np_cdiv(y, dn);
+      out[out_pos<K>(tp, i)] = y;
+    }
+  }
+  __syncthreads();
+}
+
+template <int K>
+struct SwIdx {
+  __device__ __forceinline__ int operator()(int i) const { return Geo<K>::sw(i); }
+};
+struct PlainIdx {
+  __device__ __forceinline__ int operator()(int i) const { return i; }
+};
+
+// Shared-memory layout of the one-CTA-per-signal kernels.
+template <int K>
+struct RowSmem {
+  static constexpr int N = 1 << K;
+  static constexpr size_t buf = 0;                                  // N double2
+  static constexpr size_t mag = buf + sizeof(double2) * N;          // N double
+  static constexpr size_t scratch = mag + sizeof(double) * N;       // 2*(N/8+16) double
+  static constexpr size_t bytes = scratch + sizeof(double) * 2 * (N / 8 + 16);
+};
+
+// ---------------------------------------------------------------------------
+// step_kernel: one CTA per signal.
+//   k < 0  : initialise (copy g0, initial energy, forward transform)
+//   k >= 0 : select / update / energy / record / stop / forward transform
+// ---------------------------------------------------------------------------
+template <int K>
+__global__ void __launch_bounds__(Geo<K>::T < 64 ? 64 : Geo<K>::T)
+step_kernel(int k, int max_terms, double threshold, int dc_first,
+            const double2* __restrict__ g0,       // [batch][N] (init only)
+            double2* __restrict__ rem,            // [batch][N] remainder G_k
+            double2* __restrict__ ghat,           // [batch][N] DFT(G_k)
+            const Cand* __restrict__ cand,        // [batch][ncand]
+            int ncand,
+            const double* __restrict__ radii,     // [M] global
+            const double2* __restrict__ circle,   // [N] z_m
+            const double2* __restrict__ twst,
+            State* __restrict__ state,            // [batch]
+            Step* __restrict__ steps) {           // [batch][max_terms]
+  constexpr int N = 1 << K;
+  using L = RowSmem<K>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double2* buf = reinterpret_cast<double2*>(smraw + L::buf);
+  double* mag = reinterpret_cast<double*>(smraw + L::mag);
+  double* scratch = reinterpret_cast<double*>(smraw + L::scratch);
+  __shared__ Cand red[32];
+  __shared__ int s_stop;
+  const SwIdx<K> SW;
+  const int sig = blockIdx.x;
+  State& st = state[sig];
+  double2* __restrict__ r = rem + (size_t)sig * N;
+  double2* __restrict__ gh = ghat + (size_t)sig * N;
+
+  if (k < 0) {
+    const double2* __restrict__ x = g0 + (size_t)sig * N;
+    for (int m = threadIdx.x; m < N; m += blockDim.x) {
+      const double2 v = x[m];
+      r[m] = v;
+      buf[SW(m)] = v;
+      mag[m] = np_mag2(v);
+    }
+    __syncthreads();
+    // discrete_energy (core.py:195-198): np.mean(re**2 + im**2)
+    const double e0 = pairwise_sum_block(mag, N, scratch, PlainIdx()) / (double)N;
+    if (threadIdx.x == 0) {
+      st.initial = e0;
+      st.nsteps = 0;
+      st.flags = 0;
+      st.stopped = (e0 == 0.0) ? 1 : 0;  // core.py:366-368
+      s_stop = st.stopped;
+    }
+    __syncthreads();
+    if (!s_stop) row_transform<K, false, false>(buf, twst, gh);
+    return;
+  }
+
+  if (st.stopped) return;  // block-uniform
+  long long s = 0, j = 0;
+  double radius = 0.0;
+  double2 a = make_double2(0.0, 0.0), coeff;
+  if (k == 0 && dc_first) {
+    // core.py:373-375: a = 0, coeff = complex(np.mean(remainder))
+    for (int m = threadIdx.x; m < N; m += blockDim.x) buf[SW(m)] = r[m];
+    __syncthreads();
+    const double2 sum = cpairwise_sum_block(buf, N, scratch, SW);
+    coeff = np_cdiv(sum, make_double2((double)N, 0.0));
+  } else {
+    // first maximum over the candidates (np.argmax, core.py:299)
+    Cand b;
+    b.mag = -1.0;
+    b.flat = 0x7fffffffffffffffLL;
+    b.re = b.im = 0.0;
+    for (int i = threadIdx.x; i < ncand; i += blockDim.x) cand_merge(b, cand[(size_t)sig * ncand + i]);
+    b = warp_argmax(b);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) red[wid] = b;
+    __syncthreads();
+    if (wid == 0) {
+      Cand c = lane < (int)(blockDim.x >> 5) ? red[lane] : b;
+      c = warp_argmax(c);
+      if (lane == 0) red[0] = c;
+    }
+    __syncthreads();
+    b = red[0];
+    s = b.flat / N;
+    j = b.flat % N;
+    radius = radii[s];
+    // grid.point (core.py:163-167): r * exp(2 pi i j / N) == (r Re z_j, r Im z_j)
+    const double2 zj = circle[j];
+    a = make_double2(radius * zj.x, radius * zj.y);
+    coeff = make_double2(b.re, b.im);
+  }
+
+  // remainder_update (core.py:303-314) + kernel_samples (core.py:234-238)
+  int amb = 0;
+  const double kn = kernel_norm(a, &amb);
+  const double2 sc = make_double2(kn, 0.0);
+  constexpr bool elide = (size_t)N * 16 >= 256 * 1024;  // numpy temporary elision
+  for (int m = threadIdx.x; m < N; m += blockDim.x) {
+    const double2 z = circle[m];
+    const double2 d = one_minus_conja_z(a, z);
+    const double2 e = np_cdiv(sc, d);
+    const double2 ce = elide ? np_cmul(e, coeff) : np_cmul(coeff, e);
+    const double2 g = r[m];
+    const double2 stp = make_double2(g.x - ce.x, g.y - ce.y);
+    const double2 num = elide ? np_cmul(d, stp) : np_cmul(stp, d);
+    const double2 den = make_double2(z.x - a.x, z.y - a.y);
+    const double2 out = np_cdiv(num, den);
+    r[m] = out;
+    buf[SW(m)] = out;
+    mag[m] = np_mag2(out);
+  }
+  __syncthreads();
+  const double residual = pairwise_sum_block(mag, N, scratch, PlainIdx()) / (double)N;
+  if (threadIdx.x == 0) {
+    Step rec;
+    rec.s = s;
+    rec.j = j;
+    rec.radius = radius;
+    rec.a_re = a.x;
+    rec.a_im = a.y;
+    rec.c_re = coeff.x;
+    rec.c_im = coeff.y;
+    rec.residual = residual;
+    rec.flags = amb ? kStepPowAmbiguous : 0;
+    rec.pad = 0;
+    steps[(size_t)sig * max_terms + k] = rec;
+    st.nsteps = k + 1;
+    st.flags |= rec.flags;
+    int stop = 0;
+    if (threshold > 0.0 && residual <= threshold * st.initial) stop = 1;  // core.py:386-387
+    if (residual == 0.0) stop = 1;                                         // core.py:388-389
+    if (k + 1 >= max_terms) stop = 1;
+    st.stopped = stop;
+    s_stop = stop;
+  }
+  __syncthreads();
+  if (!s_stop) row_transform<K, false, false>(buf, twst, gh);
+}
+
+// ---------------------------------------------------------------------------
+// Standalone transforms, one CTA per signal.
+//   mode 0: dft_forward   mode 1: dft_inverse   mode 2: analytic projection
+//   (real input given as complex with zero imaginary part)
+// ---------------------------------------------------------------------------
+template <int K>
+__global__ void __launch_bounds__(Geo<K>::T < 64 ? 64 : Geo<K>::T)
+fft_kernel(int mode, const double2* __restrict__ x, double2* __restrict__ y,
+           const double2* __restrict__ twst) {
+  constexpr int N = 1 << K;
+  using L = RowSmem<K>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double2* buf = reinterpret_cast<double2*>(smraw + L::buf);
+  const SwIdx<K> SW;
+  const double2* __restrict__ xs = x + (size_t)blockIdx.x * N;
+  double2* __restrict__ ys = y + (size_t)blockIdx.x * N;
+  for (int m = threadIdx.x; m < N; m += blockDim.x) buf[SW(m)] = xs[m];
+  __syncthreads();
+  if (mode == 0) {
+    row_transform<K, false, false>(buf, twst, ys);
+  } else if (mode == 1) {
+    row_transform<K, true, true>(buf, twst, ys);
+  } else {
+    // core.py:224-231: spectrum = dft_forward(x); spectrum[1:half] *= 2;
+    // spectrum[half+1:] = 0; dft_inverse(spectrum)
+    row_transform<K, false, false>(buf, twst, ys);
+    constexpr int half = N / 2;
+    for (int m = threadIdx.x; m < N; m += blockDim.x) {
+      double2 v = ys[m];
+      if (m >= 1 && m < half) v = make_double2(v.x * 2.0, v.y * 2.0);
+      if (m > half) v = make_double2(0.0, 0.0);
+      buf[SW(m)] = v;
+    }
+    __syncthreads();
+    row_transform<K, true, true>(buf, twst, ys);
+  }
+}
+
+}  // namespace afd

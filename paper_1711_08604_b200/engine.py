@@ -1,0 +1,266 @@
+"""Device-level engine: plans and torch-tensor entry points over the C ABI.
+
+PyTorch is used only for device memory, streams and the host<->device
+handoff; every computation is a kernel of libafd_b200.so.  All functions
+here take / return CUDA tensors (complex128, row-major ``[batch, N]``), so
+callers that keep data resident in HBM never touch the host.
+
+Host tables are built with numpy exactly as the reference builds them
+(``transform.py:65`` twiddles, ``core.py:87`` circle, ``transform.py:153``
+scales), so the device starts from the reference's bits.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _capi
+
+try:  # torch is plumbing only; the product cannot run without it and a GPU
+    import torch
+except ImportError as exc:  # pragma: no cover
+    raise _capi.AfdCudaUnavailable("torch is required for device memory") from exc
+
+__all__ = ["Plan", "get_plan", "host_tables", "DeviceDecomposition", "require_cuda"]
+
+
+def require_cuda(device=None):
+    if not torch.cuda.is_available():
+        raise _capi.AfdCudaUnavailable(
+            "no CUDA device: the B200 engine has no CPU fallback")
+    _capi.load()
+    return torch.device("cuda", torch.cuda.current_device() if device is None else device)
+
+
+def host_tables(radii, n):
+    """(twiddles, circle, scales) exactly as the reference computes them."""
+    r = np.ascontiguousarray(radii, dtype=np.float64)
+    tw = np.ascontiguousarray(np.exp(-2j * np.pi * np.arange(n // 2) / n))  # transform.py:65
+    circle = np.ascontiguousarray(np.exp(2j * np.pi * np.arange(n) / n))     # core.py:87
+    scales = np.ascontiguousarray(np.sqrt(1.0 - r * r) / (n * (1.0 - r ** n)))  # transform.py:153
+    return tw, circle, scales
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+@dataclass
+class DeviceDecomposition:
+    steps: torch.Tensor      # uint8 [batch, max_terms, 80] (afd_step records)
+    n_steps: torch.Tensor    # int32 [batch]
+    initial: torch.Tensor    # float64 [batch]
+    remainder: torch.Tensor  # complex128 [batch, N]
+
+    def host_steps(self):
+        """(steps structured array [batch, max_terms], n_steps) on the host."""
+        raw = self.steps.cpu().numpy()
+        return raw.view(_capi.STEP_DTYPE)[..., 0], self.n_steps.cpu().numpy()
+
+
+class Plan:
+    """One afd_plan: device tables for (N, radii, radius shard, batch)."""
+
+    def __init__(self, radii, n, m0=0, m1=None, max_batch=1, device=None):
+        self.device = require_cuda(device)
+        self.lib = _capi.load()
+        self.radii = tuple(float(r) for r in radii)
+        self.n = int(n)
+        self.m = len(self.radii)
+        self.m0 = int(m0)
+        self.m1 = self.m if m1 is None else int(m1)
+        self.max_batch = int(max_batch)
+        tw, circle, scales = host_tables(self.radii, self.n)
+        r = np.ascontiguousarray(self.radii, dtype=np.float64)
+        handle = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _capi.check(self.lib.afd_plan_create(
+                C.byref(handle), self.device.index, self.n, self.m, self.m0, self.m1,
+                self.max_batch, r.ctypes.data, scales.ctypes.data, tw.ctypes.data,
+                circle.ctypes.data))
+        self.handle = handle
+        self._keep = (tw, circle, scales, r)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self.lib.afd_plan_destroy(h)
+            except Exception:  # pragma: no cover - interpreter teardown
+                pass
+            self.handle = None
+
+    # -- helpers ------------------------------------------------------------
+    def _signal(self, g, batch=None):
+        g = g.to(device=self.device, dtype=torch.complex128).contiguous()
+        if g.dim() == 1:
+            g = g.unsqueeze(0)
+        if g.shape[-1] != self.n:
+            raise ValueError("signal length %d does not match plan N %d" % (g.shape[-1], self.n))
+        if g.shape[0] > self.max_batch:
+            raise ValueError("batch %d exceeds plan max_batch %d" % (g.shape[0], self.max_batch))
+        return g
+
+    def launch_count(self):
+        return int(self.lib.afd_launch_count(self.handle))
+
+    # -- transforms -----------------------------------------------------------
+    def _fft(self, fn, x, stream=None):
+        x = self._signal(x)
+        out = torch.empty_like(x)
+        _capi.check(fn(self.handle, _ptr(x), _ptr(out), x.shape[0], _stream(stream)))
+        return out
+
+    def dft_forward(self, x, stream=None):
+        return self._fft(self.lib.afd_dft_forward, x, stream)
+
+    def dft_inverse(self, c, stream=None):
+        return self._fft(self.lib.afd_dft_inverse, c, stream)
+
+    def analytic_projection(self, x, stream=None):
+        return self._fft(self.lib.afd_analytic_projection, x, stream)
+
+    def field(self, ghat, r0=None, r1=None, stream=None):
+        ghat = self._signal(ghat)[0]
+        r0 = self.m0 if r0 is None else int(r0)
+        r1 = self.m1 if r1 is None else int(r1)
+        out = torch.empty((max(r1 - r0, 0), self.n), dtype=torch.complex128, device=self.device)
+        _capi.check(self.lib.afd_field(self.handle, _ptr(ghat), _ptr(out), r0, r1,
+                                       _stream(stream)))
+        return out
+
+    def field_argmax(self, ghat, stream=None):
+        ghat = self._signal(ghat)
+        out = torch.empty((ghat.shape[0], 32), dtype=torch.uint8, device=self.device)
+        _capi.check(self.lib.afd_field_argmax(self.handle, _ptr(ghat), _ptr(out), ghat.shape[0],
+                                              _stream(stream)))
+        return out
+
+    def argmax(self, field, stream=None):
+        field = field.to(device=self.device, dtype=torch.complex128).contiguous()
+        if field.dim() != 2 or field.shape[1] != self.n:
+            raise ValueError("field must be (rows, N)")
+        out = torch.empty(32, dtype=torch.uint8, device=self.device)
+        _capi.check(self.lib.afd_argmax(self.handle, _ptr(field), field.shape[0], _ptr(out),
+                                        _stream(stream)))
+        return out
+
+    def atom(self, kind, a, c=0j, g=None, stream=None):
+        a = complex(a)
+        c = complex(c)
+        out = torch.empty(self.n, dtype=torch.complex128, device=self.device)
+        if g is not None:
+            g = self._signal(g)[0]
+        _capi.check(self.lib.afd_atom(self.handle, kind, _ptr(g), a.real, a.imag, c.real, c.imag,
+                                      _ptr(out), _stream(stream)))
+        return out
+
+    def energy(self, g, stream=None):
+        g = self._signal(g)
+        out = torch.empty(g.shape[0], dtype=torch.float64, device=self.device)
+        _capi.check(self.lib.afd_energy(self.handle, _ptr(g), _ptr(out), g.shape[0],
+                                        _stream(stream)))
+        return out
+
+    def energy_diff(self, g, s, stream=None):
+        g = self._signal(g)
+        s = self._signal(s)
+        out = torch.empty(g.shape[0], dtype=torch.float64, device=self.device)
+        _capi.check(self.lib.afd_energy_diff(self.handle, _ptr(g), _ptr(s), _ptr(out),
+                                             g.shape[0], _stream(stream)))
+        return out
+
+    # -- the hot path -----------------------------------------------------------
+    def decompose(self, g, max_terms, threshold=None, dc_first=False, stream=None, out=None):
+        """Device-resident decomposition of g ([batch, N] CUDA complex128)."""
+        g = self._signal(g)
+        b = g.shape[0]
+        if out is None:
+            out = self.alloc_outputs(b, max_terms)
+        _capi.check(self.lib.afd_decompose(
+            self.handle, _ptr(g), b, int(max_terms),
+            0.0 if threshold is None else float(threshold), int(bool(dc_first)),
+            _ptr(out.steps), _ptr(out.n_steps), _ptr(out.initial), _ptr(out.remainder),
+            _stream(stream)))
+        return out
+
+    def alloc_outputs(self, batch, max_terms):
+        dev = self.device
+        return DeviceDecomposition(
+            steps=torch.empty((batch, max_terms, _capi.STEP_DTYPE.itemsize), dtype=torch.uint8,
+                              device=dev),
+            n_steps=torch.empty(batch, dtype=torch.int32, device=dev),
+            initial=torch.empty(batch, dtype=torch.float64, device=dev),
+            remainder=torch.empty((batch, self.n), dtype=torch.complex128, device=dev))
+
+    def error_trace(self, g, dec, stream=None):
+        """errors [batch, max_terms] and reconstructions [batch, N] (device)."""
+        g = self._signal(g)
+        b, max_terms = dec.steps.shape[0], dec.steps.shape[1]
+        errors = torch.zeros((b, max_terms), dtype=torch.float64, device=self.device)
+        recon = torch.empty((b, self.n), dtype=torch.complex128, device=self.device)
+        _capi.check(self.lib.afd_error_trace(self.handle, _ptr(g), _ptr(dec.steps), max_terms,
+                                             _ptr(dec.n_steps), b, _ptr(errors), _ptr(recon),
+                                             _stream(stream)))
+        return errors, recon
+
+    # -- radius-sharded stepping (multi-GPU) ---------------------------------------
+    def sharded_begin(self, g, stream=None):
+        g = self._signal(g)
+        _capi.check(self.lib.afd_sharded_begin(self.handle, _ptr(g), g.shape[0], _stream(stream)))
+        return g.shape[0]
+
+    def select_local(self, k, dc_first, batch, stream=None):
+        out = torch.empty((batch, 32), dtype=torch.uint8, device=self.device)
+        _capi.check(self.lib.afd_select_local(self.handle, int(k), int(bool(dc_first)), _ptr(out),
+                                              batch, _stream(stream)))
+        return out
+
+    def apply_step(self, k, max_terms, threshold, dc_first, cands, steps, stream=None):
+        """cands: uint8 [batch, ncand, 32] (rank-major), steps: uint8 [batch, max_terms, 80]."""
+        cands = cands.contiguous()
+        _capi.check(self.lib.afd_apply_step(
+            self.handle, int(k), int(max_terms), 0.0 if threshold is None else float(threshold),
+            int(bool(dc_first)), _ptr(cands), cands.shape[1], cands.shape[0], _ptr(steps),
+            _stream(stream)))
+
+    def sharded_finish(self, batch, stream=None):
+        dev = self.device
+        n_steps = torch.empty(batch, dtype=torch.int32, device=dev)
+        initial = torch.empty(batch, dtype=torch.float64, device=dev)
+        rem = torch.empty((batch, self.n), dtype=torch.complex128, device=dev)
+        stopped = torch.empty(batch, dtype=torch.int32, device=dev)
+        _capi.check(self.lib.afd_sharded_finish(self.handle, batch, _ptr(n_steps), _ptr(initial),
+                                                _ptr(rem), _ptr(stopped), _stream(stream)))
+        return n_steps, initial, rem, stopped
+
+
+_PLANS = {}
+_PLANS_LOCK = threading.Lock()
+_MAX_PLANS = 16
+
+
+def get_plan(radii, n, batch=1, m0=0, m1=None, device=None):
+    """Cached plan for (device, N, radii, shard) with max_batch >= batch."""
+    dev = require_cuda(device)
+    radii = tuple(float(r) for r in radii)
+    key = (dev.index, int(n), radii, int(m0), m1)
+    with _PLANS_LOCK:
+        p = _PLANS.get(key)
+        if p is None or p.max_batch < batch:
+            if p is not None:
+                del _PLANS[key]
+            if len(_PLANS) >= _MAX_PLANS:
+                _PLANS.pop(next(iter(_PLANS)))
+            p = Plan(radii, n, m0=m0, m1=m1, max_batch=max(int(batch), 1), device=dev.index)
+            _PLANS[key] = p
+        return p
