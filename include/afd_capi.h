@@ -158,6 +158,16 @@ int afd_error_trace(afd_plan *plan, const double *g, const afd_step *steps, int 
  * launches issued, including those replayed inside CUDA graphs). */
 int64_t afd_launch_count(afd_plan *plan);
 
+/* Diagnostics (not reference functions).
+ * afd_time_field: `reps` back-to-back launches of the fused field+argmax
+ * kernel over the plan's rows for `batch` spectra, each bracketed by CUDA
+ * events on `stream`; *avg_ms = mean event time per launch.
+ * afd_fp64_peak: DFMA throughput microbenchmark on `device` (independent
+ * FMA chains on every SM), *tflops counts 2 flops per DFMA. */
+int afd_time_field(afd_plan *plan, const double *ghat, int64_t batch, int reps, double *avg_ms,
+                   void *stream);
+int afd_fp64_peak(int device, double *tflops, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

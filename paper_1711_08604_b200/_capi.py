@@ -58,6 +58,8 @@ SIGNATURES = [
     ("afd_sharded_finish", _I, [_VP, _I64, _VP, _VP, _VP, _VP, _VP]),
     ("afd_error_trace", _I, [_VP, _VP, _VP, _I, _VP, _I64, _VP, _VP, _VP]),
     ("afd_launch_count", _I64, [_VP]),
+    ("afd_time_field", _I, [_VP, _VP, _I64, _I, _VP, _VP]),
+    ("afd_fp64_peak", _I, [_I, _VP, _VP]),
 ]
 
 _LIB = None

@@ -218,3 +218,24 @@ __global__ void gather_outputs_kernel(int n, int max_terms, const Step* __restri
 }
 
 }  // namespace afd
+
+namespace afd {
+
+// DFMA throughput probe: 8 independent chains per thread, ITERS rounds.
+template <int ITERS>
+__global__ void __launch_bounds__(256) fp64_peak_kernel(double* out, double seed) {
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = seed + threadIdx.x * 1e-9 + i;
+  const double b = 0.999999, c = 1e-7;
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fma(a[i], b, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
+}  // namespace afd

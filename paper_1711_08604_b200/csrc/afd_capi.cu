@@ -632,4 +632,65 @@ int afd_error_trace(afd_plan* p, const double* g, const afd_step* steps, int max
 
 int64_t afd_launch_count(afd_plan* p) { return p ? p->launches : 0; }
 
+int afd_time_field(afd_plan* p, const double* ghat, int64_t batch, int reps, double* avg_ms,
+                   void* stream) {
+  if (!p || !ghat || !avg_ms || reps < 1) return fail(AFD_E_INVALID, "bad argument");
+  int rc;
+  if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int ncta = field_ctas(p, p->m1 - p->m0, groups_of(p->K), batch);
+  if ((rc = ensure_cand(p, batch, ncta))) return rc;
+  std::vector<cudaEvent_t> ev(2 * (size_t)reps);
+  for (auto& e : ev) CU(cudaEventCreate(&e));
+  for (int r = 0; r < reps; ++r) {
+    CU(cudaEventRecord(ev[2 * r], st));
+    AFD_DISPATCH(p->K, {
+      if ((rc = launch_field<KK>(p, (const double2*)ghat, p->m0, p->m1, batch, p->cand, ncta,
+                                 nullptr, nullptr, st)))
+        return rc;
+      break;
+    });
+    CU(cudaEventRecord(ev[2 * r + 1], st));
+  }
+  CU(cudaEventSynchronize(ev.back()));
+  double tot = 0.0;
+  for (int r = 0; r < reps; ++r) {
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, ev[2 * r], ev[2 * r + 1]));
+    tot += ms;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  *avg_ms = tot / reps;
+  return 0;
+}
+
+int afd_fp64_peak(int device, double* tflops, void* stream) {
+  if (!tflops) return fail(AFD_E_INVALID, "NULL argument");
+  CU(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int sms = 0;
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  double* out;
+  CU(cudaMalloc(&out, sizeof(double)));
+  constexpr int kIters = 1 << 14;
+  const int blocks = sms * 8, threads = 256;
+  cudaEvent_t e0, e1;
+  CU(cudaEventCreate(&e0));
+  CU(cudaEventCreate(&e1));
+  fp64_peak_kernel<kIters><<<blocks, threads, 0, st>>>(out, 1.0);  // warm-up
+  CU(cudaEventRecord(e0, st));
+  const int reps = 5;
+  for (int r = 0; r < reps; ++r) fp64_peak_kernel<kIters><<<blocks, threads, 0, st>>>(out, 1.0);
+  CU(cudaEventRecord(e1, st));
+  CU(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  const double flops = 2.0 * 8.0 * kIters * (double)blocks * threads * reps;
+  *tflops = flops / (ms * 1e-3) / 1e12;
+  return 0;
+}
+
 }  // extern "C"

@@ -113,6 +113,14 @@ class Plan:
     def launch_count(self):
         return int(self.lib.afd_launch_count(self.handle))
 
+    def time_field(self, ghat, reps=20, stream=None):
+        """Mean CUDA-event time (ms) of one fused field+argmax launch."""
+        ghat = self._signal(ghat)
+        ms = C.c_double()
+        _capi.check(self.lib.afd_time_field(self.handle, _ptr(ghat), ghat.shape[0], int(reps),
+                                            C.byref(ms), _stream(stream)))
+        return ms.value
+
     # -- transforms -----------------------------------------------------------
     def _fft(self, fn, x, stream=None):
         x = self._signal(x)
@@ -242,6 +250,14 @@ class Plan:
         _capi.check(self.lib.afd_sharded_finish(self.handle, batch, _ptr(n_steps), _ptr(initial),
                                                 _ptr(rem), _ptr(stopped), _stream(stream)))
         return n_steps, initial, rem, stopped
+
+
+def fp64_peak_tflops(device=None, stream=None):
+    """Measured DFMA throughput of this GPU (TFLOP/s, 2 flops per DFMA)."""
+    dev = require_cuda(device)
+    out = C.c_double()
+    _capi.check(_capi.load().afd_fp64_peak(dev.index, C.byref(out), _stream(stream)))
+    return out.value
 
 
 _PLANS = {}
