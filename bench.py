@@ -1,0 +1,357 @@
+"""AFD grid-evaluation throughput on B200 (BASELINE.json metric), one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl reference]
+
+Workload (BASELINE.json configs[1], "c1"): one analytic signal (32-pole sum,
+|b| < 0.95, seeded), N = 4096 samples, M = 512 radii r_m = m/M, 30 AFD steps.
+A bench step is one full decomposition (30 AFD steps = M*N*30 grid evals)
+through the device-resident decomposition (CUDA graph of fused field+argmax
+and step kernels, input resident in HBM).  `value` = whole-job grid evals/s;
+`e2e` = the same through the public API `core.decompose` with the signal in
+host memory (pinned H2D + D2H of the result inside the timed region).
+
+Multi-GPU (torchrun, one rank per GPU): c1 does not shard (SURVEY.md §8(e):
+"replicas only"); every rank decomposes its own replica, time = max over
+ranks, value = all ranks' evals / that time, scaling "weak".
+
+--impl reference times the reference's CPU implementation: the oracle port
+(oracle/afd_oracle.c, a bit-exact C restatement of the reference; the
+reference itself is pure Python and cannot travel to the GPU box) on all
+host threads, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+import warnings
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+warnings.simplefilter("ignore", UserWarning)
+
+METRIC = "AFD grid evals/sec (M*N*steps/s)"
+UNIT = "grid_evals/s"
+
+
+def flops_per_eval(n):
+    """F(N) = 5 log2 N + 7 FP64 flops per grid eval."""
+    return 5 * (int(n).bit_length() - 1) + 7
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload(cfg):
+    from paper_1711_08604_b200 import workloads as W
+    w = W.CONFIGS[cfg]
+    return w, W.radii_for(w.m)
+
+
+def host_signals(w, cfg, project=None):
+    from paper_1711_08604_b200 import workloads as W
+    sig = np.stack([W.signal_for(cfg, i) for i in range(w.batch)])
+    if w.real:
+        sig = project(sig)
+    return sig
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML, ~200 Hz)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], 0, False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                fn = getattr(self.nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    self.nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                self.reasons |= fn(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port on the host cores
+# ---------------------------------------------------------------------------
+def cpu_baseline(w, radii, g, seconds, afd_steps=None):
+    import oracle as O
+    threads = O.max_threads()
+    steps = w.steps if afd_steps is None else afd_steps
+    r = np.array(radii)
+    O.decompose(g, r, max_terms=1, threads=threads)  # warm tables / pages
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        O.decompose(g, r, max_terms=steps, threads=threads)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or reps >= 1000:
+            break
+    value = w.m * w.n * steps * reps / el
+    return {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": "%d x oracle decompose of %s signal 0 (%d AFD steps of M=%d x N=%d) "
+                      "in %.1f s on %d threads" % (reps, w.name, steps, w.m, w.n, el, threads)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle as O
+    w, radii = workload(args.config)
+    g = host_signals(w, args.config, project=lambda s: np.stack([O.analytic_projection(x.real)
+                                                                  for x in s]))[0]
+    r = np.array(radii)
+    threads = O.max_threads()
+    # size the sample: one AFD step costs t1; budget ~90 s for warmup + steps
+    t0 = time.perf_counter()
+    O.decompose(g, r, max_terms=1, threads=threads)
+    t1 = time.perf_counter() - t0
+    budget = 90.0 / max(1, args.steps + args.warmup)
+    afd = int(max(1, min(w.steps, budget // max(t1, 1e-6))))
+    for _ in range(args.warmup):
+        O.decompose(g, r, max_terms=afd, threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.decompose(g, r, max_terms=afd, threads=threads)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    evals = w.m * w.n * afd * w.batch
+    value = evals * args.steps / total
+    sample = ("oracle port (bit-exact C restatement of the reference) decomposing %s signal 0: "
+              "first %d of %d AFD steps (M=%d, N=%d) per step, %d threads"
+              % (w.name, afd, w.steps, w.m, w.n, threads))
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE generator)", "impl": "reference",
+        "config": {"workload": w.name, "n": w.n, "m": w.m, "afd_steps": w.steps,
+                   "signals": w.batch, "sampled_afd_steps_per_bench_step": afd},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1711_08604_b200 import core, engine
+    dev = torch.device("cuda", local)
+    w, radii = workload(args.config)
+    plan = engine.get_plan(radii, w.n, batch=w.batch)
+
+    def project(sig):
+        p = engine.get_plan((0.0,), w.n, batch=len(sig))
+        return plan_to_np(p.analytic_projection(torch.from_numpy(sig.astype(np.complex128))
+                                                .to(dev)))
+
+    def plan_to_np(t):
+        return t.cpu().numpy()
+
+    sig = host_signals(w, args.config, project=project)
+    g_dev = torch.from_numpy(sig).to(dev)
+    out = plan.alloc_outputs(w.batch, w.steps)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        plan.decompose(g_dev, w.steps, out=out)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    l0 = plan.launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)  # L2 flush between timed iterations (not timed)
+            ev[i][0].record(stream)
+            plan.decompose(g_dev, w.steps, out=out)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    launches = plan.launch_count() - l0
+    barrier()
+    torch.cuda.synchronize()
+    per = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(per))
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    evals = w.batch * w.m * w.n * w.steps
+    value = world * evals * args.steps / (total_ms * 1e-3)
+
+    # parity of the benchmarked output against the oracle (first signal)
+    import oracle as O
+    recs, counts = out.host_steps()
+    o = O.decompose(sig[0], np.array(radii), max_terms=w.steps)
+    parity = bool(counts[0] == len(o.steps) and
+                  np.array_equal(recs[0]["j"][:counts[0]], o.steps["j"]) and
+                  np.array_equal(recs[0]["radius"][:counts[0]], o.steps["radius"]) and
+                  np.array_equal(recs[0]["c_re"][:counts[0]], o.steps["c_re"]) and
+                  np.array_equal(recs[0]["residual"][:counts[0]], o.steps["residual"]))
+
+    # roofline: the fused field+argmax kernel, CUDA events on this stream
+    ghat = plan.dft_forward(g_dev)
+    plan.time_field(ghat, reps=5)
+    field_ms = plan.time_field(ghat, reps=50)
+    fpe = flops_per_eval(w.n)
+    field_flops = w.batch * w.m * w.n * fpe
+    achieved = field_flops / (field_ms * 1e-3) / 1e12
+    peak = engine.fp64_peak_tflops(local)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get("field_kernel_%s" % w.name)
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "field_kernel (fused prologue + inverse DIT + scale + |.|^2 + argmax)",
+                "flops_per_eval": fpe, "evals_per_launch": w.batch * w.m * w.n,
+                "launch_ms": field_ms,
+                "peak_source": "measured in-run DFMA microbenchmark (afd_fp64_peak); "
+                               "MEASURED_PEAKS.json has no FP64 entry",
+                "field_share_of_step": (field_ms * (w.steps) / (total_ms / args.steps))}
+
+    # e2e through the public API, host buffers, pinned H2D + D2H in the region
+    grid = core.ParameterGrid(radii, w.n)
+    e2e_reps = max(3, min(args.steps, 200))
+    for _ in range(3):
+        plan.decompose_host(sig, w.steps)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_reps):
+        if w.batch == 1:
+            core.decompose(sig[0], grid, max_terms=w.steps)
+        else:
+            core.decompose_batch(sig, grid, max_terms=w.steps)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    _, _, _, _, h2d, d2h = plan.decompose_host(sig, w.steps)
+    e2e = {"value": world * evals * e2e_reps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "api": "paper_1711_08604_b200.core.decompose"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(w, radii, sig[0], args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE generator, SURVEY.md §8(d))",
+            "config": {"workload": w.name, "n": w.n, "m": w.m, "afd_steps": w.steps,
+                       "signals": w.batch, "radii": "r_m = m/M",
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "flushed (512 MiB write) between timed iterations",
+                       "mode": "exact (bit-identical to reference)"},
+            "gpu_launches": launches,
+            "parity_vs_oracle": parity,
+            "roofline": roofline,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

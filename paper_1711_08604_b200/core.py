@@ -342,11 +342,9 @@ def decompose_batch(signals, grid, max_terms=10, threshold=None, engine="fft", d
     _check_decompose_args(sig, grid, max_terms, threshold, engine)
     b, n = sig.shape
     plan = _plan(n, grid.radii, batch=b)
-    out = plan.decompose(_to_dev(sig, plan), int(max_terms), threshold, dc_first)
-    rec, counts = out.host_steps()
-    initial = _host(out.initial)
-    rem = _host(out.remainder)
-    return [_build(grid, n, engine, rec[i], int(counts[i]), initial[i], rem[i].copy())
+    rec, counts, initial, rem, _, _ = plan.decompose_host(sig, int(max_terms), threshold,
+                                                          dc_first)
+    return [_build(grid, n, engine, rec[i], int(counts[i]), initial[i], rem[i])
             for i in range(b)]
 
 

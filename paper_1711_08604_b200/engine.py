@@ -201,6 +201,45 @@ class Plan:
             _stream(stream)))
         return out
 
+    def decompose_host(self, signals, max_terms, threshold=None, dc_first=False, stream=None):
+        """Host numpy [batch, N] in -> host results out, through pinned staging.
+
+        Returns (steps structured [batch, max_terms], n_steps, initial,
+        remainder [batch, N]) as numpy arrays, plus the bytes moved
+        (h2d, d2h)."""
+        sig = np.ascontiguousarray(signals, dtype=np.complex128)
+        b = sig.shape[0]
+        st = torch.cuda.current_stream() if stream is None else stream
+        key = (b, int(max_terms))
+        stage = getattr(self, "_stage", None)
+        if stage is None or stage[0] != key:
+            pin = dict(pin_memory=True)
+            stage = (key, dict(
+                gin=torch.empty((b, self.n), dtype=torch.complex128, **pin),
+                g=torch.empty((b, self.n), dtype=torch.complex128, device=self.device),
+                out=self.alloc_outputs(b, max_terms),
+                steps=torch.empty((b, max_terms, _capi.STEP_DTYPE.itemsize), dtype=torch.uint8,
+                                  **pin),
+                n_steps=torch.empty(b, dtype=torch.int32, **pin),
+                initial=torch.empty(b, dtype=torch.float64, **pin),
+                rem=torch.empty((b, self.n), dtype=torch.complex128, **pin)))
+            self._stage = stage
+        s = stage[1]
+        s["gin"].numpy()[...] = sig
+        with torch.cuda.stream(st):
+            s["g"].copy_(s["gin"], non_blocking=True)
+            out = self.decompose(s["g"], max_terms, threshold, dc_first, stream=st, out=s["out"])
+            s["steps"].copy_(out.steps, non_blocking=True)
+            s["n_steps"].copy_(out.n_steps, non_blocking=True)
+            s["initial"].copy_(out.initial, non_blocking=True)
+            s["rem"].copy_(out.remainder, non_blocking=True)
+        st.synchronize()
+        steps = s["steps"].numpy().view(_capi.STEP_DTYPE)[..., 0].copy()
+        h2d = sig.nbytes
+        d2h = (s["steps"].numel() + 4 * b + 8 * b + 16 * b * self.n)
+        return (steps, s["n_steps"].numpy().copy(), s["initial"].numpy().copy(),
+                s["rem"].numpy().copy(), h2d, d2h)
+
     def alloc_outputs(self, batch, max_terms):
         dev = self.device
         return DeviceDecomposition(
