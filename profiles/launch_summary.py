@@ -1,0 +1,35 @@
+"""Summarise an `ncu --metrics gpu__time_duration.sum --csv` launch list.
+
+    python profiles/launch_summary.py gpurun_out/launches.csv
+Prints per-kernel launch counts, mean and total device time, and shares.
+(ncu serialises launches and runs them cold, so compare shares, not
+absolute step times.)
+"""
+import collections
+import csv
+import sys
+
+
+def summarise(path):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h, data = rows[hi], rows[hi + 1:]
+    ik, iv, iu = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    agg = collections.defaultdict(list)
+    for r in data:
+        if len(r) <= iv:
+            continue
+        name = r[ik].split("(")[0].replace("void ", "")
+        v = float(r[iv].replace(",", ""))
+        v = v / 1000 if r[iu] == "ns" else (v * 1000 if r[iu] == "ms" else v)
+        agg[name].append(v)
+    tot = sum(sum(v) for v in agg.values())
+    out = []
+    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+        out.append("%-70s n=%5d mean=%9.2f us total=%10.1f us share=%5.1f%%"
+                   % (k[:70], len(v), sum(v) / len(v), sum(v), 100 * sum(v) / tot))
+    return "\n".join(out)
+
+
+if __name__ == "__main__":
+    print(summarise(sys.argv[1]))
