@@ -69,11 +69,14 @@ class AfdCudaUnavailable(RuntimeError):
     """The CUDA extension is missing or unusable; there is no CPU fallback."""
 
 
-def load(path=LIB_PATH):
-    """Load libafd_b200.so and declare every exported signature."""
+def load(path=None):
+    """Load libafd_b200.so and declare every exported signature.
+
+    AFD_LIB_PATH overrides the in-tree library (used to A/B kernel variants)."""
     global _LIB
     if _LIB is not None:
         return _LIB
+    path = path or os.environ.get("AFD_LIB_PATH") or LIB_PATH
     if not os.path.exists(path):
         raise AfdCudaUnavailable(
             "libafd_b200.so not built (%s); run __graft_entry__.build()" % path)

@@ -13,6 +13,7 @@
 #include "../../include/afd_capi.h"
 #include "afd_kernels.cuh"
 #include "afd_aux.cuh"
+#include "afd_step_cluster.cuh"
 
 using namespace afd;
 
@@ -85,19 +86,35 @@ struct afd_plan {
 // ---------------------------------------------------------------------------
 namespace {
 
+// Field kernel geometry: 8 points per thread (radix-8 register passes,
+// ~64 registers) so two 512-thread CTAs share an SM; rows of N <= 2048
+// are grouped to fill 512 threads.
+#ifndef AFD_FIELD_RB
+#define AFD_FIELD_RB 3
+#endif
+constexpr int kFieldRB = AFD_FIELD_RB;
+
 template <int K>
 constexpr int groups_for() {
-  return Geo<K>::T >= 256 ? 1 : 256 / Geo<K>::T;
+  return Geo<K, kFieldRB>::T >= 512 ? 1 : 512 / Geo<K, kFieldRB>::T;
 }
 
 template <int K>
 int field_block() {
-  return Geo<K>::T * groups_for<K>();
+  return Geo<K, kFieldRB>::T * groups_for<K>();
 }
 
 template <int K>
 size_t field_smem() {
-  return sizeof(double2) * Geo<K>::N * groups_for<K>();
+  return sizeof(double2) *
+         (Geo<K, kFieldRB>::SMEM * groups_for<K>() + SmemTw<K, kFieldRB>::ENTRIES);
+}
+
+// Single-signal steps spread over an 8-CTA cluster for 1024 <= N <= 8192
+// (afd_step_cluster.cuh); smaller N use one CTA per signal.
+template <int K>
+constexpr bool use_cluster_step() {
+  return K >= 10 && K <= 13;
 }
 
 template <int K>
@@ -107,7 +124,7 @@ int row_block() {
 
 template <int K, bool MAT>
 int setup_field_kernel(int* occ) {
-  auto kern = field_kernel<K, groups_for<K>(), MAT>;
+  auto kern = field_kernel<K, kFieldRB, groups_for<K>(), MAT>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem<K>()));
   if (occ) CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, field_block<K>(), field_smem<K>()));
   return 0;
@@ -120,6 +137,10 @@ int setup_kernels(afd_plan* p) {
   if ((rc = setup_field_kernel<K, true>(nullptr))) return rc;
   CU(cudaFuncSetAttribute(step_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)RowSmem<K>::bytes));
+  if constexpr (use_cluster_step<K>()) {
+    CU(cudaFuncSetAttribute(step_cluster_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)ClusterSmem<K>::bytes));
+  }
   CU(cudaFuncSetAttribute(fft_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)RowSmem<K>::bytes));
   if (p->field_occ < 1) p->field_occ = 1;
@@ -152,10 +173,10 @@ int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64
   constexpr int G = groups_for<K>();
   dim3 grid(ncta, (unsigned)batch);
   if (field_out) {
-    field_kernel<K, G, true><<<grid, field_block<K>(), field_smem<K>(), st>>>(
+    field_kernel<K, kFieldRB, G, true><<<grid, field_block<K>(), field_smem<K>(), st>>>(
         ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, nullptr, field_out, nullptr);
   } else {
-    field_kernel<K, G, false><<<grid, field_block<K>(), field_smem<K>(), st>>>(
+    field_kernel<K, kFieldRB, G, false><<<grid, field_block<K>(), field_smem<K>(), st>>>(
         ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, cand, nullptr, state);
   }
   p->launches++;
@@ -166,9 +187,16 @@ int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64
 template <int K>
 int launch_step(afd_plan* p, int k, int max_terms, double thr, int dc_first, const double2* g0,
                 const Cand* cand, int ncand, int64_t batch, Step* steps, cudaStream_t st) {
-  step_kernel<K><<<(unsigned)batch, row_block<K>(), RowSmem<K>::bytes, st>>>(
-      k, max_terms, thr, dc_first, g0, p->rem, p->ghat, cand, ncand, p->radii, p->circle,
-      p->twst, p->state, steps);
+  if constexpr (use_cluster_step<K>()) {
+    step_cluster_kernel<K><<<(unsigned)(batch * kClusterCtas), ClusterGeo<K>::THREADS,
+                             ClusterSmem<K>::bytes, st>>>(
+        k, max_terms, thr, dc_first, g0, p->rem, p->ghat, cand, ncand, p->radii, p->circle,
+        p->twst, p->state, steps);
+  } else {
+    step_kernel<K><<<(unsigned)batch, row_block<K>(), RowSmem<K>::bytes, st>>>(
+        k, max_terms, thr, dc_first, g0, p->rem, p->ghat, cand, ncand, p->radii, p->circle,
+        p->twst, p->state, steps);
+  }
   p->launches++;
   CU(cudaGetLastError());
   return 0;

@@ -25,7 +25,7 @@
 // of every pass conflict-free (each quarter-warp hits 8 distinct 16-B bank
 // groups).  Twiddles come from per-stage tables S_b[k] = w[k << (K-1-b)]
 // (offset 2^b - 1, N-1 entries total): warp-uniform in pass 0, consecutive
-// across lanes later.
+// across lanes later.  (Shared-memory slots are padded, see Geo::sw.)
 #pragma once
 
 #include "afd_common.cuh"
@@ -38,24 +38,25 @@ __host__ __device__ constexpr int brev_bits(int x, int bits) {
   return r;
 }
 
-template <int K>
+template <int K, int RBITS = 4>
 struct Geo {
   static constexpr int N = 1 << K;
-  static constexpr int RB = K >= 4 ? 4 : K;  // register (stage) bits per pass
-  static constexpr int P = 1 << RB;          // points per thread
-  static constexpr int T = N / P;            // threads per row
-  static constexpr int TB = K - RB;          // thread-index bits
-  static constexpr int NPASS = (K + 3) / 4;
+  static constexpr int RB = K >= RBITS ? RBITS : K;  // register (stage) bits per pass
+  static constexpr int P = 1 << RB;                  // points per thread
+  static constexpr int T = N / P;                    // threads per row
+  static constexpr int TB = K - RB;                  // thread-index bits
+  static constexpr int NPASS = (K + RB - 1) / RB;
 
-  __device__ __forceinline__ static int sw(int p) {
-    if constexpr (K >= 6) {
-      return p ^ ((p >> (K - 3)) & 7);
-    } else {
-      return p;
-    }
+  // Shared-memory slot of position p: one pad slot per 2^(K-3) positions.
+  // pos() is an OR of disjoint bit fields of the thread index and of the
+  // register index, so SW(pos) = base(thread) + const(register): every
+  // exchange access is a register base plus an immediate offset.
+  __host__ __device__ __forceinline__ static constexpr int sw(int p) {
+    return K >= 6 ? p + (p >> (K - 3)) : p;
   }
+  static constexpr int SMEM = K >= 6 ? N + (N >> (K - 3)) : N;  // slots per row
   __host__ __device__ static constexpr int c_of(int pass) {
-    return ((4 * pass + 4) < K ? (4 * pass + 4) : K) - RB;
+    return ((RB * pass + RB) < K ? (RB * pass + RB) : K) - RB;
   }
   __device__ __forceinline__ static int pos(int c, int t, int i) {
     return (t & ((1 << c) - 1)) | (i << c) | ((t >> c) << (c + RB));
@@ -66,14 +67,49 @@ struct Geo {
   }
 };
 
-// Twiddle used by the butterfly: numpy's table value, conjugated for the
-// inverse direction (np.conj(w), transform.py:132,199).
-template <bool INV>
-__device__ __forceinline__ double2 twiddle(const double2* __restrict__ tb, int k) {
-  double2 w = __ldg(tb + k);
-  if (INV) w.y = -w.y;
-  return w;
-}
+// Twiddle sources.  tw(b, k) returns numpy's w[k << (K-1-b)] for stage b.
+//
+// GlobalTw: per-stage tables S_b (offset 2^b - 1) in global memory, read
+// through the read-only path.
+struct GlobalTw {
+  const double2* __restrict__ st;
+  __device__ __forceinline__ double2 operator()(int b, int k) const {
+    return __ldg(st + ((1 << b) - 1) + k);
+  }
+};
+
+// SmemTw<K>: shared-memory copy laid out so every warp access is
+// conflict-free.  Stages b < 4 (pass 0) are warp-uniform and stages
+// b >= K-4 read the half table w[0..N/2) at lane stride 2^(K-1-b) <= 8,
+// stored XOR-swizzled (i ^ ((i >> 3) & 7)) so strides 1, 2, 4 and 8 all hit
+// 8 distinct 16-byte bank groups per quarter-warp.  The middle stages
+// 4 <= b < K-4 (lane stride >= 16) use compact per-stage tables.
+template <int K, int RB = 4>
+struct SmemTw {
+  static constexpr int HALF = 1 << (K - 1);
+  static constexpr int HALF_SLOTS = HALF + HALF / 8;  // padded half table
+  static constexpr int LO = RB;      // first thread-dependent stage
+  static constexpr int HI = K - 4;   // stages >= HI read the half table
+  static constexpr int MID = (HI > LO) ? (1 << HI) - (1 << LO) : 0;  // S_LO..S_{HI-1}
+  static constexpr int ENTRIES = HALF_SLOTS + MID;
+  const double2* sm;
+  // padded slot: strides 1, 2, 4, 8 over a quarter-warp hit 8 distinct
+  // 16-byte bank groups, and slot(a | b) = slot(a) + slot(b) for disjoint
+  // bit fields (base + immediate addressing)
+  __device__ __forceinline__ static int swz(int i) { return i + (i >> 3); }
+  __device__ __forceinline__ double2 operator()(int b, int k) const {
+    if (b >= LO && b < HI) return sm[HALF_SLOTS + (1 << b) - (1 << LO) + k];
+    return sm[swz(k << (K - 1 - b))];
+  }
+  // Fill from the global stage tables (all threads of the block).
+  __device__ static void load(double2* dst, const double2* __restrict__ st) {
+    // half table = stage K-1 table S_{K-1}[k] = w[k]
+    const double2* half = st + (1 << (K - 1)) - 1;
+    for (int i = threadIdx.x; i < HALF; i += blockDim.x) dst[swz(i)] = __ldg(half + i);
+    for (int i = threadIdx.x; i < MID; i += blockDim.x)
+      dst[HALF_SLOTS + i] = __ldg(st + (1 << LO) - 1 + i);
+  }
+};
 
 // One butterfly exactly as transform.py:89-91 evaluates it.
 __device__ __forceinline__ void bfly(double2& lo, double2& hi, double2 w) {
@@ -91,12 +127,11 @@ __device__ __forceinline__ void bfly1(double2& lo, double2& hi) {
 }
 
 // Butterflies of pass PASS on the 16 registers of logical thread t.
-template <int K, int PASS, bool INV>
-__device__ __forceinline__ void fft_pass(double2 (&v)[Geo<K>::P], int t,
-                                         const double2* __restrict__ twst) {
-  using G = Geo<K>;
-  constexpr int b0 = 4 * PASS;
-  constexpr int b1 = (4 * PASS + 4) < K ? (4 * PASS + 4) : K;
+template <int K, int RB, int PASS, bool INV, class Tw>
+__device__ __forceinline__ void fft_pass(double2 (&v)[Geo<K, RB>::P], int t, const Tw& tw) {
+  using G = Geo<K, RB>;
+  constexpr int b0 = G::RB * PASS;
+  constexpr int b1 = (G::RB * PASS + G::RB) < K ? (G::RB * PASS + G::RB) : K;
   constexpr int c = G::c_of(PASS);
   const int tlow = t & ((1 << c) - 1);
 #pragma unroll
@@ -107,10 +142,10 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[Geo<K>::P], int t,
       for (int h = 0; h < G::P / 2; ++h) bfly1(v[2 * h], v[2 * h + 1]);
       continue;
     }
-    const double2* __restrict__ tb = twst + ((1 << b) - 1);
 #pragma unroll
     for (int kk = 0; kk < (1 << q); ++kk) {
-      const double2 w = twiddle<INV>(tb, tlow | (kk << c));
+      double2 w = tw(b, tlow | (kk << c));
+      if (INV) w.y = -w.y;  // np.conj(w), transform.py:132,199
 #pragma unroll
       for (int h = 0; h < (G::P >> (q + 1)); ++h) {
         const int i = kk | (h << (q + 1));
@@ -121,17 +156,17 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[Geo<K>::P], int t,
 }
 
 // Store the registers of pass PASS to shared memory (swizzled positions).
-template <int K, int PASS>
-__device__ __forceinline__ void pass_store(const double2 (&v)[Geo<K>::P], int t, double2* sm) {
-  using G = Geo<K>;
+template <int K, int RB, int PASS>
+__device__ __forceinline__ void pass_store(const double2 (&v)[Geo<K, RB>::P], int t, double2* sm) {
+  using G = Geo<K, RB>;
   constexpr int c = G::c_of(PASS);
 #pragma unroll
   for (int i = 0; i < G::P; ++i) sm[G::sw(G::pos(c, t, i))] = v[i];
 }
 
-template <int K, int PASS>
-__device__ __forceinline__ void pass_load(double2 (&v)[Geo<K>::P], int t, const double2* sm) {
-  using G = Geo<K>;
+template <int K, int RB, int PASS>
+__device__ __forceinline__ void pass_load(double2 (&v)[Geo<K, RB>::P], int t, const double2* sm) {
+  using G = Geo<K, RB>;
   constexpr int c = G::c_of(PASS);
 #pragma unroll
   for (int i = 0; i < G::P; ++i) v[i] = sm[G::sw(G::pos(c, t, i))];
@@ -143,25 +178,25 @@ __device__ __forceinline__ void pass_load(double2 (&v)[Geo<K>::P], int t, const 
 // calls this (block-uniform __syncthreads), `active` masks threads that own
 // no row this round.  On return v holds pass NPASS-1's outputs at natural
 // positions pos(c_last, tp, i).
-template <int K, bool INV, int PASS = 0>
-__device__ __forceinline__ void fft_passes(double2 (&v)[Geo<K>::P], int tp, bool active,
-                                           double2* sm, const double2* __restrict__ twst) {
-  using G = Geo<K>;
+template <int K, bool INV, int RB = 4, int PASS = 0, class Tw>
+__device__ __forceinline__ void fft_passes(double2 (&v)[Geo<K, RB>::P], int tp, bool active,
+                                           double2* sm, const Tw& tw) {
+  using G = Geo<K, RB>;
   const int t = PASS == 0 ? brev_bits(tp, G::TB) : tp;
-  if (active) fft_pass<K, PASS, INV>(v, t, twst);
+  if (active) fft_pass<K, RB, PASS, INV>(v, t, tw);
   if constexpr (PASS + 1 < G::NPASS) {
-    if (active) pass_store<K, PASS>(v, t, sm);
+    if (active) pass_store<K, RB, PASS>(v, t, sm);
     __syncthreads();
-    if (active) pass_load<K, PASS + 1>(v, tp, sm);
+    if (active) pass_load<K, RB, PASS + 1>(v, tp, sm);
     __syncthreads();
-    fft_passes<K, INV, PASS + 1>(v, tp, active, sm, twst);
+    fft_passes<K, INV, RB, PASS + 1>(v, tp, active, sm, tw);
   }
 }
 
 // Natural output position of register i after the last pass.
-template <int K>
+template <int K, int RB = 4>
 __device__ __forceinline__ int out_pos(int tp, int i) {
-  using G = Geo<K>;
+  using G = Geo<K, RB>;
   return G::pos(G::c_of(G::NPASS - 1), tp, i);
 }
 

@@ -21,6 +21,8 @@
 // afd_common.cuh); the library is compiled with -fmad=false.
 #pragma once
 
+#include <type_traits>
+
 #include "afd_fft.cuh"
 
 namespace afd {
@@ -48,8 +50,8 @@ enum : int { kStepPowAmbiguous = 1 };
 // each group evaluates one radius row per round; rows are strided over the
 // CTAs of a signal (blockIdx.y).
 // ---------------------------------------------------------------------------
-template <int K, int G, bool MATERIALIZE>
-__global__ void __launch_bounds__(Geo<K>::T * G, (Geo<K>::T * G <= 256) ? 2 : 1)
+template <int K, int RB, int G, bool MATERIALIZE>
+__global__ void __launch_bounds__(Geo<K, RB>::T * G, (Geo<K, RB>::T * G <= 512) ? 2 : 1)
 field_kernel(const double2* __restrict__ ghat,     // [batch][N]
              const double* __restrict__ pw,        // [rows of plan][N], r^l natural l
              const double* __restrict__ scales,    // [M] (global radius index)
@@ -59,21 +61,26 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
              Cand* __restrict__ cand_out,          // [batch][gridDim.x]
              double2* __restrict__ field_out,      // [row1-row0][N] (MATERIALIZE)
              const State* __restrict__ state) {    // per-signal stop flags or null
-  using Gm = Geo<K>;
+  using Gm = Geo<K, RB>;
   constexpr int N = Gm::N, T = Gm::T, P = Gm::P;
   extern __shared__ double2 smem[];
   const int sig = blockIdx.y;
   if (state != nullptr && state[sig].stopped) return;
   const int g = threadIdx.x / T;
   const int tp = threadIdx.x % T;
-  double2* sm = smem + g * N;
+  using TwT = SmemTw<K, RB>;
+  TwT::load(smem, twst);
+  const TwT tw{smem};
+  double2* sm = smem + TwT::ENTRIES + g * Gm::SMEM;
   const double2* __restrict__ gh = ghat + (size_t)sig * N;
 
-  Cand best;
-  best.mag = -1.0;
-  best.flat = 0x7fffffffffffffffLL;
-  best.re = 0.0;
-  best.im = 0.0;
+  // Running first maximum.  Rows are visited in increasing s and, within a
+  // row, a thread's outputs j = out_pos(tp, i) increase with i, so a strict
+  // '>' keeps the lowest flat index among equal magnitudes; the flat index is
+  // formed once at the end.
+  double best_mag = -1.0, best_re = 0.0, best_im = 0.0;
+  int best_rd = -1, best_i = 0;
+  __syncthreads();
 
   const long long rows = row1 - row0;
   const long long per_round = (long long)gridDim.x * G;
@@ -93,30 +100,36 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
         v[i] = make_double2(p * c.x, p * c.y);
       }
     }
-    fft_passes<K, true>(v, tp, active, sm, twst);
+    fft_passes<K, true, RB>(v, tp, active, sm, tw);
     if (active) {
       const double sc = __ldg(scales + s);
 #pragma unroll
       for (int i = 0; i < P; ++i) {
-        const int j = out_pos<K>(tp, i);
         // y *= scales[:, None] (transform.py:200)
         const double2 f = make_double2(v[i].x * sc, v[i].y * sc);
         if (MATERIALIZE) {
-          field_out[(size_t)(s - row0) * N + j] = f;
+          field_out[(size_t)(s - row0) * N + out_pos<K, RB>(tp, i)] = f;
         } else {
-          const double mg = np_mag2(f);
-          const long long flat = s * (long long)N + j;
-          if (cand_better(mg, flat, best.mag, best.flat)) {
-            best.mag = mg;
-            best.flat = flat;
-            best.re = f.x;
-            best.im = f.y;
+          const double mg = np_mag2(f);  // core.py:298
+          if (__builtin_expect(mg > best_mag, 0)) {
+            best_mag = mg;
+            best_re = f.x;
+            best_im = f.y;
+            best_rd = (int)rd;
+            best_i = i;
           }
         }
       }
     }
   }
   if (MATERIALIZE) return;
+  Cand best;
+  best.mag = best_mag;
+  const long long best_s = row0 + (long long)best_rd * per_round + (long long)blockIdx.x * G + g;
+  best.flat =
+      best_rd >= 0 ? best_s * (long long)N + out_pos<K, RB>(tp, best_i) : 0x7fffffffffffffffLL;
+  best.re = best_re;
+  best.im = best_im;
   // CTA reduction of the candidates (first maximum).
   __shared__ Cand red[32];
   best = warp_argmax(best);
@@ -138,9 +151,8 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
 // Forward (INV=false) or inverse transform of the row held in `buf`
 // (natural order, swizzled), result written to `out` (natural order,
 // global).  For the inverse, SCALE_N applies `y /= n` (transform.py:133).
-template <int K, bool INV, bool SCALE_N>
-__device__ void row_transform(double2* buf, const double2* __restrict__ twst,
-                              double2* __restrict__ out) {
+template <int K, bool INV, bool SCALE_N, class Tw>
+__device__ void row_transform(double2* buf, const Tw& tw, double2* __restrict__ out) {
   using Gm = Geo<K>;
   constexpr int T = Gm::T, P = Gm::P;
   const int tp = threadIdx.x;
@@ -151,7 +163,7 @@ __device__ void row_transform(double2* buf, const double2* __restrict__ twst,
     for (int i = 0; i < P; ++i) v[i] = buf[Gm::sw(Gm::l0(tp, i))];
   }
   __syncthreads();
-  fft_passes<K, INV>(v, tp, active, buf, twst);
+  fft_passes<K, INV>(v, tp, active, buf, tw);
   if (active) {
     const double2 dn = make_double2((double)Gm::N, 0.0);
 #pragma unroll
@@ -164,6 +176,15 @@ __device__ void row_transform(double2* buf, const double2* __restrict__ twst,
   __syncthreads();
 }
 
+template <int K, bool SMEM>
+__device__ __forceinline__ auto make_tw(double2* sm, const double2* __restrict__ st) {
+  if constexpr (SMEM) {
+    return SmemTw<K>{sm};
+  } else {
+    return GlobalTw{st};
+  }
+}
+
 template <int K>
 struct SwIdx {
   __device__ __forceinline__ int operator()(int i) const { return Geo<K>::sw(i); }
@@ -173,11 +194,23 @@ struct PlainIdx {
 };
 
 // Shared-memory layout of the one-CTA-per-signal kernels.
+// Twiddles go to shared memory when they fit beside the row buffers
+// (all N <= 4096); N = 8192 reads the global stage tables.
+template <int K>
+struct RowSmemBase {
+  static constexpr int N = 1 << K;
+  static constexpr size_t rest = sizeof(double2) * Geo<K>::SMEM + sizeof(double) * N +
+                                 sizeof(double) * 2 * (N / 8 + 16);
+  static constexpr bool smem_tw = sizeof(double2) * SmemTw<K>::ENTRIES + rest <= 200 * 1024;
+};
+
 template <int K>
 struct RowSmem {
   static constexpr int N = 1 << K;
-  static constexpr size_t buf = 0;                                  // N double2
-  static constexpr size_t mag = buf + sizeof(double2) * N;          // N double
+  static constexpr bool smem_tw = RowSmemBase<K>::smem_tw;
+  static constexpr size_t tw = 0;                                   // SmemTw<K> (if smem_tw)
+  static constexpr size_t buf = smem_tw ? sizeof(double2) * SmemTw<K>::ENTRIES : 0;  // N double2
+  static constexpr size_t mag = buf + sizeof(double2) * Geo<K>::SMEM;  // N double
   static constexpr size_t scratch = mag + sizeof(double) * N;       // 2*(N/8+16) double
   static constexpr size_t bytes = scratch + sizeof(double) * 2 * (N / 8 + 16);
 };
@@ -206,14 +239,18 @@ step_kernel(int k, int max_terms, double threshold, int dc_first,
   double2* buf = reinterpret_cast<double2*>(smraw + L::buf);
   double* mag = reinterpret_cast<double*>(smraw + L::mag);
   double* scratch = reinterpret_cast<double*>(smraw + L::scratch);
+  double2* twsm = reinterpret_cast<double2*>(smraw + L::tw);
   __shared__ Cand red[32];
   __shared__ int s_stop;
+  using TwT = typename std::conditional<L::smem_tw, SmemTw<K>, GlobalTw>::type;
+  const TwT tw = make_tw<K, L::smem_tw>(twsm, twst);
   const SwIdx<K> SW;
   const int sig = blockIdx.x;
   State& st = state[sig];
   double2* __restrict__ r = rem + (size_t)sig * N;
   double2* __restrict__ gh = ghat + (size_t)sig * N;
 
+  if (L::smem_tw && (k < 0 || !st.stopped)) SmemTw<K>::load(twsm, twst);  // after next barrier
   if (k < 0) {
     const double2* __restrict__ x = g0 + (size_t)sig * N;
     for (int m = threadIdx.x; m < N; m += blockDim.x) {
@@ -233,7 +270,7 @@ step_kernel(int k, int max_terms, double threshold, int dc_first,
       s_stop = st.stopped;
     }
     __syncthreads();
-    if (!s_stop) row_transform<K, false, false>(buf, twst, gh);
+    if (!s_stop) row_transform<K, false, false>(buf, tw, gh);
     return;
   }
 
@@ -318,7 +355,7 @@ step_kernel(int k, int max_terms, double threshold, int dc_first,
     s_stop = stop;
   }
   __syncthreads();
-  if (!s_stop) row_transform<K, false, false>(buf, twst, gh);
+  if (!s_stop) row_transform<K, false, false>(buf, tw, gh);
 }
 
 // ---------------------------------------------------------------------------
@@ -334,19 +371,23 @@ fft_kernel(int mode, const double2* __restrict__ x, double2* __restrict__ y,
   using L = RowSmem<K>;
   extern __shared__ __align__(16) unsigned char smraw[];
   double2* buf = reinterpret_cast<double2*>(smraw + L::buf);
+  double2* twsm = reinterpret_cast<double2*>(smraw + L::tw);
+  if (L::smem_tw) SmemTw<K>::load(twsm, twst);
+  using TwT = typename std::conditional<L::smem_tw, SmemTw<K>, GlobalTw>::type;
+  const TwT tw = make_tw<K, L::smem_tw>(twsm, twst);
   const SwIdx<K> SW;
   const double2* __restrict__ xs = x + (size_t)blockIdx.x * N;
   double2* __restrict__ ys = y + (size_t)blockIdx.x * N;
   for (int m = threadIdx.x; m < N; m += blockDim.x) buf[SW(m)] = xs[m];
   __syncthreads();
   if (mode == 0) {
-    row_transform<K, false, false>(buf, twst, ys);
+    row_transform<K, false, false>(buf, tw, ys);
   } else if (mode == 1) {
-    row_transform<K, true, true>(buf, twst, ys);
+    row_transform<K, true, true>(buf, tw, ys);
   } else {
     // core.py:224-231: spectrum = dft_forward(x); spectrum[1:half] *= 2;
     // spectrum[half+1:] = 0; dft_inverse(spectrum)
-    row_transform<K, false, false>(buf, twst, ys);
+    row_transform<K, false, false>(buf, tw, ys);
     constexpr int half = N / 2;
     for (int m = threadIdx.x; m < N; m += blockDim.x) {
       double2 v = ys[m];
@@ -355,7 +396,7 @@ fft_kernel(int mode, const double2* __restrict__ x, double2* __restrict__ y,
       buf[SW(m)] = v;
     }
     __syncthreads();
-    row_transform<K, true, true>(buf, twst, ys);
+    row_transform<K, true, true>(buf, tw, ys);
   }
 }
 

@@ -1,0 +1,284 @@
+// afd_step_cluster.cuh — the per-step select / update / energy / forward
+// transform of one signal spread over a thread-block cluster of 8 CTAs
+// (8 SMs) with distributed shared memory, for N = 2^K, 10 <= K <= 13.
+//
+// Same arithmetic, same results as step_kernel (afd_kernels.cuh); only the
+// work distribution differs:
+//   * CTA c owns natural samples m in [c*NC, (c+1)*NC), NC = N/8: it
+//     updates them (core.py:303-314) and sums their |G|^2 - with NC >= 128 a
+//     power of two, that slice is exactly one node of numpy's pairwise-sum
+//     tree, so the 8 node sums combined as ((e0+e1)+(e2+e3))+((e4+e5)+(e6+e7))
+//     reproduce np.mean bit for bit (core.py:195-198).  dc_first's complex
+//     mean (core.py:375) is combined the same way.
+//   * The forward DIT (transform.py:106-124): stages 0..K-4 pair positions
+//     inside aligned blocks of NC bit-reversed positions, so CTA c runs them
+//     on positions [c*NC, (c+1)*NC) (inputs gathered over DSMEM: natural
+//     index l = 8*rev(q) + rev3(c)); stages K-3..K-1 pair positions that
+//     differ in the top 3 bits, so after a cluster barrier CTA c runs them
+//     as radix-8 butterflies on NC/8 position groups q + NC*u, u = 0..7,
+//     gathered from all 8 CTAs over DSMEM.  Every butterfly uses numpy's
+//     N-point table value, as in the reference.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "afd_kernels.cuh"
+
+namespace afd {
+
+namespace cg = cooperative_groups;
+
+constexpr int kClusterCtas = 8;
+
+template <int K>
+struct ClusterGeo {
+  static constexpr int N = 1 << K;
+  static constexpr int NC = N / kClusterCtas;       // samples / positions per CTA
+  static constexpr int KL = K - 3;                  // bits of the CTA-local transform
+  static constexpr int RB = 3;                      // local pass register bits
+  using GL = Geo<KL, RB>;                           // local transform geometry
+  static constexpr int LOCAL_THREADS = GL::T;       // threads of the local transform
+  static constexpr int GROUPS = NC / 8;             // radix-8 groups per CTA in phase 2
+  static constexpr int THREADS = 256;
+  static_assert(NC >= 128, "slice must be a pairwise-sum tree node");
+  static_assert(LOCAL_THREADS <= THREADS && GROUPS <= THREADS, "block too small");
+};
+
+template <int K>
+struct ClusterSmem {
+  using CG = ClusterGeo<K>;
+  static constexpr size_t slice = 0;                                   // NC double2 (natural)
+  static constexpr size_t part = slice + sizeof(double2) * CG::NC;     // GL::SMEM double2
+  static constexpr size_t mag = part + sizeof(double2) * CG::GL::SMEM; // NC double
+  static constexpr size_t twl = mag + sizeof(double) * CG::NC;         // 2^(K-3)-1 double2
+  static constexpr size_t scratch = twl + sizeof(double2) * (CG::NC - 1);  // 2*(NC/8+16)
+  static constexpr size_t bytes = scratch + sizeof(double) * 2 * (CG::NC / 8 + 16);
+};
+
+// Local stage tables S_0..S_{K-4} copied to shared memory.
+struct LocalTw {
+  const double2* sm;
+  __device__ __forceinline__ double2 operator()(int b, int k) const { return sm[(1 << b) - 1 + k]; }
+};
+
+template <int K>
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(256)
+step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
+                    const double2* __restrict__ g0, double2* __restrict__ rem,
+                    double2* __restrict__ ghat, const Cand* __restrict__ cand, int ncand,
+                    const double* __restrict__ radii, const double2* __restrict__ circle,
+                    const double2* __restrict__ twst, State* __restrict__ state,
+                    Step* __restrict__ steps) {
+  using CG = ClusterGeo<K>;
+  using L = ClusterSmem<K>;
+  using GL = typename CG::GL;
+  constexpr int N = CG::N, NC = CG::NC;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int c = (int)cluster.block_rank();
+  const int sig = blockIdx.x / kClusterCtas;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double2* slice = reinterpret_cast<double2*>(smraw + L::slice);
+  double2* part = reinterpret_cast<double2*>(smraw + L::part);
+  double* mag = reinterpret_cast<double*>(smraw + L::mag);
+  double2* twl = reinterpret_cast<double2*>(smraw + L::twl);
+  double* scratch = reinterpret_cast<double*>(smraw + L::scratch);
+  __shared__ double s_node[2];   // this CTA's pairwise-tree node sums
+  __shared__ Cand red[32];
+  __shared__ int s_stop;
+  State& st = state[sig];
+  double2* __restrict__ r = rem + (size_t)sig * N;
+  double2* __restrict__ gh = ghat + (size_t)sig * N;
+  const int tid = threadIdx.x;
+  const int m0 = c * NC;
+
+  if (k >= 0 && st.stopped) return;  // cluster-uniform
+
+  // local stage tables S_0..S_{K-4} (== twst[0 .. 2^(K-3)-1))
+  for (int i = tid; i < NC - 1; i += blockDim.x) twl[i] = __ldg(twst + i);
+  // phase-2 twiddles of this thread, prefetched: stage b = K-3+e uses
+  // w[(q + NC*(u mod 2^e)) << (2-e)], q = c*GROUPS + tid
+  const int q = c * CG::GROUPS + tid;
+  double2 w2[7];
+  if (tid < CG::GROUPS) {
+    const double2* half = twst + (N / 2) - 1;  // S_{K-1}[k] = w[k]
+#pragma unroll
+    for (int e = 0; e < 3; ++e)
+#pragma unroll
+      for (int h = 0; h < (1 << e); ++h) w2[(1 << e) - 1 + h] = __ldg(half + ((q + NC * h) << (2 - e)));
+  }
+
+  // ---- select ---------------------------------------------------------------
+  long long s = 0, j = 0;
+  double radius = 0.0;
+  double2 a = make_double2(0.0, 0.0), coeff = make_double2(0.0, 0.0);
+  if (k == 0 && dc_first) {
+    // core.py:373-375: coeff = complex(np.mean(remainder)), pairwise over N
+    for (int i = tid; i < NC; i += blockDim.x) slice[i] = r[m0 + i];
+    __syncthreads();
+    const double2 node = cpairwise_sum_block(slice, NC, scratch, PlainIdx());
+    if (tid == 0) {
+      s_node[0] = node.x;
+      s_node[1] = node.y;
+    }
+    cluster.sync();
+    double re[kClusterCtas], im[kClusterCtas];
+#pragma unroll
+    for (int u = 0; u < kClusterCtas; ++u) {
+      const double* rn = cluster.map_shared_rank(s_node, u);
+      re[u] = rn[0];
+      im[u] = rn[1];
+    }
+    const double2 sum =
+        make_double2(((re[0] + re[1]) + (re[2] + re[3])) + ((re[4] + re[5]) + (re[6] + re[7])),
+                     ((im[0] + im[1]) + (im[2] + im[3])) + ((im[4] + im[5]) + (im[6] + im[7])));
+    coeff = np_cdiv(sum, make_double2((double)N, 0.0));
+    cluster.sync();  // everyone has read s_node before it is reused
+  } else if (k >= 0) {
+    Cand b;
+    b.mag = -1.0;
+    b.flat = 0x7fffffffffffffffLL;
+    b.re = b.im = 0.0;
+    for (int i = tid; i < ncand; i += blockDim.x) cand_merge(b, cand[(size_t)sig * ncand + i]);
+    b = warp_argmax(b);
+    const int lane = tid & 31, wid = tid >> 5;
+    if (lane == 0) red[wid] = b;
+    __syncthreads();
+    if (wid == 0) {
+      Cand cc = lane < (int)(blockDim.x >> 5) ? red[lane] : b;
+      cc = warp_argmax(cc);
+      if (lane == 0) red[0] = cc;
+    }
+    __syncthreads();
+    b = red[0];
+    s = b.flat / N;
+    j = b.flat % N;
+    radius = radii[s];
+    const double2 zj = circle[j];
+    a = make_double2(radius * zj.x, radius * zj.y);  // grid.point, core.py:163-167
+    coeff = make_double2(b.re, b.im);
+  }
+
+  // ---- update this CTA's slice (or copy g0 at init) --------------------------
+  int amb = 0;
+  if (k < 0) {
+    const double2* __restrict__ x = g0 + (size_t)sig * N;
+    for (int i = tid; i < NC; i += blockDim.x) {
+      const double2 v = x[m0 + i];
+      r[m0 + i] = v;
+      slice[i] = v;
+      mag[i] = np_mag2(v);
+    }
+  } else {
+    const double kn = kernel_norm(a, &amb);
+    const double2 sc = make_double2(kn, 0.0);
+    for (int i = tid; i < NC; i += blockDim.x) {
+      const int m = m0 + i;
+      const double2 z = circle[m];
+      const double2 d = one_minus_conja_z(a, z);
+      const double2 e = np_cdiv(sc, d);
+      const double2 ce = np_cmul(coeff, e);  // N <= 8192: no numpy elision
+      const double2 g = r[m];
+      const double2 stp = make_double2(g.x - ce.x, g.y - ce.y);
+      const double2 num = np_cmul(stp, d);
+      const double2 out = np_cdiv(num, make_double2(z.x - a.x, z.y - a.y));
+      r[m] = out;
+      slice[i] = out;
+      mag[i] = np_mag2(out);
+    }
+  }
+  __syncthreads();
+  const double node = pairwise_sum_block(mag, NC, scratch, PlainIdx());
+  if (tid == 0) s_node[0] = node;
+  cluster.sync();  // slices and node sums visible cluster-wide
+  double e[kClusterCtas];
+#pragma unroll
+  for (int u = 0; u < kClusterCtas; ++u) e[u] = cluster.map_shared_rank(s_node, u)[0];
+  const double energy = (((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]))) / (double)N;
+
+  if (tid == 0) {
+    int stop;
+    if (k < 0) {
+      stop = (energy == 0.0) ? 1 : 0;  // core.py:366-368
+      if (c == 0) {
+        st.initial = energy;
+        st.nsteps = 0;
+        st.flags = 0;
+        st.stopped = stop;
+      }
+    } else {
+      stop = 0;
+      if (threshold > 0.0 && energy <= threshold * st.initial) stop = 1;  // core.py:386-387
+      if (energy == 0.0) stop = 1;                                         // core.py:388-389
+      if (k + 1 >= max_terms) stop = 1;
+      if (c == 0) {
+        Step rec;
+        rec.s = s;
+        rec.j = j;
+        rec.radius = radius;
+        rec.a_re = a.x;
+        rec.a_im = a.y;
+        rec.c_re = coeff.x;
+        rec.c_im = coeff.y;
+        rec.residual = energy;
+        rec.flags = amb ? kStepPowAmbiguous : 0;
+        rec.pad = 0;
+        steps[(size_t)sig * max_terms + k] = rec;
+        st.nsteps = k + 1;
+        st.flags |= rec.flags;
+        st.stopped = stop;
+      }
+    }
+    s_stop = stop;
+  }
+  __syncthreads();
+  if (s_stop) {
+    cluster.sync();  // keep this CTA's shared memory alive for remote readers
+    return;
+  }
+
+  // ---- forward transform, stages 0..K-4 on positions [c*NC, (c+1)*NC) --------
+  {
+    const int tp = tid;
+    const bool active = tp < CG::LOCAL_THREADS;
+    const int r3 = brev_bits(c, 3);
+    double2 v[GL::P];
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < GL::P; ++i) {
+        const int l = 8 * GL::l0(tp, i) + r3;  // natural index of this position
+        const double2* src = cluster.map_shared_rank(slice, l / NC);
+        v[i] = src[l % NC];
+      }
+    }
+    fft_passes<CG::KL, false, CG::RB>(v, tp, active, part, LocalTw{twl});
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < GL::P; ++i) part[GL::sw(out_pos<CG::KL, CG::RB>(tp, i))] = v[i];
+    }
+  }
+  cluster.sync();
+
+  // ---- stages K-3..K-1: radix-8 over the top 3 position bits ------------------
+  if (tid < CG::GROUPS) {
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = cluster.map_shared_rank(part, u)[GL::sw(q)];
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+#pragma unroll
+      for (int h = 0; h < (1 << e); ++h) {
+        const double2 w = w2[(1 << e) - 1 + h];
+#pragma unroll
+        for (int g = 0; g < (8 >> (e + 1)); ++g) {
+          const int i = h | (g << (e + 1));
+          bfly(v[i], v[i | (1 << e)], w);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) gh[q + NC * u] = v[u];
+  }
+  cluster.sync();  // remote readers of `part` are done before exit
+}
+
+}  // namespace afd
