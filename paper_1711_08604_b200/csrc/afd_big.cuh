@@ -1,0 +1,424 @@
+// afd_big.cuh — transform lengths N = 2^K > 8192 (BASELINE c2: 2^16,
+// c4: 2^20), where one row no longer fits in shared memory.
+//
+// The reference's radix-2 DIT (transform.py:73-93) is split by stage bits:
+//   pass A  stages 0..11: they pair positions inside aligned blocks of 4096
+//           bit-reversed positions, so one CTA runs them on-chip exactly as
+//           afd_fft.cuh does (the N-table stage twiddles S_b, b < 12, are the
+//           same per-stage tables; SmemTw<12> reads them from the N plan);
+//   pass C  stages b0..b0+3 (b0 = 12, 16): they pair positions that differ
+//           in bits b0..b0+3 only, so each thread owns one "column"
+//           q + 2^b0 u, u < 16, and runs 4 stages in registers; lanes own
+//           consecutive q, so every load/store is coalesced.
+// Intermediates live in a row-batch buffer sized to stay L2-resident.  The
+// input of pass A is in position (bit-reversed) order: the plan keeps the
+// r^l table as pw_rev[m][p] = r^rev(p) and the field spectrum as
+// ghat_rev[p] = Ghat[rev(p)] (transform.py:151,198 gather the same way).
+// Every butterfly is the reference's, so results stay bit-identical.
+//
+// Per-step bookkeeping for large N is split over grid kernels: the numpy
+// pairwise sum over N (core.py:195-198) is reproduced from per-CTA node sums
+// over aligned 2048-sample slices (nodes of numpy's halving tree) combined
+// left+right by a single CTA.
+#pragma once
+
+#include "afd_kernels.cuh"
+
+namespace afd {
+
+constexpr int kNodeLen = 2048;             // samples per energy node
+constexpr int kColThreads = 256;
+
+// Pass-A bits: K = KA + 4 c with 9 <= KA <= 12 (K = 14..22).
+__host__ __device__ constexpr int big_ka(int K) { return K - 4 * ((K - 9) / 4); }
+
+template <int KA>
+__host__ __device__ constexpr size_t big_a_smem() {
+  return sizeof(double2) * (SmemTw<KA, 4>::ENTRIES + Geo<KA, 4>::SMEM);
+}
+
+__device__ __forceinline__ int brev_rt(int x, int bits) { return (int)(__brev((unsigned)x) >> (32 - bits)); }
+
+// ---------------------------------------------------------------------------
+// Pass A.  mode 0: field prologue y[p] = pw_rev[row][p] * ghat_rev[p]
+//          mode 1: transform of one signal, input gathered x[rev(p)] (natural x)
+// blockIdx.x = 4096-block, blockIdx.y = row within the batch.
+// ---------------------------------------------------------------------------
+template <int KA, bool INV>
+__global__ void __launch_bounds__(Geo<KA, 4>::T, 2)
+big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0,
+           const double2* __restrict__ ghat_rev, const double2* __restrict__ x,
+           const double2* __restrict__ twst, long long row0, long long row1,
+           double2* __restrict__ Y, const int* __restrict__ stopped) {
+  using GA = Geo<KA, 4>;
+  using TwA = SmemTw<KA, 4>;
+  constexpr int BLK = 1 << KA;
+  extern __shared__ double2 smem[];
+  if (stopped && *stopped) return;
+  const long long N = 1LL << K;
+  const long long row = row0 + blockIdx.y;
+  if (row >= row1) return;
+  TwA::load(smem, twst);  // N-table stage twiddles S_b, b < KA
+  const TwA tw{smem};
+  double2* buf = smem + TwA::ENTRIES;
+  const long long base = (long long)blockIdx.x * BLK;
+  const int tid = threadIdx.x;
+  // stage the block's DIT inputs in position order (coalesced loads)
+  if (mode == 0) {
+    const double* __restrict__ pr = pw_rev + (size_t)(row - pw_row0) * N + base;
+    const double2* __restrict__ gr = ghat_rev + base;
+    for (int q = tid; q < BLK; q += GA::T) {
+      const double p = __ldg(pr + q);
+      const double2 c = __ldg(gr + q);
+      buf[GA::sw(q)] = make_double2(p * c.x, p * c.y);  // transform.py:198
+    }
+  } else {
+    for (int q = tid; q < BLK; q += GA::T) buf[GA::sw(q)] = x[brev_rt((int)(base + q), K)];
+  }
+  __syncthreads();
+  double2 v[GA::P];
+  const int t0 = brev_bits(tid, GA::TB);
+#pragma unroll
+  for (int i = 0; i < GA::P; ++i) v[i] = buf[GA::sw(GA::pos(0, t0, i))];
+  __syncthreads();
+  fft_passes<KA, INV, 4>(v, tid, true, buf, tw);
+  double2* __restrict__ y = Y + (size_t)blockIdx.y * N + base;
+#pragma unroll
+  for (int i = 0; i < GA::P; ++i) y[out_pos<KA, 4>(tid, i)] = v[i];
+}
+
+// ---------------------------------------------------------------------------
+// Column pass over stage bits [b0, b0+4).  Thread = column q (bits b0..b0+3
+// of q clear); blockIdx.y = row within the batch.
+//   out_mode 0: write back to Y in place
+//   out_mode 1: field epilogue: scale, |.|^2, running first maximum -> cand
+//   out_mode 2: field epilogue, materialise rows into fout[row - row0][j]
+//   out_mode 3: transform output in natural order fout[j] (optionally / N)
+//   out_mode 4: transform output bit-reversed: fout[rev(j)] (field spectrum)
+// ---------------------------------------------------------------------------
+template <bool INV>
+__global__ void __launch_bounds__(kColThreads)
+big_pass_col(int K, int b0, int out_mode, int scale_n, double2* __restrict__ Y,
+             const double2* __restrict__ twst, const double* __restrict__ scales,
+             long long row0, long long row1, Cand* __restrict__ cand,
+             double2* __restrict__ fout, const int* __restrict__ stopped) {
+  if (stopped && *stopped) return;
+  const long long N = 1LL << K;
+  const long long row = row0 + blockIdx.y;
+  const long long x = (long long)blockIdx.x * kColThreads + threadIdx.x;  // column index
+  Cand best;
+  best.mag = -1.0;
+  best.flat = 0x7fffffffffffffffLL;
+  best.re = best.im = 0.0;
+  if (row < row1 && x < (N >> 4)) {
+    const long long lowmask = (1LL << b0) - 1;
+    const long long q = (x & lowmask) | ((x >> b0) << (b0 + 4));
+    double2* __restrict__ y = Y + (size_t)blockIdx.y * N;
+    double2 v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = y[q + ((long long)u << b0)];
+    const double2* __restrict__ half = twst + (N / 2) - 1;  // S_{K-1}[k] = w[k]
+    const long long qlow = q & lowmask;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int b = b0 + e;
+#pragma unroll
+      for (int kk = 0; kk < (1 << e); ++kk) {
+        double2 w = __ldg(half + ((qlow + ((long long)kk << b0)) << (K - 1 - b)));
+        if (INV) w.y = -w.y;
+#pragma unroll
+        for (int h = 0; h < (16 >> (e + 1)); ++h) {
+          const int i = kk | (h << (e + 1));
+          bfly(v[i], v[i | (1 << e)], w);
+        }
+      }
+    }
+    if (out_mode == 0) {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) y[q + ((long long)u << b0)] = v[u];
+    } else if (out_mode == 1 || out_mode == 2) {
+      const double sc = __ldg(scales + row);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const long long j = q + ((long long)u << b0);
+        const double2 f = make_double2(v[u].x * sc, v[u].y * sc);  // transform.py:200
+        if (out_mode == 2) {
+          fout[(size_t)(row - row0) * N + j] = f;
+        } else {
+          const double mg = np_mag2(f);
+          if (mg > best.mag) {  // j increases with u: first maximum
+            best.mag = mg;
+            best.flat = row * N + j;
+            best.re = f.x;
+            best.im = f.y;
+          }
+        }
+      }
+    } else {
+      const double2 dn = make_double2((double)N, 0.0);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const long long j = q + ((long long)u << b0);
+        double2 o = v[u];
+        if (scale_n) o = np_cdiv(o, dn);  // `y /= n`, transform.py:133
+        if (out_mode == 3) fout[j] = o;
+        else fout[brev_rt((int)j, K)] = o;
+      }
+    }
+  }
+  if (out_mode != 1) return;
+  // merge this CTA's first maximum into its slot (slots persist over the
+  // row batches of one step; the (mag, flat) order makes merging order-free)
+  __shared__ Cand red[32];
+  best = warp_argmax(best);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red[wid] = best;
+  __syncthreads();
+  if (wid == 0) {
+    Cand c = lane < (kColThreads >> 5) ? red[lane] : best;
+    c = warp_argmax(c);
+    if (lane == 0) {
+      Cand& slot = cand[(size_t)blockIdx.y * gridDim.x + blockIdx.x];
+      Cand o = slot;
+      cand_merge(o, c);
+      slot = o;
+    }
+  }
+}
+
+__global__ void cand_init_kernel(Cand* c, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    c[i].mag = -1.0;
+    c[i].flat = 0x7fffffffffffffffLL;
+    c[i].re = c[i].im = 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Per-step bookkeeping for one signal, large N.
+// ---------------------------------------------------------------------------
+struct BigSel {
+  long long s, j;
+  double radius;
+  double2 a, coeff;
+  int valid;
+  int pad;
+};
+
+// numpy pairwise node sums over aligned kNodeLen slices:
+// kind 0: |x|^2 of a complex signal, kind 1: complex sum of the signal
+// (one CTA per slice, 256 threads).
+__global__ void __launch_bounds__(256)
+node_sums_kernel(int kind, const double2* __restrict__ x, double* __restrict__ nodes) {
+  __shared__ double buf[kNodeLen * 2];
+  __shared__ double scratch[2 * (kNodeLen / 8 + 16)];
+  const double2* xs = x + (size_t)blockIdx.x * kNodeLen;
+  if (kind == 0) {
+    for (int i = threadIdx.x; i < kNodeLen; i += blockDim.x) buf[i] = np_mag2(xs[i]);
+    __syncthreads();
+    const double s = pairwise_sum_block(buf, kNodeLen, scratch, PlainIdx());
+    if (threadIdx.x == 0) nodes[blockIdx.x] = s;
+  } else {
+    double2* b2 = reinterpret_cast<double2*>(buf);
+    for (int i = threadIdx.x; i < kNodeLen; i += blockDim.x) b2[i] = xs[i];
+    __syncthreads();
+    const double2 s = cpairwise_sum_block(b2, kNodeLen, scratch, PlainIdx());
+    if (threadIdx.x == 0) {
+      nodes[2 * blockIdx.x] = s.x;
+      nodes[2 * blockIdx.x + 1] = s.y;
+    }
+  }
+}
+
+// Left+right tree over `n` (power of two) node values held in shared memory.
+__device__ double tree_sum(double* v, int n) {
+  for (int w = n; w > 1; w >>= 1) {
+    for (int b = threadIdx.x; b < w / 2; b += blockDim.x) v[b] = v[2 * b] + v[2 * b + 1];
+    __syncthreads();
+  }
+  return v[0];
+}
+
+// Select: candidates -> pole + coefficient (or the dc_first mean atom).
+__global__ void __launch_bounds__(256)
+big_select_kernel(int k, int dc_first, int K, const Cand* __restrict__ cand, int ncand,
+                  const double* __restrict__ nodes, int nnodes,
+                  const double* __restrict__ radii, const double2* __restrict__ circle,
+                  const State* __restrict__ state, BigSel* __restrict__ sel) {
+  __shared__ double re[1024], im[1024];
+  if (state->stopped) return;
+  const long long N = 1LL << K;
+  BigSel out;
+  out.valid = 1;
+  out.pad = 0;
+  if (k == 0 && dc_first) {
+    for (int i = threadIdx.x; i < nnodes; i += blockDim.x) {
+      re[i] = nodes[2 * i];
+      im[i] = nodes[2 * i + 1];
+    }
+    __syncthreads();
+    const double sr = tree_sum(re, nnodes);
+    const double si = tree_sum(im, nnodes);
+    out.s = out.j = 0;
+    out.radius = 0.0;
+    out.a = make_double2(0.0, 0.0);
+    out.coeff = np_cdiv(make_double2(sr, si), make_double2((double)N, 0.0));  // core.py:375
+  } else {
+    Cand b;
+    b.mag = -1.0;
+    b.flat = 0x7fffffffffffffffLL;
+    b.re = b.im = 0.0;
+    for (int i = threadIdx.x; i < ncand; i += blockDim.x) cand_merge(b, cand[i]);
+    __shared__ Cand red[32];
+    b = warp_argmax(b);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) red[wid] = b;
+    __syncthreads();
+    if (wid == 0) {
+      Cand c = lane < (int)(blockDim.x >> 5) ? red[lane] : b;
+      c = warp_argmax(c);
+      if (lane == 0) red[0] = c;
+    }
+    __syncthreads();
+    b = red[0];
+    out.s = b.flat / N;
+    out.j = b.flat % N;
+    out.radius = radii[out.s];
+    const double2 zj = circle[out.j];
+    out.a = make_double2(out.radius * zj.x, out.radius * zj.y);  // core.py:163-167
+    out.coeff = make_double2(b.re, b.im);
+  }
+  if (threadIdx.x == 0) *sel = out;
+}
+
+// Update (core.py:303-314; numpy's temporary elision applies for N >= 16384)
+// or, at init (sel == null), copy g0.  Writes the remainder and the |.|^2
+// node sums of each kNodeLen slice.
+__global__ void __launch_bounds__(256)
+big_update_kernel(int K, const BigSel* __restrict__ sel, const double2* __restrict__ g0,
+                  double2* __restrict__ rem, const double2* __restrict__ circle,
+                  const State* __restrict__ state, double* __restrict__ nodes,
+                  int* __restrict__ amb_out) {
+  __shared__ double buf[kNodeLen];
+  __shared__ double scratch[2 * (kNodeLen / 8 + 16)];
+  if (sel && state->stopped) return;
+  const long long N = 1LL << K;
+  const bool elide = (size_t)N * 16 >= 256 * 1024;
+  const long long m0 = (long long)blockIdx.x * kNodeLen;
+  int amb = 0;
+  if (!sel) {
+    for (int i = threadIdx.x; i < kNodeLen; i += blockDim.x) {
+      const double2 v = g0[m0 + i];
+      rem[m0 + i] = v;
+      buf[i] = np_mag2(v);
+    }
+  } else {
+    const BigSel s = *sel;
+    const double kn = kernel_norm(s.a, &amb);
+    const double2 sc = make_double2(kn, 0.0);
+    for (int i = threadIdx.x; i < kNodeLen; i += blockDim.x) {
+      const long long m = m0 + i;
+      const double2 z = circle[m];
+      const double2 d = one_minus_conja_z(s.a, z);
+      const double2 e = np_cdiv(sc, d);
+      const double2 ce = elide ? np_cmul(e, s.coeff) : np_cmul(s.coeff, e);
+      const double2 g = rem[m];
+      const double2 stp = make_double2(g.x - ce.x, g.y - ce.y);
+      const double2 num = elide ? np_cmul(d, stp) : np_cmul(stp, d);
+      const double2 out = np_cdiv(num, make_double2(z.x - s.a.x, z.y - s.a.y));
+      rem[m] = out;
+      buf[i] = np_mag2(out);
+    }
+  }
+  __syncthreads();
+  const double ns = pairwise_sum_block(buf, kNodeLen, scratch, PlainIdx());
+  if (threadIdx.x == 0) {
+    nodes[blockIdx.x] = ns;
+    if (blockIdx.x == 0 && amb_out) *amb_out = amb;
+  }
+}
+
+// Energy + record + stop rules (k < 0: initial energy).
+__global__ void __launch_bounds__(256)
+big_finalize_kernel(int k, int K, int max_terms, double threshold, const double* __restrict__ nodes,
+                    int nnodes, const BigSel* __restrict__ sel, const int* __restrict__ amb,
+                    State* __restrict__ state, Step* __restrict__ steps) {
+  __shared__ double v[1024];
+  if (k >= 0 && state->stopped) return;
+  const double N = (double)(1LL << K);
+  for (int i = threadIdx.x; i < nnodes; i += blockDim.x) v[i] = nodes[i];
+  __syncthreads();
+  const double energy = tree_sum(v, nnodes) / N;
+  if (threadIdx.x != 0) return;
+  if (k < 0) {
+    state->initial = energy;
+    state->nsteps = 0;
+    state->flags = 0;
+    state->stopped = energy == 0.0 ? 1 : 0;  // core.py:366-368
+    return;
+  }
+  const BigSel s = *sel;
+  Step rec;
+  rec.s = s.s;
+  rec.j = s.j;
+  rec.radius = s.radius;
+  rec.a_re = s.a.x;
+  rec.a_im = s.a.y;
+  rec.c_re = s.coeff.x;
+  rec.c_im = s.coeff.y;
+  rec.residual = energy;
+  rec.flags = *amb ? kStepPowAmbiguous : 0;
+  rec.pad = 0;
+  steps[k] = rec;
+  state->nsteps = k + 1;
+  state->flags |= rec.flags;
+  int stop = 0;
+  if (threshold > 0.0 && energy <= threshold * state->initial) stop = 1;  // core.py:386-387
+  if (energy == 0.0) stop = 1;                                            // core.py:388-389
+  if (k + 1 >= max_terms) stop = 1;
+  state->stopped = stop;
+}
+
+// In-place bit reversal of rows of length 2^K (K >= 10), used to turn the
+// natural-order r^l table into pw_rev.  Index l = (hi, mid, lo) with 5, K-10
+// and 5 bits; rev(l) = (rev5(lo), rev(mid), rev5(hi)), so the 32x32 tile of
+// (hi, lo) at `mid` and the tile at rev(mid) swap through shared memory with
+// coalesced loads and stores.  blockIdx.x = mid, blockIdx.y = row.
+__global__ void __launch_bounds__(1024) bitrev_rows_kernel(double* __restrict__ pw, int K) {
+  __shared__ double A[32][33], B[32][33];
+  const int mb = K - 10;
+  const int mid = blockIdx.x;
+  const int mid2 = mb > 0 ? brev_rt(mid, mb) : 0;
+  if (mid2 < mid) return;
+  double* row = pw + ((size_t)blockIdx.y << K);
+  const int hi = threadIdx.y, lo = threadIdx.x;
+  const size_t la = ((size_t)hi << (K - 5)) | ((size_t)mid << 5) | lo;
+  const size_t lb = ((size_t)hi << (K - 5)) | ((size_t)mid2 << 5) | lo;
+  A[hi][lo] = row[la];
+  B[hi][lo] = row[lb];
+  __syncthreads();
+  const int rh = brev_rt(hi, 5), rl = brev_rt(lo, 5);
+  // element (h, m, l) moves to (rev5(l), rev(m), rev5(h))
+  row[lb] = A[rl][rh];
+  if (mid2 != mid) row[la] = B[rl][rh];
+}
+
+// dst[p] = src[rev(p)] (natural spectrum -> field input order)
+__global__ void bitrev_copy_kernel(int K, const double2* __restrict__ src, double2* __restrict__ dst) {
+  const long long N = 1LL << K;
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N;
+       p += (long long)gridDim.x * blockDim.x)
+    dst[p] = src[brev_rt((int)p, K)];
+}
+
+// natural-order spectrum mask of the analytic projection (core.py:229-230)
+__global__ void analytic_mask_kernel(int K, double2* __restrict__ s) {
+  const long long N = 1LL << K, half = N / 2;
+  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < N;
+       m += (long long)gridDim.x * blockDim.x) {
+    if (m >= 1 && m < half) s[m] = make_double2(s[m].x * 2.0, s[m].y * 2.0);
+    else if (m > half) s[m] = make_double2(0.0, 0.0);
+  }
+}
+
+}  // namespace afd

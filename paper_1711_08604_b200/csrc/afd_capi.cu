@@ -14,6 +14,7 @@
 #include "afd_kernels.cuh"
 #include "afd_aux.cuh"
 #include "afd_step_cluster.cuh"
+#include "afd_big.cuh"
 
 using namespace afd;
 
@@ -44,6 +45,8 @@ int fail(int code, const char* fmt, ...) {
 
 constexpr int kMinK = 3;
 constexpr int kMaxOnChipK = 13;
+constexpr int kMaxK = 22;
+constexpr size_t kBigBatchBytes = 48ull << 20;  // L2-resident row batch
 
 }  // namespace
 
@@ -79,6 +82,16 @@ struct afd_plan {
   cudaStream_t g_stream = nullptr;
   int64_t launches = 0;
   int64_t graph_launches_per_replay = 0;
+  // large N (K > 13): pw holds pw_rev, ghat holds ghat_rev
+  bool big = false;
+  int ka = 0;
+  int64_t big_rows = 0;        // rows per batch
+  double2* Y = nullptr;        // [big_rows][N]
+  Cand* big_cand = nullptr;    // [big_rows][N/16/256]
+  double* nodes = nullptr;     // [2 * N / kNodeLen]
+  BigSel* sel = nullptr;
+  int* amb = nullptr;
+  double2* tmp = nullptr;      // [N] projection spectrum
 };
 
 // ---------------------------------------------------------------------------
@@ -90,7 +103,7 @@ namespace {
 // ~64 registers) so two 512-thread CTAs share an SM; rows of N <= 2048
 // are grouped to fill 512 threads.
 #ifndef AFD_FIELD_RB
-#define AFD_FIELD_RB 3
+#define AFD_FIELD_RB 4
 #endif
 constexpr int kFieldRB = AFD_FIELD_RB;
 
@@ -212,19 +225,19 @@ int launch_fft(afd_plan* p, int mode, const double2* x, double2* y, int64_t batc
 }
 
 // Dispatch helper: calls F<K>::run(args...) for the plan's K.
-#define AFD_DISPATCH(KV, EXPR)                 \
+#define AFD_DISPATCH(KV, ...)                 \
   switch (KV) {                                \
-    case 3: { constexpr int KK = 3; EXPR; }    \
-    case 4: { constexpr int KK = 4; EXPR; }    \
-    case 5: { constexpr int KK = 5; EXPR; }    \
-    case 6: { constexpr int KK = 6; EXPR; }    \
-    case 7: { constexpr int KK = 7; EXPR; }    \
-    case 8: { constexpr int KK = 8; EXPR; }    \
-    case 9: { constexpr int KK = 9; EXPR; }    \
-    case 10: { constexpr int KK = 10; EXPR; }  \
-    case 11: { constexpr int KK = 11; EXPR; }  \
-    case 12: { constexpr int KK = 12; EXPR; }  \
-    case 13: { constexpr int KK = 13; EXPR; }  \
+    case 3: { constexpr int KK = 3; __VA_ARGS__; }    \
+    case 4: { constexpr int KK = 4; __VA_ARGS__; }    \
+    case 5: { constexpr int KK = 5; __VA_ARGS__; }    \
+    case 6: { constexpr int KK = 6; __VA_ARGS__; }    \
+    case 7: { constexpr int KK = 7; __VA_ARGS__; }    \
+    case 8: { constexpr int KK = 8; __VA_ARGS__; }    \
+    case 9: { constexpr int KK = 9; __VA_ARGS__; }    \
+    case 10: { constexpr int KK = 10; __VA_ARGS__; }  \
+    case 11: { constexpr int KK = 11; __VA_ARGS__; }  \
+    case 12: { constexpr int KK = 12; __VA_ARGS__; }  \
+    case 13: { constexpr int KK = 13; __VA_ARGS__; }  \
     default:                                   \
       return fail(AFD_E_UNSUPPORTED, "transform length 2^%d not supported yet", KV); \
   }
@@ -305,6 +318,141 @@ int enqueue_decompose(afd_plan* p, int64_t batch, int max_terms, double thr, int
   });
 }
 
+// ---------------------------------------------------------------------------
+// Large N (K > 13): row-batched two-level DIT (afd_big.cuh).
+// ---------------------------------------------------------------------------
+#define AFD_KA_DISPATCH(KAV, ...)             \
+  switch (KAV) {                               \
+    case 9: { constexpr int KA = 9; __VA_ARGS__; }    \
+    case 10: { constexpr int KA = 10; __VA_ARGS__; }  \
+    case 11: { constexpr int KA = 11; __VA_ARGS__; }  \
+    case 12: { constexpr int KA = 12; __VA_ARGS__; }  \
+    default:                                   \
+      return fail(AFD_E_UNSUPPORTED, "bad pass-A size %d", KAV); \
+  }
+
+int big_col_ctas(const afd_plan* p) { return (int)((p->n / 16 + kColThreads - 1) / kColThreads); }
+
+int big_setup(afd_plan* p) {
+  AFD_KA_DISPATCH(p->ka, {
+    CU(cudaFuncSetAttribute(big_pass_a<KA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)big_a_smem<KA>()));
+    CU(cudaFuncSetAttribute(big_pass_a<KA, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)big_a_smem<KA>()));
+    return 0;
+  });
+}
+
+// Pass A over rows [r0, r0+rows) (mode 0: field prologue) or one signal (mode 1).
+int big_launch_a(afd_plan* p, bool inv, int mode, const double2* ghat_rev, const double2* x,
+                 int64_t r0, int64_t rows, const int* stopped, cudaStream_t st) {
+  const unsigned nb = (unsigned)(p->n >> p->ka);
+  AFD_KA_DISPATCH(p->ka, {
+    dim3 grid(nb, (unsigned)rows);
+    if (inv)
+      big_pass_a<KA, true><<<grid, Geo<KA, 4>::T, big_a_smem<KA>(), st>>>(
+          p->K, mode, p->pw, p->m0, ghat_rev, x, p->twst, r0, r0 + rows, p->Y, stopped);
+    else
+      big_pass_a<KA, false><<<grid, Geo<KA, 4>::T, big_a_smem<KA>(), st>>>(
+          p->K, mode, p->pw, p->m0, ghat_rev, x, p->twst, r0, r0 + rows, p->Y, stopped);
+    p->launches++;
+    CU(cudaGetLastError());
+    return 0;
+  });
+}
+
+int big_launch_cols(afd_plan* p, bool inv, int last_mode, int scale_n, int64_t r0, int64_t rows,
+                    double2* fout, const int* stopped, cudaStream_t st) {
+  dim3 grid((unsigned)big_col_ctas(p), (unsigned)rows);
+  for (int b0 = p->ka; b0 < p->K; b0 += 4) {
+    const int mode = (b0 + 4 >= p->K) ? last_mode : 0;
+    if (inv)
+      big_pass_col<true><<<grid, kColThreads, 0, st>>>(p->K, b0, mode, scale_n, p->Y, p->twst,
+                                                       p->scales, r0, r0 + rows, p->big_cand,
+                                                       fout, stopped);
+    else
+      big_pass_col<false><<<grid, kColThreads, 0, st>>>(p->K, b0, mode, scale_n, p->Y, p->twst,
+                                                        p->scales, r0, r0 + rows, p->big_cand,
+                                                        fout, stopped);
+    p->launches++;
+    CU(cudaGetLastError());
+  }
+  return 0;
+}
+
+// Field rows [r0, r1) of one spectrum: argmax into big_cand (fout == null,
+// slots initialised here) or materialised rows into fout.
+int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, double2* fout,
+              const int* stopped, cudaStream_t st) {
+  int rc;
+  if (!fout) {
+    const int n = (int)(p->big_rows * big_col_ctas(p));
+    cand_init_kernel<<<(n + 255) / 256, 256, 0, st>>>(p->big_cand, n);
+    p->launches++;
+  }
+  for (int64_t b = r0; b < r1; b += p->big_rows) {
+    const int64_t rows = std::min<int64_t>(p->big_rows, r1 - b);
+    if ((rc = big_launch_a(p, true, 0, ghat_rev, nullptr, b, rows, stopped, st))) return rc;
+    if ((rc = big_launch_cols(p, true, fout ? 2 : 1, 0, b, rows,
+                              fout ? fout + (size_t)(b - r0) * p->n : nullptr, stopped, st)))
+      return rc;
+  }
+  return 0;
+}
+
+// One signal's transform: out_mode 3 (natural) or 4 (bit-reversed).
+int big_fft(afd_plan* p, const double2* x, double2* out, bool inv, int scale_n, int out_mode,
+            const int* stopped, cudaStream_t st) {
+  int rc;
+  if ((rc = big_launch_a(p, inv, 1, nullptr, x, 0, 1, stopped, st))) return rc;
+  return big_launch_cols(p, inv, out_mode, scale_n, 0, 1, out, stopped, st);
+}
+
+int big_nnodes(const afd_plan* p) { return (int)(p->n / kNodeLen); }
+
+// init (k < 0) or one step of signal `sig`; cands == null uses the local field.
+int big_step(afd_plan* p, int sig, int k, int max_terms, double thr, int dc_first,
+             const double2* g0, const Cand* cands, int ncand, Step* steps, cudaStream_t st) {
+  int rc;
+  const size_t N = (size_t)p->n;
+  double2* rem = p->rem + sig * N;
+  double2* ghat_rev = p->ghat + sig * N;
+  State* state = p->state + sig;
+  const int* stopped = &state->stopped;
+  const int nn = big_nnodes(p);
+  if (k < 0) {
+    big_update_kernel<<<nn, 256, 0, st>>>(p->K, nullptr, g0, rem, p->circle, state, p->nodes,
+                                          nullptr);
+    big_finalize_kernel<<<1, 256, 0, st>>>(-1, p->K, max_terms, thr, p->nodes, nn, nullptr,
+                                           nullptr, state, nullptr);
+    p->launches += 2;
+    CU(cudaGetLastError());
+    return big_fft(p, rem, ghat_rev, false, 0, 4, stopped, st);
+  }
+  if (k == 0 && dc_first) {
+    node_sums_kernel<<<nn, 256, 0, st>>>(1, rem, p->nodes);
+    big_select_kernel<<<1, 256, 0, st>>>(k, dc_first, p->K, nullptr, 0, p->nodes, nn, p->radii,
+                                         p->circle, state, p->sel);
+    p->launches += 2;
+  } else {
+    if (!cands) {
+      if ((rc = big_field(p, ghat_rev, p->m0, p->m1, nullptr, stopped, st))) return rc;
+      cands = p->big_cand;
+      ncand = (int)(p->big_rows * big_col_ctas(p));
+    }
+    big_select_kernel<<<1, 256, 0, st>>>(k, dc_first, p->K, cands, ncand, nullptr, 0, p->radii,
+                                         p->circle, state, p->sel);
+    p->launches++;
+  }
+  big_update_kernel<<<nn, 256, 0, st>>>(p->K, p->sel, nullptr, rem, p->circle, state, p->nodes,
+                                        p->amb);
+  big_finalize_kernel<<<1, 256, 0, st>>>(k, p->K, max_terms, thr, p->nodes, nn, p->sel, p->amb,
+                                         state, steps + (size_t)sig * max_terms);
+  p->launches += 2;
+  CU(cudaGetLastError());
+  return big_fft(p, rem, ghat_rev, false, 0, 4, stopped, st);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -326,8 +474,8 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
                 (long long)n);
   int K = 0;
   while ((1LL << K) < n) ++K;
-  if (K < kMinK || K > kMaxOnChipK)
-    return fail(AFD_E_UNSUPPORTED, "transform length 2^%d not supported yet", K);
+  if (K < kMinK || K > kMaxK)
+    return fail(AFD_E_UNSUPPORTED, "transform length 2^%d not supported (max 2^%d)", K, kMaxK);
   if (m < 1) return fail(AFD_E_INVALID, "grid needs at least one radius");
   if (m0 < 0 || m1 > m || m0 >= m1) return fail(AFD_E_INVALID, "bad radius shard [%lld, %lld)",
                                                 (long long)m0, (long long)m1);
@@ -375,6 +523,11 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
   ALLOC(p->gin, sizeof(double2) * N * max_batch);
   ALLOC(p->state, sizeof(State) * max_batch);
 #undef ALLOC
+#define ALLOC2(ptr, bytes)                                                         \
+  do {                                                                             \
+    if (cudaMalloc(&(ptr), (bytes)) != cudaSuccess)                                \
+      return cleanup(fail(AFD_E_NOMEM, "cudaMalloc(%zu) failed", (size_t)(bytes))); \
+  } while (0)
   if (cudaMemcpy(p->radii, radii_host, sizeof(double) * m, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(p->scales, scales_host, sizeof(double) * m, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(p->twst, st.data(), sizeof(double2) * (N - 1), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -388,8 +541,25 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
     p->launches++;
     if (cudaGetLastError() != cudaSuccess) return cleanup(fail(AFD_E_CUDA, "power table launch"));
   }
-  int rc;
-  AFD_DISPATCH(K, { rc = setup_kernels<KK>(p); break; });
+  int rc = 0;
+  if (K > kMaxOnChipK) {
+    // large N: bit-reversed power rows (transform.py:151) and batch buffers
+    p->big = true;
+    p->ka = big_ka(K);
+    bitrev_rows_kernel<<<dim3(1u << (K - 10), (unsigned)(m1 - m0)), dim3(32, 32)>>>(p->pw, K);
+    p->launches++;
+    if (cudaGetLastError() != cudaSuccess) return cleanup(fail(AFD_E_CUDA, "bitrev launch"));
+    p->big_rows = std::max<int64_t>(1, std::min<int64_t>(m1 - m0, (int64_t)(kBigBatchBytes / (N * 16))));
+    ALLOC2(p->Y, sizeof(double2) * N * p->big_rows);
+    ALLOC2(p->big_cand, sizeof(Cand) * p->big_rows * big_col_ctas(p));
+    ALLOC2(p->nodes, sizeof(double) * 2 * (N / kNodeLen));
+    ALLOC2(p->sel, sizeof(BigSel));
+    ALLOC2(p->amb, sizeof(int));
+    ALLOC2(p->tmp, sizeof(double2) * N);
+    rc = big_setup(p);
+  } else {
+    AFD_DISPATCH(K, { rc = setup_kernels<KK>(p); break; });
+  }
   if (rc) return cleanup(rc);
   if (cudaDeviceSynchronize() != cudaSuccess) return cleanup(fail(AFD_E_CUDA, "plan init: %s",
                                                                   cudaGetErrorString(cudaGetLastError())));
@@ -413,6 +583,12 @@ int afd_plan_destroy(afd_plan* p) {
   cudaFree(p->cand);
   cudaFree(p->steps);
   cudaFree(p->scratch);
+  cudaFree(p->Y);
+  cudaFree(p->big_cand);
+  cudaFree(p->nodes);
+  cudaFree(p->sel);
+  cudaFree(p->amb);
+  cudaFree(p->tmp);
   delete p;
   return AFD_OK;
 }
@@ -423,6 +599,25 @@ static int fft_entry(afd_plan* p, int mode, const double* x, double* out, int64_
   int rc;
   if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  if (p->big) {
+    const size_t N = (size_t)p->n;
+    for (int64_t b = 0; b < batch; ++b) {
+      const double2* xb = (const double2*)x + b * N;
+      double2* ob = (double2*)out + b * N;
+      if (mode == 0) {
+        if ((rc = big_fft(p, xb, ob, false, 0, 3, nullptr, st))) return rc;
+      } else if (mode == 1) {
+        if ((rc = big_fft(p, xb, ob, true, 1, 3, nullptr, st))) return rc;
+      } else {
+        // core.py:224-231: forward, fold the spectrum one-sided, 1/N inverse
+        if ((rc = big_fft(p, xb, p->tmp, false, 0, 3, nullptr, st))) return rc;
+        analytic_mask_kernel<<<256, 256, 0, st>>>(p->K, p->tmp);
+        p->launches++;
+        if ((rc = big_fft(p, p->tmp, ob, true, 1, 3, nullptr, st))) return rc;
+      }
+    }
+    return 0;
+  }
   AFD_DISPATCH(p->K, return launch_fft<KK>(p, mode, (const double2*)x, (double2*)out, batch, st));
 }
 
@@ -445,6 +640,13 @@ int afd_field(afd_plan* p, const double* ghat, double* field, int64_t r0, int64_
                 (long long)r0, (long long)r1, (long long)p->m0, (long long)p->m1);
   int rc;
   if ((rc = set_device(p))) return rc;
+  if (p->big) {
+    // the large-N field kernels read the spectrum bit-reversed
+    cudaStream_t st = (cudaStream_t)stream;
+    bitrev_copy_kernel<<<256, 256, 0, st>>>(p->K, (const double2*)ghat, p->tmp);
+    p->launches++;
+    return big_field(p, p->tmp, r0, r1, (double2*)field, nullptr, st);
+  }
   const int ncta = field_ctas(p, r1 - r0, groups_of(p->K), 1);
   AFD_DISPATCH(p->K, return launch_field<KK>(p, (const double2*)ghat, r0, r1, 1, nullptr, ncta,
                                              (double2*)field, nullptr, (cudaStream_t)stream));
@@ -456,6 +658,18 @@ int afd_field_argmax(afd_plan* p, const double* ghat, afd_candidate* out, int64_
   int rc;
   if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  if (p->big) {
+    const int nc = (int)(p->big_rows * big_col_ctas(p));
+    for (int64_t b = 0; b < batch; ++b) {
+      bitrev_copy_kernel<<<256, 256, 0, st>>>(p->K, (const double2*)ghat + b * p->n, p->tmp);
+      p->launches++;
+      if ((rc = big_field(p, p->tmp, p->m0, p->m1, nullptr, nullptr, st))) return rc;
+      cand_reduce_kernel<<<1, 256, 0, st>>>(p->big_cand, nc, (Cand*)out + b);
+      p->launches++;
+    }
+    CU(cudaGetLastError());
+    return 0;
+  }
   const int ncta = field_ctas(p, p->m1 - p->m0, groups_of(p->K), batch);
   if ((rc = ensure_cand(p, batch, ncta))) return rc;
   AFD_DISPATCH(p->K, {
@@ -537,6 +751,25 @@ int afd_decompose(afd_plan* p, const double* g0, int64_t batch, int max_terms, d
   const double thr = threshold > 0.0 ? threshold : 0.0;
   const size_t sig_bytes = sizeof(double2) * (size_t)p->n * batch;
   CU(cudaMemcpyAsync(p->gin, g0, sig_bytes, cudaMemcpyDeviceToDevice, st));
+  if (p->big) {
+    // large N: host-driven loop (each step is dominated by ~M*N/4096-CTA
+    // field launches; a graph would only add instantiation cost)
+    for (int64_t b = 0; b < batch; ++b) {
+      if ((rc = big_step(p, (int)b, -1, max_terms, thr, dc_first, p->gin + b * p->n, nullptr, 0,
+                         p->steps, st)))
+        return rc;
+      for (int k = 0; k < max_terms; ++k)
+        if ((rc = big_step(p, (int)b, k, max_terms, thr, dc_first, nullptr, nullptr, 0, p->steps,
+                           st)))
+          return rc;
+    }
+    gather_outputs_kernel<<<(unsigned)batch, 256, 0, st>>>(
+        (int)p->n, max_terms, p->steps, p->state, p->rem, (Step*)steps, n_steps, initial,
+        (double2*)remainder, nullptr);
+    p->launches++;
+    CU(cudaGetLastError());
+    return 0;
+  }
   const bool reuse = p->gexec && p->g_max_terms == max_terms && p->g_dc_first == dc_first &&
                      p->g_threshold == thr && p->g_batch == batch && p->g_stream == st;
   if (!reuse) {
@@ -584,6 +817,12 @@ int afd_sharded_begin(afd_plan* p, const double* g0, int64_t batch, void* stream
   cudaStream_t st = (cudaStream_t)stream;
   CU(cudaMemcpyAsync(p->gin, g0, sizeof(double2) * (size_t)p->n * batch,
                      cudaMemcpyDeviceToDevice, st));
+  if (p->big) {
+    for (int64_t b = 0; b < batch; ++b)
+      if ((rc = big_step(p, (int)b, -1, 1, 0.0, 0, p->gin + b * p->n, nullptr, 0, p->steps, st)))
+        return rc;
+    return 0;
+  }
   AFD_DISPATCH(p->K, return launch_step<KK>(p, -1, 1, 0.0, 0, p->gin, nullptr, 0, batch, p->steps,
                                             st));
 }
@@ -598,6 +837,17 @@ int afd_select_local(afd_plan* p, int k, int dc_first, afd_candidate* cand, int6
     // the pinned mean atom needs no field; emit a neutral candidate
     neutral_cand_kernel<<<1, 128, 0, st>>>((Cand*)cand, (int)batch);
     p->launches++;
+    CU(cudaGetLastError());
+    return 0;
+  }
+  if (p->big) {
+    const int nc = (int)(p->big_rows * big_col_ctas(p));
+    for (int64_t b = 0; b < batch; ++b) {
+      if ((rc = big_field(p, p->ghat + b * p->n, p->m0, p->m1, nullptr, &p->state[b].stopped, st)))
+        return rc;
+      cand_reduce_kernel<<<1, 256, 0, st>>>(p->big_cand, nc, (Cand*)cand + b);
+      p->launches++;
+    }
     CU(cudaGetLastError());
     return 0;
   }
@@ -623,6 +873,14 @@ int afd_apply_step(afd_plan* p, int k, int max_terms, double threshold, int dc_f
   int rc;
   if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
   const double thr = threshold > 0.0 ? threshold : 0.0;
+  if (p->big) {
+    for (int64_t b = 0; b < batch; ++b)
+      if ((rc = big_step(p, (int)b, k, max_terms, thr, dc_first, nullptr,
+                         (const Cand*)cands + b * ncand, ncand, (Step*)steps,
+                         (cudaStream_t)stream)))
+        return rc;
+    return 0;
+  }
   AFD_DISPATCH(p->K, return launch_step<KK>(p, k, max_terms, thr, dc_first, nullptr,
                                             (const Cand*)cands, ncand, batch, (Step*)steps,
                                             (cudaStream_t)stream));

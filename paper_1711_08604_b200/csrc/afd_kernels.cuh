@@ -51,7 +51,7 @@ enum : int { kStepPowAmbiguous = 1 };
 // CTAs of a signal (blockIdx.y).
 // ---------------------------------------------------------------------------
 template <int K, int RB, int G, bool MATERIALIZE>
-__global__ void __launch_bounds__(Geo<K, RB>::T * G, (Geo<K, RB>::T * G <= 512) ? 2 : 1)
+__global__ void __launch_bounds__(Geo<K, RB>::T * G, (RB <= 3 && Geo<K, RB>::T * G <= 512) ? 2 : 1)
 field_kernel(const double2* __restrict__ ghat,     // [batch][N]
              const double* __restrict__ pw,        // [rows of plan][N], r^l natural l
              const double* __restrict__ scales,    // [M] (global radius index)

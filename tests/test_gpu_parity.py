@@ -176,3 +176,75 @@ def test_launch_count_advances(afd):
     before = plan.launch_count()
     core.decompose(W.signal_for("c0"), core.ParameterGrid(radii, w.n), max_terms=w.steps)
     assert plan.launch_count() - before >= 1 + 2 * w.steps
+
+
+# ---------------------------------------------------------------------------
+# large N (two-level DIT, afd_big.cuh)
+# ---------------------------------------------------------------------------
+
+def _big_input(n, seed):
+    rng = np.random.Generator(np.random.Philox(seed))
+    return rng.standard_normal(n) + 1j * rng.standard_normal(n)
+
+
+@pytest.mark.parametrize("n", [16384, 65536, 1 << 20])
+def test_big_n_transforms_bitwise(afd, n):
+    core, _ = afd
+    from paper_1711_08604_b200 import transform
+    b = load_golden("big.npz")
+    x = _big_input(n, n)
+    sel = np.arange(0, n, 4099) if n > 16384 else np.arange(n)
+    a, c = complex(b["a_%d" % n]), complex(b["c_%d" % n])
+    fwd = transform.dft_forward(x)
+    assert np.array_equal(fwd[sel], b["fwd_%d" % n])
+    assert np.array_equal(transform.dft_inverse(x)[sel], b["inv_%d" % n])
+    assert np.array_equal(core.kernel_samples(a, n)[sel], b["ks_%d" % n])
+    assert np.array_equal(core.blaschke_samples(a, n)[sel], b["bs_%d" % n])
+    upd = core.remainder_update(x, a, c)
+    assert np.array_equal(upd[sel], b["upd_%d" % n])
+    assert core.discrete_energy(x) == b["energy_%d" % n]
+    assert core.discrete_energy(upd) == b["upd_energy_%d" % n]
+    if n <= 65536:
+        f = transform.weighted_inverse_grid(fwd, tuple(b["radii_%d" % n]))
+        assert np.array_equal(f[:, sel], b["field_%d" % n])
+
+
+def test_big_n_decompose_matches_reference(afd):
+    core, _ = afd
+    g = load_golden("decomp_big16384.npz")
+    grid = core.ParameterGrid(tuple(g["radii"]), g["g"].shape[0])
+    d = core.decompose(g["g"], grid, max_terms=int(g["max_terms"]))
+    _check_decomp(d, g)
+    assert np.array_equal(np.array(core.error_trace(d, g["g"])), g["trace"])
+
+
+def test_c2_projection_and_first_steps(afd):
+    """BASELINE c2 (N=65536, M=4096, real input): projection + 2 AFD steps."""
+    core, _ = afd
+    g = load_golden("c2_step.npz")
+    proj = core.analytic_projection(g["x"])
+    assert np.array_equal(proj, g["g"])
+    grid = core.ParameterGrid(tuple(g["radii"]), proj.shape[0])
+    d = core.decompose(proj, grid, max_terms=len(g["s"]))
+    for k, st in enumerate(d.steps):
+        assert grid.radii.index(st.point.radius) == g["s"][k]
+        assert st.point.angle_index == g["j"][k]
+        assert st.coefficient == g["coeff"][k]
+        assert st.residual_energy == g["residual"][k]
+    assert d.initial_energy == g["initial"]
+    assert np.array_equal(d.remainder, g["remainder"])
+
+
+def test_c4_length_decompose_matches_oracle(afd):
+    """N = 2^20 (c4's length) on a small radius grid vs the CPU oracle."""
+    core, _ = afd
+    from paper_1711_08604_b200 import workloads as W
+    n = 1 << 20
+    g = W.pole_sum(n, 128, 0.99, 4)
+    radii = (0.0, 0.5, 0.9, 0.99, 0.999)
+    d = core.decompose(g, core.ParameterGrid(radii, n), max_terms=3)
+    o = O.decompose(g, np.array(radii), max_terms=3)
+    assert [s.point.angle_index for s in d.steps] == list(o.steps["j"])
+    assert [s.coefficient for s in d.steps] == list(o.steps["c_re"] + 1j * o.steps["c_im"])
+    assert [s.residual_energy for s in d.steps] == list(o.steps["residual"])
+    assert np.array_equal(d.remainder, o.remainder)
