@@ -248,3 +248,43 @@ def test_c4_length_decompose_matches_oracle(afd):
     assert [s.coefficient for s in d.steps] == list(o.steps["c_re"] + 1j * o.steps["c_im"])
     assert [s.residual_energy for s in d.steps] == list(o.steps["residual"])
     assert np.array_equal(d.remainder, o.remainder)
+
+
+@pytest.mark.parametrize("case", ["c0", "f2_dc", "big16384"])
+def test_sharded_step_api_on_one_gpu(afd, case):
+    """Two radius shards driven through afd_select_local / afd_apply_step,
+    with the all-gather emulated by concatenation (no cross-rank waiting),
+    reproduce the reference decomposition exactly."""
+    core, engine = afd
+    import torch
+    from paper_1711_08604_b200 import _capi
+    from paper_1711_08604_b200.distributed import shard_bounds
+    g = load_golden("decomp_%s.npz" % case)
+    radii = tuple(g["radii"])
+    n = g["g"].shape[0]
+    max_terms = int(g["max_terms"])
+    thr = float(g["threshold"])
+    thr = None if np.isnan(thr) else thr
+    dc = bool(g["dc_first"])
+    world = 2
+    plans = [engine.Plan(radii, n, *shard_bounds(len(radii), r, world), max_batch=1)
+             for r in range(world)]
+    x = torch.from_numpy(g["g"][None, :]).cuda()
+    steps = [torch.zeros((1, max_terms, _capi.STEP_DTYPE.itemsize), dtype=torch.uint8,
+                         device="cuda") for _ in plans]
+    for p in plans:
+        p.sharded_begin(x)
+    for k in range(max_terms):
+        local = [p.select_local(k, dc, 1) for p in plans]
+        cands = torch.stack(local, 1).contiguous()
+        for p, s in zip(plans, steps):
+            p.apply_step(k, max_terms, thr, dc, cands, s)
+    for p, s in zip(plans, steps):
+        n_steps, initial, rem, _ = p.sharded_finish(1)
+        count = int(n_steps.cpu()[0])
+        rec = s.cpu().numpy().view(_capi.STEP_DTYPE)[0, :count, 0]
+        assert count == len(g["j"])
+        assert np.array_equal(rec["j"], g["j"]) and np.array_equal(rec["radius"], g["radius"])
+        assert np.array_equal(rec["c_re"] + 1j * rec["c_im"], g["coeff"])
+        assert np.array_equal(rec["residual"], g["residual"])
+        assert np.array_equal(rem.cpu().numpy()[0], g["remainder"])

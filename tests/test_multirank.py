@@ -1,0 +1,83 @@
+"""Radius-sharded decomposition across 2 ranks (gloo, CPU) == single-process result.
+
+Exercises distributed.decompose_sharded's host logic (shard bounds, the
+per-step all-gather of 32-byte candidates, the rank-major merge, the step
+loop) with an oracle-backed stand-in for the CUDA plan.
+"""
+
+import os
+import socket
+import warnings
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+import oracle as O
+from conftest import load_golden
+
+warnings.simplefilter("ignore", UserWarning)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, case, out_q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle_plan import OraclePlan
+        from paper_1711_08604_b200 import core, distributed
+        g = load_golden("decomp_%s.npz" % case)
+        thr = float(g["threshold"])
+        grid = core.ParameterGrid(tuple(g["radii"]), g["g"].shape[0])
+        ds = distributed.decompose_sharded(
+            g["g"], grid, max_terms=int(g["max_terms"]),
+            threshold=None if np.isnan(thr) else thr, dc_first=bool(g["dc_first"]),
+            plan_factory=OraclePlan)
+        d = ds[0]
+        out_q.put((rank, [s.point.angle_index for s in d.steps],
+                   [s.point.radius for s in d.steps], [s.coefficient for s in d.steps],
+                   [s.residual_energy for s in d.steps], d.remainder))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,world", [("c0", 2), ("f2_dc", 2), ("f1_thr", 3)])
+def test_radius_sharded_equals_reference(case, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = load_golden("decomp_%s.npz" % case)
+    for rank, j, radius, coeff, resid, rem in res:
+        assert j == list(g["j"]), rank
+        assert radius == list(g["radius"]), rank
+        assert coeff == list(g["coeff"]), rank
+        assert resid == list(g["residual"]), rank
+        assert np.array_equal(rem, g["remainder"]), rank
+
+
+def test_shard_bounds():
+    from paper_1711_08604_b200.distributed import shard_bounds
+    for m in (1, 7, 100, 16384):
+        for world in (1, 2, 3, 8):
+            if world > m:
+                continue
+            blocks = [shard_bounds(m, r, world) for r in range(world)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == m
+            assert all(a[1] == b[0] for a, b in zip(blocks, blocks[1:]))
+            assert max(h - l for l, h in blocks) - min(h - l for l, h in blocks) <= 1
