@@ -178,18 +178,31 @@ __device__ __forceinline__ void pass_load(double2 (&v)[Geo<K, RB>::P], int t, co
 // calls this (block-uniform __syncthreads), `active` masks threads that own
 // no row this round.  On return v holds pass NPASS-1's outputs at natural
 // positions pos(c_last, tp, i).
-template <int K, bool INV, int RB = 4, int PASS = 0, class Tw>
+// Barrier between passes: the whole block (default) or only the row-group
+// that shares `sm` (named barrier `id` over `count` threads), so several rows
+// of one CTA can run out of phase.
+struct BlockSync {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+struct GroupSync {
+  int id, count;
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+  }
+};
+
+template <int K, bool INV, int RB = 4, int PASS = 0, class Tw, class Sync = BlockSync>
 __device__ __forceinline__ void fft_passes(double2 (&v)[Geo<K, RB>::P], int tp, bool active,
-                                           double2* sm, const Tw& tw) {
+                                           double2* sm, const Tw& tw, Sync sync = Sync()) {
   using G = Geo<K, RB>;
   const int t = PASS == 0 ? brev_bits(tp, G::TB) : tp;
   if (active) fft_pass<K, RB, PASS, INV>(v, t, tw);
   if constexpr (PASS + 1 < G::NPASS) {
     if (active) pass_store<K, RB, PASS>(v, t, sm);
-    __syncthreads();
+    sync();
     if (active) pass_load<K, RB, PASS + 1>(v, tp, sm);
-    __syncthreads();
-    fft_passes<K, INV, RB, PASS + 1>(v, tp, active, sm, tw);
+    sync();
+    fft_passes<K, INV, RB, PASS + 1>(v, tp, active, sm, tw, sync);
   }
 }
 

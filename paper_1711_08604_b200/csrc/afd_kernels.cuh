@@ -84,7 +84,14 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
 
   const long long rows = row1 - row0;
   const long long per_round = (long long)gridDim.x * G;
-  const long long rounds = (rows + per_round - 1) / per_round;
+  // Row-groups of >= 32 threads synchronise on their own named barrier and
+  // loop over their own rows independently, so the G rows of a CTA drift out
+  // of phase (one group's loads overlap another's FP64 passes); smaller
+  // groups share warps and step together with the whole block.
+  constexpr bool kGroupSync = (T % 32 == 0) && G > 1;
+  const long long rounds =
+      kGroupSync ? (rows - ((long long)blockIdx.x * G + g) + per_round - 1) / per_round
+                 : (rows + per_round - 1) / per_round;
   for (long long rd = 0; rd < rounds; ++rd) {
     const long long s = row0 + rd * per_round + (long long)blockIdx.x * G + g;
     const bool active = s < row1;
@@ -100,7 +107,11 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
         v[i] = make_double2(p * c.x, p * c.y);
       }
     }
-    fft_passes<K, true, RB>(v, tp, active, sm, tw);
+    if constexpr (kGroupSync) {
+      fft_passes<K, true, RB>(v, tp, active, sm, tw, GroupSync{1 + g, T});
+    } else {
+      fft_passes<K, true, RB>(v, tp, active, sm, tw);
+    }
     if (active) {
       const double sc = __ldg(scales + s);
 #pragma unroll
@@ -123,6 +134,7 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     }
   }
   if (MATERIALIZE) return;
+  __syncthreads();  // all groups done before the block-wide reduction
   Cand best;
   best.mag = best_mag;
   const long long best_s = row0 + (long long)best_rd * per_round + (long long)blockIdx.x * G + g;
