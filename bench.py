@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--e2e-reps", type=int, default=0)
     return ap.parse_args()
 
 
@@ -263,15 +265,20 @@ def run_ours(args):
     evals = w.batch * w.m * w.n * w.steps
     value = world * evals * args.steps / (total_ms * 1e-3)
 
-    # parity of the benchmarked output against the oracle (first signal)
+    # parity of the benchmarked output against the oracle (first signal;
+    # for the big configs only the first `check` steps, replayed by the oracle)
     import oracle as O
     recs, counts = out.host_steps()
-    o = O.decompose(sig[0], np.array(radii), max_terms=w.steps)
-    parity = bool(counts[0] == len(o.steps) and
-                  np.array_equal(recs[0]["j"][:counts[0]], o.steps["j"]) and
-                  np.array_equal(recs[0]["radius"][:counts[0]], o.steps["radius"]) and
-                  np.array_equal(recs[0]["c_re"][:counts[0]], o.steps["c_re"]) and
-                  np.array_equal(recs[0]["residual"][:counts[0]], o.steps["residual"]))
+    check = w.steps if w.m * w.n * w.steps <= (1 << 31) else 2
+    parity = None
+    if not args.no_parity:
+        o = O.decompose(sig[0], np.array(radii), max_terms=check)
+        c = min(int(counts[0]), check)
+        parity = bool(c == len(o.steps) and
+                      np.array_equal(recs[0]["j"][:c], o.steps["j"]) and
+                      np.array_equal(recs[0]["radius"][:c], o.steps["radius"]) and
+                      np.array_equal(recs[0]["c_re"][:c], o.steps["c_re"]) and
+                      np.array_equal(recs[0]["residual"][:c], o.steps["residual"]))
 
     # roofline: the fused field+argmax kernel, CUDA events on this stream
     ghat = plan.dft_forward(g_dev)
@@ -296,8 +303,8 @@ def run_ours(args):
 
     # e2e through the public API, host buffers, pinned H2D + D2H in the region
     grid = core.ParameterGrid(radii, w.n)
-    e2e_reps = max(3, min(args.steps, 200))
-    for _ in range(3):
+    e2e_reps = args.e2e_reps or max(3, min(args.steps, 200))
+    for _ in range(min(3, e2e_reps)):
         plan.decompose_host(sig, w.steps)
     barrier()
     torch.cuda.synchronize()

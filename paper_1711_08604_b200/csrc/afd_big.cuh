@@ -44,47 +44,64 @@ __device__ __forceinline__ int brev_rt(int x, int bits) { return (int)(__brev((u
 //          mode 1: transform of one signal, input gathered x[rev(p)] (natural x)
 // blockIdx.x = 4096-block, blockIdx.y = row within the batch.
 // ---------------------------------------------------------------------------
+// Persistent over work items (row, block): 2 row-groups of T threads per
+// CTA, each with its own buffer and named barrier, so one group's loads
+// overlap the other's butterflies; twiddles are loaded once per CTA.
+constexpr int kBigGroups = 2;
+
+template <int KA>
+__host__ __device__ constexpr size_t big_a_smem_g() {
+  return sizeof(double2) * (SmemTw<KA, 4>::ENTRIES + kBigGroups * Geo<KA, 4>::SMEM);
+}
+
 template <int KA, bool INV>
-__global__ void __launch_bounds__(Geo<KA, 4>::T, 2)
+__global__ void __launch_bounds__(Geo<KA, 4>::T * kBigGroups, 1)
 big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0,
            const double2* __restrict__ ghat_rev, const double2* __restrict__ x,
            const double2* __restrict__ twst, long long row0, long long row1,
            double2* __restrict__ Y, const int* __restrict__ stopped) {
   using GA = Geo<KA, 4>;
   using TwA = SmemTw<KA, 4>;
-  constexpr int BLK = 1 << KA;
+  constexpr int BLK = 1 << KA, T = GA::T;
   extern __shared__ double2 smem[];
   if (stopped && *stopped) return;
   const long long N = 1LL << K;
-  const long long row = row0 + blockIdx.y;
-  if (row >= row1) return;
+  const long long nblk = N >> KA;
+  const long long items = (row1 - row0) * nblk;
   TwA::load(smem, twst);  // N-table stage twiddles S_b, b < KA
+  __syncthreads();
   const TwA tw{smem};
-  double2* buf = smem + TwA::ENTRIES;
-  const long long base = (long long)blockIdx.x * BLK;
-  const int tid = threadIdx.x;
-  // stage the block's DIT inputs in position order (coalesced loads)
-  if (mode == 0) {
-    const double* __restrict__ pr = pw_rev + (size_t)(row - pw_row0) * N + base;
-    const double2* __restrict__ gr = ghat_rev + base;
-    for (int q = tid; q < BLK; q += GA::T) {
-      const double p = __ldg(pr + q);
-      const double2 c = __ldg(gr + q);
-      buf[GA::sw(q)] = make_double2(p * c.x, p * c.y);  // transform.py:198
-    }
-  } else {
-    for (int q = tid; q < BLK; q += GA::T) buf[GA::sw(q)] = x[brev_rt((int)(base + q), K)];
-  }
-  __syncthreads();
-  double2 v[GA::P];
+  const int g = threadIdx.x / T, tid = threadIdx.x % T;
+  double2* buf = smem + TwA::ENTRIES + g * GA::SMEM;
+  const GroupSync sync{1 + g, T};
   const int t0 = brev_bits(tid, GA::TB);
+  for (long long it = (long long)blockIdx.x * kBigGroups + g; it < items;
+       it += (long long)gridDim.x * kBigGroups) {
+    const long long rl = it / nblk;               // row within the batch
+    const long long base = (it % nblk) * BLK;
+    // stage the block's DIT inputs in position order (coalesced loads)
+    if (mode == 0) {
+      const double* __restrict__ pr = pw_rev + (size_t)(row0 + rl - pw_row0) * N + base;
+      const double2* __restrict__ gr = ghat_rev + base;
+      for (int q = tid; q < BLK; q += T) {
+        const double p = __ldg(pr + q);
+        const double2 c = __ldg(gr + q);
+        buf[GA::sw(q)] = make_double2(p * c.x, p * c.y);  // transform.py:198
+      }
+    } else {
+      for (int q = tid; q < BLK; q += T) buf[GA::sw(q)] = x[brev_rt((int)(base + q), K)];
+    }
+    sync();
+    double2 v[GA::P];
 #pragma unroll
-  for (int i = 0; i < GA::P; ++i) v[i] = buf[GA::sw(GA::pos(0, t0, i))];
-  __syncthreads();
-  fft_passes<KA, INV, 4>(v, tid, true, buf, tw);
-  double2* __restrict__ y = Y + (size_t)blockIdx.y * N + base;
+    for (int i = 0; i < GA::P; ++i) v[i] = buf[GA::sw(GA::pos(0, t0, i))];
+    sync();
+    fft_passes<KA, INV, 4>(v, tid, true, buf, tw, sync);
+    double2* __restrict__ y = Y + (size_t)rl * N + base;
 #pragma unroll
-  for (int i = 0; i < GA::P; ++i) y[out_pos<KA, 4>(tid, i)] = v[i];
+    for (int i = 0; i < GA::P; ++i) y[out_pos<KA, 4>(tid, i)] = v[i];
+    sync();  // buffer reuse by the next item
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -97,7 +114,7 @@ big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0
 //   out_mode 4: transform output bit-reversed: fout[rev(j)] (field spectrum)
 // ---------------------------------------------------------------------------
 template <bool INV>
-__global__ void __launch_bounds__(kColThreads)
+__global__ void __launch_bounds__(kColThreads, 2)
 big_pass_col(int K, int b0, int out_mode, int scale_n, double2* __restrict__ Y,
              const double2* __restrict__ twst, const double* __restrict__ scales,
              long long row0, long long row1, Cand* __restrict__ cand,

@@ -74,6 +74,7 @@ struct afd_plan {
   size_t scratch_bytes = 0;
   // field launch geometry
   int field_occ = 1;
+  int field_block = 1;
   // graph cache
   cudaGraphExec_t gexec = nullptr;
   int g_max_terms = -1, g_dc_first = -1;
@@ -146,6 +147,7 @@ int setup_field_kernel(int* occ) {
 template <int K>
 int setup_kernels(afd_plan* p) {
   int rc;
+  p->field_block = field_block<K>();
   if ((rc = setup_field_kernel<K, false>(&p->field_occ))) return rc;
   if ((rc = setup_field_kernel<K, true>(nullptr))) return rc;
   CU(cudaFuncSetAttribute(step_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -161,9 +163,12 @@ int setup_kernels(afd_plan* p) {
 }
 
 // Number of CTAs per signal for `rows` rows: minimise waves x rows-per-CTA.
-int field_ctas(const afd_plan* p, int64_t rows, int G, int64_t batch) {
+int field_ctas(const afd_plan* p, int64_t rows, int G, int64_t batch, int block = 0) {
   const int64_t units = (rows + G - 1) / G;
-  const int64_t slots = (int64_t)p->sms * p->field_occ;
+  // a reduced block (fewer row-groups) fits proportionally more CTAs per SM
+  const int occ = block > 0 ? std::max(1, std::min(32, (int)(p->field_occ * (int64_t)p->field_block / block)))
+                            : p->field_occ;
+  const int64_t slots = (int64_t)p->sms * occ;
   int64_t best_x = 1;
   double best_t = 1e300;
   for (int64_t x = 1; x <= units && x <= 65535; ++x) {
@@ -180,16 +185,30 @@ int field_ctas(const afd_plan* p, int64_t rows, int G, int64_t batch) {
   return (int)best_x;
 }
 
+// Row-groups per CTA actually launched: fewer than G when the launch is too
+// small to fill the GPU with full CTAs (small M, e.g. BASELINE c0).
+template <int K>
+int groups_eff(const afd_plan* p, int64_t rows, int64_t batch) {
+  constexpr int G = groups_for<K>();
+  int g = G;
+  while (g > 1 && ((rows + g - 1) / g) * batch < 2 * p->sms) g >>= 1;
+  return g;
+}
+
 template <int K>
 int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64_t batch,
                  Cand* cand, int ncta, double2* field_out, const State* state, cudaStream_t st) {
   constexpr int G = groups_for<K>();
+  const int ge = groups_eff<K>(p, r1 - r0, batch);  // ncta from field_ctas_for
   dim3 grid(ncta, (unsigned)batch);
+  const int block = Geo<K, kFieldRB>::T * ge;
+  const size_t smem = sizeof(double2) *
+                      (Geo<K, kFieldRB>::SMEM * ge + SmemTw<K, kFieldRB>::ENTRIES);
   if (field_out) {
-    field_kernel<K, kFieldRB, G, true><<<grid, field_block<K>(), field_smem<K>(), st>>>(
+    field_kernel<K, kFieldRB, G, true><<<grid, block, smem, st>>>(
         ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, nullptr, field_out, nullptr);
   } else {
-    field_kernel<K, kFieldRB, G, false><<<grid, field_block<K>(), field_smem<K>(), st>>>(
+    field_kernel<K, kFieldRB, G, false><<<grid, block, smem, st>>>(
         ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, cand, nullptr, state);
   }
   p->launches++;
@@ -246,6 +265,17 @@ int groups_of(int K) {
   AFD_DISPATCH(K, return groups_for<KK>());
 }
 
+// CTAs per signal of a field launch over `rows` rows (what launch_field uses).
+int field_ctas_for(const afd_plan* p, int64_t rows, int64_t batch) {
+  AFD_DISPATCH(p->K, {
+    constexpr int G = groups_for<KK>();
+    const int ge = groups_eff<KK>(p, rows, batch);
+    return ge == G ? field_ctas(p, rows, G, batch)
+                   : field_ctas(p, rows, ge, batch, Geo<KK, kFieldRB>::T * ge);
+  });
+}
+
+
 int ensure_cand(afd_plan* p, int64_t batch, int ncta) {
   if (ncta > p->ncand_cap) {
     if (p->cand) cudaFree(p->cand);
@@ -297,7 +327,7 @@ int enqueue_decompose(afd_plan* p, int64_t batch, int max_terms, double thr, int
                       cudaStream_t st) {
   const int64_t rows = p->m1 - p->m0;
   const int G = groups_of(p->K);
-  const int ncta = field_ctas(p, rows, G, batch);
+  const int ncta = field_ctas_for(p, rows, batch);
   int rc;
   if ((rc = ensure_cand(p, batch, ncta))) return rc;
   AFD_DISPATCH(p->K, {
@@ -336,9 +366,9 @@ int big_col_ctas(const afd_plan* p) { return (int)((p->n / 16 + kColThreads - 1)
 int big_setup(afd_plan* p) {
   AFD_KA_DISPATCH(p->ka, {
     CU(cudaFuncSetAttribute(big_pass_a<KA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)big_a_smem<KA>()));
+                            (int)big_a_smem_g<KA>()));
     CU(cudaFuncSetAttribute(big_pass_a<KA, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)big_a_smem<KA>()));
+                            (int)big_a_smem_g<KA>()));
     return 0;
   });
 }
@@ -346,14 +376,16 @@ int big_setup(afd_plan* p) {
 // Pass A over rows [r0, r0+rows) (mode 0: field prologue) or one signal (mode 1).
 int big_launch_a(afd_plan* p, bool inv, int mode, const double2* ghat_rev, const double2* x,
                  int64_t r0, int64_t rows, const int* stopped, cudaStream_t st) {
-  const unsigned nb = (unsigned)(p->n >> p->ka);
+  const int64_t items = (p->n >> p->ka) * rows;
   AFD_KA_DISPATCH(p->ka, {
-    dim3 grid(nb, (unsigned)rows);
+    // persistent: one CTA per SM (2 row-groups each), work items strided
+    const unsigned grid = (unsigned)std::min<int64_t>(p->sms, (items + kBigGroups - 1) / kBigGroups);
+    const int block = Geo<KA, 4>::T * kBigGroups;
     if (inv)
-      big_pass_a<KA, true><<<grid, Geo<KA, 4>::T, big_a_smem<KA>(), st>>>(
+      big_pass_a<KA, true><<<grid, block, big_a_smem_g<KA>(), st>>>(
           p->K, mode, p->pw, p->m0, ghat_rev, x, p->twst, r0, r0 + rows, p->Y, stopped);
     else
-      big_pass_a<KA, false><<<grid, Geo<KA, 4>::T, big_a_smem<KA>(), st>>>(
+      big_pass_a<KA, false><<<grid, block, big_a_smem_g<KA>(), st>>>(
           p->K, mode, p->pw, p->m0, ghat_rev, x, p->twst, r0, r0 + rows, p->Y, stopped);
     p->launches++;
     CU(cudaGetLastError());
@@ -647,7 +679,7 @@ int afd_field(afd_plan* p, const double* ghat, double* field, int64_t r0, int64_
     p->launches++;
     return big_field(p, p->tmp, r0, r1, (double2*)field, nullptr, st);
   }
-  const int ncta = field_ctas(p, r1 - r0, groups_of(p->K), 1);
+  const int ncta = field_ctas_for(p, r1 - r0, 1);
   AFD_DISPATCH(p->K, return launch_field<KK>(p, (const double2*)ghat, r0, r1, 1, nullptr, ncta,
                                              (double2*)field, nullptr, (cudaStream_t)stream));
 }
@@ -670,7 +702,7 @@ int afd_field_argmax(afd_plan* p, const double* ghat, afd_candidate* out, int64_
     CU(cudaGetLastError());
     return 0;
   }
-  const int ncta = field_ctas(p, p->m1 - p->m0, groups_of(p->K), batch);
+  const int ncta = field_ctas_for(p, p->m1 - p->m0, batch);
   if ((rc = ensure_cand(p, batch, ncta))) return rc;
   AFD_DISPATCH(p->K, {
     if ((rc = launch_field<KK>(p, (const double2*)ghat, p->m0, p->m1, batch, p->cand, ncta,
@@ -776,7 +808,7 @@ int afd_decompose(afd_plan* p, const double* g0, int64_t batch, int max_terms, d
     if (p->gexec) cudaGraphExecDestroy(p->gexec);
     p->gexec = nullptr;
     // make sure buffers exist before capture (allocation is not capturable)
-    const int ncta = field_ctas(p, p->m1 - p->m0, groups_of(p->K), batch);
+    const int ncta = field_ctas_for(p, p->m1 - p->m0, batch);
     if ((rc = ensure_cand(p, batch, ncta))) return rc;
     cudaStream_t cap;
     CU(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
@@ -851,7 +883,7 @@ int afd_select_local(afd_plan* p, int k, int dc_first, afd_candidate* cand, int6
     CU(cudaGetLastError());
     return 0;
   }
-  const int ncta = field_ctas(p, p->m1 - p->m0, groups_of(p->K), batch);
+  const int ncta = field_ctas_for(p, p->m1 - p->m0, batch);
   if ((rc = ensure_cand(p, batch, ncta))) return rc;
   AFD_DISPATCH(p->K, {
     if ((rc = launch_field<KK>(p, p->ghat, p->m0, p->m1, batch, p->cand, ncta, nullptr, p->state,
@@ -924,7 +956,26 @@ int afd_time_field(afd_plan* p, const double* ghat, int64_t batch, int reps, dou
   int rc;
   if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  const int ncta = field_ctas(p, p->m1 - p->m0, groups_of(p->K), batch);
+  if (p->big) {
+    // one whole large-N field evaluation (all row batches) per timed rep
+    bitrev_copy_kernel<<<256, 256, 0, st>>>(p->K, (const double2*)ghat, p->tmp);
+    p->launches++;
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    CU(cudaEventRecord(e0, st));
+    for (int r = 0; r < reps; ++r)
+      if ((rc = big_field(p, p->tmp, p->m0, p->m1, nullptr, nullptr, st))) return rc;
+    CU(cudaEventRecord(e1, st));
+    CU(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *avg_ms = ms / reps;
+    return 0;
+  }
+  const int ncta = field_ctas_for(p, p->m1 - p->m0, batch);
   if ((rc = ensure_cand(p, batch, ncta))) return rc;
   std::vector<cudaEvent_t> ev(2 * (size_t)reps);
   for (auto& e : ev) CU(cudaEventCreate(&e));

@@ -68,6 +68,7 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   if (state != nullptr && state[sig].stopped) return;
   const int g = threadIdx.x / T;
   const int tp = threadIdx.x % T;
+  const int Gr = blockDim.x / T;  // row-groups actually launched (<= G)
   using TwT = SmemTw<K, RB>;
   TwT::load(smem, twst);
   const TwT tw{smem};
@@ -83,17 +84,17 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   __syncthreads();
 
   const long long rows = row1 - row0;
-  const long long per_round = (long long)gridDim.x * G;
+  const long long per_round = (long long)gridDim.x * Gr;
   // Row-groups of >= 32 threads synchronise on their own named barrier and
   // loop over their own rows independently, so the G rows of a CTA drift out
   // of phase (one group's loads overlap another's FP64 passes); smaller
   // groups share warps and step together with the whole block.
   constexpr bool kGroupSync = (T % 32 == 0) && G > 1;
   const long long rounds =
-      kGroupSync ? (rows - ((long long)blockIdx.x * G + g) + per_round - 1) / per_round
+      kGroupSync ? (rows - ((long long)blockIdx.x * Gr + g) + per_round - 1) / per_round
                  : (rows + per_round - 1) / per_round;
   for (long long rd = 0; rd < rounds; ++rd) {
-    const long long s = row0 + rd * per_round + (long long)blockIdx.x * G + g;
+    const long long s = row0 + rd * per_round + (long long)blockIdx.x * Gr + g;
     const bool active = s < row1;
     double2 v[P];
     if (active) {
@@ -137,7 +138,8 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   __syncthreads();  // all groups done before the block-wide reduction
   Cand best;
   best.mag = best_mag;
-  const long long best_s = row0 + (long long)best_rd * per_round + (long long)blockIdx.x * G + g;
+  const long long best_s =
+      row0 + (long long)best_rd * per_round + (long long)blockIdx.x * Gr + g;
   best.flat =
       best_rd >= 0 ? best_s * (long long)N + out_pos<K, RB>(tp, best_i) : 0x7fffffffffffffffLL;
   best.re = best_re;
