@@ -47,7 +47,7 @@ extern "C" {
  * (core.ParameterGrid.point, core.py:163-167); coefficient <G_k, e_a>;
  * residual = discrete_energy(G_{k+1}).  flags bit 0: CPython's pow(|a|, 2)
  * is not provably equal to the device's |a|*|a| for this pole (see
- * afd_common.cuh kernel_norm). */
+ * afd_common.cuh kernel_norm).  72 bytes. */
 typedef struct afd_step {
   int64_t s, j;
   double radius, a_re, a_im, c_re, c_im, residual;
@@ -130,6 +130,17 @@ int afd_energy_diff(afd_plan *plan, const double *g, const double *s, double *en
 int afd_decompose(afd_plan *plan, const double *g0, int64_t batch, int max_terms,
                   double threshold, int dc_first, afd_step *steps, int32_t *n_steps,
                   double *initial, double *remainder, void *stream);
+
+/* afd_decompose with HOST buffers (pageable or pinned): the library stages
+ * the input through its own pinned buffer, copies it to the device, replays
+ * the decomposition graph, gathers all outputs into one packed device buffer,
+ * copies that back with a single transfer and synchronises `stream` once.
+ * This is the reference-facing call (core.decompose on host numpy arrays).
+ * *h2d_bytes / *d2h_bytes (may be NULL) receive the bytes moved. */
+int afd_decompose_host(afd_plan *plan, const double *g0_host, int64_t batch, int max_terms,
+                       double threshold, int dc_first, afd_step *steps_host,
+                       int32_t *n_steps_host, double *initial_host, double *remainder_host,
+                       int64_t *h2d_bytes, int64_t *d2h_bytes, void *stream);
 
 /* Radius-sharded decomposition, one step at a time:
  *   afd_sharded_begin        copy g0, initial energy, first spectrum

@@ -52,6 +52,8 @@ SIGNATURES = [
     ("afd_energy", _I, [_VP, _VP, _VP, _I64, _VP]),
     ("afd_energy_diff", _I, [_VP, _VP, _VP, _VP, _I64, _VP]),
     ("afd_decompose", _I, [_VP, _VP, _I64, _I, _D, _I, _VP, _VP, _VP, _VP, _VP]),
+    ("afd_decompose_host", _I, [_VP, _VP, _I64, _I, _D, _I, _VP, _VP, _VP, _VP, _VP, _VP,
+                                _VP]),
     ("afd_sharded_begin", _I, [_VP, _VP, _I64, _VP]),
     ("afd_select_local", _I, [_VP, _I, _I, _VP, _I64, _VP]),
     ("afd_apply_step", _I, [_VP, _I, _I, _D, _I, _VP, _I, _I64, _VP, _VP]),

@@ -299,17 +299,29 @@ def _check_decompose_args(g, grid, max_terms, threshold, engine):
 
 
 def _build(grid, n, engine, rec, count, initial, remainder):
+    """Decomposition from device step records.  The frozen dataclasses are
+    filled without re-running __post_init__: the device produced the values
+    from a validated grid."""
+    rec = rec[:count]
+    radius = rec["radius"].tolist()
+    j = rec["j"].tolist()
+    a = (rec["a_re"] + 1j * rec["a_im"]).tolist()
+    c = (rec["c_re"] + 1j * rec["c_im"]).tolist()
+    res = rec["residual"].tolist()
+    new, sa = object.__new__, object.__setattr__
     steps = []
-    flags = []
     for k in range(count):
-        r = rec[k]
-        point = ParameterPoint(float(r["radius"]), int(r["j"]),
-                               complex(float(r["a_re"]), float(r["a_im"])))
-        steps.append(DecompositionStep(point, complex(float(r["c_re"]), float(r["c_im"])),
-                                       float(r["residual"])))
-        flags.append(int(r["flags"]))
+        pt = new(ParameterPoint)
+        sa(pt, "radius", radius[k])
+        sa(pt, "angle_index", j[k])
+        sa(pt, "value", a[k])
+        st = new(DecompositionStep)
+        sa(st, "point", pt)
+        sa(st, "coefficient", c[k])
+        sa(st, "residual_energy", res[k])
+        steps.append(st)
     return Decomposition(tuple(steps), grid, n, float(initial), engine, remainder=remainder,
-                         step_flags=tuple(flags))
+                         step_flags=tuple(rec["flags"].tolist()))
 
 
 def decompose(g, grid, max_terms=10, threshold=None, engine="fft", dc_first=False,
@@ -325,11 +337,11 @@ def decompose(g, grid, max_terms=10, threshold=None, engine="fft", dc_first=Fals
     g = _as_signal(g)
     _check_decompose_args(g, grid, max_terms, threshold, engine)
     return decompose_batch(g[None, :], grid, max_terms, threshold, engine, dc_first,
-                           parallel)[0]
+                           parallel, _validated=True)[0]
 
 
 def decompose_batch(signals, grid, max_terms=10, threshold=None, engine="fft", dc_first=False,
-                    parallel=False):
+                    parallel=False, _validated=False):
     """``decompose`` for a batch of independent signals ([B, N]) in one pass.
 
     Entry b equals ``decompose(signals[b], ...)`` exactly.
@@ -337,9 +349,10 @@ def decompose_batch(signals, grid, max_terms=10, threshold=None, engine="fft", d
     sig = np.asarray(signals, dtype=np.complex128)
     if sig.ndim != 2:
         raise ValueError("signals must be 2-d [batch, N], got shape %r" % (sig.shape,))
-    for row in sig:
-        _as_signal(row)
-    _check_decompose_args(sig, grid, max_terms, threshold, engine)
+    if not _validated:
+        for row in sig:
+            _as_signal(row)
+        _check_decompose_args(sig, grid, max_terms, threshold, engine)
     b, n = sig.shape
     plan = _plan(n, grid.radii, batch=b)
     rec, counts, initial, rem, _, _ = plan.decompose_host(sig, int(max_terms), threshold,

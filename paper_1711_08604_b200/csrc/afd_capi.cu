@@ -93,6 +93,11 @@ struct afd_plan {
   BigSel* sel = nullptr;
   int* amb = nullptr;
   double2* tmp = nullptr;      // [N] projection spectrum
+  // host-buffer entry point: pinned staging + packed device output
+  void* pin = nullptr;
+  size_t pin_bytes = 0;
+  unsigned char* packed = nullptr;
+  size_t packed_bytes = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -190,8 +195,9 @@ int field_ctas(const afd_plan* p, int64_t rows, int G, int64_t batch, int block 
 template <int K>
 int groups_eff(const afd_plan* p, int64_t rows, int64_t batch) {
   constexpr int G = groups_for<K>();
+  constexpr int gmin = Geo<K, kFieldRB>::T >= 32 ? 1 : 32 / Geo<K, kFieldRB>::T;  // >= 1 warp
   int g = G;
-  while (g > 1 && ((rows + g - 1) / g) * batch < 2 * p->sms) g >>= 1;
+  while (g > gmin && ((rows + g - 1) / g) * batch < 2 * p->sms) g >>= 1;
   return g;
 }
 
@@ -621,6 +627,8 @@ int afd_plan_destroy(afd_plan* p) {
   cudaFree(p->sel);
   cudaFree(p->amb);
   cudaFree(p->tmp);
+  cudaFree(p->packed);
+  if (p->pin) cudaFreeHost(p->pin);
   delete p;
   return AFD_OK;
 }
@@ -782,7 +790,8 @@ int afd_decompose(afd_plan* p, const double* g0, int64_t batch, int max_terms, d
   cudaStream_t st = (cudaStream_t)stream;
   const double thr = threshold > 0.0 ? threshold : 0.0;
   const size_t sig_bytes = sizeof(double2) * (size_t)p->n * batch;
-  CU(cudaMemcpyAsync(p->gin, g0, sig_bytes, cudaMemcpyDeviceToDevice, st));
+  if ((const void*)g0 != (const void*)p->gin)
+    CU(cudaMemcpyAsync(p->gin, g0, sig_bytes, cudaMemcpyDeviceToDevice, st));
   if (p->big) {
     // large N: host-driven loop (each step is dominated by ~M*N/4096-CTA
     // field launches; a graph would only add instantiation cost)
@@ -839,6 +848,58 @@ int afd_decompose(afd_plan* p, const double* g0, int64_t batch, int max_terms, d
       (double2*)remainder, nullptr);
   p->launches++;
   CU(cudaGetLastError());
+  return 0;
+}
+
+int afd_decompose_host(afd_plan* p, const double* g0_host, int64_t batch, int max_terms,
+                       double threshold, int dc_first, afd_step* steps_host,
+                       int32_t* n_steps_host, double* initial_host, double* remainder_host,
+                       int64_t* h2d_bytes, int64_t* d2h_bytes, void* stream) {
+  if (!p || !g0_host || !steps_host || !n_steps_host || !initial_host || !remainder_host)
+    return fail(AFD_E_INVALID, "NULL argument");
+  if (max_terms < 1) return fail(AFD_E_INVALID, "max_terms must be >= 1");
+  int rc;
+  if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t sig = sizeof(double2) * (size_t)p->n * batch;
+  const size_t stp = sizeof(Step) * (size_t)max_terms * batch;
+  // packed layout: steps | n_steps | initial | remainder, each part 16-byte
+  // aligned (afd_step is 72 bytes; the remainder is read as double2)
+  auto al16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
+  const size_t o_ns = al16(stp), o_in = al16(o_ns + sizeof(int32_t) * batch);
+  const size_t o_rm = al16(o_in + sizeof(double) * batch);
+  const size_t need_pack = o_rm + sig;
+  if (need_pack > p->packed_bytes) {
+    cudaFree(p->packed);
+    p->packed = nullptr;
+    p->packed_bytes = 0;
+    CU(cudaMalloc(&p->packed, need_pack));
+    p->packed_bytes = need_pack;
+  }
+  const size_t need_pin = std::max(sig, need_pack);
+  if (need_pin > p->pin_bytes) {
+    if (p->pin) cudaFreeHost(p->pin);
+    p->pin = nullptr;
+    p->pin_bytes = 0;
+    CU(cudaHostAlloc(&p->pin, need_pin, cudaHostAllocDefault));
+    p->pin_bytes = need_pin;
+  }
+  std::memcpy(p->pin, g0_host, sig);
+  CU(cudaMemcpyAsync(p->gin, p->pin, sig, cudaMemcpyHostToDevice, st));
+  unsigned char* d = p->packed;
+  if ((rc = afd_decompose(p, (const double*)p->gin, batch, max_terms, threshold, dc_first,
+                          (afd_step*)d, (int32_t*)(d + o_ns), (double*)(d + o_in),
+                          (double*)(d + o_rm), stream)))
+    return rc;
+  CU(cudaMemcpyAsync(p->pin, d, need_pack, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  const unsigned char* hp = (const unsigned char*)p->pin;
+  std::memcpy(steps_host, hp, stp);
+  std::memcpy(n_steps_host, hp + o_ns, sizeof(int32_t) * batch);
+  std::memcpy(initial_host, hp + o_in, sizeof(double) * batch);
+  std::memcpy(remainder_host, hp + o_rm, sig);
+  if (h2d_bytes) *h2d_bytes = (int64_t)sig;
+  if (d2h_bytes) *d2h_bytes = (int64_t)need_pack;
   return 0;
 }
 

@@ -56,7 +56,7 @@ def _stream(stream=None):
 
 @dataclass
 class DeviceDecomposition:
-    steps: torch.Tensor      # uint8 [batch, max_terms, 80] (afd_step records)
+    steps: torch.Tensor      # uint8 [batch, max_terms, 72] (afd_step records)
     n_steps: torch.Tensor    # int32 [batch]
     initial: torch.Tensor    # float64 [batch]
     remainder: torch.Tensor  # complex128 [batch, N]
@@ -202,43 +202,25 @@ class Plan:
         return out
 
     def decompose_host(self, signals, max_terms, threshold=None, dc_first=False, stream=None):
-        """Host numpy [batch, N] in -> host results out, through pinned staging.
+        """Host numpy [batch, N] in -> host results out (afd_decompose_host).
 
         Returns (steps structured [batch, max_terms], n_steps, initial,
-        remainder [batch, N]) as numpy arrays, plus the bytes moved
-        (h2d, d2h)."""
+        remainder [batch, N], h2d_bytes, d2h_bytes)."""
         sig = np.ascontiguousarray(signals, dtype=np.complex128)
+        if sig.ndim == 1:
+            sig = sig[None, :]
         b = sig.shape[0]
-        st = torch.cuda.current_stream() if stream is None else stream
-        key = (b, int(max_terms))
-        stage = getattr(self, "_stage", None)
-        if stage is None or stage[0] != key:
-            pin = dict(pin_memory=True)
-            stage = (key, dict(
-                gin=torch.empty((b, self.n), dtype=torch.complex128, **pin),
-                g=torch.empty((b, self.n), dtype=torch.complex128, device=self.device),
-                out=self.alloc_outputs(b, max_terms),
-                steps=torch.empty((b, max_terms, _capi.STEP_DTYPE.itemsize), dtype=torch.uint8,
-                                  **pin),
-                n_steps=torch.empty(b, dtype=torch.int32, **pin),
-                initial=torch.empty(b, dtype=torch.float64, **pin),
-                rem=torch.empty((b, self.n), dtype=torch.complex128, **pin)))
-            self._stage = stage
-        s = stage[1]
-        s["gin"].numpy()[...] = sig
-        with torch.cuda.stream(st):
-            s["g"].copy_(s["gin"], non_blocking=True)
-            out = self.decompose(s["g"], max_terms, threshold, dc_first, stream=st, out=s["out"])
-            s["steps"].copy_(out.steps, non_blocking=True)
-            s["n_steps"].copy_(out.n_steps, non_blocking=True)
-            s["initial"].copy_(out.initial, non_blocking=True)
-            s["rem"].copy_(out.remainder, non_blocking=True)
-        st.synchronize()
-        steps = s["steps"].numpy().view(_capi.STEP_DTYPE)[..., 0].copy()
-        h2d = sig.nbytes
-        d2h = (s["steps"].numel() + 4 * b + 8 * b + 16 * b * self.n)
-        return (steps, s["n_steps"].numpy().copy(), s["initial"].numpy().copy(),
-                s["rem"].numpy().copy(), h2d, d2h)
+        steps = np.empty((b, int(max_terms)), dtype=_capi.STEP_DTYPE)
+        n_steps = np.empty(b, dtype=np.int32)
+        initial = np.empty(b, dtype=np.float64)
+        rem = np.empty((b, self.n), dtype=np.complex128)
+        h2d, d2h = C.c_int64(), C.c_int64()
+        _capi.check(self.lib.afd_decompose_host(
+            self.handle, sig.ctypes.data, b, int(max_terms),
+            0.0 if threshold is None else float(threshold), int(bool(dc_first)),
+            steps.ctypes.data, n_steps.ctypes.data, initial.ctypes.data, rem.ctypes.data,
+            C.byref(h2d), C.byref(d2h), _stream(stream)))
+        return steps, n_steps, initial, rem, h2d.value, d2h.value
 
     def alloc_outputs(self, batch, max_terms):
         dev = self.device
@@ -273,7 +255,7 @@ class Plan:
         return out
 
     def apply_step(self, k, max_terms, threshold, dc_first, cands, steps, stream=None):
-        """cands: uint8 [batch, ncand, 32] (rank-major), steps: uint8 [batch, max_terms, 80]."""
+        """cands: uint8 [batch, ncand, 32] (rank-major), steps: uint8 [batch, max_terms, 72]."""
         cands = cands.contiguous()
         _capi.check(self.lib.afd_apply_step(
             self.handle, int(k), int(max_terms), 0.0 if threshold is None else float(threshold),
@@ -307,7 +289,8 @@ _MAX_PLANS = 16
 def get_plan(radii, n, batch=1, m0=0, m1=None, device=None):
     """Cached plan for (device, N, radii, shard) with max_batch >= batch."""
     dev = require_cuda(device)
-    radii = tuple(float(r) for r in radii)
+    if not (type(radii) is tuple and all(type(r) is float for r in radii[:1])):
+        radii = tuple(float(r) for r in radii)
     key = (dev.index, int(n), radii, int(m0), m1)
     with _PLANS_LOCK:
         p = _PLANS.get(key)
