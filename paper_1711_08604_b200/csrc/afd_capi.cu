@@ -61,6 +61,7 @@ struct afd_plan {
   double2* twst = nullptr;    // stage tables [N-1]
   double2* circle = nullptr;  // [N]
   double* pw = nullptr;       // [m1-m0][N] cumprod r^l
+  double2* tw_img = nullptr;  // field kernel's shared-memory twiddle image
   // per-signal working buffers
   double2* ghat = nullptr;    // [max_batch][N]
   double2* rem = nullptr;     // [max_batch][N]
@@ -150,8 +151,17 @@ int setup_field_kernel(int* occ) {
 }
 
 template <int K>
+__global__ void build_tw_image_kernel(double2* img, const double2* st) {
+  SmemTw<K, kFieldRB>::build_image(img, st);
+}
+
+template <int K>
 int setup_kernels(afd_plan* p) {
   int rc;
+  CU(cudaMalloc(&p->tw_img, sizeof(double2) * SmemTw<K, kFieldRB>::ENTRIES));
+  build_tw_image_kernel<K><<<32, 256>>>(p->tw_img, p->twst);
+  p->launches++;
+  CU(cudaGetLastError());
   p->field_block = field_block<K>();
   if ((rc = setup_field_kernel<K, false>(&p->field_occ))) return rc;
   if ((rc = setup_field_kernel<K, true>(nullptr))) return rc;
@@ -212,10 +222,10 @@ int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64
                       (Geo<K, kFieldRB>::SMEM * ge + SmemTw<K, kFieldRB>::ENTRIES);
   if (field_out) {
     field_kernel<K, kFieldRB, G, true><<<grid, block, smem, st>>>(
-        ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, nullptr, field_out, nullptr);
+        ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, nullptr, field_out, nullptr, p->tw_img);
   } else {
     field_kernel<K, kFieldRB, G, false><<<grid, block, smem, st>>>(
-        ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, cand, nullptr, state);
+        ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, cand, nullptr, state, p->tw_img);
   }
   p->launches++;
   CU(cudaGetLastError());
@@ -614,6 +624,7 @@ int afd_plan_destroy(afd_plan* p) {
   cudaFree(p->twst);
   cudaFree(p->circle);
   cudaFree(p->pw);
+  cudaFree(p->tw_img);
   cudaFree(p->ghat);
   cudaFree(p->rem);
   cudaFree(p->gin);

@@ -67,6 +67,36 @@ struct Geo {
   }
 };
 
+// TMA bulk copy global -> shared completing on an mbarrier (one thread
+// issues; every thread waits with mbar_wait).  16-byte aligned, size % 16 == 0.
+__device__ __forceinline__ void mbar_init(unsigned long long* mbar, unsigned count) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(mbar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, unsigned bytes,
+                                          unsigned long long* mbar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const unsigned m = (unsigned)__cvta_generic_to_shared(mbar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(m), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(d), "l"(gsrc), "r"(bytes), "r"(m)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mbar, unsigned parity) {
+  const unsigned m = (unsigned)__cvta_generic_to_shared(mbar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(m), "r"(parity)
+        : "memory");
+  }
+}
+
 // Twiddle sources.  tw(b, k) returns numpy's w[k << (K-1-b)] for stage b.
 //
 // GlobalTw: per-stage tables S_b (offset 2^b - 1) in global memory, read
@@ -100,6 +130,23 @@ struct SmemTw {
   __device__ __forceinline__ double2 operator()(int b, int k) const {
     if (b >= LO && b < HI) return sm[HALF_SLOTS + (1 << b) - (1 << LO) + k];
     return sm[swz(k << (K - 1 - b))];
+  }
+  // Build the shared-memory image (ENTRIES double2, this layout) in global
+  // memory once per plan, so kernels can fetch it with one bulk copy.
+  __device__ static void build_image(double2* img, const double2* __restrict__ st) {
+    const double2* half = st + (1 << (K - 1)) - 1;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ENTRIES;
+         i += gridDim.x * blockDim.x) {
+      double2 v = make_double2(0.0, 0.0);
+      if (i >= HALF_SLOTS) {
+        v = st[(1 << LO) - 1 + (i - HALF_SLOTS)];
+      } else {
+        // slot i holds half[k] with swz(k) == i (pad slots stay zero)
+        const int k = i - i / 9;  // inverse of k + k/8 on non-pad slots
+        if (swz(k) == i) v = half[k];
+      }
+      img[i] = v;
+    }
   }
   // Fill from the global stage tables (all threads of the block).
   __device__ static void load(double2* dst, const double2* __restrict__ st) {

@@ -60,7 +60,8 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
              long long pw_row0,                    // global row of pw[0]
              Cand* __restrict__ cand_out,          // [batch][gridDim.x]
              double2* __restrict__ field_out,      // [row1-row0][N] (MATERIALIZE)
-             const State* __restrict__ state) {    // per-signal stop flags or null
+             const State* __restrict__ state,      // per-signal stop flags or null
+             const double2* __restrict__ tw_img) { // SmemTw<K,RB> image (one bulk copy)
   using Gm = Geo<K, RB>;
   constexpr int N = Gm::N, T = Gm::T, P = Gm::P;
   extern __shared__ double2 smem[];
@@ -70,7 +71,27 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   const int tp = threadIdx.x % T;
   const int Gr = blockDim.x / T;  // row-groups actually launched (<= G)
   using TwT = SmemTw<K, RB>;
-  TwT::load(smem, twst);
+  // Twiddle image: one TMA bulk copy (issued by thread 0, completes on an
+  // mbarrier) overlapping the first row's prologue loads.
+  __shared__ unsigned long long tw_bar;
+  if (threadIdx.x == 0) mbar_init(&tw_bar, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    constexpr unsigned bytes = sizeof(double2) * TwT::ENTRIES;
+    const unsigned m = (unsigned)__cvta_generic_to_shared(&tw_bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(m), "r"(bytes)
+                 : "memory");
+    constexpr unsigned chunk = 16384;
+    for (unsigned off = 0; off < bytes; off += chunk) {
+      const unsigned nb = bytes - off < chunk ? bytes - off : chunk;
+      const unsigned d = (unsigned)__cvta_generic_to_shared((char*)smem + off);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          ::"r"(d), "l"((const char*)tw_img + off), "r"(nb), "r"(m)
+          : "memory");
+    }
+  }
+  bool tw_ready = false;
   const TwT tw{smem};
   double2* sm = smem + TwT::ENTRIES + g * Gm::SMEM;
   const double2* __restrict__ gh = ghat + (size_t)sig * N;
@@ -81,7 +102,6 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   // formed once at the end.
   double best_mag = -1.0, best_re = 0.0, best_im = 0.0;
   int best_rd = -1, best_i = 0;
-  __syncthreads();
 
   const long long rows = row1 - row0;
   const long long per_round = (long long)gridDim.x * Gr;
@@ -107,6 +127,10 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
         const double2 c = __ldg(gh + l);
         v[i] = make_double2(p * c.x, p * c.y);
       }
+    }
+    if (!tw_ready) {  // twiddle image landed (pass 0 reads it)
+      mbar_wait(&tw_bar, 0);
+      tw_ready = true;
     }
     if constexpr (kGroupSync) {
       fft_passes<K, true, RB>(v, tp, active, sm, tw, GroupSync{1 + g, T});
