@@ -101,6 +101,25 @@ struct afd_plan {
   size_t packed_bytes = 0;
 };
 
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while its predecessor in the stream drains (it calls pdl_wait() before
+// touching the predecessor's outputs).  Captured graphs keep the edges.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // ---------------------------------------------------------------------------
 // Templated launchers, dispatched on K.
 // ---------------------------------------------------------------------------
@@ -224,8 +243,10 @@ int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64
     field_kernel<K, kFieldRB, G, true><<<grid, block, smem, st>>>(
         ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, nullptr, field_out, nullptr, p->tw_img);
   } else {
-    field_kernel<K, kFieldRB, G, false><<<grid, block, smem, st>>>(
-        ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, cand, nullptr, state, p->tw_img);
+    CU(launch_pdl(field_kernel<K, kFieldRB, G, false>, grid, dim3(block), smem, st, ghat,
+                  (const double*)p->pw, (const double*)p->scales, (const double2*)p->twst,
+                  (long long)r0, (long long)r1, (long long)p->m0, cand, (double2*)nullptr, state,
+                  (const double2*)p->tw_img));
   }
   p->launches++;
   CU(cudaGetLastError());
@@ -236,14 +257,15 @@ template <int K>
 int launch_step(afd_plan* p, int k, int max_terms, double thr, int dc_first, const double2* g0,
                 const Cand* cand, int ncand, int64_t batch, Step* steps, cudaStream_t st) {
   if constexpr (use_cluster_step<K>()) {
-    step_cluster_kernel<K><<<(unsigned)(batch * kClusterCtas), ClusterGeo<K>::THREADS,
-                             ClusterSmem<K>::bytes, st>>>(
-        k, max_terms, thr, dc_first, g0, p->rem, p->ghat, cand, ncand, p->radii, p->circle,
-        p->twst, p->state, steps);
+    CU(launch_pdl(step_cluster_kernel<K>, dim3((unsigned)(batch * kClusterCtas)),
+                  dim3(ClusterGeo<K>::THREADS), ClusterSmem<K>::bytes, st, k, max_terms, thr,
+                  dc_first, g0, p->rem, p->ghat, cand, ncand, (const double*)p->radii,
+                  (const double2*)p->circle, (const double2*)p->twst, p->state, steps));
   } else {
-    step_kernel<K><<<(unsigned)batch, row_block<K>(), RowSmem<K>::bytes, st>>>(
-        k, max_terms, thr, dc_first, g0, p->rem, p->ghat, cand, ncand, p->radii, p->circle,
-        p->twst, p->state, steps);
+    CU(launch_pdl(step_kernel<K>, dim3((unsigned)batch), dim3(row_block<K>()),
+                  RowSmem<K>::bytes, st, k, max_terms, thr, dc_first, g0, p->rem, p->ghat, cand,
+                  ncand, (const double*)p->radii, (const double2*)p->circle,
+                  (const double2*)p->twst, p->state, steps));
   }
   p->launches++;
   CU(cudaGetLastError());

@@ -96,6 +96,15 @@ __device__ __forceinline__ double2 one_minus_conja_z(double2 a, double2 z) {
   return make_double2(1.0 - p.x, 0.0 - p.y);
 }
 
+// Programmatic dependent launch (PDL): kernels launched with programmatic
+// stream serialization may start while their predecessor drains; everything
+// before pdl_wait() must not read the predecessor's outputs.  Both are
+// no-ops for ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Candidate of the grid argmax: first maximum in row-major (s, j) order.
 struct __align__(16) Cand {
   double mag;

@@ -66,7 +66,6 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   constexpr int N = Gm::N, T = Gm::T, P = Gm::P;
   extern __shared__ double2 smem[];
   const int sig = blockIdx.y;
-  if (state != nullptr && state[sig].stopped) return;
   const int g = threadIdx.x / T;
   const int tp = threadIdx.x % T;
   const int Gr = blockDim.x / T;  // row-groups actually launched (<= G)
@@ -93,6 +92,14 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   }
   bool tw_ready = false;
   const TwT tw{smem};
+  // everything above is step-independent; the spectrum and the stop flags
+  // come from the previous kernel (PDL)
+  pdl_wait();
+  if (state != nullptr && state[sig].stopped) {
+    mbar_wait(&tw_bar, 0);  // no bulk copy may target an exited CTA
+    return;
+  }
+  pdl_trigger();
   double2* sm = smem + TwT::ENTRIES + g * Gm::SMEM;
   const double2* __restrict__ gh = ghat + (size_t)sig * N;
 
@@ -288,7 +295,9 @@ step_kernel(int k, int max_terms, double threshold, int dc_first,
   double2* __restrict__ r = rem + (size_t)sig * N;
   double2* __restrict__ gh = ghat + (size_t)sig * N;
 
-  if (L::smem_tw && (k < 0 || !st.stopped)) SmemTw<K>::load(twsm, twst);  // after next barrier
+  if (L::smem_tw) SmemTw<K>::load(twsm, twst);  // visible after the next barrier
+  pdl_wait();  // candidates, state and the remainder come from earlier kernels
+  pdl_trigger();
   if (k < 0) {
     const double2* __restrict__ x = g0 + (size_t)sig * N;
     for (int m = threadIdx.x; m < N; m += blockDim.x) {

@@ -91,8 +91,6 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   const int tid = threadIdx.x;
   const int m0 = c * NC;
 
-  if (k >= 0 && st.stopped) return;  // cluster-uniform
-
   // local stage tables S_0..S_{K-4} (== twst[0 .. 2^(K-3)-1))
   for (int i = tid; i < NC - 1; i += blockDim.x) twl[i] = __ldg(twst + i);
   // phase-2 twiddles of this thread, prefetched: stage b = K-3+e uses
@@ -106,6 +104,11 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
 #pragma unroll
       for (int h = 0; h < (1 << e); ++h) w2[(1 << e) - 1 + h] = __ldg(half + ((q + NC * h) << (2 - e)));
   }
+  // the tables above are step-independent; candidates, state and the
+  // remainder come from the previous kernels (PDL)
+  pdl_wait();
+  if (k >= 0 && st.stopped) return;  // cluster-uniform
+  pdl_trigger();
 
   // ---- select ---------------------------------------------------------------
   long long s = 0, j = 0;
