@@ -1125,3 +1125,11 @@ int afd_fp64_peak(int device, double* tflops, void* stream) {
 }
 
 }  // extern "C"
+
+#ifdef AFD_STEP_TIMING
+// Debug builds only: globaltimer stamps of step_cluster_kernel phases.
+extern "C" int afd_debug_step_stamps(unsigned long long* host_out) {
+  CU(cudaMemcpyFromSymbol(host_out, afd::g_step_stamps, sizeof(afd::g_step_stamps)));
+  return 0;
+}
+#endif

@@ -92,14 +92,6 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   }
   bool tw_ready = false;
   const TwT tw{smem};
-  // everything above is step-independent; the spectrum and the stop flags
-  // come from the previous kernel (PDL)
-  pdl_wait();
-  if (state != nullptr && state[sig].stopped) {
-    mbar_wait(&tw_bar, 0);  // no bulk copy may target an exited CTA
-    return;
-  }
-  pdl_trigger();
   double2* sm = smem + TwT::ENTRIES + g * Gm::SMEM;
   const double2* __restrict__ gh = ghat + (size_t)sig * N;
 
@@ -120,11 +112,36 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   const long long rounds =
       kGroupSync ? (rows - ((long long)blockIdx.x * Gr + g) + per_round - 1) / per_round
                  : (rows + per_round - 1) / per_round;
+  // First row: its r^l values are step-independent and are loaded before the
+  // PDL wait; the spectrum and the stop flags come from the previous kernel.
+  double2 v[P];
+  {
+    const long long s0 = row0 + (long long)blockIdx.x * Gr + g;
+    const bool act0 = rounds > 0 && s0 < row1;
+    double pv[P];
+    if (act0) {
+      const double* __restrict__ pr = pw + (size_t)(s0 - pw_row0) * N;
+#pragma unroll
+      for (int i = 0; i < P; ++i) pv[i] = __ldg(pr + Gm::l0(tp, i));
+    }
+    pdl_wait();
+    if (state != nullptr && state[sig].stopped) {
+      mbar_wait(&tw_bar, 0);  // no bulk copy may target an exited CTA
+      return;
+    }
+    pdl_trigger();
+    if (act0) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const double2 c = __ldg(gh + Gm::l0(tp, i));
+        v[i] = make_double2(pv[i] * c.x, pv[i] * c.y);  // transform.py:198
+      }
+    }
+  }
   for (long long rd = 0; rd < rounds; ++rd) {
     const long long s = row0 + rd * per_round + (long long)blockIdx.x * Gr + g;
     const bool active = s < row1;
-    double2 v[P];
-    if (active) {
+    if (rd > 0 && active) {
       // prologue: y = powers * c[rev] (transform.py:198), per component
       const double* __restrict__ pr = pw + (size_t)(s - pw_row0) * N;
 #pragma unroll

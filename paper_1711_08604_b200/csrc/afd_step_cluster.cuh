@@ -30,6 +30,22 @@ namespace cg = cooperative_groups;
 
 constexpr int kClusterCtas = 8;
 
+#ifdef AFD_STEP_TIMING
+__device__ unsigned long long g_step_stamps[64][16];
+#define STAMP(i)                                                                       \
+  do {                                                                                 \
+    if (threadIdx.x == 0 && blockIdx.x == 0 && k >= 0 && k < 64) {                     \
+      unsigned long long t_;                                                           \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                           \
+      g_step_stamps[k][i] = t_;                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define STAMP(i) \
+  do {           \
+  } while (0)
+#endif
+
 template <int K>
 struct ClusterGeo {
   static constexpr int N = 1 << K;
@@ -90,6 +106,7 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   double2* __restrict__ gh = ghat + (size_t)sig * N;
   const int tid = threadIdx.x;
   const int m0 = c * NC;
+  STAMP(0);
 
   // local stage tables S_0..S_{K-4} (== twst[0 .. 2^(K-3)-1))
   for (int i = tid; i < NC - 1; i += blockDim.x) twl[i] = __ldg(twst + i);
@@ -106,7 +123,23 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   }
   // the tables above are step-independent; candidates, state and the
   // remainder come from the previous kernels (PDL)
+  // This CTA's slice of the circle (static) and of the remainder: G_k was
+  // written by the previous step kernel, which completed before our PDL
+  // predecessor (the field kernel) passed its own pdl_wait and triggered
+  // us, so it is final here.
+  constexpr int PER = (NC + CG::THREADS - 1) / CG::THREADS;
+  double2 zs[PER], gs[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int i = tid + u * CG::THREADS;
+    if (i < NC) {
+      zs[u] = circle[m0 + i];
+      gs[u] = k >= 0 ? r[m0 + i] : g0[(size_t)sig * N + m0 + i];
+    }
+  }
+  STAMP(1);
   pdl_wait();
+  STAMP(2);
   if (k >= 0 && st.stopped) return;  // cluster-uniform
   pdl_trigger();
 
@@ -161,38 +194,47 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
     coeff = make_double2(b.re, b.im);
   }
 
+  STAMP(3);
   // ---- update this CTA's slice (or copy g0 at init) --------------------------
   int amb = 0;
   if (k < 0) {
-    const double2* __restrict__ x = g0 + (size_t)sig * N;
-    for (int i = tid; i < NC; i += blockDim.x) {
-      const double2 v = x[m0 + i];
-      r[m0 + i] = v;
-      slice[i] = v;
-      mag[i] = np_mag2(v);
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int i = tid + u * CG::THREADS;
+      if (i < NC) {
+        r[m0 + i] = gs[u];
+        slice[i] = gs[u];
+        mag[i] = np_mag2(gs[u]);
+      }
     }
   } else {
     const double kn = kernel_norm(a, &amb);
     const double2 sc = make_double2(kn, 0.0);
-    for (int i = tid; i < NC; i += blockDim.x) {
-      const int m = m0 + i;
-      const double2 z = circle[m];
-      const double2 d = one_minus_conja_z(a, z);
-      const double2 e = np_cdiv(sc, d);
-      const double2 ce = np_cmul(coeff, e);  // N <= 8192: no numpy elision
-      const double2 g = r[m];
-      const double2 stp = make_double2(g.x - ce.x, g.y - ce.y);
-      const double2 num = np_cmul(stp, d);
-      const double2 out = np_cdiv(num, make_double2(z.x - a.x, z.y - a.y));
-      r[m] = out;
-      slice[i] = out;
-      mag[i] = np_mag2(out);
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int i = tid + u * CG::THREADS;
+      if (i < NC) {
+        const double2 z = zs[u];
+        const double2 d = one_minus_conja_z(a, z);
+        const double2 e = np_cdiv(sc, d);
+        const double2 ce = np_cmul(coeff, e);  // N <= 8192: no numpy elision
+        const double2 g = gs[u];
+        const double2 stp = make_double2(g.x - ce.x, g.y - ce.y);
+        const double2 num = np_cmul(stp, d);
+        const double2 out = np_cdiv(num, make_double2(z.x - a.x, z.y - a.y));
+        r[m0 + i] = out;
+        slice[i] = out;
+        mag[i] = np_mag2(out);
+      }
     }
   }
   __syncthreads();
+  STAMP(4);
   const double node = pairwise_sum_block(mag, NC, scratch, PlainIdx());
   if (tid == 0) s_node[0] = node;
+  STAMP(5);
   cluster.sync();  // slices and node sums visible cluster-wide
+  STAMP(6);
   double e[kClusterCtas];
 #pragma unroll
   for (int u = 0; u < kClusterCtas; ++u) e[u] = cluster.map_shared_rank(s_node, u)[0];
@@ -239,6 +281,7 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
     return;
   }
 
+  STAMP(7);
   // ---- forward transform, stages 0..K-4 on positions [c*NC, (c+1)*NC) --------
   {
     const int tp = tid;
@@ -253,13 +296,16 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
         v[i] = src[l % NC];
       }
     }
+    STAMP(8);
     fft_passes<CG::KL, false, CG::RB>(v, tp, active, part, LocalTw{twl});
+    STAMP(9);
     if (active) {
 #pragma unroll
       for (int i = 0; i < GL::P; ++i) part[GL::sw(out_pos<CG::KL, CG::RB>(tp, i))] = v[i];
     }
   }
   cluster.sync();
+  STAMP(10);
 
   // ---- stages K-3..K-1: radix-8 over the top 3 position bits ------------------
   if (tid < CG::GROUPS) {
@@ -281,7 +327,9 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
 #pragma unroll
     for (int u = 0; u < 8; ++u) gh[q + NC * u] = v[u];
   }
+  STAMP(11);
   cluster.sync();  // remote readers of `part` are done before exit
+  STAMP(12);
 }
 
 }  // namespace afd

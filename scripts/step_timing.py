@@ -1,0 +1,33 @@
+"""Phase timings of the cluster step kernel from the AFD_STEP_TIMING debug build."""
+import ctypes as C
+import os
+import sys
+import warnings
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+warnings.simplefilter("ignore")
+os.environ["AFD_LIB_PATH"] = "paper_1711_08604_b200/lib/libafd_b200_timing.so"
+from paper_1711_08604_b200 import engine, workloads as W, _capi  # noqa: E402
+
+w = W.CONFIGS["c1"]
+plan = engine.get_plan(W.radii_for(w.m), w.n)
+g = torch.from_numpy(W.signal_for("c1")[None, :]).cuda()
+for _ in range(3):
+    plan.decompose(g, w.steps)
+torch.cuda.synchronize()
+out = np.zeros((64, 16), np.uint64)
+lib = _capi.load()
+lib.afd_debug_step_stamps.argtypes = [C.c_void_p]
+assert lib.afd_debug_step_stamps(out.ctypes.data) == 0
+names = ["start", "tables", "pdl_wait", "select", "update", "node", "csync1", "energy+rec",
+         "fft_in", "fft_local", "csync2", "radix8", "csync3"]
+rows = out[1:29].astype(np.int64)
+d = np.diff(rows[:, :13], axis=1)
+print("phase (ns, median over steps 1..28):")
+for i in range(12):
+    print("  %-12s -> %-12s %8.0f" % (names[i], names[i + 1], np.median(d[:, i])))
+print("  total %.0f ns; gap step k start -> step k+1 start %.0f ns" %
+      (np.median(rows[:, 12] - rows[:, 0]), np.median(np.diff(rows[:, 0]))))
