@@ -105,19 +105,33 @@ struct afd_plan {
 // while its predecessor in the stream drains (it calls pdl_wait() before
 // touching the predecessor's outputs).  Captured graphs keep the edges.
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                       cudaStream_t st, Args... args) {
+cudaError_t launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                               cudaStream_t st, int cluster, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  int n = 1;
+  if (cluster > 1) {
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = cluster;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    n = 2;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  return launch_pdl_cluster(kern, grid, block, smem, st, 1, args...);
 }
 
 // ---------------------------------------------------------------------------
@@ -189,6 +203,8 @@ int setup_kernels(afd_plan* p) {
   if constexpr (use_cluster_step<K>()) {
     CU(cudaFuncSetAttribute(step_cluster_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)ClusterSmem<K>::bytes));
+    CU(cudaFuncSetAttribute(step_cluster_kernel<K>,
+                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   }
   CU(cudaFuncSetAttribute(fft_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)RowSmem<K>::bytes));
@@ -257,10 +273,11 @@ template <int K>
 int launch_step(afd_plan* p, int k, int max_terms, double thr, int dc_first, const double2* g0,
                 const Cand* cand, int ncand, int64_t batch, Step* steps, cudaStream_t st) {
   if constexpr (use_cluster_step<K>()) {
-    CU(launch_pdl(step_cluster_kernel<K>, dim3((unsigned)(batch * kClusterCtas)),
-                  dim3(ClusterGeo<K>::THREADS), ClusterSmem<K>::bytes, st, k, max_terms, thr,
-                  dc_first, g0, p->rem, p->ghat, cand, ncand, (const double*)p->radii,
-                  (const double2*)p->circle, (const double2*)p->twst, p->state, steps));
+    CU(launch_pdl_cluster(step_cluster_kernel<K>, dim3((unsigned)(batch * ClusterGeo<K>::C)),
+                  dim3(ClusterGeo<K>::THREADS), ClusterSmem<K>::bytes, st, ClusterGeo<K>::C, k,
+                  max_terms, thr, dc_first, g0, p->rem, p->ghat, cand, ncand,
+                  (const double*)p->radii, (const double2*)p->circle, (const double2*)p->twst,
+                  p->state, steps));
   } else {
     CU(launch_pdl(step_kernel<K>, dim3((unsigned)batch), dim3(row_block<K>()),
                   RowSmem<K>::bytes, st, k, max_terms, thr, dc_first, g0, p->rem, p->ghat, cand,

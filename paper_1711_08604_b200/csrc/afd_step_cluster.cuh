@@ -1,23 +1,24 @@
 // afd_step_cluster.cuh — the per-step select / update / energy / forward
-// transform of one signal spread over a thread-block cluster of 8 CTAs
-// (8 SMs) with distributed shared memory, for N = 2^K, 10 <= K <= 13.
+// transform of one signal spread over a thread-block cluster of C CTAs
+// (C SMs; C = 8 for N = 1024, 16 - a non-portable cluster size - for
+// 2048 <= N <= 8192) with distributed shared memory.
 //
 // Same arithmetic, same results as step_kernel (afd_kernels.cuh); only the
 // work distribution differs:
-//   * CTA c owns natural samples m in [c*NC, (c+1)*NC), NC = N/8: it
+//   * CTA c owns natural samples m in [c*NC, (c+1)*NC), NC = N/C: it
 //     updates them (core.py:303-314) and sums their |G|^2 - with NC >= 128 a
 //     power of two, that slice is exactly one node of numpy's pairwise-sum
-//     tree, so the 8 node sums combined as ((e0+e1)+(e2+e3))+((e4+e5)+(e6+e7))
+//     tree, so the C node sums combined as a left+right binary tree
 //     reproduce np.mean bit for bit (core.py:195-198).  dc_first's complex
 //     mean (core.py:375) is combined the same way.
-//   * The forward DIT (transform.py:106-124): stages 0..K-4 pair positions
-//     inside aligned blocks of NC bit-reversed positions, so CTA c runs them
-//     on positions [c*NC, (c+1)*NC) (inputs gathered over DSMEM: natural
-//     index l = 8*rev(q) + rev3(c)); stages K-3..K-1 pair positions that
-//     differ in the top 3 bits, so after a cluster barrier CTA c runs them
-//     as radix-8 butterflies on NC/8 position groups q + NC*u, u = 0..7,
-//     gathered from all 8 CTAs over DSMEM.  Every butterfly uses numpy's
-//     N-point table value, as in the reference.
+//   * The forward DIT (transform.py:106-124): stages 0..K-CB-1 (CB = log2 C)
+//     pair positions inside aligned blocks of NC bit-reversed positions, so
+//     CTA c runs them on positions [c*NC, (c+1)*NC) (inputs gathered over
+//     DSMEM: natural index l = C*rev(q) + rev_CB(c)); stages K-CB..K-1 pair
+//     positions that differ in the top CB bits, so after a cluster barrier
+//     CTA c runs them as radix-C butterflies on NC/C position groups
+//     q + NC*u, u < C, gathered from all C CTAs over DSMEM.  Every butterfly
+//     uses numpy's N-point table value, as in the reference.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -28,7 +29,8 @@ namespace afd {
 
 namespace cg = cooperative_groups;
 
-constexpr int kClusterCtas = 8;
+// cluster size used for a transform length 2^K (the slice must stay >= 128)
+__host__ __device__ constexpr int cluster_ctas(int K) { return K >= 11 ? 16 : 8; }
 
 #ifdef AFD_STEP_TIMING
 __device__ unsigned long long g_step_stamps[64][16];
@@ -48,13 +50,15 @@ __device__ unsigned long long g_step_stamps[64][16];
 
 template <int K>
 struct ClusterGeo {
+  static constexpr int C = cluster_ctas(K);         // CTAs per cluster
+  static constexpr int CB = C == 16 ? 4 : 3;        // log2 C
   static constexpr int N = 1 << K;
-  static constexpr int NC = N / kClusterCtas;       // samples / positions per CTA
-  static constexpr int KL = K - 3;                  // bits of the CTA-local transform
+  static constexpr int NC = N / C;                  // samples / positions per CTA
+  static constexpr int KL = K - CB;                 // bits of the CTA-local transform
   static constexpr int RB = 3;                      // local pass register bits
   using GL = Geo<KL, RB>;                           // local transform geometry
   static constexpr int LOCAL_THREADS = GL::T;       // threads of the local transform
-  static constexpr int GROUPS = NC / 8;             // radix-8 groups per CTA in phase 2
+  static constexpr int GROUPS = NC / C;             // radix-C groups per CTA in phase 2
   static constexpr int THREADS = 256;
   static_assert(NC >= 128, "slice must be a pairwise-sum tree node");
   static_assert(LOCAL_THREADS <= THREADS && GROUPS <= THREADS, "block too small");
@@ -66,10 +70,20 @@ struct ClusterSmem {
   static constexpr size_t slice = 0;                                   // NC double2 (natural)
   static constexpr size_t part = slice + sizeof(double2) * CG::NC;     // GL::SMEM double2
   static constexpr size_t mag = part + sizeof(double2) * CG::GL::SMEM; // NC double
-  static constexpr size_t twl = mag + sizeof(double) * CG::NC;         // 2^(K-3)-1 double2
+  static constexpr size_t twl = mag + sizeof(double) * CG::NC;         // NC-1 double2
   static constexpr size_t scratch = twl + sizeof(double2) * (CG::NC - 1);  // 2*(NC/8+16)
   static constexpr size_t bytes = scratch + sizeof(double) * 2 * (CG::NC / 8 + 16);
 };
+
+// left+right binary tree over C values (numpy pairwise halves)
+template <int C>
+__device__ __forceinline__ double tree_combine(const double* v) {
+  if constexpr (C == 1) {
+    return v[0];
+  } else {
+    return tree_combine<C / 2>(v) + tree_combine<C / 2>(v + C / 2);
+  }
+}
 
 // Local stage tables S_0..S_{K-4} copied to shared memory.
 struct LocalTw {
@@ -77,8 +91,9 @@ struct LocalTw {
   __device__ __forceinline__ double2 operator()(int b, int k) const { return sm[(1 << b) - 1 + k]; }
 };
 
+// Launched with a runtime cluster dimension of ClusterGeo<K>::C.
 template <int K>
-__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(256)
+__global__ void __launch_bounds__(256)
 step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
                     const double2* __restrict__ g0, double2* __restrict__ rem,
                     double2* __restrict__ ghat, const Cand* __restrict__ cand, int ncand,
@@ -88,10 +103,10 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   using CG = ClusterGeo<K>;
   using L = ClusterSmem<K>;
   using GL = typename CG::GL;
-  constexpr int N = CG::N, NC = CG::NC;
+  constexpr int N = CG::N, NC = CG::NC, C = CG::C, CB = CG::CB;
   cg::cluster_group cluster = cg::this_cluster();
   const int c = (int)cluster.block_rank();
-  const int sig = blockIdx.x / kClusterCtas;
+  const int sig = blockIdx.x / C;
   extern __shared__ __align__(16) unsigned char smraw[];
   double2* slice = reinterpret_cast<double2*>(smraw + L::slice);
   double2* part = reinterpret_cast<double2*>(smraw + L::part);
@@ -110,16 +125,17 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
 
   // local stage tables S_0..S_{K-4} (== twst[0 .. 2^(K-3)-1))
   for (int i = tid; i < NC - 1; i += blockDim.x) twl[i] = __ldg(twst + i);
-  // phase-2 twiddles of this thread, prefetched: stage b = K-3+e uses
-  // w[(q + NC*(u mod 2^e)) << (2-e)], q = c*GROUPS + tid
+  // phase-2 twiddles of this thread, prefetched: stage b = K-CB+e uses
+  // w[(q + NC*(u mod 2^e)) << (CB-1-e)], q = c*GROUPS + tid
   const int q = c * CG::GROUPS + tid;
-  double2 w2[7];
+  double2 w2[C - 1];
   if (tid < CG::GROUPS) {
     const double2* half = twst + (N / 2) - 1;  // S_{K-1}[k] = w[k]
 #pragma unroll
-    for (int e = 0; e < 3; ++e)
+    for (int e = 0; e < CB; ++e)
 #pragma unroll
-      for (int h = 0; h < (1 << e); ++h) w2[(1 << e) - 1 + h] = __ldg(half + ((q + NC * h) << (2 - e)));
+      for (int h = 0; h < (1 << e); ++h)
+        w2[(1 << e) - 1 + h] = __ldg(half + ((q + NC * h) << (CB - 1 - e)));
   }
   // the tables above are step-independent; candidates, state and the
   // remainder come from the previous kernels (PDL)
@@ -157,16 +173,14 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
       s_node[1] = node.y;
     }
     cluster.sync();
-    double re[kClusterCtas], im[kClusterCtas];
+    double re[C], im[C];
 #pragma unroll
-    for (int u = 0; u < kClusterCtas; ++u) {
+    for (int u = 0; u < C; ++u) {
       const double* rn = cluster.map_shared_rank(s_node, u);
       re[u] = rn[0];
       im[u] = rn[1];
     }
-    const double2 sum =
-        make_double2(((re[0] + re[1]) + (re[2] + re[3])) + ((re[4] + re[5]) + (re[6] + re[7])),
-                     ((im[0] + im[1]) + (im[2] + im[3])) + ((im[4] + im[5]) + (im[6] + im[7])));
+    const double2 sum = make_double2(tree_combine<C>(re), tree_combine<C>(im));
     coeff = np_cdiv(sum, make_double2((double)N, 0.0));
     cluster.sync();  // everyone has read s_node before it is reused
   } else if (k >= 0) {
@@ -235,10 +249,10 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   STAMP(5);
   cluster.sync();  // slices and node sums visible cluster-wide
   STAMP(6);
-  double e[kClusterCtas];
+  double e[C];
 #pragma unroll
-  for (int u = 0; u < kClusterCtas; ++u) e[u] = cluster.map_shared_rank(s_node, u)[0];
-  const double energy = (((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]))) / (double)N;
+  for (int u = 0; u < C; ++u) e[u] = cluster.map_shared_rank(s_node, u)[0];
+  const double energy = tree_combine<C>(e) / (double)N;
 
   if (tid == 0) {
     int stop;
@@ -286,12 +300,12 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   {
     const int tp = tid;
     const bool active = tp < CG::LOCAL_THREADS;
-    const int r3 = brev_bits(c, 3);
+    const int rc = brev_bits(c, CB);
     double2 v[GL::P];
     if (active) {
 #pragma unroll
       for (int i = 0; i < GL::P; ++i) {
-        const int l = 8 * GL::l0(tp, i) + r3;  // natural index of this position
+        const int l = C * GL::l0(tp, i) + rc;  // natural index of this position
         const double2* src = cluster.map_shared_rank(slice, l / NC);
         v[i] = src[l % NC];
       }
@@ -307,25 +321,25 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   cluster.sync();
   STAMP(10);
 
-  // ---- stages K-3..K-1: radix-8 over the top 3 position bits ------------------
+  // ---- stages K-CB..K-1: radix-C over the top CB position bits ----------------
   if (tid < CG::GROUPS) {
-    double2 v[8];
+    double2 v[C];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = cluster.map_shared_rank(part, u)[GL::sw(q)];
+    for (int u = 0; u < C; ++u) v[u] = cluster.map_shared_rank(part, u)[GL::sw(q)];
 #pragma unroll
-    for (int e = 0; e < 3; ++e) {
+    for (int e = 0; e < CB; ++e) {
 #pragma unroll
       for (int h = 0; h < (1 << e); ++h) {
         const double2 w = w2[(1 << e) - 1 + h];
 #pragma unroll
-        for (int g = 0; g < (8 >> (e + 1)); ++g) {
+        for (int g = 0; g < (C >> (e + 1)); ++g) {
           const int i = h | (g << (e + 1));
           bfly(v[i], v[i | (1 << e)], w);
         }
       }
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) gh[q + NC * u] = v[u];
+    for (int u = 0; u < C; ++u) gh[q + NC * u] = v[u];
   }
   STAMP(11);
   cluster.sync();  // remote readers of `part` are done before exit
