@@ -288,3 +288,94 @@ def test_sharded_step_api_on_one_gpu(afd, case):
         assert np.array_equal(rec["c_re"] + 1j * rec["c_im"], g["coeff"])
         assert np.array_equal(rec["residual"], g["residual"])
         assert np.array_equal(rem.cpu().numpy()[0], g["remainder"])
+
+
+# ---------------------------------------------------------------------------
+# size-independent properties at BASELINE sizes (reference acceptance
+# criteria 2, 7, 8: tests/test_acceptance.py:66-76, 135-166)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("cfg", ["c1", "c3"])
+def test_energy_and_reconstruction_identities_at_baseline_size(afd, cfg):
+    core, _ = afd
+    from paper_1711_08604_b200 import workloads as W
+    w = W.CONFIGS[cfg]
+    g = W.signal_for(cfg, 5)
+    grid = core.ParameterGrid(W.radii_for(w.m), w.n)
+    d = core.decompose(g, grid, max_terms=w.steps)
+    e0 = d.initial_energy
+    spent = 0.0
+    for st in d.steps:                                   # criterion 2
+        spent += abs(st.coefficient) ** 2
+        assert abs((e0 - spent) - st.residual_energy) < 1e-10 * e0
+    tail = d.remainder.copy()                            # criterion 7
+    for st in d.steps:
+        tail *= core.blaschke_samples(st.point, w.n)
+    gap = np.max(np.abs(g - core.reconstruct(d, len(d.steps)) - tail))
+    assert gap < 1e-10 * np.max(np.abs(g))
+    res = [e0] + [s.residual_energy for s in d.steps]     # monotone residuals
+    assert all(b <= a * (1 + 1e-12) for a, b in zip(res, res[1:]))
+
+
+def test_basis_orthonormality_of_selected_poles(afd):
+    """Criterion 8 on the c0 decomposition's poles (Gram deviation < 1e-9)."""
+    core, _ = afd
+    g = load_golden("decomp_c0.npz")
+    n = g["g"].shape[0]
+    poles = list(g["a"])
+    basis = [core.tm_basis_samples(poles[: k + 1], n) for k in range(len(poles))]
+    gram = np.array([[np.mean(bi * np.conj(bj)) for bj in basis] for bi in basis])
+    assert np.max(np.abs(gram - np.eye(len(poles)))) < 1e-9
+
+
+def test_parallel_flag_and_single_rows_identical(afd):
+    """parallel=True is result-identical (test_core.py:175-182); single-radius
+    rows equal grid rows bitwise (test_transform.py:206-213)."""
+    core, _ = afd
+    from paper_1711_08604_b200 import transform
+    g = load_golden("decomp_rand3.npz")
+    grid = core.ParameterGrid(tuple(g["radii"]), g["g"].shape[0])
+    a = core.decompose(g["g"], grid, max_terms=6)
+    b = core.decompose(g["g"], grid, max_terms=6, parallel=True)
+    assert [s.point for s in a.steps] == [s.point for s in b.steps]
+    assert [s.coefficient for s in a.steps] == [s.coefficient for s in b.steps]
+    c = transform.dft_forward(g["g"])
+    rows = transform.weighted_inverse_grid(c, (0.0, 0.25, 0.5, 0.8))
+    for i, r in enumerate((0.0, 0.25, 0.5, 0.8)):
+        assert np.array_equal(rows[i], transform.weighted_inverse(c, r))
+
+
+def test_scale_invariance_of_selection(afd):
+    """test_core.py:350-360: scaling G scales coefficients, keeps poles."""
+    core, _ = afd
+    g = load_golden("decomp_rand11.npz")["g"]
+    grid = core.ParameterGrid.experiment_default(g.shape[0])
+    base = core.decompose(g, grid, max_terms=4)
+    for scale in (1e-6, 137.0, 1e6):
+        sc = core.decompose(scale * g, grid, max_terms=4)
+        for sb, ss in zip(base.steps, sc.steps):
+            assert sb.point.value == ss.point.value
+            assert abs(ss.coefficient - scale * sb.coefficient) < 1e-12 * scale * abs(sb.coefficient)
+
+
+def test_pow_ambiguity_flags_consistent(afd):
+    """Steps flagged 'pow-ambiguous' are exactly those whose |a|*|a| low part
+    exceeds 0.49 ulp; unflagged steps are provably bit-identical."""
+    core, _ = afd
+    import math
+    g = load_golden("decomp_c1.npz")
+    grid = core.ParameterGrid(tuple(g["radii"]), g["g"].shape[0])
+    d = core.decompose(g["g"], grid, max_terms=int(g["max_terms"]))
+    for st, fl in zip(d.steps, d.step_flags):
+        h = abs(st.point.value)
+        hh = h * h
+        # exact low part of h*h via Dekker's split
+        sp = 134217729.0
+        t = sp * h
+        hi = t - (t - h)
+        lo_ = h - hi
+        err = ((hi * hi - hh) + 2 * hi * lo_) + lo_ * lo_
+        ulp = math.ulp(hh) if hh else 0.0
+        assert bool(fl & 1) == (hh != 0.0 and abs(err) > 0.49 * ulp)
+        if not fl & 1:
+            assert h ** 2 == hh  # CPython's pow agrees with the device's h*h
