@@ -17,6 +17,6 @@ if [ "$2" == "ncu" ]; then
       --log-file gpurun_out/${tag}_launches.csv $cmd > gpurun_out/${tag}_ncu1.log 2>&1
   ncu --set full --clock-control none --import-source on -k regex:field_kernel -s 3 -c 1 \
       -o gpurun_out/${tag}_field $cmd > gpurun_out/${tag}_ncu2.log 2>&1
-  ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 3 -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:"step_cluster_kernel|step_kernel" -s 3 -c 1 \
       -o gpurun_out/${tag}_step $cmd > gpurun_out/${tag}_ncu3.log 2>&1
 fi
