@@ -95,6 +95,17 @@ int afd_analytic_projection(afd_plan *plan, const double *x, double *out, int64_
 int afd_field(afd_plan *plan, const double *ghat, double *field, int64_t r0, int64_t r1,
               void *stream);
 
+/* Engine of the plan's decompositions (core.py:357-358, 377-381):
+ * 0 = "fft" (default; transform engine, bit-identical to the reference),
+ * 1 = "direct" (oracle.field_direct, O(M N^2) literal sums of the signal;
+ *     matches the reference to its engine-agreement tolerance, N <= 8192). */
+int afd_plan_set_engine(afd_plan *plan, int engine);
+
+/* oracle.field_direct (oracle.py:51-73) rows [r0, r1) of ONE signal g (not
+ * its spectrum): (r1-r0) x N complex. */
+int afd_field_direct(afd_plan *plan, const double *g, double *field, int64_t r0, int64_t r1,
+                     void *stream);
+
 /* Fused field + maximal_selection over the plan's rows for `batch` spectra
  * (core.inner_product_field + core.maximal_selection, core.py:259-300):
  * writes one candidate per signal to out[batch]. */

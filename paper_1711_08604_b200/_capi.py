@@ -47,6 +47,8 @@ SIGNATURES = [
     ("afd_analytic_projection", _I, [_VP, _VP, _VP, _I64, _VP]),
     ("afd_field", _I, [_VP, _VP, _VP, _I64, _I64, _VP]),
     ("afd_field_argmax", _I, [_VP, _VP, _VP, _I64, _VP]),
+    ("afd_plan_set_engine", _I, [_VP, _I]),
+    ("afd_field_direct", _I, [_VP, _VP, _VP, _I64, _I64, _VP]),
     ("afd_argmax", _I, [_VP, _VP, _I64, _VP, _VP]),
     ("afd_atom", _I, [_VP, _I, _VP, _D, _D, _D, _D, _VP, _VP]),
     ("afd_energy", _I, [_VP, _VP, _VP, _I64, _VP]),

@@ -12,11 +12,14 @@ device or the built library every compute entry point raises
 ``AfdCudaUnavailable``.
 
 Engines.  ``engine="fft"`` is the reference's transform engine (the hot
-path accelerated here).  ``engine="direct"`` (the reference's O(M N^2)
-quadrature baseline, ``oracle.field_direct``) is not part of this hot path
-and raises ``NotImplementedError``.  ``parallel`` is accepted for
-signature compatibility; the device path is always parallel and, like the
-reference's threaded path, produces identical results.
+path accelerated here), bit-identical to the reference.  ``engine="direct"``
+is the reference's O(M N^2) quadrature baseline (``oracle.field_direct``),
+also on the device (``csrc/afd_direct.cuh``, N <= 8192); its sums are
+ordered differently from np.correlate, so it agrees with the reference to
+the reference's own engine tolerance (identical poles, 1e-9), not bitwise.
+``parallel`` is accepted for signature compatibility; the device path is
+always parallel and, like the reference's threaded path, produces
+identical results.
 """
 
 from __future__ import annotations
@@ -293,9 +296,8 @@ def _check_decompose_args(g, grid, max_terms, threshold, engine):
         raise ValueError("max_terms must be >= 1")
     if threshold is not None and not 0.0 < threshold <= 1.0:
         raise ValueError("threshold must lie in (0, 1]")
-    if engine == "direct":
-        raise NotImplementedError("engine 'direct' (O(M N^2) quadrature baseline) is not part "
-                                  "of the B200 hot path; use engine='fft'")
+    if engine == "direct" and g.shape[-1] > 8192:
+        raise NotImplementedError("engine 'direct' (O(M N^2) literal sums) supports N <= 8192")
 
 
 def _build(grid, n, engine, rec, count, initial, remainder):
@@ -354,7 +356,7 @@ def decompose_batch(signals, grid, max_terms=10, threshold=None, engine="fft", d
             _as_signal(row)
         _check_decompose_args(sig, grid, max_terms, threshold, engine)
     b, n = sig.shape
-    plan = _plan(n, grid.radii, batch=b)
+    plan = _engine().get_plan(grid.radii, n, batch=b, engine=1 if engine == "direct" else 0)
     rec, counts, initial, rem, _, _ = plan.decompose_host(sig, int(max_terms), threshold,
                                                           dc_first)
     return [_build(grid, n, engine, rec[i], int(counts[i]), initial[i], rem[i])

@@ -15,6 +15,7 @@
 #include "afd_aux.cuh"
 #include "afd_step_cluster.cuh"
 #include "afd_big.cuh"
+#include "afd_direct.cuh"
 
 using namespace afd;
 
@@ -84,6 +85,8 @@ struct afd_plan {
   cudaStream_t g_stream = nullptr;
   int64_t launches = 0;
   int64_t graph_launches_per_replay = 0;
+  // 0 = fft engine (bit-exact), 1 = direct engine (O(M N^2) quadrature)
+  int engine = 0;
   // large N (K > 13): pw holds pw_rev, ghat holds ghat_rev
   bool big = false;
   int ka = 0;
@@ -191,6 +194,13 @@ __global__ void build_tw_image_kernel(double2* img, const double2* st) {
 template <int K>
 int setup_kernels(afd_plan* p) {
   int rc;
+  {
+    const int smem = (int)(sizeof(double2) * dpad(1 << K));
+    CU(cudaFuncSetAttribute(direct_field_kernel<false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CU(cudaFuncSetAttribute(direct_field_kernel<true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  }
   CU(cudaMalloc(&p->tw_img, sizeof(double2) * SmemTw<K, kFieldRB>::ENTRIES));
   build_tw_image_kernel<K><<<32, 256>>>(p->tw_img, p->twst);
   p->launches++;
@@ -320,8 +330,27 @@ int groups_of(int K) {
   AFD_DISPATCH(K, return groups_for<KK>());
 }
 
+// Direct engine: one CTA per (row, signal) reading the remainder G_k.
+int launch_direct(afd_plan* p, const double2* g, int64_t r0, int64_t r1, int64_t batch,
+                  Cand* cand, double2* field_out, const State* state, cudaStream_t st) {
+  const size_t smem = sizeof(double2) * (size_t)dpad((int)p->n);
+  dim3 grid((unsigned)(r1 - r0), (unsigned)batch);
+  if (field_out) {
+    direct_field_kernel<true><<<grid, kDirectThreads, smem, st>>>(
+        (int)p->n, g, p->radii, p->circle, r0, r1, nullptr, field_out, nullptr);
+  } else {
+    CU(launch_pdl(direct_field_kernel<false>, grid, dim3(kDirectThreads), smem, st, (int)p->n,
+                  g, (const double*)p->radii, (const double2*)p->circle, (long long)r0,
+                  (long long)r1, cand, (double2*)nullptr, state));
+  }
+  p->launches++;
+  CU(cudaGetLastError());
+  return 0;
+}
+
 // CTAs per signal of a field launch over `rows` rows (what launch_field uses).
 int field_ctas_for(const afd_plan* p, int64_t rows, int64_t batch) {
+  if (p->engine == 1) return (int)rows;
   AFD_DISPATCH(p->K, {
     constexpr int G = groups_for<KK>();
     const int ge = groups_eff<KK>(p, rows, batch);
@@ -391,9 +420,12 @@ int enqueue_decompose(afd_plan* p, int64_t batch, int max_terms, double thr, int
       return rc;
     for (int k = 0; k < max_terms; ++k) {
       if (!(k == 0 && dc_first)) {
-        if ((rc = launch_field<KK>(p, p->ghat, p->m0, p->m1, batch, p->cand, ncta, nullptr,
-                                   p->state, st)))
-          return rc;
+        if (p->engine == 1)
+          rc = launch_direct(p, p->rem, p->m0, p->m1, batch, p->cand, nullptr, p->state, st);
+        else
+          rc = launch_field<KK>(p, p->ghat, p->m0, p->m1, batch, p->cand, ncta, nullptr,
+                                p->state, st);
+        if (rc) return rc;
       }
       if ((rc = launch_step<KK>(p, k, max_terms, thr, dc_first, nullptr, p->cand, ncta, batch,
                                 p->steps, st)))
@@ -742,6 +774,31 @@ int afd_field(afd_plan* p, const double* ghat, double* field, int64_t r0, int64_
                                              (double2*)field, nullptr, (cudaStream_t)stream));
 }
 
+int afd_field_direct(afd_plan* p, const double* g, double* field, int64_t r0, int64_t r1,
+                     void* stream) {
+  if (!p || !g || !field) return fail(AFD_E_INVALID, "NULL argument");
+  if (p->big) return fail(AFD_E_UNSUPPORTED, "direct engine supports N <= 8192");
+  if (r0 < p->m0 || r1 > p->m1 || r0 >= r1)
+    return fail(AFD_E_INVALID, "rows [%lld, %lld) outside the plan's [%lld, %lld)",
+                (long long)r0, (long long)r1, (long long)p->m0, (long long)p->m1);
+  int rc;
+  if ((rc = set_device(p))) return rc;
+  return launch_direct(p, (const double2*)g, r0, r1, 1, nullptr, (double2*)field, nullptr,
+                       (cudaStream_t)stream);
+}
+
+int afd_plan_set_engine(afd_plan* p, int engine) {
+  if (!p) return fail(AFD_E_INVALID, "NULL plan");
+  if (engine != 0 && engine != 1) return fail(AFD_E_INVALID, "engine must be 0 (fft) or 1 (direct)");
+  if (engine == 1 && p->big) return fail(AFD_E_UNSUPPORTED, "direct engine supports N <= 8192");
+  if (engine != p->engine && p->gexec) {
+    cudaGraphExecDestroy(p->gexec);
+    p->gexec = nullptr;
+  }
+  p->engine = engine;
+  return 0;
+}
+
 int afd_field_argmax(afd_plan* p, const double* ghat, afd_candidate* out, int64_t batch,
                      void* stream) {
   if (!p || !ghat || !out) return fail(AFD_E_INVALID, "NULL argument");
@@ -996,12 +1053,17 @@ int afd_select_local(afd_plan* p, int k, int dc_first, afd_candidate* cand, int6
   }
   const int ncta = field_ctas_for(p, p->m1 - p->m0, batch);
   if ((rc = ensure_cand(p, batch, ncta))) return rc;
-  AFD_DISPATCH(p->K, {
-    if ((rc = launch_field<KK>(p, p->ghat, p->m0, p->m1, batch, p->cand, ncta, nullptr, p->state,
-                               st)))
+  if (p->engine == 1) {
+    if ((rc = launch_direct(p, p->rem, p->m0, p->m1, batch, p->cand, nullptr, p->state, st)))
       return rc;
-    break;
-  });
+  } else {
+    AFD_DISPATCH(p->K, {
+      if ((rc = launch_field<KK>(p, p->ghat, p->m0, p->m1, batch, p->cand, ncta, nullptr,
+                                 p->state, st)))
+        return rc;
+      break;
+    });
+  }
   cand_reduce_kernel<<<(unsigned)batch, 128, 0, st>>>(p->cand, ncta, (Cand*)cand);
   p->launches++;
   CU(cudaGetLastError());

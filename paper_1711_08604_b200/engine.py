@@ -70,7 +70,7 @@ class DeviceDecomposition:
 class Plan:
     """One afd_plan: device tables for (N, radii, radius shard, batch)."""
 
-    def __init__(self, radii, n, m0=0, m1=None, max_batch=1, device=None):
+    def __init__(self, radii, n, m0=0, m1=None, max_batch=1, device=None, engine=0):
         self.device = require_cuda(device)
         self.lib = _capi.load()
         self.radii = tuple(float(r) for r in radii)
@@ -89,6 +89,9 @@ class Plan:
                 circle.ctypes.data))
         self.handle = handle
         self._keep = (tw, circle, scales, r)
+        self.engine = int(engine)
+        if self.engine:
+            _capi.check(self.lib.afd_plan_set_engine(handle, self.engine))
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -144,6 +147,16 @@ class Plan:
         out = torch.empty((max(r1 - r0, 0), self.n), dtype=torch.complex128, device=self.device)
         _capi.check(self.lib.afd_field(self.handle, _ptr(ghat), _ptr(out), r0, r1,
                                        _stream(stream)))
+        return out
+
+    def field_direct(self, g, r0=None, r1=None, stream=None):
+        """oracle.field_direct rows (direct engine) of one signal g (not its spectrum)."""
+        g = self._signal(g)[0]
+        r0 = self.m0 if r0 is None else int(r0)
+        r1 = self.m1 if r1 is None else int(r1)
+        out = torch.empty((max(r1 - r0, 0), self.n), dtype=torch.complex128, device=self.device)
+        _capi.check(self.lib.afd_field_direct(self.handle, _ptr(g), _ptr(out), r0, r1,
+                                              _stream(stream)))
         return out
 
     def field_argmax(self, ghat, stream=None):
@@ -286,12 +299,12 @@ _PLANS_LOCK = threading.Lock()
 _MAX_PLANS = 16
 
 
-def get_plan(radii, n, batch=1, m0=0, m1=None, device=None):
-    """Cached plan for (device, N, radii, shard) with max_batch >= batch."""
+def get_plan(radii, n, batch=1, m0=0, m1=None, device=None, engine=0):
+    """Cached plan for (device, N, radii, shard, engine) with max_batch >= batch."""
     dev = require_cuda(device)
     if not (type(radii) is tuple and all(type(r) is float for r in radii[:1])):
         radii = tuple(float(r) for r in radii)
-    key = (dev.index, int(n), radii, int(m0), m1)
+    key = (dev.index, int(n), radii, int(m0), m1, int(engine))
     with _PLANS_LOCK:
         p = _PLANS.get(key)
         if p is None or p.max_batch < batch:
@@ -299,6 +312,7 @@ def get_plan(radii, n, batch=1, m0=0, m1=None, device=None):
                 del _PLANS[key]
             if len(_PLANS) >= _MAX_PLANS:
                 _PLANS.pop(next(iter(_PLANS)))
-            p = Plan(radii, n, m0=m0, m1=m1, max_batch=max(int(batch), 1), device=dev.index)
+            p = Plan(radii, n, m0=m0, m1=m1, max_batch=max(int(batch), 1), device=dev.index,
+                     engine=engine)
             _PLANS[key] = p
         return p

@@ -40,7 +40,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REF)
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
-from fastafd import core, signals, transform  # noqa: E402  (reference, read-only)
+from fastafd import core, oracle, signals, transform  # noqa: E402  (reference, read-only)
 
 from paper_1711_08604_b200 import workloads as W  # noqa: E402
 
@@ -206,9 +206,38 @@ def c2_case(nsteps=2):
     print("c2           %d steps %.1fs" % (nsteps, el))
 
 
+def direct_case():
+    """Reference decompositions with engine="direct" (oracle.field_direct via
+    np.correlate, core.py:381): compared at the reference's own engine
+    agreement tolerance (test_core.py:313-326), not bitwise."""
+    cases = {}
+    for seed in (3, 11, 42):
+        cases["rand%d" % seed] = (signals.synth_random_hardy(128, seed=seed),
+                                  core.ParameterGrid.experiment_default(128), 6)
+    w = W.CONFIGS["c0"]
+    cases["c0"] = (W.signal_for("c0"), core.ParameterGrid(W.radii_for(w.m), w.n), w.steps)
+    out = {}
+    for name, (g, grid, terms) in cases.items():
+        d = core.decompose(g, grid, max_terms=terms, engine="direct")
+        arr = _steps_arrays(d)
+        out["g_" + name] = g
+        out["radii_" + name] = np.array(grid.radii)
+        out["terms_" + name] = terms
+        for k, v in arr.items():
+            out["%s_%s" % (k, name)] = v
+        out["remainder_" + name] = d.remainder
+        f = oracle.field_direct(g, grid)
+        out["field_" + name] = f
+    np.savez_compressed(os.path.join(HERE, "direct.npz"), **out)
+    print("direct       done")
+
+
 def main():
     if "--only-big" in sys.argv:
         big_case()
+        return
+    if "--only-direct" in sys.argv:
+        direct_case()
         return
     transforms_case()
     n = 1024
@@ -237,6 +266,7 @@ def main():
         decomp_case("c3_s%d" % idx, W.signal_for("c3", idx),
                     core.ParameterGrid(W.radii_for(w.m), w.n), max_terms=w.steps)
     big_case()
+    direct_case()
     if "--no-c2" not in sys.argv:
         c2_case()
 

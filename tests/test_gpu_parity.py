@@ -379,3 +379,33 @@ def test_pow_ambiguity_flags_consistent(afd):
         assert bool(fl & 1) == (hh != 0.0 and abs(err) > 0.49 * ulp)
         if not fl & 1:
             assert h ** 2 == hh  # CPython's pow agrees with the device's h*h
+
+
+# ---------------------------------------------------------------------------
+# direct engine (oracle.field_direct on the device)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("case", ["rand3", "rand11", "rand42", "c0"])
+def test_direct_engine_matches_reference(afd, case):
+    """engine="direct": the reference's engine-agreement contract
+    (test_core.py:313-326): identical poles, coefficients and residuals to
+    1e-9; field rows vs oracle.field_direct to 1e-9 (criterion 1)."""
+    core, _ = afd
+    from paper_1711_08604_b200 import direct
+    dg = load_golden("direct.npz")
+    g = dg["g_" + case]
+    grid = core.ParameterGrid(tuple(dg["radii_" + case]), g.shape[0])
+    f = direct.field_direct(g, grid)
+    ref = dg["field_" + case]
+    assert np.max(np.abs(f - ref) / np.maximum(np.abs(ref), 1e-300)) < 1e-9
+    d = core.decompose(g, grid, max_terms=int(dg["terms_" + case]), engine="direct")
+    assert d.engine == "direct"
+    assert [s.point.angle_index for s in d.steps] == list(dg["j_" + case])
+    assert [s.point.radius for s in d.steps] == list(dg["radius_" + case])
+    e0 = d.initial_energy
+    for st, c, r in zip(d.steps, dg["coeff_" + case], dg["residual_" + case]):
+        assert abs(st.coefficient - c) < 1e-9 * abs(c)
+        assert abs(st.residual_energy - r) < 1e-9 * e0
+    # and the fft engine selects the same poles (test_core.py:313-326)
+    d2 = core.decompose(g, grid, max_terms=int(dg["terms_" + case]), engine="fft")
+    assert [s.point for s in d2.steps] == [s.point for s in d.steps]

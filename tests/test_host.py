@@ -88,7 +88,8 @@ def test_decompose_argument_validation_before_device():
     with pytest.raises(ValueError):
         core.decompose(np.ones(12, complex), grid)
     with pytest.raises(NotImplementedError):
-        core.decompose(g, grid, engine="direct")
+        core.decompose(np.ones(16384, complex), core.ParameterGrid((0.0,), 16384),
+                       engine="direct")
 
 
 def test_no_cpu_fallback_without_gpu():
