@@ -115,7 +115,6 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   double* scratch = reinterpret_cast<double*>(smraw + L::scratch);
   __shared__ double s_node[2];   // this CTA's pairwise-tree node sums
   __shared__ Cand red[32];
-  __shared__ int s_stop;
   State& st = state[sig];
   double2* __restrict__ r = rem + (size_t)sig * N;
   double2* __restrict__ gh = ghat + (size_t)sig * N;
@@ -249,27 +248,30 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   STAMP(5);
   cluster.sync();  // slices and node sums visible cluster-wide
   STAMP(6);
-  double e[C];
+  // The forward transform does not need the energy: warp(s) 0.. run the
+  // CTA-local DIT on a named barrier while the last warp combines the
+  // energy tree, writes the step record and evaluates the stop rules.
+  constexpr int kFftWarps = (CG::LOCAL_THREADS + 31) / 32;
+  static_assert(kFftWarps * 32 < CG::THREADS, "need a spare warp for the energy");
+  const int warp = tid >> 5;
+  if (warp == CG::THREADS / 32 - 1) {
+    if ((tid & 31) == 0) {
+      double e[C];
 #pragma unroll
-  for (int u = 0; u < C; ++u) e[u] = cluster.map_shared_rank(s_node, u)[0];
-  const double energy = tree_combine<C>(e) / (double)N;
-
-  if (tid == 0) {
-    int stop;
-    if (k < 0) {
-      stop = (energy == 0.0) ? 1 : 0;  // core.py:366-368
-      if (c == 0) {
-        st.initial = energy;
-        st.nsteps = 0;
-        st.flags = 0;
-        st.stopped = stop;
-      }
-    } else {
-      stop = 0;
-      if (threshold > 0.0 && energy <= threshold * st.initial) stop = 1;  // core.py:386-387
-      if (energy == 0.0) stop = 1;                                         // core.py:388-389
-      if (k + 1 >= max_terms) stop = 1;
-      if (c == 0) {
+      for (int u = 0; u < C; ++u) e[u] = cluster.map_shared_rank(s_node, u)[0];
+      const double energy = tree_combine<C>(e) / (double)N;
+      if (k < 0) {
+        if (c == 0) {
+          st.initial = energy;
+          st.nsteps = 0;
+          st.flags = 0;
+          st.stopped = (energy == 0.0) ? 1 : 0;  // core.py:366-368
+        }
+      } else if (c == 0) {
+        int stop = 0;
+        if (threshold > 0.0 && energy <= threshold * st.initial) stop = 1;  // core.py:386-387
+        if (energy == 0.0) stop = 1;                                         // core.py:388-389
+        if (k + 1 >= max_terms) stop = 1;
         Step rec;
         rec.s = s;
         rec.j = j;
@@ -287,17 +289,11 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
         st.stopped = stop;
       }
     }
-    s_stop = stop;
-  }
-  __syncthreads();
-  if (s_stop) {
-    cluster.sync();  // keep this CTA's shared memory alive for remote readers
-    return;
-  }
-
-  STAMP(7);
-  // ---- forward transform, stages 0..K-4 on positions [c*NC, (c+1)*NC) --------
-  {
+  } else if (warp < kFftWarps) {
+    // ---- forward transform, stages 0..K-CB-1 on positions [c*NC, (c+1)*NC) ----
+    // (computed even on the last step: harmless, and keeps it off the
+    // energy's critical path)
+    STAMP(7);
     const int tp = tid;
     const bool active = tp < CG::LOCAL_THREADS;
     const int rc = brev_bits(c, CB);
@@ -311,7 +307,8 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
       }
     }
     STAMP(8);
-    fft_passes<CG::KL, false, CG::RB>(v, tp, active, part, LocalTw{twl});
+    fft_passes<CG::KL, false, CG::RB>(v, tp, active, part, LocalTw{twl},
+                                      GroupSync{1, kFftWarps * 32});
     STAMP(9);
     if (active) {
 #pragma unroll
@@ -326,6 +323,8 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
     double2 v[C];
 #pragma unroll
     for (int u = 0; u < C; ++u) v[u] = cluster.map_shared_rank(part, u)[GL::sw(q)];
+    // my remote reads are done: let the other CTAs go (split cluster barrier)
+    asm volatile("barrier.cluster.arrive.release;" ::: "memory");
 #pragma unroll
     for (int e = 0; e < CB; ++e) {
 #pragma unroll
@@ -340,9 +339,12 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
     }
 #pragma unroll
     for (int u = 0; u < C; ++u) gh[q + NC * u] = v[u];
+  } else {
+    asm volatile("barrier.cluster.arrive.release;" ::: "memory");
   }
   STAMP(11);
-  cluster.sync();  // remote readers of `part` are done before exit
+  // no CTA leaves while another may still read its shared memory
+  asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
   STAMP(12);
 }
 
