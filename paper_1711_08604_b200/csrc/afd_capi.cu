@@ -286,8 +286,8 @@ int launch_step(afd_plan* p, int k, int max_terms, double thr, int dc_first, con
     CU(launch_pdl_cluster(step_cluster_kernel<K>, dim3((unsigned)(batch * ClusterGeo<K>::C)),
                   dim3(ClusterGeo<K>::THREADS), ClusterSmem<K>::bytes, st, ClusterGeo<K>::C, k,
                   max_terms, thr, dc_first, g0, p->rem, p->ghat, cand, ncand,
-                  (const double*)p->radii, (const double2*)p->circle, (const double2*)p->twst,
-                  p->state, steps));
+                  (const double*)p->radii, (int)p->m, (const double2*)p->circle,
+                  (const double2*)p->twst, p->state, steps));
   } else {
     CU(launch_pdl(step_kernel<K>, dim3((unsigned)batch), dim3(row_block<K>()),
                   RowSmem<K>::bytes, st, k, max_terms, thr, dc_first, g0, p->rem, p->ghat, cand,

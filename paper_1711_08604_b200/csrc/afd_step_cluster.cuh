@@ -72,7 +72,10 @@ struct ClusterSmem {
   static constexpr size_t mag = part + sizeof(double2) * CG::GL::SMEM; // NC double
   static constexpr size_t twl = mag + sizeof(double) * CG::NC;         // NC-1 double2
   static constexpr size_t scratch = twl + sizeof(double2) * (CG::NC - 1);  // 2*(NC/8+16)
-  static constexpr size_t bytes = scratch + sizeof(double) * 2 * (CG::NC / 8 + 16);
+  static constexpr size_t zsl = scratch + sizeof(double) * 2 * (CG::NC / 8 + 16);  // NC double2
+  static constexpr size_t rad = zsl + sizeof(double2) * CG::NC;  // up to kRadSmem radii
+  static constexpr int kRadSmem = 4096;
+  static constexpr size_t bytes = rad + sizeof(double) * kRadSmem;
 };
 
 // left+right binary tree over C values (numpy pairwise halves)
@@ -97,9 +100,9 @@ __global__ void __launch_bounds__(256)
 step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
                     const double2* __restrict__ g0, double2* __restrict__ rem,
                     double2* __restrict__ ghat, const Cand* __restrict__ cand, int ncand,
-                    const double* __restrict__ radii, const double2* __restrict__ circle,
-                    const double2* __restrict__ twst, State* __restrict__ state,
-                    Step* __restrict__ steps) {
+                    const double* __restrict__ radii, int nrad,
+                    const double2* __restrict__ circle, const double2* __restrict__ twst,
+                    State* __restrict__ state, Step* __restrict__ steps) {
   using CG = ClusterGeo<K>;
   using L = ClusterSmem<K>;
   using GL = typename CG::GL;
@@ -113,6 +116,8 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   double* mag = reinterpret_cast<double*>(smraw + L::mag);
   double2* twl = reinterpret_cast<double2*>(smraw + L::twl);
   double* scratch = reinterpret_cast<double*>(smraw + L::scratch);
+  double2* zsl = reinterpret_cast<double2*>(smraw + L::zsl);  // this CTA's circle slice
+  double* rad = reinterpret_cast<double*>(smraw + L::rad);    // radii (if <= kRadSmem)
   __shared__ double s_node[2];   // this CTA's pairwise-tree node sums
   __shared__ Cand red[32];
   State& st = state[sig];
@@ -149,9 +154,16 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
     const int i = tid + u * CG::THREADS;
     if (i < NC) {
       zs[u] = circle[m0 + i];
+      zsl[i] = zs[u];
       gs[u] = k >= 0 ? r[m0 + i] : g0[(size_t)sig * N + m0 + i];
     }
   }
+  // radii for grid.point: staged in shared memory when they fit
+  const bool rad_smem = nrad <= L::kRadSmem;
+  if (rad_smem)
+    for (int i = tid; i < nrad; i += blockDim.x) rad[i] = radii[i];
+  // publish the circle slices cluster-wide (waited on before the lookup)
+  asm volatile("barrier.cluster.arrive.release;" ::: "memory");
   STAMP(1);
   pdl_wait();
   STAMP(2);
@@ -163,6 +175,7 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   double radius = 0.0;
   double2 a = make_double2(0.0, 0.0), coeff = make_double2(0.0, 0.0);
   if (k == 0 && dc_first) {
+    asm volatile("barrier.cluster.wait.acquire;" ::: "memory");  // close the split barrier
     // core.py:373-375: coeff = complex(np.mean(remainder)), pairwise over N
     for (int i = tid; i < NC; i += blockDim.x) slice[i] = r[m0 + i];
     __syncthreads();
@@ -201,11 +214,13 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
     b = red[0];
     s = b.flat / N;
     j = b.flat % N;
-    radius = radii[s];
-    const double2 zj = circle[j];
+    radius = rad_smem ? rad[s] : radii[s];
+    asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
+    const double2 zj = cluster.map_shared_rank(zsl, (int)(j / NC))[j % NC];  // circle[j]
     a = make_double2(radius * zj.x, radius * zj.y);  // grid.point, core.py:163-167
     coeff = make_double2(b.re, b.im);
   }
+  if (k < 0) asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
 
   STAMP(3);
   // ---- update this CTA's slice (or copy g0 at init) --------------------------
