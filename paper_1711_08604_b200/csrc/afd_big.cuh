@@ -11,9 +11,12 @@
 //           q + 2^b0 u, u < 16, and runs 4 stages in registers; lanes own
 //           consecutive q, so every load/store is coalesced.
 // Intermediates live in a row-batch buffer sized to stay L2-resident.  The
-// input of pass A is in position (bit-reversed) order: the plan keeps the
-// r^l table as pw_rev[m][p] = r^rev(p) and the field spectrum as
-// ghat_rev[p] = Ghat[rev(p)] (transform.py:151,198 gather the same way).
+// input of pass A is the bit-reversed gather of transform.py:151,198, stored
+// directly in pass A's register layout: inside each 2^KA block, position
+// (rev(t) << 4) | i (what register i of thread t holds in pass 0) lives at
+// index i*T + t, so pass A loads straight into registers, coalesced.  The
+// plan keeps the r^l table that way (pw_perm) and the step kernels write the
+// field spectrum that way (ghat_perm).
 // Every butterfly is the reference's, so results stay bit-identical.
 //
 // Per-step bookkeeping for large N is split over grid kernels: the numpy
@@ -38,6 +41,14 @@ __host__ __device__ constexpr size_t big_a_smem() {
 }
 
 __device__ __forceinline__ int brev_rt(int x, int bits) { return (int)(__brev((unsigned)x) >> (32 - bits)); }
+
+// index of bit-reversed-array position p in the pass-A register layout
+__device__ __forceinline__ long long perm_of_pos(long long p, int ka) {
+  const int T = 1 << (ka - 4);
+  const int q = (int)(p & ((1LL << ka) - 1));
+  const int tp = brev_rt(q >> 4, ka - 4);
+  return (p & ~((1LL << ka) - 1)) + (long long)(q & 15) * T + tp;
+}
 
 // ---------------------------------------------------------------------------
 // Pass A.  mode 0: field prologue y[p] = pw_rev[row][p] * ghat_rev[p]
@@ -79,23 +90,26 @@ big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0
        it += (long long)gridDim.x * kBigGroups) {
     const long long rl = it / nblk;               // row within the batch
     const long long base = (it % nblk) * BLK;
-    // stage the block's DIT inputs in position order (coalesced loads)
+    double2 v[GA::P];
     if (mode == 0) {
+      // prologue y = powers * c[rev] (transform.py:198) straight from the
+      // register-layout tables (coalesced over t)
       const double* __restrict__ pr = pw_rev + (size_t)(row0 + rl - pw_row0) * N + base;
       const double2* __restrict__ gr = ghat_rev + base;
-      for (int q = tid; q < BLK; q += T) {
-        const double p = __ldg(pr + q);
-        const double2 c = __ldg(gr + q);
-        buf[GA::sw(q)] = make_double2(p * c.x, p * c.y);  // transform.py:198
+#pragma unroll
+      for (int i = 0; i < GA::P; ++i) {
+        const double p = __ldg(pr + i * T + tid);
+        const double2 c = __ldg(gr + i * T + tid);
+        v[i] = make_double2(p * c.x, p * c.y);
       }
     } else {
+      // transform of one natural-order signal: gather x[rev(p)] via smem
       for (int q = tid; q < BLK; q += T) buf[GA::sw(q)] = x[brev_rt((int)(base + q), K)];
-    }
-    sync();
-    double2 v[GA::P];
+      sync();
 #pragma unroll
-    for (int i = 0; i < GA::P; ++i) v[i] = buf[GA::sw(GA::pos(0, t0, i))];
-    sync();
+      for (int i = 0; i < GA::P; ++i) v[i] = buf[GA::sw(GA::pos(0, t0, i))];
+      sync();
+    }
     fft_passes<KA, INV, 4>(v, tid, true, buf, tw, sync);
     double2* __restrict__ y = Y + (size_t)rl * N + base;
 #pragma unroll
@@ -111,11 +125,11 @@ big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0
 //   out_mode 1: field epilogue: scale, |.|^2, running first maximum -> cand
 //   out_mode 2: field epilogue, materialise rows into fout[row - row0][j]
 //   out_mode 3: transform output in natural order fout[j] (optionally / N)
-//   out_mode 4: transform output bit-reversed: fout[rev(j)] (field spectrum)
+//   out_mode 4: field spectrum: position rev(j) in pass-A layout (ghat_perm)
 // ---------------------------------------------------------------------------
 template <bool INV>
 __global__ void __launch_bounds__(kColThreads, 2)
-big_pass_col(int K, int b0, int out_mode, int scale_n, double2* __restrict__ Y,
+big_pass_col(int K, int ka, int b0, int out_mode, int scale_n, double2* __restrict__ Y,
              const double2* __restrict__ twst, const double* __restrict__ scales,
              long long row0, long long row1, Cand* __restrict__ cand,
              double2* __restrict__ fout, const int* __restrict__ stopped) {
@@ -134,14 +148,15 @@ big_pass_col(int K, int b0, int out_mode, int scale_n, double2* __restrict__ Y,
     double2 v[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) v[u] = y[q + ((long long)u << b0)];
-    const double2* __restrict__ half = twst + (N / 2) - 1;  // S_{K-1}[k] = w[k]
     const long long qlow = q & lowmask;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int b = b0 + e;
+      // per-stage table S_b[k] = w[k << (K-1-b)]: lanes read consecutive entries
+      const double2* __restrict__ sb = twst + ((1LL << b) - 1);
 #pragma unroll
       for (int kk = 0; kk < (1 << e); ++kk) {
-        double2 w = __ldg(half + ((qlow + ((long long)kk << b0)) << (K - 1 - b)));
+        double2 w = __ldg(sb + qlow + ((long long)kk << b0));
         if (INV) w.y = -w.y;
 #pragma unroll
         for (int h = 0; h < (16 >> (e + 1)); ++h) {
@@ -179,7 +194,7 @@ big_pass_col(int K, int b0, int out_mode, int scale_n, double2* __restrict__ Y,
         double2 o = v[u];
         if (scale_n) o = np_cdiv(o, dn);  // `y /= n`, transform.py:133
         if (out_mode == 3) fout[j] = o;
-        else fout[brev_rt((int)j, K)] = o;
+        else fout[perm_of_pos(brev_rt((int)j, K), ka)] = o;
       }
     }
   }
@@ -420,12 +435,27 @@ __global__ void __launch_bounds__(1024) bitrev_rows_kernel(double* __restrict__ 
   if (mid2 != mid) row[la] = B[rl][rh];
 }
 
-// dst[p] = src[rev(p)] (natural spectrum -> field input order)
-__global__ void bitrev_copy_kernel(int K, const double2* __restrict__ src, double2* __restrict__ dst) {
+// natural spectrum -> field input order: dst[perm(p)] = src[rev(p)]
+__global__ void bitrev_copy_kernel(int K, int ka, const double2* __restrict__ src,
+                                   double2* __restrict__ dst) {
   const long long N = 1LL << K;
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N;
        p += (long long)gridDim.x * blockDim.x)
-    dst[p] = src[brev_rt((int)p, K)];
+    dst[perm_of_pos(p, ka)] = src[brev_rt((int)p, K)];
+}
+
+// In-place reorder of each 2^ka block of position-ordered rows into the
+// pass-A register layout (pw_rev -> pw_perm).  blockIdx.x = block, y = row.
+__global__ void __launch_bounds__(256) perm_blocks_kernel(double* __restrict__ pw, int K, int ka) {
+  extern __shared__ double blk[];
+  const int BLK = 1 << ka, T = 1 << (ka - 4);
+  double* row = pw + ((size_t)blockIdx.y << K) + ((size_t)blockIdx.x << ka);
+  for (int q = threadIdx.x; q < BLK; q += blockDim.x) blk[q] = row[q];
+  __syncthreads();
+  for (int e = threadIdx.x; e < BLK; e += blockDim.x) {
+    const int i = e / T, tp = e % T;
+    row[e] = blk[(brev_rt(tp, ka - 4) << 4) | i];
+  }
 }
 
 // natural-order spectrum mask of the analytic projection (core.py:229-230)

@@ -486,11 +486,11 @@ int big_launch_cols(afd_plan* p, bool inv, int last_mode, int scale_n, int64_t r
   for (int b0 = p->ka; b0 < p->K; b0 += 4) {
     const int mode = (b0 + 4 >= p->K) ? last_mode : 0;
     if (inv)
-      big_pass_col<true><<<grid, kColThreads, 0, st>>>(p->K, b0, mode, scale_n, p->Y, p->twst,
+      big_pass_col<true><<<grid, kColThreads, 0, st>>>(p->K, p->ka, b0, mode, scale_n, p->Y, p->twst,
                                                        p->scales, r0, r0 + rows, p->big_cand,
                                                        fout, stopped);
     else
-      big_pass_col<false><<<grid, kColThreads, 0, st>>>(p->K, b0, mode, scale_n, p->Y, p->twst,
+      big_pass_col<false><<<grid, kColThreads, 0, st>>>(p->K, p->ka, b0, mode, scale_n, p->Y, p->twst,
                                                         p->scales, r0, r0 + rows, p->big_cand,
                                                         fout, stopped);
     p->launches++;
@@ -666,7 +666,9 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
     p->big = true;
     p->ka = big_ka(K);
     bitrev_rows_kernel<<<dim3(1u << (K - 10), (unsigned)(m1 - m0)), dim3(32, 32)>>>(p->pw, K);
-    p->launches++;
+    perm_blocks_kernel<<<dim3(1u << (K - p->ka), (unsigned)(m1 - m0)), 256,
+                         sizeof(double) << p->ka>>>(p->pw, K, p->ka);
+    p->launches += 2;
     if (cudaGetLastError() != cudaSuccess) return cleanup(fail(AFD_E_CUDA, "bitrev launch"));
     p->big_rows = std::max<int64_t>(1, std::min<int64_t>(m1 - m0, (int64_t)(kBigBatchBytes / (N * 16))));
     ALLOC2(p->Y, sizeof(double2) * N * p->big_rows);
@@ -765,7 +767,7 @@ int afd_field(afd_plan* p, const double* ghat, double* field, int64_t r0, int64_
   if (p->big) {
     // the large-N field kernels read the spectrum bit-reversed
     cudaStream_t st = (cudaStream_t)stream;
-    bitrev_copy_kernel<<<256, 256, 0, st>>>(p->K, (const double2*)ghat, p->tmp);
+    bitrev_copy_kernel<<<256, 256, 0, st>>>(p->K, p->ka, (const double2*)ghat, p->tmp);
     p->launches++;
     return big_field(p, p->tmp, r0, r1, (double2*)field, nullptr, st);
   }
@@ -808,7 +810,8 @@ int afd_field_argmax(afd_plan* p, const double* ghat, afd_candidate* out, int64_
   if (p->big) {
     const int nc = (int)(p->big_rows * big_col_ctas(p));
     for (int64_t b = 0; b < batch; ++b) {
-      bitrev_copy_kernel<<<256, 256, 0, st>>>(p->K, (const double2*)ghat + b * p->n, p->tmp);
+      bitrev_copy_kernel<<<256, 256, 0, st>>>(p->K, p->ka, (const double2*)ghat + b * p->n,
+                                              p->tmp);
       p->launches++;
       if ((rc = big_field(p, p->tmp, p->m0, p->m1, nullptr, nullptr, st))) return rc;
       cand_reduce_kernel<<<1, 256, 0, st>>>(p->big_cand, nc, (Cand*)out + b);
@@ -1131,7 +1134,7 @@ int afd_time_field(afd_plan* p, const double* ghat, int64_t batch, int reps, dou
   cudaStream_t st = (cudaStream_t)stream;
   if (p->big) {
     // one whole large-N field evaluation (all row batches) per timed rep
-    bitrev_copy_kernel<<<256, 256, 0, st>>>(p->K, (const double2*)ghat, p->tmp);
+    bitrev_copy_kernel<<<256, 256, 0, st>>>(p->K, p->ka, (const double2*)ghat, p->tmp);
     p->launches++;
     cudaEvent_t e0, e1;
     CU(cudaEventCreate(&e0));
