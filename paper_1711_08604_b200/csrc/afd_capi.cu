@@ -149,6 +149,9 @@ namespace {
 #define AFD_FIELD_RB 4
 #endif
 constexpr int kFieldRB = AFD_FIELD_RB;
+#ifndef AFD_GE_FACTOR
+#define AFD_GE_FACTOR 1
+#endif
 
 template <int K>
 constexpr int groups_for() {
@@ -252,7 +255,7 @@ int groups_eff(const afd_plan* p, int64_t rows, int64_t batch) {
   constexpr int G = groups_for<K>();
   constexpr int gmin = Geo<K, kFieldRB>::T >= 32 ? 1 : 32 / Geo<K, kFieldRB>::T;  // >= 1 warp
   int g = G;
-  while (g > gmin && ((rows + g - 1) / g) * batch < 2 * p->sms) g >>= 1;
+  while (g > gmin && ((rows + g - 1) / g) * batch < AFD_GE_FACTOR * p->sms) g >>= 1;
   return g;
 }
 
