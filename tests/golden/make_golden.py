@@ -232,7 +232,34 @@ def direct_case():
     print("direct       done")
 
 
+def cli_case():
+    """Files written by the reference's own command line (fastafd.cli):
+    signal CSVs, decomposition JSON documents and reconstruction outputs."""
+    import tempfile
+    from fastafd import cli
+    out = os.path.join(HERE, "cli")
+    os.makedirs(out, exist_ok=True)
+    runs = [
+        ("f1_256", ["synth", "f1", "--samples", "256"], ["--terms", "10"]),
+        ("f2_1024", ["synth", "f2", "--samples", "1024"], ["--terms", "10"]),
+        ("rand_512", ["synth", "random", "--samples", "512", "--seed", "7"],
+         ["--terms", "8", "--no-dc-first", "--radii", "0.05,0.3,0.55,0.8,0.9"]),
+    ]
+    for name, synth, dec in runs:
+        csv = os.path.join(out, name + ".csv")
+        js = os.path.join(out, name + ".json")
+        assert cli.run_command(synth + ["--output", csv]) == 0
+        assert cli.run_command(["decompose", "--input", csv, "--output", js] + dec) == 0
+        assert cli.run_command(["reconstruct", "--input", js, "--terms", "4", "--output",
+                                os.path.join(out, name + ".s4.csv"), "--emit-errors",
+                                os.path.join(out, name + ".err.csv")]) == 0
+    print("cli          done")
+
+
 def main():
+    if "--only-cli" in sys.argv:
+        cli_case()
+        return
     if "--only-big" in sys.argv:
         big_case()
         return
@@ -267,6 +294,7 @@ def main():
                     core.ParameterGrid(W.radii_for(w.m), w.n), max_terms=w.steps)
     big_case()
     direct_case()
+    cli_case()
     if "--no-c2" not in sys.argv:
         c2_case()
 

@@ -6,6 +6,7 @@ operation.  All calls go through the C ABI (libafd_b200.so) via the
 package's public API.
 """
 
+import json
 import warnings
 
 import numpy as np
@@ -409,3 +410,40 @@ def test_direct_engine_matches_reference(afd, case):
     # and the fft engine selects the same poles (test_core.py:313-326)
     d2 = core.decompose(g, grid, max_terms=int(dg["terms_" + case]), engine="fft")
     assert [s.point for s in d2.steps] == [s.point for s in d.steps]
+
+
+# ---------------------------------------------------------------------------
+# command line on the device: files byte-identical to the reference CLI's
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("case", ["f1_256", "f2_1024", "rand_512"])
+def test_cli_outputs_byte_identical(afd, tmp_path, case):
+    import os
+    from conftest import GOLDEN
+    from paper_1711_08604_b200 import cli
+    ref = os.path.join(GOLDEN, "cli")
+    dec = {"rand_512": ["--terms", "8", "--no-dc-first", "--radii", "0.05,0.3,0.55,0.8,0.9"]}
+    js = tmp_path / "d.json"
+    assert cli.run_command(["decompose", "--input", os.path.join(ref, case + ".csv"),
+                            "--output", str(js)] + dec.get(case, ["--terms", "10"])) == 0
+    assert js.read_bytes() == open(os.path.join(ref, case + ".json"), "rb").read()
+    s4, err = tmp_path / "s4.csv", tmp_path / "err.csv"
+    assert cli.run_command(["reconstruct", "--input", str(js), "--terms", "4", "--output",
+                            str(s4), "--emit-errors", str(err)]) == 0
+    assert s4.read_bytes() == open(os.path.join(ref, case + ".s4.csv"), "rb").read()
+    assert err.read_bytes() == open(os.path.join(ref, case + ".err.csv"), "rb").read()
+    if case == "f2_1024":  # synth f2 runs the analytic projection on the device
+        sc = tmp_path / "f2.csv"
+        assert cli.run_command(["synth", "f2", "--samples", "1024", "--output", str(sc)]) == 0
+        assert sc.read_bytes() == open(os.path.join(ref, "f2_1024.csv"), "rb").read()
+
+
+def test_cli_bench_runs(afd, tmp_path):
+    from paper_1711_08604_b200 import cli
+    out = tmp_path / "b.csv"
+    assert cli.run_command(["bench", "--sizes", "256,512,1024", "--repeats", "2", "--output",
+                            str(out)]) == 0
+    rows = out.read_text().strip().splitlines()
+    assert rows[0] == "engine,N,M,terms,repeat,seconds" and len(rows) == 1 + 2 * 3 * 2
+    summary = json.loads((tmp_path / "b.summary.json").read_text())
+    assert set(summary["engines"]) == {"fft", "direct"}
