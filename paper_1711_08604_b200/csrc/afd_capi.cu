@@ -176,6 +176,16 @@ constexpr bool use_cluster_step() {
   return K >= 10 && K <= 13;
 }
 
+// Phase offset between the two row-groups of a field CTA (FieldHook);
+// AFD_FIELD_PP=0 turns it off (experiments).
+static int field_pp() {
+  static int v = [] {
+    const char* e = getenv("AFD_FIELD_PP");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 template <int K>
 int row_block() {
   return Geo<K>::T < 64 ? 64 : Geo<K>::T;
@@ -270,12 +280,13 @@ int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64
                       (Geo<K, kFieldRB>::SMEM * ge + SmemTw<K, kFieldRB>::ENTRIES);
   if (field_out) {
     field_kernel<K, kFieldRB, G, true><<<grid, block, smem, st>>>(
-        ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, nullptr, field_out, nullptr, p->tw_img);
+        ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, nullptr, field_out, nullptr, p->tw_img,
+        field_pp());
   } else {
     CU(launch_pdl(field_kernel<K, kFieldRB, G, false>, grid, dim3(block), smem, st, ghat,
                   (const double*)p->pw, (const double*)p->scales, (const double2*)p->twst,
                   (long long)r0, (long long)r1, (long long)p->m0, cand, (double2*)nullptr, state,
-                  (const double2*)p->tw_img));
+                  (const double2*)p->tw_img, field_pp()));
   }
   p->launches++;
   CU(cudaGetLastError());
@@ -1215,6 +1226,14 @@ int afd_fp64_peak(int device, double* tflops, void* stream) {
 // Debug builds only: globaltimer stamps of step_cluster_kernel phases.
 extern "C" int afd_debug_step_stamps(unsigned long long* host_out) {
   CU(cudaMemcpyFromSymbol(host_out, afd::g_step_stamps, sizeof(afd::g_step_stamps)));
+  return 0;
+}
+#endif
+
+#ifdef AFD_FIELD_TIMING
+// Debug builds only: clock64 stamps of field_kernel row phases.
+extern "C" int afd_debug_field_stamps(long long* host_out) {
+  CU(cudaMemcpyFromSymbol(host_out, afd::g_field_stamps, sizeof(afd::g_field_stamps)));
   return 0;
 }
 #endif

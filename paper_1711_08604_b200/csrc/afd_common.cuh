@@ -96,6 +96,31 @@ __device__ __forceinline__ double2 one_minus_conja_z(double2 a, double2 z) {
   return make_double2(1.0 - p.x, 0.0 - p.y);
 }
 
+// Opaque register copy: the compiler can neither fold the value nor
+// rematerialise it from the constant bank later.  Kernels copy the
+// parameters they need after griddepcontrol.wait through opq() before the
+// wait: constant-bank reads issued after the wait were measured to cost up
+// to ~0.7 us each on the critical path of the per-step kernel.
+__device__ __forceinline__ int opq(int v) {
+  int r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ long long opq(long long v) {
+  long long r;
+  asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ double opq(double v) {
+  double r;
+  asm volatile("mov.b64 %0, %1;" : "=d"(r) : "d"(v));
+  return r;
+}
+template <class T>
+__device__ __forceinline__ T* opq(T* p) {
+  return reinterpret_cast<T*>(opq(reinterpret_cast<long long>(p)));
+}
+
 // Programmatic dependent launch (PDL): kernels launched with programmatic
 // stream serialization may start while their predecessor drains; everything
 // before pdl_wait() must not read the predecessor's outputs.  Both are
@@ -142,11 +167,13 @@ __device__ __forceinline__ Cand warp_argmax(Cand c) {
 // accumulators, combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), halves added
 // left + right.  `scratch` needs max(n/16, 8) doubles.
 template <class Idx>
-__device__ double pairwise_sum_block(const double* buf, int n, double* scratch, Idx SW) {
+__device__ double pairwise_sum_block(const double* buf, int n, double* scratch, Idx SW,
+                                     int nthreads = -1) {
+  const int nt = nthreads > 0 ? nthreads : (int)blockDim.x;
   const int nblk = n >= 128 ? n / 128 : 1;
   const int bl = n >= 128 ? 128 : n;
   // phase 1: accumulator k of block b sums elements b*bl + k + 8 i
-  for (int a = threadIdx.x; a < nblk * 8; a += blockDim.x) {
+  for (int a = threadIdx.x; a < nblk * 8; a += nt) {
     const int b = a >> 3, k = a & 7;
     const int base = b * bl;
     double r = buf[SW(base + k)];
@@ -156,14 +183,14 @@ __device__ double pairwise_sum_block(const double* buf, int n, double* scratch, 
   __syncthreads();
   // phase 2: per block ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))
   double* sums = scratch + nblk * 8;
-  for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+  for (int b = threadIdx.x; b < nblk; b += nt) {
     const double* r = scratch + b * 8;
     sums[b] = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
   }
   __syncthreads();
   // phase 3: binary tree over blocks, left + right
   for (int w = nblk; w > 1; w >>= 1) {
-    for (int b = threadIdx.x; b < w / 2; b += blockDim.x) sums[b] = sums[2 * b] + sums[2 * b + 1];
+    for (int b = threadIdx.x; b < w / 2; b += nt) sums[b] = sums[2 * b] + sums[2 * b + 1];
     __syncthreads();
   }
   const double res = sums[0];
@@ -176,10 +203,12 @@ __device__ double pairwise_sum_block(const double* buf, int n, double* scratch, 
 // complex accumulators, rr = (r0+r2)+(r4+r6), ri = (r1+r3)+(r5+r7).
 // `scratch` needs max(n/8, 8) * 2 doubles.
 template <class Idx>
-__device__ double2 cpairwise_sum_block(const double2* buf, int n, double* scratch, Idx SW) {
+__device__ double2 cpairwise_sum_block(const double2* buf, int n, double* scratch, Idx SW,
+                                       int nthreads = -1) {
+  const int nt = nthreads > 0 ? nthreads : (int)blockDim.x;
   const int nblk = n >= 64 ? n / 64 : 1;
   const int bl = n >= 64 ? 64 : n;
-  for (int a = threadIdx.x; a < nblk * 4; a += blockDim.x) {
+  for (int a = threadIdx.x; a < nblk * 4; a += nt) {
     const int b = a >> 2, q = a & 3;
     const int base = b * bl;
     double2 v = buf[SW(base + q)];
@@ -194,14 +223,14 @@ __device__ double2 cpairwise_sum_block(const double2* buf, int n, double* scratc
   }
   __syncthreads();
   double* sums = scratch + nblk * 8;
-  for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+  for (int b = threadIdx.x; b < nblk; b += nt) {
     const double* r = scratch + b * 8;
     sums[2 * b] = (r[0] + r[2]) + (r[4] + r[6]);
     sums[2 * b + 1] = (r[1] + r[3]) + (r[5] + r[7]);
   }
   __syncthreads();
   for (int w = nblk; w > 1; w >>= 1) {
-    for (int b = threadIdx.x; b < w / 2; b += blockDim.x) {
+    for (int b = threadIdx.x; b < w / 2; b += nt) {
       sums[2 * b] = sums[4 * b] + sums[4 * b + 2];
       sums[2 * b + 1] = sums[4 * b + 1] + sums[4 * b + 3];
     }

@@ -238,18 +238,32 @@ struct GroupSync {
   }
 };
 
-template <int K, bool INV, int RB = 4, int PASS = 0, class Tw, class Sync = BlockSync>
+// Optional per-pass hook: before(PASS) / after(PASS) around a pass's
+// butterflies, exch(PASS) after the exchange that follows it (timing
+// probes, inter-group scheduling).
+struct NoHook {
+  __device__ __forceinline__ void before(int) const {}
+  __device__ __forceinline__ void after(int) const {}
+  __device__ __forceinline__ void exch(int) const {}
+};
+
+template <int K, bool INV, int RB = 4, int PASS = 0, class Tw, class Sync = BlockSync,
+          class Hook = NoHook>
 __device__ __forceinline__ void fft_passes(double2 (&v)[Geo<K, RB>::P], int tp, bool active,
-                                           double2* sm, const Tw& tw, Sync sync = Sync()) {
+                                           double2* sm, const Tw& tw, Sync sync = Sync(),
+                                           const Hook& hook = Hook()) {
   using G = Geo<K, RB>;
   const int t = PASS == 0 ? brev_bits(tp, G::TB) : tp;
+  hook.before(PASS);
   if (active) fft_pass<K, RB, PASS, INV>(v, t, tw);
+  hook.after(PASS);
   if constexpr (PASS + 1 < G::NPASS) {
     if (active) pass_store<K, RB, PASS>(v, t, sm);
     sync();
     if (active) pass_load<K, RB, PASS + 1>(v, tp, sm);
     sync();
-    fft_passes<K, INV, RB, PASS + 1>(v, tp, active, sm, tw, sync);
+    hook.exch(PASS);
+    fft_passes<K, INV, RB, PASS + 1>(v, tp, active, sm, tw, sync, hook);
   }
 }
 

@@ -45,6 +45,47 @@ struct Step {
 
 enum : int { kStepPowAmbiguous = 1 };
 
+#ifdef AFD_FIELD_TIMING
+// clock64 stamps of each row-group leader: [cta][group][row][slot]
+//   0 start, 1 after the PDL wait, per row: 2 prologue done, 3/5/7 pass
+//   ends, 4/6 exchange ends, 14 epilogue done; 15 = SM id (row 0 only)
+__device__ long long g_field_stamps[512][2][4][16];
+#define FSTAMP(r, i)                                                                      \
+  do {                                                                                    \
+    if (tp == 0 && blockIdx.x < 512 && g < 2 && (r) < 4) g_field_stamps[blockIdx.x][g][r][i] = \
+        clock64();                                                                        \
+  } while (0)
+#else
+#define FSTAMP(r, i) \
+  do {               \
+  } while (0)
+#endif
+
+// Phase offset between the two row-groups of a field CTA.  The butterfly
+// passes are FP64-bound and the exchanges / prologue / epilogue shared-memory
+// or L1 bound; started together the groups run in lock step and the FP64
+// pipe idles through every exchange.  Group 1 therefore starts its first
+// pass only when group 0 has finished its own first pass (named barrier 3:
+// group 0 arrives, group 1 syncs), after which the groups run free, one
+// phase apart (AFD_FIELD_PP=0 disables it; measured 8.8e10 -> 9.3e10 c1).
+struct FieldHook {
+  bool arrive;     // group 0, first row: release group 1 after pass 0
+  int count;       // threads of both groups
+  long long* st;   // timing stamps of this row (timing builds) or null
+  __device__ __forceinline__ void before(int) const {}
+  __device__ __forceinline__ void after(int pass) const {
+    if (pass == 0 && arrive) asm volatile("bar.arrive 3, %0;" ::"r"(count) : "memory");
+#ifdef AFD_FIELD_TIMING
+    if (st) st[3 + 2 * pass] = clock64();
+#endif
+  }
+  __device__ __forceinline__ void exch(int pass) const {
+#ifdef AFD_FIELD_TIMING
+    if (st) st[4 + 2 * pass] = clock64();
+#endif
+  }
+};
+
 // ---------------------------------------------------------------------------
 // Field + argmax (or materialised field).  Block = G row-groups of T threads;
 // each group evaluates one radius row per round; rows are strided over the
@@ -61,7 +102,8 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
              Cand* __restrict__ cand_out,          // [batch][gridDim.x]
              double2* __restrict__ field_out,      // [row1-row0][N] (MATERIALIZE)
              const State* __restrict__ state,      // per-signal stop flags or null
-             const double2* __restrict__ tw_img) { // SmemTw<K,RB> image (one bulk copy)
+             const double2* __restrict__ tw_img,   // SmemTw<K,RB> image (one bulk copy)
+             int pp) {                             // 1: offset the row-groups (FieldHook)
   using Gm = Geo<K, RB>;
   constexpr int N = Gm::N, T = Gm::T, P = Gm::P;
   extern __shared__ double2 smem[];
@@ -70,6 +112,14 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   const int tp = threadIdx.x % T;
   const int Gr = blockDim.x / T;  // row-groups actually launched (<= G)
   using TwT = SmemTw<K, RB>;
+  FSTAMP(0, 0);
+#ifdef AFD_FIELD_TIMING
+  if (tp == 0 && blockIdx.x < 512 && g < 2) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_field_stamps[blockIdx.x][g][0][15] = smid;
+  }
+#endif
   // Twiddle image: one TMA bulk copy (issued by thread 0, completes on an
   // mbarrier) overlapping the first row's prologue loads.
   __shared__ unsigned long long tw_bar;
@@ -112,6 +162,9 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   const long long rounds =
       kGroupSync ? (rows - ((long long)blockIdx.x * Gr + g) + per_round - 1) / per_round
                  : (rows + per_round - 1) / per_round;
+  // phase offset of group 1 (FieldHook): only when both groups have rows
+  const bool offset = kGroupSync && Gr == 2 && pp > 0 &&
+                      (long long)blockIdx.x * Gr + 1 < rows;
   // First row: its r^l values are step-independent and are loaded before the
   // PDL wait; the spectrum and the stop flags come from the previous kernel.
   double2 v[P];
@@ -125,18 +178,23 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
       for (int i = 0; i < P; ++i) pv[i] = __ldg(pr + Gm::l0(tp, i));
     }
     pdl_wait();
-    if (state != nullptr && state[sig].stopped) {
-      mbar_wait(&tw_bar, 0);  // no bulk copy may target an exited CTA
-      return;
-    }
-    pdl_trigger();
+    // the stop flag's load overlaps the spectrum loads (both are L2 round
+    // trips on the critical path); the flag is tested once v is formed
+    const int stopped = state != nullptr ? *(volatile const int*)&state[sig].stopped : 0;
     if (act0) {
 #pragma unroll
       for (int i = 0; i < P; ++i) {
         const double2 c = __ldg(gh + Gm::l0(tp, i));
         v[i] = make_double2(pv[i] * c.x, pv[i] * c.y);  // transform.py:198
+        asm volatile("" ::"d"(v[i].x), "d"(v[i].y));  // formed before the test
       }
     }
+    if (stopped) {
+      mbar_wait(&tw_bar, 0);  // no bulk copy may target an exited CTA
+      return;
+    }
+    pdl_trigger();
+    FSTAMP(0, 1);
   }
   for (long long rd = 0; rd < rounds; ++rd) {
     const long long s = row0 + rd * per_round + (long long)blockIdx.x * Gr + g;
@@ -156,8 +214,15 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
       mbar_wait(&tw_bar, 0);
       tw_ready = true;
     }
+    FSTAMP(rd, 2);
     if constexpr (kGroupSync) {
-      fft_passes<K, true, RB>(v, tp, active, sm, tw, GroupSync{1 + g, T});
+      long long* st = nullptr;
+#ifdef AFD_FIELD_TIMING
+      if (tp == 0 && blockIdx.x < 512 && g < 2 && rd < 4) st = &g_field_stamps[blockIdx.x][g][rd][0];
+#endif
+      if (offset && rd == 0 && g == 1) asm volatile("bar.sync 3, %0;" ::"r"(2 * T) : "memory");
+      const FieldHook hook{offset && rd == 0 && g == 0, 2 * T, st};
+      fft_passes<K, true, RB>(v, tp, active, sm, tw, GroupSync{1 + g, T}, hook);
     } else {
       fft_passes<K, true, RB>(v, tp, active, sm, tw);
     }
@@ -181,6 +246,7 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
         }
       }
     }
+    FSTAMP(rd, 14);
   }
   if (MATERIALIZE) return;
   __syncthreads();  // all groups done before the block-wide reduction

@@ -34,12 +34,14 @@ __host__ __device__ constexpr int cluster_ctas(int K) { return K >= 11 ? 16 : 8;
 
 #ifdef AFD_STEP_TIMING
 __device__ unsigned long long g_step_stamps[64][16];
+// stamp row of this step, resolved once (opaque register) so that a stamp
+// never waits on a constant-bank load
 #define STAMP(i)                                                                       \
   do {                                                                                 \
-    if (threadIdx.x == 0 && blockIdx.x == 0 && k >= 0 && k < 64) {                     \
+    if (stamp_row != nullptr) {                                                        \
       unsigned long long t_;                                                           \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                           \
-      g_step_stamps[k][i] = t_;                                                        \
+      stamp_row[i] = t_;                                                               \
     }                                                                                  \
   } while (0)
 #else
@@ -55,13 +57,17 @@ struct ClusterGeo {
   static constexpr int N = 1 << K;
   static constexpr int NC = N / C;                  // samples / positions per CTA
   static constexpr int KL = K - CB;                 // bits of the CTA-local transform
-  static constexpr int RB = 3;                      // local pass register bits
+  static constexpr int RB = 2;                      // local pass register bits
   using GL = Geo<KL, RB>;                           // local transform geometry
   static constexpr int LOCAL_THREADS = GL::T;       // threads of the local transform
   static constexpr int GROUPS = NC / C;             // radix-C groups per CTA in phase 2
+  static constexpr int H = C / 4;                   // phase-2 threads per group (4 points each)
+  static constexpr int LH = H == 4 ? 2 : 1;         // log2 H
+  static constexpr int P2_THREADS = GROUPS * H;     // = NC / 4
   static constexpr int THREADS = 256;
   static_assert(NC >= 128, "slice must be a pairwise-sum tree node");
-  static_assert(LOCAL_THREADS <= THREADS && GROUPS <= THREADS, "block too small");
+  static_assert(LOCAL_THREADS < THREADS && P2_THREADS <= THREADS, "block too small");
+  static_assert(P2_THREADS % 32 == 0, "phase-2 groups must not straddle warps");
 };
 
 template <int K>
@@ -72,10 +78,11 @@ struct ClusterSmem {
   static constexpr size_t mag = part + sizeof(double2) * CG::GL::SMEM; // NC double
   static constexpr size_t twl = mag + sizeof(double) * CG::NC;         // NC-1 double2
   static constexpr size_t scratch = twl + sizeof(double2) * (CG::NC - 1);  // 2*(NC/8+16)
-  static constexpr size_t zsl = scratch + sizeof(double) * 2 * (CG::NC / 8 + 16);  // NC double2
-  static constexpr size_t rad = zsl + sizeof(double2) * CG::NC;  // up to kRadSmem radii
+  static constexpr size_t circ = scratch + sizeof(double) * 2 * (CG::NC / 8 + 16);  // N double2
+  static constexpr size_t rad = circ + sizeof(double2) * CG::N;  // up to kRadSmem radii
   static constexpr int kRadSmem = 4096;
   static constexpr size_t bytes = rad + sizeof(double) * kRadSmem;
+  static_assert(circ % 16 == 0, "bulk-copy destination must be 16-byte aligned");
 };
 
 // left+right binary tree over C values (numpy pairwise halves)
@@ -107,6 +114,19 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   using L = ClusterSmem<K>;
   using GL = typename CG::GL;
   constexpr int N = CG::N, NC = CG::NC, C = CG::C, CB = CG::CB;
+  // parameters used after the PDL wait live in registers (see opq)
+  k = opq(k);
+  max_terms = opq(max_terms);
+  threshold = opq(threshold);
+  dc_first = opq(dc_first);
+  ncand = opq(ncand);
+  nrad = opq(nrad);
+  cand = opq(cand);
+  radii = opq(radii);
+  steps = opq(steps);
+  state = opq(state);
+  rem = opq(rem);
+  ghat = opq(ghat);
   cg::cluster_group cluster = cg::this_cluster();
   const int c = (int)cluster.block_rank();
   const int sig = blockIdx.x / C;
@@ -116,7 +136,7 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   double* mag = reinterpret_cast<double*>(smraw + L::mag);
   double2* twl = reinterpret_cast<double2*>(smraw + L::twl);
   double* scratch = reinterpret_cast<double*>(smraw + L::scratch);
-  double2* zsl = reinterpret_cast<double2*>(smraw + L::zsl);  // this CTA's circle slice
+  double2* circ = reinterpret_cast<double2*>(smraw + L::circ);  // z_m, all N
   double* rad = reinterpret_cast<double*>(smraw + L::rad);    // radii (if <= kRadSmem)
   __shared__ double s_node[2];   // this CTA's pairwise-tree node sums
   __shared__ Cand red[32];
@@ -125,61 +145,104 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   double2* __restrict__ gh = ghat + (size_t)sig * N;
   const int tid = threadIdx.x;
   const int m0 = c * NC;
+#ifdef AFD_STEP_TIMING
+  unsigned long long* stamp_row = nullptr;
+  if (threadIdx.x == 0 && blockIdx.x == 0 && k >= 0 && k < 64) {
+    unsigned long long* p_ = &g_step_stamps[k][0];
+    asm volatile("mov.b64 %0, %1;" : "=l"(stamp_row) : "l"(p_));
+  }
+#endif
   STAMP(0);
 
-  // local stage tables S_0..S_{K-4} (== twst[0 .. 2^(K-3)-1))
-  for (int i = tid; i < NC - 1; i += blockDim.x) twl[i] = __ldg(twst + i);
-  // phase-2 twiddles of this thread, prefetched: stage b = K-CB+e uses
-  // w[(q + NC*(u mod 2^e)) << (CB-1-e)], q = c*GROUPS + tid
-  const int q = c * CG::GROUPS + tid;
-  double2 w2[C - 1];
-  if (tid < CG::GROUPS) {
-    const double2* half = twst + (N / 2) - 1;  // S_{K-1}[k] = w[k]
-#pragma unroll
-    for (int e = 0; e < CB; ++e)
-#pragma unroll
-      for (int h = 0; h < (1 << e); ++h)
-        w2[(1 << e) - 1 + h] = __ldg(half + ((q + NC * h) << (CB - 1 - e)));
+  // The whole circle z_m (step-independent) lands in shared memory by bulk
+  // copy: the pole lookup circle[j] and this CTA's update slice read it there.
+  __shared__ unsigned long long circ_bar;
+  if (tid == 0) {
+    mbar_init(&circ_bar, 1);
+    const unsigned m = (unsigned)__cvta_generic_to_shared(&circ_bar);
+    constexpr unsigned bytes = sizeof(double2) * N;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(m), "r"(bytes)
+                 : "memory");
+    constexpr unsigned chunk = 32768;
+    for (unsigned off = 0; off < bytes; off += chunk) {
+      const unsigned nb = bytes - off < chunk ? bytes - off : chunk;
+      const unsigned d = (unsigned)__cvta_generic_to_shared((char*)circ + off);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          ::"r"(d), "l"((const char*)circle + off), "r"(nb), "r"(m)
+          : "memory");
+    }
   }
-  // the tables above are step-independent; candidates, state and the
-  // remainder come from the previous kernels (PDL)
-  // This CTA's slice of the circle (static) and of the remainder: G_k was
-  // written by the previous step kernel, which completed before our PDL
-  // predecessor (the field kernel) passed its own pdl_wait and triggered
-  // us, so it is final here.
+  // local stage tables S_0..S_{K-CB-1} (== twst[0 .. NC-1))
+  for (int i = tid; i < NC - 1; i += CG::THREADS) twl[i] = __ldg(twst + i);
+  // Phase-2 twiddles of this thread (radix-C group q, sub-thread h; stage
+  // b = K-CB+e uses w[(q + NC*(u mod 2^e)) << (CB-1-e)]), prefetched:
+  //   layout A (u = 4h + i, e = 0, 1): u mod 2^e = i mod 2^e
+  //   layout B (u = h + H i, e >= 2): u mod 2^e = h + H (i mod 2^(e-LH))
+  constexpr int H = CG::H, LH = CG::LH;
+  const int gq = tid / H, hh = tid % H;
+  const int q = c * CG::GROUPS + gq;
+  double2 wa[3], wb[4];
+  if (tid < CG::P2_THREADS) {
+    const double2* half = twst + (N / 2) - 1;  // S_{K-1}[k] = w[k]
+    wa[0] = __ldg(half + (q << (CB - 1)));
+    wa[1] = __ldg(half + (q << (CB - 2)));
+    wa[2] = __ldg(half + ((q + NC) << (CB - 2)));
+#pragma unroll
+    for (int e = 2; e < CB; ++e)
+#pragma unroll
+      for (int mm = 0; mm < (1 << (e - LH)); ++mm)
+        wb[(1 << (e - LH)) - 1 + mm] = __ldg(half + ((q + NC * (hh + H * mm)) << (CB - 1 - e)));
+  }
+  // this CTA's slice of the remainder: G_k was written by the previous step
+  // kernel, which completed before our PDL predecessor (the field kernel)
+  // passed its own pdl_wait and triggered us, so it is final here (except
+  // for the dc_first step 0, loaded after the wait)
   constexpr int PER = (NC + CG::THREADS - 1) / CG::THREADS;
-  double2 zs[PER], gs[PER];
+  double2 gs[PER];
 #pragma unroll
   for (int u = 0; u < PER; ++u) {
     const int i = tid + u * CG::THREADS;
-    if (i < NC) {
-      zs[u] = circle[m0 + i];
-      zsl[i] = zs[u];
-      gs[u] = k >= 0 ? r[m0 + i] : g0[(size_t)sig * N + m0 + i];
-    }
+    if (i < NC && !(k == 0 && dc_first)) gs[u] = k >= 0 ? r[m0 + i] : g0[(size_t)sig * N + m0 + i];
   }
   // radii for grid.point: staged in shared memory when they fit
   const bool rad_smem = nrad <= L::kRadSmem;
   if (rad_smem)
-    for (int i = tid; i < nrad; i += blockDim.x) rad[i] = radii[i];
-  // publish the circle slices cluster-wide (waited on before the lookup)
-  asm volatile("barrier.cluster.arrive.release;" ::: "memory");
+    for (int i = tid; i < nrad; i += CG::THREADS) rad[i] = radii[i];
+  __syncthreads();  // rad / twl / barrier init visible
   STAMP(1);
+
   pdl_wait();
   STAMP(2);
-  if (k >= 0 && st.stopped) return;  // cluster-uniform
-  pdl_trigger();
+  if (k == 0 && dc_first) {
+    // this kernel's PDL predecessor is the init step kernel itself (no field
+    // launch in between), so G_0 is only final after the wait
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int i = tid + u * CG::THREADS;
+      if (i < NC) gs[u] = r[m0 + i];
+    }
+  }
+  // the stop flag's load overlaps the candidate loads below; it is tested
+  // once the candidates are in (cluster-uniform)
+  const int stopped = k >= 0 ? *(volatile const int*)&st.stopped : 0;
 
   // ---- select ---------------------------------------------------------------
   long long s = 0, j = 0;
   double radius = 0.0;
   double2 a = make_double2(0.0, 0.0), coeff = make_double2(0.0, 0.0);
+  if (!(k >= 0 && !(k == 0 && dc_first))) {  // select-free paths
+    if (stopped) {
+      mbar_wait(&circ_bar, 0);
+      return;
+    }
+    pdl_trigger();
+  }
   if (k == 0 && dc_first) {
-    asm volatile("barrier.cluster.wait.acquire;" ::: "memory");  // close the split barrier
     // core.py:373-375: coeff = complex(np.mean(remainder)), pairwise over N
-    for (int i = tid; i < NC; i += blockDim.x) slice[i] = r[m0 + i];
+    for (int i = tid; i < NC; i += CG::THREADS) slice[i] = r[m0 + i];
     __syncthreads();
-    const double2 node = cpairwise_sum_block(slice, NC, scratch, PlainIdx());
+    const double2 node = cpairwise_sum_block(slice, NC, scratch, PlainIdx(), CG::THREADS);
     if (tid == 0) {
       s_node[0] = node.x;
       s_node[1] = node.y;
@@ -196,41 +259,56 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
     coeff = np_cdiv(sum, make_double2((double)N, 0.0));
     cluster.sync();  // everyone has read s_node before it is reused
   } else if (k >= 0) {
+    // every warp reduces all candidates itself (first maximum): no block
+    // barrier on the critical path
     Cand b;
     b.mag = -1.0;
     b.flat = 0x7fffffffffffffffLL;
     b.re = b.im = 0.0;
-    for (int i = tid; i < ncand; i += blockDim.x) cand_merge(b, cand[(size_t)sig * ncand + i]);
-    b = warp_argmax(b);
-    const int lane = tid & 31, wid = tid >> 5;
-    if (lane == 0) red[wid] = b;
-    __syncthreads();
-    if (wid == 0) {
-      Cand cc = lane < (int)(blockDim.x >> 5) ? red[lane] : b;
-      cc = warp_argmax(cc);
-      if (lane == 0) red[0] = cc;
+    const int lane = tid & 31;
+    for (int i = lane; i < ncand; i += 32) {
+      const Cand* cp = cand + (size_t)sig * ncand + i;
+      Cand x;
+      const double2 lo = __ldcg(reinterpret_cast<const double2*>(cp));
+      const double2 hi = __ldcg(reinterpret_cast<const double2*>(cp) + 1);
+      x.mag = lo.x;
+      x.flat = __double_as_longlong(lo.y);
+      x.re = hi.x;
+      x.im = hi.y;
+      cand_merge(b, x);
     }
-    __syncthreads();
-    b = red[0];
+    if (stopped) {
+      mbar_wait(&circ_bar, 0);  // no bulk copy may target an exited CTA
+      return;
+    }
+    pdl_trigger();
+    b = warp_argmax(b);
+    b.mag = __shfl_sync(0xffffffffu, b.mag, 0);
+    b.flat = __shfl_sync(0xffffffffu, b.flat, 0);
+    b.re = __shfl_sync(0xffffffffu, b.re, 0);
+    b.im = __shfl_sync(0xffffffffu, b.im, 0);
+    STAMP(13);
     s = b.flat / N;
     j = b.flat % N;
     radius = rad_smem ? rad[s] : radii[s];
-    asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
-    const double2 zj = cluster.map_shared_rank(zsl, (int)(j / NC))[j % NC];  // circle[j]
+    mbar_wait(&circ_bar, 0);
+    const double2 zj = circ[j];
     a = make_double2(radius * zj.x, radius * zj.y);  // grid.point, core.py:163-167
     coeff = make_double2(b.re, b.im);
+    STAMP(14);
   }
-  if (k < 0) asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
+  mbar_wait(&circ_bar, 0);  // (no-op when already passed) circle slice for the update
 
   STAMP(3);
   // ---- update this CTA's slice (or copy g0 at init) --------------------------
   int amb = 0;
+  double2 rout[PER];  // new remainder slice, stored after the first cluster barrier
   if (k < 0) {
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
       const int i = tid + u * CG::THREADS;
       if (i < NC) {
-        r[m0 + i] = gs[u];
+        rout[u] = gs[u];
         slice[i] = gs[u];
         mag[i] = np_mag2(gs[u]);
       }
@@ -238,11 +316,12 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   } else {
     const double kn = kernel_norm(a, &amb);
     const double2 sc = make_double2(kn, 0.0);
+    STAMP(15);
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
       const int i = tid + u * CG::THREADS;
       if (i < NC) {
-        const double2 z = zs[u];
+        const double2 z = circ[m0 + i];
         const double2 d = one_minus_conja_z(a, z);
         const double2 e = np_cdiv(sc, d);
         const double2 ce = np_cmul(coeff, e);  // N <= 8192: no numpy elision
@@ -250,7 +329,7 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
         const double2 stp = make_double2(g.x - ce.x, g.y - ce.y);
         const double2 num = np_cmul(stp, d);
         const double2 out = np_cdiv(num, make_double2(z.x - a.x, z.y - a.y));
-        r[m0 + i] = out;
+        rout[u] = out;
         slice[i] = out;
         mag[i] = np_mag2(out);
       }
@@ -258,11 +337,18 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   }
   __syncthreads();
   STAMP(4);
-  const double node = pairwise_sum_block(mag, NC, scratch, PlainIdx());
+  const double node = pairwise_sum_block(mag, NC, scratch, PlainIdx(), CG::THREADS);
   if (tid == 0) s_node[0] = node;
   STAMP(5);
   cluster.sync();  // slices and node sums visible cluster-wide
   STAMP(6);
+  // G_{k+1} to global memory only now: a store pending at a cluster barrier
+  // (release = MEMBAR.GPU) would hold the barrier for an L2 round trip
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int i = tid + u * CG::THREADS;
+    if (i < NC) r[m0 + i] = rout[u];
+  }
   // The forward transform does not need the energy: warp(s) 0.. run the
   // CTA-local DIT on a named barrier while the last warp combines the
   // energy tree, writes the step record and evaluates the stop rules.
@@ -334,26 +420,39 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   STAMP(10);
 
   // ---- stages K-CB..K-1: radix-C over the top CB position bits ----------------
-  if (tid < CG::GROUPS) {
-    double2 v[C];
+  // Group q (positions q + NC*u, u < C) is held by H threads, 4 points each:
+  // stages e = 0, 1 in layout A (thread h holds u = 4h + i), then a 4x4
+  // transpose through shared memory (the group's H threads share a warp),
+  // then stages e >= 2 in layout B (u = h + H i).
+  if (tid < CG::P2_THREADS) {
+    double2 v[4];
 #pragma unroll
-    for (int u = 0; u < C; ++u) v[u] = cluster.map_shared_rank(part, u)[GL::sw(q)];
+    for (int i = 0; i < 4; ++i) v[i] = cluster.map_shared_rank(part, 4 * hh + i)[GL::sw(q)];
     // my remote reads are done: let the other CTAs go (split cluster barrier)
     asm volatile("barrier.cluster.arrive.release;" ::: "memory");
+    bfly(v[0], v[1], wa[0]);  // e = 0
+    bfly(v[2], v[3], wa[0]);
+    bfly(v[0], v[2], wa[1]);  // e = 1: u mod 2 = i mod 2
+    bfly(v[1], v[3], wa[2]);
+    double2* x = slice + gq * C;  // slice is free after the cluster barrier
 #pragma unroll
-    for (int e = 0; e < CB; ++e) {
+    for (int i = 0; i < 4; ++i) x[4 * hh + i] = v[i];
+    __syncwarp();
 #pragma unroll
-      for (int h = 0; h < (1 << e); ++h) {
-        const double2 w = w2[(1 << e) - 1 + h];
+    for (int i = 0; i < 4; ++i) v[i] = x[hh + H * i];
 #pragma unroll
-        for (int g = 0; g < (C >> (e + 1)); ++g) {
-          const int i = h | (g << (e + 1));
-          bfly(v[i], v[i | (1 << e)], w);
-        }
+    for (int e = 2; e < CB; ++e) {
+      const int ib = e - LH;  // bit of i paired by stage e
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (i & (1 << ib)) continue;
+        const double2 w = wb[(1 << ib) - 1 + (i & ((1 << ib) - 1))];
+        bfly(v[i], v[i | (1 << ib)], w);
       }
     }
 #pragma unroll
-    for (int u = 0; u < C; ++u) gh[q + NC * u] = v[u];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) gh[q + NC * (hh + H * i)] = v[i];
   } else {
     asm volatile("barrier.cluster.arrive.release;" ::: "memory");
   }

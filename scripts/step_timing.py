@@ -29,5 +29,8 @@ d = np.diff(rows[:, :13], axis=1)
 print("phase (ns, median over steps 1..28):")
 for i in range(12):
     print("  %-12s -> %-12s %8.0f" % (names[i], names[i + 1], np.median(d[:, i])))
+print("  select: pdl_wait -> cands reduced %.0f, -> a formed %.0f; update: -> kernel_norm %.0f" % (
+    np.median(rows[:, 13] - rows[:, 2]), np.median(rows[:, 14] - rows[:, 2]),
+    np.median(rows[:, 15] - rows[:, 3])))
 print("  total %.0f ns; gap step k start -> step k+1 start %.0f ns" %
       (np.median(rows[:, 12] - rows[:, 0]), np.median(np.diff(rows[:, 0]))))
