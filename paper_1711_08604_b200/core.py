@@ -311,16 +311,13 @@ def _build(grid, n, engine, rec, count, initial, remainder):
     c = (rec["c_re"] + 1j * rec["c_im"]).tolist()
     res = rec["residual"].tolist()
     new, sa = object.__new__, object.__setattr__
+    P, S = ParameterPoint, DecompositionStep
     steps = []
     for k in range(count):
-        pt = new(ParameterPoint)
-        sa(pt, "radius", radius[k])
-        sa(pt, "angle_index", j[k])
-        sa(pt, "value", a[k])
-        st = new(DecompositionStep)
-        sa(st, "point", pt)
-        sa(st, "coefficient", c[k])
-        sa(st, "residual_energy", res[k])
+        pt = new(P)
+        sa(pt, "__dict__", {"radius": radius[k], "angle_index": j[k], "value": a[k]})
+        st = new(S)
+        sa(st, "__dict__", {"point": pt, "coefficient": c[k], "residual_energy": res[k]})
         steps.append(st)
     return Decomposition(tuple(steps), grid, n, float(initial), engine, remainder=remainder,
                          step_flags=tuple(rec["flags"].tolist()))

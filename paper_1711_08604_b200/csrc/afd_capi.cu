@@ -1165,29 +1165,31 @@ int afd_time_field(afd_plan* p, const double* ghat, int64_t batch, int reps, dou
     *avg_ms = ms / reps;
     return 0;
   }
+  // back-to-back launches (PDL-chained, as inside a decomposition) between
+  // two events: the average launch duration in a stream of field launches
   const int ncta = field_ctas_for(p, p->m1 - p->m0, batch);
   if ((rc = ensure_cand(p, batch, ncta))) return rc;
-  std::vector<cudaEvent_t> ev(2 * (size_t)reps);
-  for (auto& e : ev) CU(cudaEventCreate(&e));
-  for (int r = 0; r < reps; ++r) {
-    CU(cudaEventRecord(ev[2 * r], st));
+  auto one = [&]() -> int {
     AFD_DISPATCH(p->K, {
-      if ((rc = launch_field<KK>(p, (const double2*)ghat, p->m0, p->m1, batch, p->cand, ncta,
-                                 nullptr, nullptr, st)))
-        return rc;
-      break;
+      return launch_field<KK>(p, (const double2*)ghat, p->m0, p->m1, batch, p->cand, ncta,
+                              nullptr, nullptr, st);
     });
-    CU(cudaEventRecord(ev[2 * r + 1], st));
-  }
-  CU(cudaEventSynchronize(ev.back()));
-  double tot = 0.0;
-  for (int r = 0; r < reps; ++r) {
-    float ms = 0.f;
-    CU(cudaEventElapsedTime(&ms, ev[2 * r], ev[2 * r + 1]));
-    tot += ms;
-  }
-  for (auto& e : ev) cudaEventDestroy(e);
-  *avg_ms = tot / reps;
+    return fail(AFD_E_UNSUPPORTED, "transform length");
+  };
+  if ((rc = one())) return rc;  // warm
+  cudaEvent_t e0, e1;
+  CU(cudaEventCreate(&e0));
+  CU(cudaEventCreate(&e1));
+  CU(cudaEventRecord(e0, st));
+  for (int r = 0; r < reps; ++r)
+    if ((rc = one())) return rc;
+  CU(cudaEventRecord(e1, st));
+  CU(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *avg_ms = ms / reps;
   return 0;
 }
 

@@ -180,7 +180,7 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     pdl_wait();
     // the stop flag's load overlaps the spectrum loads (both are L2 round
     // trips on the critical path); the flag is tested once v is formed
-    const int stopped = state != nullptr ? *(volatile const int*)&state[sig].stopped : 0;
+    const int stopped = state != nullptr ? __ldcg(&state[sig].stopped) : 0;
     if (act0) {
 #pragma unroll
       for (int i = 0; i < P; ++i) {

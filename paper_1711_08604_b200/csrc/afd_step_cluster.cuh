@@ -33,7 +33,7 @@ namespace cg = cooperative_groups;
 __host__ __device__ constexpr int cluster_ctas(int K) { return K >= 11 ? 16 : 8; }
 
 #ifdef AFD_STEP_TIMING
-__device__ unsigned long long g_step_stamps[64][16];
+__device__ unsigned long long g_step_stamps[64][24];
 // stamp row of this step, resolved once (opaque register) so that a stamp
 // never waits on a constant-bank load
 #define STAMP(i)                                                                       \
@@ -225,7 +225,7 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   }
   // the stop flag's load overlaps the candidate loads below; it is tested
   // once the candidates are in (cluster-uniform)
-  const int stopped = k >= 0 ? *(volatile const int*)&st.stopped : 0;
+  const int stopped = k >= 0 ? __ldcg(&st.stopped) : 0;
 
   // ---- select ---------------------------------------------------------------
   long long s = 0, j = 0;
@@ -277,11 +277,13 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
       x.im = hi.y;
       cand_merge(b, x);
     }
+    STAMP(16);
     if (stopped) {
       mbar_wait(&circ_bar, 0);  // no bulk copy may target an exited CTA
       return;
     }
     pdl_trigger();
+    STAMP(17);
     b = warp_argmax(b);
     b.mag = __shfl_sync(0xffffffffu, b.mag, 0);
     b.flat = __shfl_sync(0xffffffffu, b.flat, 0);

@@ -18,7 +18,7 @@ g = torch.from_numpy(W.signal_for("c1")[None, :]).cuda()
 for _ in range(3):
     plan.decompose(g, w.steps)
 torch.cuda.synchronize()
-out = np.zeros((64, 16), np.uint64)
+out = np.zeros((64, 24), np.uint64)
 lib = _capi.load()
 lib.afd_debug_step_stamps.argtypes = [C.c_void_p]
 assert lib.afd_debug_step_stamps(out.ctypes.data) == 0
@@ -32,5 +32,8 @@ for i in range(12):
 print("  select: pdl_wait -> cands reduced %.0f, -> a formed %.0f; update: -> kernel_norm %.0f" % (
     np.median(rows[:, 13] - rows[:, 2]), np.median(rows[:, 14] - rows[:, 2]),
     np.median(rows[:, 15] - rows[:, 3])))
+print("  select detail: wait -> cand loop done %.0f -> stop tested+trigger %.0f -> argmax %.0f" % (
+    np.median(rows[:, 16] - rows[:, 2]), np.median(rows[:, 17] - rows[:, 16]),
+    np.median(rows[:, 13] - rows[:, 17])))
 print("  total %.0f ns; gap step k start -> step k+1 start %.0f ns" %
       (np.median(rows[:, 12] - rows[:, 0]), np.median(np.diff(rows[:, 0]))))
