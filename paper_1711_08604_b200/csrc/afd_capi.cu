@@ -191,10 +191,28 @@ int row_block() {
   return Geo<K>::T < 64 ? 64 : Geo<K>::T;
 }
 
+// Field launches with two full row-groups at N = 4096 keep their twiddles in
+// TMEM (TmemTw, afd_fft.cuh); AFD_FIELD_TMEM=0 turns it off (experiments).
+template <int K>
+constexpr bool field_tmem_capable() {
+  return K == 12 && kFieldRB == 4 && groups_for<K>() == 2;
+}
+static bool field_tmem_enabled() {
+  static int v = [] {
+    const char* e = getenv("AFD_FIELD_TMEM");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 template <int K, bool MAT>
 int setup_field_kernel(int* occ) {
   auto kern = field_kernel<K, kFieldRB, groups_for<K>(), MAT>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem<K>()));
+  if constexpr (field_tmem_capable<K>()) {
+    CU(cudaFuncSetAttribute(field_kernel<K, kFieldRB, groups_for<K>(), MAT, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem<K>()));
+  }
   if (occ) CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, field_block<K>(), field_smem<K>()));
   return 0;
 }
@@ -278,14 +296,25 @@ int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64
   const int block = Geo<K, kFieldRB>::T * ge;
   const size_t smem = sizeof(double2) *
                       (Geo<K, kFieldRB>::SMEM * ge + SmemTw<K, kFieldRB>::ENTRIES);
+  // TMEM twiddles need the whole TMEM of the SM: only for one full-size CTA
+  // (both row-groups) per SM
+  const bool tm = field_tmem_capable<K>() && ge == G && field_tmem_enabled();
   if (field_out) {
-    field_kernel<K, kFieldRB, G, true><<<grid, block, smem, st>>>(
-        ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, nullptr, field_out, nullptr, p->tw_img,
-        field_pp());
+    if (tm) {
+      field_kernel<K, kFieldRB, G, true, field_tmem_capable<K>()><<<grid, block, smem, st>>>(
+          ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, nullptr, field_out, nullptr,
+          p->tw_img, field_pp());
+    } else {
+      field_kernel<K, kFieldRB, G, true><<<grid, block, smem, st>>>(
+          ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, nullptr, field_out, nullptr,
+          p->tw_img, field_pp());
+    }
   } else {
-    CU(launch_pdl(field_kernel<K, kFieldRB, G, false>, grid, dim3(block), smem, st, ghat,
-                  (const double*)p->pw, (const double*)p->scales, (const double2*)p->twst,
-                  (long long)r0, (long long)r1, (long long)p->m0, cand, (double2*)nullptr, state,
+    auto kern = tm ? field_kernel<K, kFieldRB, G, false, field_tmem_capable<K>()>
+                   : field_kernel<K, kFieldRB, G, false>;
+    CU(launch_pdl(kern, grid, dim3(block), smem, st, ghat, (const double*)p->pw,
+                  (const double*)p->scales, (const double2*)p->twst, (long long)r0,
+                  (long long)r1, (long long)p->m0, cand, (double2*)nullptr, state,
                   (const double2*)p->tw_img, field_pp()));
   }
   p->launches++;

@@ -202,6 +202,145 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[Geo<K, RB>::P], int t, con
   }
 }
 
+// ---------------------------------------------------------------------------
+// Twiddles in tensor memory (TMEM).  The field kernel's two row-groups
+// alternate FP64-bound passes with shared-memory exchanges; twiddles read
+// from shared memory queue behind the other group's exchange traffic (a
+// pass measured 1.1k cycles alone, 1.9k beside an exchange).  TMEM has its
+// own data path (tcgen05.ld), so each thread keeps its per-pass twiddles
+// there: 3 passes x 15 slots x 4 words (conjugated for the inverse), lane =
+// the thread's TMEM lane in its warp's quadrant, one column set per pair of
+// warps sharing a quadrant (the two row-groups share the sets).  Filled once
+// per CTA before the PDL wait.  Used for N = 4096 (RB = 4, 3 passes).
+// ---------------------------------------------------------------------------
+template <int NW>
+__device__ __forceinline__ void tm_ld(uint32_t taddr, uint32_t (&r)[NW]);
+template <>
+__device__ __forceinline__ void tm_ld<4>(uint32_t a, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a));
+}
+template <>
+__device__ __forceinline__ void tm_ld<8>(uint32_t a, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(a));
+}
+template <>
+__device__ __forceinline__ void tm_ld<16>(uint32_t a, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(a));
+}
+template <>
+__device__ __forceinline__ void tm_ld<32>(uint32_t a, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(a));
+}
+__device__ __forceinline__ void tm_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tm_st4(uint32_t a, double2 w) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+               "r"(__double2loint(w.x)), "r"(__double2hiint(w.x)), "r"(__double2loint(w.y)),
+               "r"(__double2hiint(w.y))
+               : "memory");
+}
+
+struct TmemTw {
+  static constexpr bool kTmem = true;
+  static constexpr int kSetCols = 180;  // 3 passes x 15 slots x 4 words
+  uint32_t base;  // warp-uniform: lane quadrant of this warp, column 0 of its set
+  __device__ __forceinline__ static uint32_t col(int pass, int slot) {
+    return (uint32_t)(pass * 60 + slot * 4);
+  }
+  // Fill this thread's lane (all threads of the warp call it, same slot).
+  template <int K, int RB, bool INV, class Src>
+  __device__ __forceinline__ void fill(int tp, const Src& src) const {
+    using G = Geo<K, RB>;
+    static_assert(G::NPASS <= 3 && G::RB == 4, "TMEM twiddle layout: <= 3 passes of 4 stages");
+#pragma unroll
+    for (int pass = 0; pass < G::NPASS; ++pass) {
+      const int c = G::c_of(pass);
+      const int t = pass == 0 ? brev_bits(tp, G::TB) : tp;
+      const int tlow = t & ((1 << c) - 1);
+      const int b0 = G::RB * pass;
+      const int b1 = (b0 + G::RB) < K ? (b0 + G::RB) : K;
+#pragma unroll
+      for (int b = b0; b < b1; ++b) {
+        if (b == 0) continue;
+        const int q = b - c;
+#pragma unroll
+        for (int kk = 0; kk < (1 << q); ++kk) {
+          double2 w = src(b, tlow | (kk << c));
+          if (INV) w.y = -w.y;  // np.conj(w), transform.py:132,199
+          tm_st4(base + col(pass, (1 << q) - 1 + kk), w);
+        }
+      }
+    }
+  }
+};
+
+template <class Tw>
+struct IsTmemTw {
+  static constexpr bool value = false;
+};
+template <>
+struct IsTmemTw<TmemTw> {
+  static constexpr bool value = true;
+};
+
+// fft_pass with per-stage twiddles from TMEM (already conjugated): one
+// tcgen05.ld of the stage's 2^q twiddles, then its butterflies.
+template <int K, int RB, int PASS, int B>
+__device__ __forceinline__ void fft_stage_tm(double2 (&v)[Geo<K, RB>::P], const TmemTw& tw) {
+  using G = Geo<K, RB>;
+  constexpr int c = G::c_of(PASS);
+  constexpr int q = B - c;
+  if constexpr (B == 0) {
+#pragma unroll
+    for (int h = 0; h < G::P / 2; ++h) bfly1(v[2 * h], v[2 * h + 1]);
+  } else {
+    uint32_t r[4 << q];
+    tm_ld<(4 << q)>(tw.base + TmemTw::col(PASS, (1 << q) - 1), r);
+    tm_wait_ld();
+#pragma unroll
+    for (int kk = 0; kk < (1 << q); ++kk) {
+      const double2 w = make_double2(__hiloint2double(r[4 * kk + 1], r[4 * kk]),
+                                     __hiloint2double(r[4 * kk + 3], r[4 * kk + 2]));
+#pragma unroll
+      for (int h = 0; h < (G::P >> (q + 1)); ++h) {
+        const int i = kk | (h << (q + 1));
+        bfly(v[i], v[i | (1 << q)], w);
+      }
+    }
+  }
+}
+
+template <int K, int RB, int PASS, int B = Geo<K, RB>::RB * PASS>
+__device__ __forceinline__ void fft_pass_tm(double2 (&v)[Geo<K, RB>::P], const TmemTw& tw) {
+  using G = Geo<K, RB>;
+  constexpr int b1 = (G::RB * PASS + G::RB) < K ? (G::RB * PASS + G::RB) : K;
+  if constexpr (B < b1) {
+    fft_stage_tm<K, RB, PASS, B>(v, tw);
+    fft_pass_tm<K, RB, PASS, B + 1>(v, tw);
+  }
+}
+
 // Store the registers of pass PASS to shared memory (swizzled positions).
 template <int K, int RB, int PASS>
 __device__ __forceinline__ void pass_store(const double2 (&v)[Geo<K, RB>::P], int t, double2* sm) {
@@ -255,7 +394,12 @@ __device__ __forceinline__ void fft_passes(double2 (&v)[Geo<K, RB>::P], int tp, 
   using G = Geo<K, RB>;
   const int t = PASS == 0 ? brev_bits(tp, G::TB) : tp;
   hook.before(PASS);
-  if (active) fft_pass<K, RB, PASS, INV>(v, t, tw);
+  if constexpr (IsTmemTw<Tw>::value) {
+    static_assert(INV, "TMEM twiddles are stored conjugated (inverse transform)");
+    if (active) fft_pass_tm<K, RB, PASS>(v, tw);
+  } else {
+    if (active) fft_pass<K, RB, PASS, INV>(v, t, tw);
+  }
   hook.after(PASS);
   if constexpr (PASS + 1 < G::NPASS) {
     if (active) pass_store<K, RB, PASS>(v, t, sm);

@@ -91,7 +91,7 @@ struct FieldHook {
 // each group evaluates one radius row per round; rows are strided over the
 // CTAs of a signal (blockIdx.y).
 // ---------------------------------------------------------------------------
-template <int K, int RB, int G, bool MATERIALIZE>
+template <int K, int RB, int G, bool MATERIALIZE, bool TM = false>
 __global__ void __launch_bounds__(Geo<K, RB>::T * G, (RB <= 3 && Geo<K, RB>::T * G <= 512) ? 2 : 1)
 field_kernel(const double2* __restrict__ ghat,     // [batch][N]
              const double* __restrict__ pw,        // [rows of plan][N], r^l natural l
@@ -123,8 +123,19 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   // Twiddle image: one TMA bulk copy (issued by thread 0, completes on an
   // mbarrier) overlapping the first row's prologue loads.
   __shared__ unsigned long long tw_bar;
+  __shared__ uint32_t tm_base;  // TMEM twiddle store (TM)
   if (threadIdx.x == 0) mbar_init(&tw_bar, 1);
+  if constexpr (TM) {
+    if (threadIdx.x < 32) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(&tm_base))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
   __syncthreads();
+  if constexpr (TM) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (threadIdx.x == 0) {
     constexpr unsigned bytes = sizeof(double2) * TwT::ENTRIES;
     const unsigned m = (unsigned)__cvta_generic_to_shared(&tw_bar);
@@ -141,7 +152,15 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     }
   }
   bool tw_ready = false;
-  const TwT tw{smem};
+  using TwSrc = std::conditional_t<TM, TmemTw, TwT>;
+  TwSrc tw;
+  if constexpr (TM) {
+    const int warp = threadIdx.x >> 5;
+    tw.base = tm_base + ((uint32_t)((warp & 3) * 32) << 16) +
+              (uint32_t)(((warp & 7) >> 2) * TmemTw::kSetCols);
+  } else {
+    tw.sm = smem;
+  }
   double2* sm = smem + TwT::ENTRIES + g * Gm::SMEM;
   const double2* __restrict__ gh = ghat + (size_t)sig * N;
 
@@ -177,6 +196,17 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
 #pragma unroll
       for (int i = 0; i < P; ++i) pv[i] = __ldg(pr + Gm::l0(tp, i));
     }
+    if constexpr (TM) {  // step-independent: fill TMEM before the PDL wait
+      mbar_wait(&tw_bar, 0);
+      tw_ready = true;
+      if (g == 0) {
+        tw.template fill<K, RB, true>(tp, TwT{smem});
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
     pdl_wait();
     // the stop flag's load overlaps the spectrum loads (both are L2 round
     // trips on the critical path); the flag is tested once v is formed
@@ -191,6 +221,13 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     }
     if (stopped) {
       mbar_wait(&tw_bar, 0);  // no bulk copy may target an exited CTA
+      if constexpr (TM) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x < 32)
+          asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm_base)
+                       : "memory");
+      }
       return;
     }
     pdl_trigger();
@@ -247,6 +284,13 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
       }
     }
     FSTAMP(rd, 14);
+  }
+  if constexpr (TM) {  // all TMEM reads done: release the columns
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < 32)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm_base)
+                   : "memory");
   }
   if (MATERIALIZE) return;
   __syncthreads();  // all groups done before the block-wide reduction
