@@ -46,14 +46,19 @@ struct Step {
 enum : int { kStepPowAmbiguous = 1 };
 
 #ifdef AFD_FIELD_TIMING
-// clock64 stamps of each row-group leader: [cta][group][row][slot]
+// %globaltimer stamps (ns) of each row-group leader: [cta][group][row][slot]
 //   0 start, 1 after the PDL wait, per row: 2 prologue done, 3/5/7 pass
 //   ends, 4/6 exchange ends, 14 epilogue done; 15 = SM id (row 0 only)
 __device__ long long g_field_stamps[512][2][4][16];
+__device__ __forceinline__ long long ftime() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #define FSTAMP(r, i)                                                                      \
   do {                                                                                    \
     if (tp == 0 && blockIdx.x < 512 && g < 2 && (r) < 4) g_field_stamps[blockIdx.x][g][r][i] = \
-        clock64();                                                                        \
+        ftime();                                                                          \
   } while (0)
 #else
 #define FSTAMP(r, i) \
@@ -76,12 +81,12 @@ struct FieldHook {
   __device__ __forceinline__ void after(int pass) const {
     if (pass == 0 && arrive) asm volatile("bar.arrive 3, %0;" ::"r"(count) : "memory");
 #ifdef AFD_FIELD_TIMING
-    if (st) st[3 + 2 * pass] = clock64();
+    if (st) st[3 + 2 * pass] = ftime();
 #endif
   }
   __device__ __forceinline__ void exch(int pass) const {
 #ifdef AFD_FIELD_TIMING
-    if (st) st[4 + 2 * pass] = clock64();
+    if (st) st[4 + 2 * pass] = ftime();
 #endif
   }
 };

@@ -73,16 +73,17 @@ struct ClusterGeo {
 template <int K>
 struct ClusterSmem {
   using CG = ClusterGeo<K>;
-  static constexpr size_t slice = 0;                                   // NC double2 (natural)
+  static constexpr size_t slice = 0;                                   // NC double2
   static constexpr size_t part = slice + sizeof(double2) * CG::NC;     // GL::SMEM double2
-  static constexpr size_t mag = part + sizeof(double2) * CG::GL::SMEM; // NC double
-  static constexpr size_t twl = mag + sizeof(double) * CG::NC;         // NC-1 double2
+  static constexpr size_t emag = part + sizeof(double2) * CG::GL::SMEM;  // NC double
+  static constexpr size_t twl = emag + sizeof(double) * CG::NC;          // NC-1 double2
   static constexpr size_t scratch = twl + sizeof(double2) * (CG::NC - 1);  // 2*(NC/8+16)
   static constexpr size_t circ = scratch + sizeof(double) * 2 * (CG::NC / 8 + 16);  // N double2
   static constexpr size_t rad = circ + sizeof(double2) * CG::N;  // up to kRadSmem radii
-  static constexpr int kRadSmem = 4096;
+  static constexpr int kRadSmem = K >= 13 ? 1024 : 4096;  // N = 8192: smem is nearly full
   static constexpr size_t bytes = rad + sizeof(double) * kRadSmem;
   static_assert(circ % 16 == 0, "bulk-copy destination must be 16-byte aligned");
+  static_assert(bytes + 1024 <= 232448, "cluster step kernel exceeds shared memory");
 };
 
 // left+right binary tree over C values (numpy pairwise halves)
@@ -133,13 +134,13 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   extern __shared__ __align__(16) unsigned char smraw[];
   double2* slice = reinterpret_cast<double2*>(smraw + L::slice);
   double2* part = reinterpret_cast<double2*>(smraw + L::part);
-  double* mag = reinterpret_cast<double*>(smraw + L::mag);
+  double* emag = reinterpret_cast<double*>(smraw + L::emag);  // |G_{k+1}|^2, my natural slice
   double2* twl = reinterpret_cast<double2*>(smraw + L::twl);
   double* scratch = reinterpret_cast<double*>(smraw + L::scratch);
   double2* circ = reinterpret_cast<double2*>(smraw + L::circ);  // z_m, all N
   double* rad = reinterpret_cast<double*>(smraw + L::rad);    // radii (if <= kRadSmem)
   __shared__ double s_node[2];   // this CTA's pairwise-tree node sums
-  __shared__ Cand red[32];
+  __shared__ double s_nodes[16];  // CTA 0: every CTA's energy node sum
   State& st = state[sig];
   double2* __restrict__ r = rem + (size_t)sig * N;
   double2* __restrict__ gh = ghat + (size_t)sig * N;
@@ -198,29 +199,38 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   // kernel, which completed before our PDL predecessor (the field kernel)
   // passed its own pdl_wait and triggered us, so it is final here (except
   // for the dc_first step 0, loaded after the wait)
+  // CTA c owns the samples l = C*m + rc (m < NC, rc = bitrev(c)): exactly
+  // the inputs of its CTA-local DIT, so the update feeds the transform
+  // without a cluster exchange (only |G|^2 goes to CTA 0 for the energy)
   constexpr int PER = (NC + CG::THREADS - 1) / CG::THREADS;
+  const int rc = brev_bits(c, CB);
   double2 gs[PER];
 #pragma unroll
   for (int u = 0; u < PER; ++u) {
     const int i = tid + u * CG::THREADS;
-    if (i < NC && !(k == 0 && dc_first)) gs[u] = k >= 0 ? r[m0 + i] : g0[(size_t)sig * N + m0 + i];
+    const int l = C * i + rc;
+    if (i < NC && !(k == 0 && dc_first)) gs[u] = k >= 0 ? r[l] : g0[(size_t)sig * N + l];
   }
   // radii for grid.point: staged in shared memory when they fit
   const bool rad_smem = nrad <= L::kRadSmem;
   if (rad_smem)
     for (int i = tid; i < nrad; i += CG::THREADS) rad[i] = radii[i];
   __syncthreads();  // rad / twl / barrier init visible
+  // every CTA of the cluster is running before anyone touches distributed
+  // shared memory (waited right after the PDL wait)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   STAMP(1);
 
   pdl_wait();
   STAMP(2);
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   if (k == 0 && dc_first) {
     // this kernel's PDL predecessor is the init step kernel itself (no field
     // launch in between), so G_0 is only final after the wait
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
       const int i = tid + u * CG::THREADS;
-      if (i < NC) gs[u] = r[m0 + i];
+      if (i < NC) gs[u] = r[C * i + rc];
     }
   }
   // the stop flag's load overlaps the candidate loads below; it is tested
@@ -302,112 +312,53 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   mbar_wait(&circ_bar, 0);  // (no-op when already passed) circle slice for the update
 
   STAMP(3);
-  // ---- update this CTA's slice (or copy g0 at init) --------------------------
+  // ---- update this CTA's samples (or copy g0 at init) -------------------------
   int amb = 0;
-  double2 rout[PER];  // new remainder slice, stored after the first cluster barrier
-  if (k < 0) {
-#pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      const int i = tid + u * CG::THREADS;
-      if (i < NC) {
-        rout[u] = gs[u];
-        slice[i] = gs[u];
-        mag[i] = np_mag2(gs[u]);
-      }
-    }
-  } else {
-    const double kn = kernel_norm(a, &amb);
+  {
+    double kn = 0.0;
+    if (k >= 0) kn = kernel_norm(a, &amb);
     const double2 sc = make_double2(kn, 0.0);
     STAMP(15);
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
       const int i = tid + u * CG::THREADS;
       if (i < NC) {
-        const double2 z = circ[m0 + i];
-        const double2 d = one_minus_conja_z(a, z);
-        const double2 e = np_cdiv(sc, d);
-        const double2 ce = np_cmul(coeff, e);  // N <= 8192: no numpy elision
-        const double2 g = gs[u];
-        const double2 stp = make_double2(g.x - ce.x, g.y - ce.y);
-        const double2 num = np_cmul(stp, d);
-        const double2 out = np_cdiv(num, make_double2(z.x - a.x, z.y - a.y));
-        rout[u] = out;
+        const int l = C * i + rc;
+        double2 out = gs[u];
+        if (k >= 0) {
+          const double2 z = circ[l];
+          const double2 d = one_minus_conja_z(a, z);
+          const double2 e = np_cdiv(sc, d);
+          const double2 ce = np_cmul(coeff, e);  // N <= 8192: no numpy elision
+          const double2 g = gs[u];
+          const double2 stp = make_double2(g.x - ce.x, g.y - ce.y);
+          const double2 num = np_cmul(stp, d);
+          out = np_cdiv(num, make_double2(z.x - a.x, z.y - a.y));
+        }
         slice[i] = out;
-        mag[i] = np_mag2(out);
+        // |G|^2 to the CTA whose natural slice holds l (a pairwise-sum node)
+        cluster.map_shared_rank(emag, l / NC)[l % NC] = np_mag2(out);
+        r[l] = out;  // completes under the local DIT, before the next cluster barrier
       }
     }
   }
   __syncthreads();
   STAMP(4);
-  const double node = pairwise_sum_block(mag, NC, scratch, PlainIdx(), CG::THREADS);
-  if (tid == 0) s_node[0] = node;
   STAMP(5);
-  cluster.sync();  // slices and node sums visible cluster-wide
   STAMP(6);
-  // G_{k+1} to global memory only now: a store pending at a cluster barrier
-  // (release = MEMBAR.GPU) would hold the barrier for an L2 round trip
-#pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    const int i = tid + u * CG::THREADS;
-    if (i < NC) r[m0 + i] = rout[u];
-  }
-  // The forward transform does not need the energy: warp(s) 0.. run the
-  // CTA-local DIT on a named barrier while the last warp combines the
-  // energy tree, writes the step record and evaluates the stop rules.
   constexpr int kFftWarps = (CG::LOCAL_THREADS + 31) / 32;
   static_assert(kFftWarps * 32 < CG::THREADS, "need a spare warp for the energy");
   const int warp = tid >> 5;
-  if (warp == CG::THREADS / 32 - 1) {
-    if ((tid & 31) == 0) {
-      double e[C];
-#pragma unroll
-      for (int u = 0; u < C; ++u) e[u] = cluster.map_shared_rank(s_node, u)[0];
-      const double energy = tree_combine<C>(e) / (double)N;
-      if (k < 0) {
-        if (c == 0) {
-          st.initial = energy;
-          st.nsteps = 0;
-          st.flags = 0;
-          st.stopped = (energy == 0.0) ? 1 : 0;  // core.py:366-368
-        }
-      } else if (c == 0) {
-        int stop = 0;
-        if (threshold > 0.0 && energy <= threshold * st.initial) stop = 1;  // core.py:386-387
-        if (energy == 0.0) stop = 1;                                         // core.py:388-389
-        if (k + 1 >= max_terms) stop = 1;
-        Step rec;
-        rec.s = s;
-        rec.j = j;
-        rec.radius = radius;
-        rec.a_re = a.x;
-        rec.a_im = a.y;
-        rec.c_re = coeff.x;
-        rec.c_im = coeff.y;
-        rec.residual = energy;
-        rec.flags = amb ? kStepPowAmbiguous : 0;
-        rec.pad = 0;
-        steps[(size_t)sig * max_terms + k] = rec;
-        st.nsteps = k + 1;
-        st.flags |= rec.flags;
-        st.stopped = stop;
-      }
-    }
-  } else if (warp < kFftWarps) {
+  if (warp < kFftWarps) {
     // ---- forward transform, stages 0..K-CB-1 on positions [c*NC, (c+1)*NC) ----
-    // (computed even on the last step: harmless, and keeps it off the
-    // energy's critical path)
+    // (computed even on the last step: harmless)
     STAMP(7);
     const int tp = tid;
     const bool active = tp < CG::LOCAL_THREADS;
-    const int rc = brev_bits(c, CB);
     double2 v[GL::P];
     if (active) {
 #pragma unroll
-      for (int i = 0; i < GL::P; ++i) {
-        const int l = C * GL::l0(tp, i) + rc;  // natural index of this position
-        const double2* src = cluster.map_shared_rank(slice, l / NC);
-        v[i] = src[l % NC];
-      }
+      for (int i = 0; i < GL::P; ++i) v[i] = slice[GL::l0(tp, i)];  // l = C*l0 + rc
     }
     STAMP(8);
     fft_passes<CG::KL, false, CG::RB>(v, tp, active, part, LocalTw{twl},
@@ -418,7 +369,7 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
       for (int i = 0; i < GL::P; ++i) part[GL::sw(out_pos<CG::KL, CG::RB>(tp, i))] = v[i];
     }
   }
-  cluster.sync();
+  cluster.sync();  // DIT outputs and the |G|^2 pushes visible cluster-wide
   STAMP(10);
 
   // ---- stages K-CB..K-1: radix-C over the top CB position bits ----------------
@@ -426,6 +377,8 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   // stages e = 0, 1 in layout A (thread h holds u = 4h + i), then a 4x4
   // transpose through shared memory (the group's H threads share a warp),
   // then stages e >= 2 in layout B (u = h + H i).
+  // Meanwhile the last warp sums this CTA's |G|^2 node (numpy pairwise
+  // blocks of 128 over the natural slice) and hands it to CTA 0.
   if (tid < CG::P2_THREADS) {
     double2 v[4];
 #pragma unroll
@@ -453,8 +406,26 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
       }
     }
 #pragma unroll
-#pragma unroll
     for (int i = 0; i < 4; ++i) gh[q + NC * (hh + H * i)] = v[i];
+  } else if (tid >= CG::THREADS - 32) {
+    // node sum: accumulator a (lane) of block a/8 sums emag[128 (a/8) + a%8 + 8 i]
+    const int lane = tid & 31;
+    constexpr int NB = NC / 128;  // blocks in the slice (1..4)
+    double acc = 0.0;
+    if (lane < 8 * NB) {
+      const double* xb = emag + 128 * (lane >> 3) + (lane & 7);
+      acc = xb[0];
+#pragma unroll
+      for (int i = 8; i < 128; i += 8) acc += xb[i];
+    }
+    // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) per block, then blocks left+right
+#pragma unroll
+    for (int off = 1; off < 8 * NB; off <<= 1) {
+      const double o = __shfl_down_sync(0xffffffffu, acc, off);
+      if ((lane & (2 * off - 1)) == 0) acc = acc + o;
+    }
+    if (lane == 0) cluster.map_shared_rank(s_nodes, 0)[c] = acc;
+    asm volatile("barrier.cluster.arrive.release;" ::: "memory");
   } else {
     asm volatile("barrier.cluster.arrive.release;" ::: "memory");
   }
@@ -462,6 +433,37 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   // no CTA leaves while another may still read its shared memory
   asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
   STAMP(12);
+  if (c == 0 && tid == 0) {
+    // energy = np.mean(|G|^2) (core.py:195-198): the C node sums combined as
+    // numpy's left+right tree, then / N; record, stop rules (core.py:366-389)
+    const double energy = tree_combine<C>(s_nodes) / (double)N;
+    if (k < 0) {
+      st.initial = energy;
+      st.nsteps = 0;
+      st.flags = 0;
+      st.stopped = (energy == 0.0) ? 1 : 0;  // core.py:366-368
+    } else {
+      int stop = 0;
+      if (threshold > 0.0 && energy <= threshold * st.initial) stop = 1;  // core.py:386-387
+      if (energy == 0.0) stop = 1;                                         // core.py:388-389
+      if (k + 1 >= max_terms) stop = 1;
+      Step rec;
+      rec.s = s;
+      rec.j = j;
+      rec.radius = radius;
+      rec.a_re = a.x;
+      rec.a_im = a.y;
+      rec.c_re = coeff.x;
+      rec.c_im = coeff.y;
+      rec.residual = energy;
+      rec.flags = amb ? kStepPowAmbiguous : 0;
+      rec.pad = 0;
+      steps[(size_t)sig * max_terms + k] = rec;
+      st.nsteps = k + 1;
+      st.flags |= rec.flags;
+      st.stopped = stop;
+    }
+  }
 }
 
 }  // namespace afd

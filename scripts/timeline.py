@@ -1,0 +1,42 @@
+"""Per-step hand-off timeline (c1): field and step kernels of the last AFD
+step, from the AFD_FIELD_TIMING + AFD_STEP_TIMING build (globaltimer, ns)."""
+import ctypes as C
+import os
+import sys
+import warnings
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+warnings.simplefilter("ignore")
+os.environ["AFD_LIB_PATH"] = "paper_1711_08604_b200/lib/libafd_b200_both.so"
+from paper_1711_08604_b200 import engine, workloads as W, _capi  # noqa: E402
+
+w = W.CONFIGS["c1"]
+plan = engine.get_plan(W.radii_for(w.m), w.n)
+g = torch.from_numpy(W.signal_for("c1")[None, :]).cuda()
+for _ in range(3):
+    plan.decompose(g, w.steps)
+torch.cuda.synchronize()
+lib = _capi.load()
+lib.afd_debug_field_stamps.argtypes = [C.c_void_p]
+lib.afd_debug_step_stamps.argtypes = [C.c_void_p]
+f = np.zeros((512, 2, 4, 16), np.int64)
+s = np.zeros((64, 24), np.uint64)
+assert lib.afd_debug_field_stamps(f.ctypes.data) == 0
+assert lib.afd_debug_step_stamps(s.ctypes.data) == 0
+s = s.astype(np.int64)
+k = w.steps - 1
+ncta = int((f[:, :, 0, 0] != 0).any(axis=1).sum())
+f = f[:ncta]
+t0 = s[k - 1, 12]  # step k-1 end (cluster CTA 0)
+fstart = f[:, :, 0, 0]
+fwait = f[:, :, 0, 1]
+last = np.where(f[:, :, :, 14] != 0, f[:, :, :, 14], 0).max(axis=2)
+print("times relative to the end of step k-1 (ns), k = %d" % k)
+print("  field CTAs start: min %d max %d" % (fstart.min() - t0, fstart.max() - t0))
+print("  field PDL wait returns: min %d median %d max %d" % (fwait.min() - t0, np.median(fwait) - t0, fwait.max() - t0))
+print("  field CTAs last row done: min %d median %d max %d" % (last.min() - t0, np.median(last) - t0, last.max() - t0))
+print("  step k start %d, wait returns %d, end %d" % (s[k, 0] - t0, s[k, 2] - t0, s[k, 12] - t0))
+print("  step k-1: start %d wait %d (rel. to its own end: %d %d)" % (s[k-1, 0] - t0, s[k-1, 2] - t0, s[k-1,0]-s[k-1,12], s[k-1,2]-s[k-1,12]))
