@@ -211,7 +211,8 @@ int setup_field_kernel(int* occ) {
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem<K>()));
   if constexpr (field_tmem_capable<K>()) {
     CU(cudaFuncSetAttribute(field_kernel<K, kFieldRB, groups_for<K>(), MAT, true>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem<K>()));
+                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)field_smem<K>()));
   }
   if (occ) CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, field_block<K>(), field_smem<K>()));
   return 0;

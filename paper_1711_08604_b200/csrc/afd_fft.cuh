@@ -88,12 +88,14 @@ __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, unsi
 __device__ __forceinline__ void mbar_wait(unsigned long long* mbar, unsigned parity) {
   const unsigned m = (unsigned)__cvta_generic_to_shared(mbar);
   unsigned done = 0;
+  unsigned spins = 0;
   while (!done) {
     asm volatile(
         "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
         : "=r"(done)
         : "r"(m), "r"(parity)
         : "memory");
+    if (++spins == (1u << 28)) __trap();  // a lost transfer fails the launch, never hangs
   }
 }
 
@@ -264,6 +266,7 @@ __device__ __forceinline__ void tm_st4(uint32_t a, double2 w) {
 struct TmemTw {
   static constexpr bool kTmem = true;
   static constexpr int kSetCols = 180;  // 3 passes x 15 slots x 4 words
+  static constexpr int kGhCol = 2 * kSetCols;  // field spectrum: 2 sets x 16 values x 4 words
   uint32_t base;  // warp-uniform: lane quadrant of this warp, column 0 of its set
   __device__ __forceinline__ static uint32_t col(int pass, int slot) {
     return (uint32_t)(pass * 60 + slot * 4);

@@ -77,9 +77,13 @@ struct FieldHook {
   bool arrive;     // group 0, first row: release group 1 after pass 0
   int count;       // threads of both groups
   long long* st;   // timing stamps of this row (timing builds) or null
+  bool tm_fence;   // TMEM written before the release (gh spectrum, TM variant)
   __device__ __forceinline__ void before(int) const {}
   __device__ __forceinline__ void after(int pass) const {
-    if (pass == 0 && arrive) asm volatile("bar.arrive 3, %0;" ::"r"(count) : "memory");
+    if (pass == 0 && arrive) {
+      if (tm_fence) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("bar.arrive 3, %0;" ::"r"(count) : "memory");
+    }
 #ifdef AFD_FIELD_TIMING
     if (st) st[3 + 2 * pass] = ftime();
 #endif
@@ -168,6 +172,17 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   }
   double2* sm = smem + TwT::ENTRIES + g * Gm::SMEM;
   const double2* __restrict__ gh = ghat + (size_t)sig * N;
+  // TM variant: rows after the first take the spectrum from TMEM (written by
+  // group 0 during the first prologue) instead of re-reading it from L2
+  // (measured c1 1.09e11 -> 1.12e11 evals/s; staging r^l in shared memory by
+  // TMA as well was slower: the extra 32 KiB of shared memory costs L1)
+  uint32_t gh_tm = 0;
+  if constexpr (TM) {
+    static_assert(TmemTw::kGhCol + 2 * 4 * P <= 512, "TMEM columns");
+    const int warp = threadIdx.x >> 5;
+    gh_tm = tm_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)TmemTw::kGhCol +
+            (uint32_t)(((warp & 7) >> 2) * (4 * P));
+  }
 
   // Running first maximum.  Rows are visited in increasing s and, within a
   // row, a thread's outputs j = out_pos(tp, i) increase with i, so a strict
@@ -187,7 +202,8 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
       kGroupSync ? (rows - ((long long)blockIdx.x * Gr + g) + per_round - 1) / per_round
                  : (rows + per_round - 1) / per_round;
   // phase offset of group 1 (FieldHook): only when both groups have rows
-  const bool offset = kGroupSync && Gr == 2 && pp > 0 &&
+  // (always for TM: group 1 reads the spectrum group 0 put in TMEM)
+  const bool offset = kGroupSync && Gr == 2 && (pp > 0 || TM) &&
                       (long long)blockIdx.x * Gr + 1 < rows;
   // First row: its r^l values are step-independent and are loaded before the
   // PDL wait; the spectrum and the stop flags come from the previous kernel.
@@ -222,6 +238,12 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
         const double2 c = __ldg(gh + Gm::l0(tp, i));
         v[i] = make_double2(pv[i] * c.x, pv[i] * c.y);  // transform.py:198
         asm volatile("" ::"d"(v[i].x), "d"(v[i].y));  // formed before the test
+        if constexpr (TM) {
+          if (g == 0) tm_st4(gh_tm + 4 * i, c);
+        }
+      }
+      if constexpr (TM) {
+        if (g == 0) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
     }
     if (stopped) {
@@ -243,13 +265,31 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     const bool active = s < row1;
     if (rd > 0 && active) {
       // prologue: y = powers * c[rev] (transform.py:198), per component
-      const double* __restrict__ pr = pw + (size_t)(s - pw_row0) * N;
+      if constexpr (TM) {
+        const double* __restrict__ pr = pw + (size_t)(s - pw_row0) * N;
 #pragma unroll
-      for (int i = 0; i < P; ++i) {
-        const int l = Gm::l0(tp, i);
-        const double p = __ldg(pr + l);
-        const double2 c = __ldg(gh + l);
-        v[i] = make_double2(p * c.x, p * c.y);
+        for (int i0 = 0; i0 < P; i0 += 4) {
+          uint32_t r[16];
+          tm_ld<16>(gh_tm + 4 * i0, r);
+          tm_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int l = Gm::l0(tp, i0 + j);
+            const double2 c = make_double2(__hiloint2double(r[4 * j + 1], r[4 * j]),
+                                           __hiloint2double(r[4 * j + 3], r[4 * j + 2]));
+            const double p = __ldg(pr + l);
+            v[i0 + j] = make_double2(p * c.x, p * c.y);
+          }
+        }
+      } else {
+        const double* __restrict__ pr = pw + (size_t)(s - pw_row0) * N;
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          const int l = Gm::l0(tp, i);
+          const double p = __ldg(pr + l);
+          const double2 c = __ldg(gh + l);
+          v[i] = make_double2(p * c.x, p * c.y);
+        }
       }
     }
     if (!tw_ready) {  // twiddle image landed (pass 0 reads it)
@@ -262,8 +302,11 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
 #ifdef AFD_FIELD_TIMING
       if (tp == 0 && blockIdx.x < 512 && g < 2 && rd < 4) st = &g_field_stamps[blockIdx.x][g][rd][0];
 #endif
-      if (offset && rd == 0 && g == 1) asm volatile("bar.sync 3, %0;" ::"r"(2 * T) : "memory");
-      const FieldHook hook{offset && rd == 0 && g == 0, 2 * T, st};
+      if (offset && rd == 0 && g == 1) {
+        asm volatile("bar.sync 3, %0;" ::"r"(2 * T) : "memory");
+        if constexpr (TM) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      }
+      const FieldHook hook{offset && rd == 0 && g == 0, 2 * T, st, TM};
       fft_passes<K, true, RB>(v, tp, active, sm, tw, GroupSync{1 + g, T}, hook);
     } else {
       fft_passes<K, true, RB>(v, tp, active, sm, tw);

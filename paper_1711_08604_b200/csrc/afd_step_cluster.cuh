@@ -292,7 +292,7 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
       mbar_wait(&circ_bar, 0);  // no bulk copy may target an exited CTA
       return;
     }
-    pdl_trigger();
+    pdl_trigger();  // (releasing the next field launch later measured slower)
     STAMP(17);
     b = warp_argmax(b);
     b.mag = __shfl_sync(0xffffffffu, b.mag, 0);

@@ -40,3 +40,20 @@ print("  field PDL wait returns: min %d median %d max %d" % (fwait.min() - t0, n
 print("  field CTAs last row done: min %d median %d max %d" % (last.min() - t0, np.median(last) - t0, last.max() - t0))
 print("  step k start %d, wait returns %d, end %d" % (s[k, 0] - t0, s[k, 2] - t0, s[k, 12] - t0))
 print("  step k-1: start %d wait %d (rel. to its own end: %d %d)" % (s[k-1, 0] - t0, s[k-1, 2] - t0, s[k-1,0]-s[k-1,12], s[k-1,2]-s[k-1,12]))
+# per-CTA spread: wait return vs end, by SM id
+smid = f[:, 0, 0, 15]
+wr = fwait.min(axis=1) - t0
+en = last.max(axis=1) - t0
+dur = en - wr
+print("  per-CTA post-wait duration: min %d median %d max %d" % (dur.min(), np.median(dur), dur.max()))
+print("  corr(wait return, end) = %.2f" % np.corrcoef(wr, en)[0, 1])
+order = np.argsort(en)[-8:]
+print("  latest CTAs (cta, smid, wait, end, dur):")
+for i in order:
+    print("    %3d %3d %6d %6d %6d" % (i, smid[i], wr[i], en[i], dur[i]))
+lo = smid < 74
+print("  SM id < 74: median end %d (n=%d); >= 74: median end %d (n=%d)" % (
+    np.median(en[lo]), lo.sum(), np.median(en[~lo]), (~lo).sum()))
+# per-row durations of group leaders
+rowdur = f[:, :, 1, 14] - f[:, :, 0, 14]
+print("  row-1 duration (ns): median %d p90 %d max %d" % (np.median(rowdur), np.percentile(rowdur, 90), rowdur.max()))
