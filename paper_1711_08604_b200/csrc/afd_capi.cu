@@ -47,7 +47,7 @@ int fail(int code, const char* fmt, ...) {
 constexpr int kMinK = 3;
 constexpr int kMaxOnChipK = 13;
 constexpr int kMaxK = 22;
-constexpr size_t kBigBatchBytes = 48ull << 20;  // L2-resident row batch
+constexpr size_t kBigBatchBytes = 160ull << 20;  // row-batch intermediate (large N)
 
 }  // namespace
 
@@ -714,7 +714,22 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
                          sizeof(double) << p->ka>>>(p->pw, K, p->ka);
     p->launches += 2;
     if (cudaGetLastError() != cudaSuccess) return cleanup(fail(AFD_E_CUDA, "bitrev launch"));
-    p->big_rows = std::max<int64_t>(1, std::min<int64_t>(m1 - m0, (int64_t)(kBigBatchBytes / (N * 16))));
+    {
+      // Rows per batch: as many as kBigBatchBytes of intermediate allows
+      // (fewer launches and waves per step measured faster than keeping the
+      // batch L2-resident: c2 field 4.23 ms at 48 rows -> 3.67 ms at 148),
+      // rounded down to a whole number of pass-A rounds when possible.
+      const int64_t cap = std::max<int64_t>(1, (int64_t)(kBigBatchBytes / (N * 16)));
+      const int64_t nblk = N >> p->ka, slots = 2LL * p->sms;
+      int64_t rows = cap;
+      for (int64_t r = cap; r >= std::max<int64_t>(1, cap / 2); --r)
+        if ((r * nblk) % slots == 0) {
+          rows = r;
+          break;
+        }
+      if (const char* e = getenv("AFD_BIG_ROWS")) rows = atoll(e);  // experiments
+      p->big_rows = std::max<int64_t>(1, std::min<int64_t>(m1 - m0, rows));
+    }
     ALLOC2(p->Y, sizeof(double2) * N * p->big_rows);
     ALLOC2(p->big_cand, sizeof(Cand) * p->big_rows * big_col_ctas(p));
     ALLOC2(p->nodes, sizeof(double) * 2 * (N / kNodeLen));
