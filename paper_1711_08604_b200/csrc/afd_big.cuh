@@ -65,7 +65,10 @@ __host__ __device__ constexpr size_t big_a_smem_g() {
   return sizeof(double2) * (SmemTw<KA, 4>::ENTRIES + kBigGroups * Geo<KA, 4>::SMEM);
 }
 
-template <int KA, bool INV>
+// TM (KA = 12, field mode): the field kernel's N = 4096 machinery —
+// per-thread twiddles in TMEM (TmemTw) and the one-pass offset between the
+// two row-groups (FieldHook) — on pass A's 4096-point blocks.
+template <int KA, bool INV, bool TM = false>
 __global__ void __launch_bounds__(Geo<KA, 4>::T * kBigGroups, 1)
 big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0,
            const double2* __restrict__ ghat_rev, const double2* __restrict__ x,
@@ -74,18 +77,47 @@ big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0
   using GA = Geo<KA, 4>;
   using TwA = SmemTw<KA, 4>;
   constexpr int BLK = 1 << KA, T = GA::T;
+  static_assert(!TM || (KA == 12 && INV), "TMEM pass A: field blocks of 4096");
   extern __shared__ double2 smem[];
   if (stopped && *stopped) return;
   const long long N = 1LL << K;
   const long long nblk = N >> KA;
   const long long items = (row1 - row0) * nblk;
+  __shared__ uint32_t tm_base;
+  if constexpr (TM) {
+    if (threadIdx.x < 32) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(&tm_base))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+  }
   TwA::load(smem, twst);  // N-table stage twiddles S_b, b < KA
+  if constexpr (TM) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  const TwA tw{smem};
+  if constexpr (TM) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const int g = threadIdx.x / T, tid = threadIdx.x % T;
+  using TwSrc = std::conditional_t<TM, TmemTw, TwA>;
+  TwSrc tw;
+  if constexpr (TM) {
+    const int warp = threadIdx.x >> 5;
+    tw.base = tm_base + ((uint32_t)((warp & 3) * 32) << 16) +
+              (uint32_t)(((warp & 7) >> 2) * TmemTw::kSetCols);
+    if (g == 0) {
+      tw.template fill<KA, 4, true>(tid, TwA{smem});
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  } else {
+    tw.sm = smem;
+  }
   double2* buf = smem + TwA::ENTRIES + g * GA::SMEM;
   const GroupSync sync{1 + g, T};
   const int t0 = brev_bits(tid, GA::TB);
+  const bool offset = TM && (long long)blockIdx.x * kBigGroups + 1 < items;
+  bool first = true;
   for (long long it = (long long)blockIdx.x * kBigGroups + g; it < items;
        it += (long long)gridDim.x * kBigGroups) {
     const long long rl = it / nblk;               // row within the batch
@@ -110,11 +142,25 @@ big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0
       for (int i = 0; i < GA::P; ++i) v[i] = buf[GA::sw(GA::pos(0, t0, i))];
       sync();
     }
-    fft_passes<KA, INV, 4>(v, tid, true, buf, tw, sync);
+    if constexpr (TM) {
+      if (offset && first && g == 1) asm volatile("bar.sync 3, %0;" ::"r"(2 * T) : "memory");
+      const FieldHook hook{offset && first && g == 0, 2 * T, nullptr, false};
+      fft_passes<KA, INV, 4>(v, tid, true, buf, tw, sync, hook);
+      first = false;
+    } else {
+      fft_passes<KA, INV, 4>(v, tid, true, buf, tw, sync);
+    }
     double2* __restrict__ y = Y + (size_t)rl * N + base;
 #pragma unroll
     for (int i = 0; i < GA::P; ++i) y[out_pos<KA, 4>(tid, i)] = v[i];
     sync();  // buffer reuse by the next item
+  }
+  if constexpr (TM) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < 32)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm_base)
+                   : "memory");
   }
 }
 

@@ -500,6 +500,8 @@ int big_setup(afd_plan* p) {
                             (int)big_a_smem_g<KA>()));
     CU(cudaFuncSetAttribute(big_pass_a<KA, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)big_a_smem_g<KA>()));
+    CU(cudaFuncSetAttribute(big_pass_a<KA, true, KA == 12>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_a_smem_g<KA>()));
     return 0;
   });
 }
@@ -512,7 +514,10 @@ int big_launch_a(afd_plan* p, bool inv, int mode, const double2* ghat_rev, const
     // persistent: one CTA per SM (2 row-groups each), work items strided
     const unsigned grid = (unsigned)std::min<int64_t>(p->sms, (items + kBigGroups - 1) / kBigGroups);
     const int block = Geo<KA, 4>::T * kBigGroups;
-    if (inv)
+    if (inv && mode == 0 && KA == 12 && field_tmem_enabled())
+      big_pass_a<KA, true, KA == 12><<<grid, block, big_a_smem_g<KA>(), st>>>(
+          p->K, mode, p->pw, p->m0, ghat_rev, x, p->twst, r0, r0 + rows, p->Y, stopped);
+    else if (inv)
       big_pass_a<KA, true><<<grid, block, big_a_smem_g<KA>(), st>>>(
           p->K, mode, p->pw, p->m0, ghat_rev, x, p->twst, r0, r0 + rows, p->Y, stopped);
     else
