@@ -10,7 +10,7 @@ import torch
 
 sys.path.insert(0, ".")
 warnings.simplefilter("ignore")
-os.environ["AFD_LIB_PATH"] = "paper_1711_08604_b200/lib/libafd_b200_both.so"
+os.environ.setdefault("AFD_LIB_PATH", "paper_1711_08604_b200/lib/libafd_b200_both.so")
 from paper_1711_08604_b200 import engine, workloads as W, _capi  # noqa: E402
 
 w = W.CONFIGS["c1"]
@@ -40,6 +40,11 @@ print("  field PDL wait returns: min %d median %d max %d" % (fwait.min() - t0, n
 print("  field CTAs last row done: min %d median %d max %d" % (last.min() - t0, np.median(last) - t0, last.max() - t0))
 print("  step k start %d, wait returns %d, end %d" % (s[k, 0] - t0, s[k, 2] - t0, s[k, 12] - t0))
 print("  step k-1: start %d wait %d (rel. to its own end: %d %d)" % (s[k-1, 0] - t0, s[k-1, 2] - t0, s[k-1,0]-s[k-1,12], s[k-1,2]-s[k-1,12]))
+if os.environ.get("AFD_FLAGS"):
+    print("  step k-1 signal: syncthreads %d, after signal %d" % (s[k-1, 18] - t0, s[k-1, 19] - t0))
+    print("  field poll start: median %d; poll done: min %d median %d max %d" % (
+        np.median(f[:, :, 0, 12]) - t0, f[:, :, 0, 13].min() - t0, np.median(f[:, :, 0, 13]) - t0,
+        f[:, :, 0, 13].max() - t0))
 # per-CTA spread: wait return vs end, by SM id
 smid = f[:, 0, 0, 15]
 wr = fwait.min(axis=1) - t0
