@@ -191,20 +191,21 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   double best_mag = -1.0, best_re = 0.0, best_im = 0.0;
   int best_rd = -1, best_i = 0;
 
-  const long long rows = row1 - row0;
-  const long long per_round = (long long)gridDim.x * Gr;
+  // row counts fit 32 bits (M <= 2^31); 32-bit loop state keeps registers
+  // for the butterflies
+  const int rows = (int)(row1 - row0);
+  const int per_round = (int)gridDim.x * Gr;
   // Row-groups of >= 32 threads synchronise on their own named barrier and
   // loop over their own rows independently, so the G rows of a CTA drift out
   // of phase (one group's loads overlap another's FP64 passes); smaller
   // groups share warps and step together with the whole block.
   constexpr bool kGroupSync = (T % 32 == 0) && G > 1;
-  const long long rounds =
-      kGroupSync ? (rows - ((long long)blockIdx.x * Gr + g) + per_round - 1) / per_round
-                 : (rows + per_round - 1) / per_round;
+  const int rounds = kGroupSync ? (rows - ((int)blockIdx.x * Gr + g) + per_round - 1) / per_round
+                                : (rows + per_round - 1) / per_round;
   // phase offset of group 1 (FieldHook): only when both groups have rows
   // (always for TM: group 1 reads the spectrum group 0 put in TMEM)
   const bool offset = kGroupSync && Gr == 2 && (pp > 0 || TM) &&
-                      (long long)blockIdx.x * Gr + 1 < rows;
+                      (int)blockIdx.x * Gr + 1 < rows;
   // First row: its r^l values are step-independent and are loaded before the
   // PDL wait; the spectrum and the stop flags come from the previous kernel.
   double2 v[P];
@@ -260,8 +261,9 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     pdl_trigger();
     FSTAMP(0, 1);
   }
-  for (long long rd = 0; rd < rounds; ++rd) {
-    const long long s = row0 + rd * per_round + (long long)blockIdx.x * Gr + g;
+  for (int rd = 0; rd < rounds; ++rd) {
+    const int sl = rd * per_round + (int)blockIdx.x * Gr + g;  // row within [row0, row1)
+    const long long s = row0 + sl;
     const bool active = s < row1;
     if (rd > 0 && active) {
       // prologue: y = powers * c[rev] (transform.py:198), per component
@@ -325,7 +327,7 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
             best_mag = mg;
             best_re = f.x;
             best_im = f.y;
-            best_rd = (int)rd;
+            best_rd = rd;
             best_i = i;
           }
         }
@@ -344,8 +346,7 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   __syncthreads();  // all groups done before the block-wide reduction
   Cand best;
   best.mag = best_mag;
-  const long long best_s =
-      row0 + (long long)best_rd * per_round + (long long)blockIdx.x * Gr + g;
+  const long long best_s = row0 + (long long)best_rd * per_round + (long long)blockIdx.x * Gr + g;
   best.flat =
       best_rd >= 0 ? best_s * (long long)N + out_pos<K, RB>(tp, best_i) : 0x7fffffffffffffffLL;
   best.re = best_re;
