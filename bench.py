@@ -46,6 +46,14 @@ def flops_per_eval(n):
     return 5 * (int(n).bit_length() - 1) + 7
 
 
+def fp64_instr_per_eval(n):
+    """FP64-pipe instructions per grid eval of the exact field kernel: prologue
+    2 DMUL, stage 0 2 DADD, each later stage 4 (2 DMUL + 2 DFMA + 4 DADD per
+    butterfly), epilogue 2 DMUL scale + 3 for |.|^2 + 1 DSETP."""
+    k = int(n).bit_length() - 1
+    return 2 + 2 + 4 * (k - 1) + 6
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -311,7 +319,13 @@ def run_ours(args):
                 "launch_ms": field_ms,
                 "peak_source": "measured in-run DFMA microbenchmark (afd_fp64_peak); "
                                "MEASURED_PEAKS.json has no FP64 entry",
-                "field_share_of_step": (field_ms * (w.steps) / (total_ms / args.steps))}
+                "field_share_of_step": (field_ms * (w.steps) / (total_ms / args.steps)),
+                # bit-exact radix-2 arithmetic is mostly unfused: per eval the kernel
+                # issues fp64_instr_per_eval FP64-pipe instructions for F(N) flops, so
+                # even a saturated FP64 pipe reaches only this fraction of the DFMA peak
+                "fp64_instr_per_eval": fp64_instr_per_eval(w.n),
+                "frac_ceiling_at_this_instruction_mix":
+                    fpe / (2.0 * fp64_instr_per_eval(w.n))}
 
     # e2e through the public API, host buffers, pinned H2D + D2H in the region
     grid = core.ParameterGrid(radii, w.n)
