@@ -173,12 +173,16 @@ big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0
 //   out_mode 3: transform output in natural order fout[j] (optionally / N)
 //   out_mode 4: field spectrum: position rev(j) in pass-A layout (ghat_perm)
 // ---------------------------------------------------------------------------
-template <bool INV>
+// MODE >= 0 fixes out_mode at compile time (the field pass, MODE = 1: fewer
+// live registers than the all-modes kernel, no spills); MODE = -1 dispatches
+// on out_mode at run time.
+template <bool INV, int MODE = -1>
 __global__ void __launch_bounds__(kColThreads, 2)
-big_pass_col(int K, int ka, int b0, int out_mode, int scale_n, double2* __restrict__ Y,
+big_pass_col(int K, int ka, int b0, int out_mode_rt, int scale_n, double2* __restrict__ Y,
              const double2* __restrict__ twst, const double* __restrict__ scales,
              long long row0, long long row1, Cand* __restrict__ cand,
              double2* __restrict__ fout, const int* __restrict__ stopped) {
+  const int out_mode = MODE >= 0 ? MODE : out_mode_rt;
   if (stopped && *stopped) return;
   const long long N = 1LL << K;
   const long long row = row0 + blockIdx.y;

@@ -534,7 +534,15 @@ int big_launch_cols(afd_plan* p, bool inv, int last_mode, int scale_n, int64_t r
   dim3 grid((unsigned)big_col_ctas(p), (unsigned)rows);
   for (int b0 = p->ka; b0 < p->K; b0 += 4) {
     const int mode = (b0 + 4 >= p->K) ? last_mode : 0;
-    if (inv)
+    if (inv && mode == 1)
+      big_pass_col<true, 1><<<grid, kColThreads, 0, st>>>(p->K, p->ka, b0, mode, scale_n, p->Y,
+                                                          p->twst, p->scales, r0, r0 + rows,
+                                                          p->big_cand, fout, stopped);
+    else if (inv && mode == 0)
+      big_pass_col<true, 0><<<grid, kColThreads, 0, st>>>(p->K, p->ka, b0, mode, scale_n, p->Y,
+                                                          p->twst, p->scales, r0, r0 + rows,
+                                                          p->big_cand, fout, stopped);
+    else if (inv)
       big_pass_col<true><<<grid, kColThreads, 0, st>>>(p->K, p->ka, b0, mode, scale_n, p->Y, p->twst,
                                                        p->scales, r0, r0 + rows, p->big_cand,
                                                        fout, stopped);
