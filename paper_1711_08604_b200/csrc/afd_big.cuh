@@ -268,6 +268,118 @@ big_pass_col(int K, int ka, int b0, int out_mode_rt, int scale_n, double2* __res
   }
 }
 
+// ---------------------------------------------------------------------------
+// Two column passes in one: stage bits [b0, b0+8) (N = 2^17..2^20: everything
+// after pass A).  A column is 256 positions q + 2^b0 u, u < 256, held by 16
+// threads; stages b0..b0+3 (u bits 0-3) in layout A (thread h holds
+// u = 16h + i), a transpose through shared memory, stages b0+4..b0+7 (u bits
+// 4-7) in layout B (thread h holds u = h + 16i).  One read of the row batch
+// intermediate instead of read + write + read (HBM-bound at N = 2^20).
+// CTA = 16 consecutive columns; slots as big_pass_col (N/4096 CTAs per row).
+//   MODE 1: field epilogue -> cand;  MODE 0: write back to Y in place.
+// ---------------------------------------------------------------------------
+constexpr int kCol8Pad = 257;  // smem slots per column (256 + 1: conflict-free)
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 2)
+big_pass_col8(int K, int b0, double2* __restrict__ Y, const double2* __restrict__ twst,
+              const double* __restrict__ scales, long long row0, long long row1,
+              Cand* __restrict__ cand, const int* __restrict__ stopped) {
+  extern __shared__ double2 col_sm[];  // [16][kCol8Pad]
+  if (stopped && *stopped) return;
+  const long long N = 1LL << K;
+  const long long row = row0 + blockIdx.y;
+  const int c = threadIdx.x & 15, h = threadIdx.x >> 4;
+  const long long x = (long long)blockIdx.x * 16 + c;  // column
+  const long long lowmask = (1LL << b0) - 1;
+  const long long q = (x & lowmask) | ((x >> b0) << (b0 + 8));
+  const long long qlow = q & lowmask;
+  double2* __restrict__ y = Y + (size_t)blockIdx.y * N;
+  double2* sm = col_sm + c * kCol8Pad;
+  Cand best;
+  best.mag = -1.0;
+  best.flat = 0x7fffffffffffffffLL;
+  best.re = best.im = 0.0;
+  const bool live = row < row1;
+  double2 v[16];
+  if (live) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = y[q + ((long long)(16 * h + i) << b0)];
+    // stages b0..b0+3: u mod 2^e = i mod 2^e
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const double2* __restrict__ sb = twst + ((1LL << (b0 + e)) - 1);  // S_b[k] = w[k << (K-1-b)]
+#pragma unroll
+      for (int kk = 0; kk < (1 << e); ++kk) {
+        double2 w = __ldg(sb + qlow + ((long long)kk << b0));
+        w.y = -w.y;  // np.conj(w), transform.py:199
+#pragma unroll
+        for (int hh = 0; hh < (16 >> (e + 1)); ++hh) {
+          const int i = kk | (hh << (e + 1));
+          bfly(v[i], v[i | (1 << e)], w);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) sm[16 * h + i] = v[i];
+  }
+  __syncthreads();
+  if (live) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = sm[h + 16 * i];
+    // stages b0+4..b0+7: u mod 2^e = h + 16 (i mod 2^(e-4))
+#pragma unroll
+    for (int e = 4; e < 8; ++e) {
+      const double2* __restrict__ sb = twst + ((1LL << (b0 + e)) - 1);
+      const int ib = e - 4;
+#pragma unroll
+      for (int kk = 0; kk < (1 << ib); ++kk) {
+        double2 w = __ldg(sb + qlow + ((long long)(h + 16 * kk) << b0));
+        w.y = -w.y;
+#pragma unroll
+        for (int hh = 0; hh < (16 >> (ib + 1)); ++hh) {
+          const int i = kk | (hh << (ib + 1));
+          bfly(v[i], v[i | (1 << ib)], w);
+        }
+      }
+    }
+    if (MODE == 0) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) y[q + ((long long)(h + 16 * i) << b0)] = v[i];
+    } else {
+      const double sc = __ldg(scales + row);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const long long j = q + ((long long)(h + 16 * i) << b0);
+        const double2 f = make_double2(v[i].x * sc, v[i].y * sc);  // transform.py:200
+        const double mg = np_mag2(f);                              // core.py:298
+        if (mg > best.mag) {  // j increases with i: first maximum
+          best.mag = mg;
+          best.flat = row * N + j;
+          best.re = f.x;
+          best.im = f.y;
+        }
+      }
+    }
+  }
+  if (MODE == 0) return;
+  __shared__ Cand red[8];
+  best = warp_argmax(best);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red[wid] = best;
+  __syncthreads();
+  if (wid == 0) {
+    Cand cc = lane < 8 ? red[lane] : best;
+    cc = warp_argmax(cc);
+    if (lane == 0) {
+      Cand& slot = cand[(size_t)blockIdx.y * gridDim.x + blockIdx.x];
+      Cand o = slot;
+      cand_merge(o, cc);
+      slot = o;
+    }
+  }
+}
+
 __global__ void cand_init_kernel(Cand* c, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     c[i].mag = -1.0;

@@ -502,6 +502,10 @@ int big_setup(afd_plan* p) {
                             (int)big_a_smem_g<KA>()));
     CU(cudaFuncSetAttribute(big_pass_a<KA, true, KA == 12>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_a_smem_g<KA>()));
+    CU(cudaFuncSetAttribute(big_pass_col8<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(sizeof(double2) * 16 * kCol8Pad)));
+    CU(cudaFuncSetAttribute(big_pass_col8<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(sizeof(double2) * 16 * kCol8Pad)));
     return 0;
   });
 }
@@ -529,10 +533,28 @@ int big_launch_a(afd_plan* p, bool inv, int mode, const double2* ghat_rev, const
   });
 }
 
+static const bool kCol8Enabled = !(getenv("AFD_COL8") && atoi(getenv("AFD_COL8")) == 0);
+
 int big_launch_cols(afd_plan* p, bool inv, int last_mode, int scale_n, int64_t r0, int64_t rows,
                     double2* fout, const int* stopped, cudaStream_t st) {
   dim3 grid((unsigned)big_col_ctas(p), (unsigned)rows);
   for (int b0 = p->ka; b0 < p->K; b0 += 4) {
+    // 8 stages at once (big_pass_col8) where they are the field's last eight
+    // or are followed by more column stages (in-place)
+    if (inv && b0 + 8 <= p->K && (last_mode == 1 || b0 + 8 < p->K) && kCol8Enabled) {
+      const int mode8 = (b0 + 8 >= p->K) ? 1 : 0;
+      const size_t sm8 = sizeof(double2) * 16 * kCol8Pad;
+      if (mode8 == 1)
+        big_pass_col8<1><<<grid, 256, sm8, st>>>(p->K, b0, p->Y, p->twst, p->scales, r0,
+                                                 r0 + rows, p->big_cand, stopped);
+      else
+        big_pass_col8<0><<<grid, 256, sm8, st>>>(p->K, b0, p->Y, p->twst, p->scales, r0,
+                                                 r0 + rows, p->big_cand, stopped);
+      p->launches++;
+      CU(cudaGetLastError());
+      b0 += 4;
+      continue;
+    }
     const int mode = (b0 + 4 >= p->K) ? last_mode : 0;
     if (inv && mode == 1)
       big_pass_col<true, 1><<<grid, kColThreads, 0, st>>>(p->K, p->ka, b0, mode, scale_n, p->Y,

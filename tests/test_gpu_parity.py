@@ -251,6 +251,23 @@ def test_c4_length_decompose_matches_oracle(afd):
     assert np.array_equal(d.remainder, o.remainder)
 
 
+@pytest.mark.parametrize("k", [17, 18, 19])
+def test_fused_column_pass_lengths_match_oracle(afd, k):
+    """N = 2^17..2^19: pass A of 2^9..2^11 points then the 8-stage fused
+    column pass (big_pass_col8), field argmax + update vs the CPU oracle."""
+    core, _ = afd
+    from paper_1711_08604_b200 import workloads as W
+    n = 1 << k
+    g = W.pole_sum(n, 24, 0.97, k)
+    radii = (0.0, 0.3, 0.7, 0.9, 0.97, 0.995)
+    d = core.decompose(g, core.ParameterGrid(radii, n), max_terms=3)
+    o = O.decompose(g, np.array(radii), max_terms=3)
+    assert [s.point.angle_index for s in d.steps] == list(o.steps["j"])
+    assert [s.coefficient for s in d.steps] == list(o.steps["c_re"] + 1j * o.steps["c_im"])
+    assert [s.residual_energy for s in d.steps] == list(o.steps["residual"])
+    assert np.array_equal(d.remainder, o.remainder)
+
+
 @pytest.mark.parametrize("case", ["c0", "f2_dc", "big16384"])
 def test_sharded_step_api_on_one_gpu(afd, case):
     """Two radius shards driven through afd_select_local / afd_apply_step,
