@@ -47,7 +47,10 @@ int fail(int code, const char* fmt, ...) {
 constexpr int kMinK = 3;
 constexpr int kMaxOnChipK = 13;
 constexpr int kMaxK = 22;
-constexpr size_t kBigBatchBytes = 160ull << 20;  // row-batch intermediate (large N)
+// Row-batch intermediate for large N.  Larger batches measured faster all the
+// way up (fewer launches and launch tails; L2 residency matters less): c2
+// field 3.34 ms at 148 rows -> 2.59 ms with all 4096 rows (4 GiB).
+constexpr size_t kBigBatchBytes = 4ull << 30;
 
 }  // namespace
 
@@ -750,18 +753,20 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
     p->launches += 2;
     if (cudaGetLastError() != cudaSuccess) return cleanup(fail(AFD_E_CUDA, "bitrev launch"));
     {
-      // Rows per batch: as many as kBigBatchBytes of intermediate allows
-      // (fewer launches and waves per step measured faster than keeping the
-      // batch L2-resident: c2 field 4.23 ms at 48 rows -> 3.67 ms at 148),
-      // rounded down to a whole number of pass-A rounds when possible.
+      // Rows per batch: all of them if kBigBatchBytes allows, else as many as
+      // it allows rounded down to a whole number of pass-A rounds.
       const int64_t cap = std::max<int64_t>(1, (int64_t)(kBigBatchBytes / (N * 16)));
       const int64_t nblk = N >> p->ka, slots = 2LL * p->sms;
       int64_t rows = cap;
-      for (int64_t r = cap; r >= std::max<int64_t>(1, cap / 2); --r)
-        if ((r * nblk) % slots == 0) {
-          rows = r;
-          break;
-        }
+      if (m1 - m0 <= cap) {
+        rows = m1 - m0;  // one batch: no per-batch launch tails at all
+      } else {
+        for (int64_t r = cap; r >= std::max<int64_t>(1, cap / 2); --r)
+          if ((r * nblk) % slots == 0) {
+            rows = r;
+            break;
+          }
+      }
       if (const char* e = getenv("AFD_BIG_ROWS")) rows = atoll(e);  // experiments
       p->big_rows = std::max<int64_t>(1, std::min<int64_t>(m1 - m0, rows));
     }
