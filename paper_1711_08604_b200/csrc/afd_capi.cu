@@ -96,6 +96,7 @@ struct afd_plan {
   int64_t big_rows = 0;        // rows per batch
   double2* Y = nullptr;        // [big_rows][N]
   Cand* big_cand = nullptr;    // [big_rows][N/16/256]
+  unsigned* row_ctr = nullptr; // [max_batch][2] field row counters (dynamic rows)
   double* nodes = nullptr;     // [2 * N / kNodeLen]
   BigSel* sel = nullptr;
   int* amb = nullptr;
@@ -293,7 +294,8 @@ int groups_eff(const afd_plan* p, int64_t rows, int64_t batch) {
 
 template <int K>
 int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64_t batch,
-                 Cand* cand, int ncta, double2* field_out, const State* state, cudaStream_t st) {
+                 Cand* cand, int ncta, double2* field_out, const State* state, cudaStream_t st,
+                 unsigned* row_ctr = nullptr, int launch_id = 0) {
   constexpr int G = groups_for<K>();
   const int ge = groups_eff<K>(p, r1 - r0, batch);  // ncta from field_ctas_for
   dim3 grid(ncta, (unsigned)batch);
@@ -307,11 +309,11 @@ int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64
     if (tm) {
       field_kernel<K, kFieldRB, G, true, field_tmem_capable<K>()><<<grid, block, smem, st>>>(
           ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, nullptr, field_out, nullptr,
-          p->tw_img, field_pp());
+          p->tw_img, field_pp(), (unsigned*)nullptr, 0);
     } else {
       field_kernel<K, kFieldRB, G, true><<<grid, block, smem, st>>>(
           ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, nullptr, field_out, nullptr,
-          p->tw_img, field_pp());
+          p->tw_img, field_pp(), (unsigned*)nullptr, 0);
     }
   } else {
     auto kern = tm ? field_kernel<K, kFieldRB, G, false, field_tmem_capable<K>()>
@@ -319,7 +321,7 @@ int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64
     CU(launch_pdl(kern, grid, dim3(block), smem, st, ghat, (const double*)p->pw,
                   (const double*)p->scales, (const double2*)p->twst, (long long)r0,
                   (long long)r1, (long long)p->m0, cand, (double2*)nullptr, state,
-                  (const double2*)p->tw_img, field_pp()));
+                  (const double2*)p->tw_img, field_pp(), row_ctr, launch_id));
   }
   p->launches++;
   CU(cudaGetLastError());
@@ -407,6 +409,36 @@ int field_ctas_for(const afd_plan* p, int64_t rows, int64_t batch) {
 }
 
 
+// Dynamic field rows (field_kernel row_ctr): a single signal whose rows fill
+// both row-groups of every CTA runs on every SM, later rows claimed at run
+// time.  Off by default (AFD_FIELD_DYN=1 turns it on): on c1 the 148-CTA
+// launch with run-time rows measured slower (1.095e11 vs 1.163e11 evals/s)
+// than the static 128-CTA schedule.  0 = not used.
+static bool field_dyn_enabled() {
+  static int v = [] {
+    const char* e = getenv("AFD_FIELD_DYN");
+    return e ? atoi(e) : 0;
+  }();
+  return v != 0;
+}
+int field_dyn_ctas(const afd_plan* p, int64_t rows, int64_t batch) {
+  if (!field_dyn_enabled() || p->big || p->engine != 0 || batch != 1) return 0;
+  AFD_DISPATCH(p->K, {
+    constexpr int G = groups_for<KK>();
+    if (G < 2 || Geo<KK, kFieldRB>::T % 32 != 0 || groups_eff<KK>(p, rows, batch) != G) return 0;
+    const int64_t slots = (int64_t)p->sms * p->field_occ;
+    if ((rows + G - 1) / G <= slots) return 0;  // one row per group already: nothing to balance
+    return (int)slots;
+  });
+}
+
+// CTAs per signal of the decomposition's field launches
+int decomp_field_ctas(const afd_plan* p, int64_t batch) {
+  const int64_t rows = p->m1 - p->m0;
+  const int d = field_dyn_ctas(p, rows, batch);
+  return d ? d : field_ctas_for(p, rows, batch);
+}
+
 int ensure_cand(afd_plan* p, int64_t batch, int ncta) {
   if (ncta > p->ncand_cap) {
     if (p->cand) cudaFree(p->cand);
@@ -458,9 +490,11 @@ int enqueue_decompose(afd_plan* p, int64_t batch, int max_terms, double thr, int
                       cudaStream_t st) {
   const int64_t rows = p->m1 - p->m0;
   const int G = groups_of(p->K);
-  const int ncta = field_ctas_for(p, rows, batch);
+  const int ncta = decomp_field_ctas(p, batch);
+  const bool dyn = field_dyn_ctas(p, rows, batch) > 0;
   int rc;
   if ((rc = ensure_cand(p, batch, ncta))) return rc;
+  if (dyn) CU(cudaMemsetAsync(p->row_ctr, 0, sizeof(unsigned) * 2 * (size_t)batch, st));
   AFD_DISPATCH(p->K, {
     if ((rc = launch_step<KK>(p, -1, max_terms, thr, dc_first, p->gin, nullptr, 0, batch,
                               p->steps, st)))
@@ -471,7 +505,7 @@ int enqueue_decompose(afd_plan* p, int64_t batch, int max_terms, double thr, int
           rc = launch_direct(p, p->rem, p->m0, p->m1, batch, p->cand, nullptr, p->state, st);
         else
           rc = launch_field<KK>(p, p->ghat, p->m0, p->m1, batch, p->cand, ncta, nullptr,
-                                p->state, st);
+                                p->state, st, dyn ? p->row_ctr : nullptr, k);
         if (rc) return rc;
       }
       if ((rc = launch_step<KK>(p, k, max_terms, thr, dc_first, nullptr, p->cand, ncta, batch,
@@ -723,6 +757,7 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
   ALLOC(p->rem, sizeof(double2) * N * max_batch);
   ALLOC(p->gin, sizeof(double2) * N * max_batch);
   ALLOC(p->state, sizeof(State) * max_batch);
+  ALLOC(p->row_ctr, sizeof(unsigned) * 2 * max_batch);
 #undef ALLOC
 #define ALLOC2(ptr, bytes)                                                         \
   do {                                                                             \
@@ -803,6 +838,7 @@ int afd_plan_destroy(afd_plan* p) {
   cudaFree(p->state);
   cudaFree(p->cand);
   cudaFree(p->steps);
+  cudaFree(p->row_ctr);
   cudaFree(p->scratch);
   cudaFree(p->Y);
   cudaFree(p->big_cand);
@@ -1026,7 +1062,7 @@ int afd_decompose(afd_plan* p, const double* g0, int64_t batch, int max_terms, d
     if (p->gexec) cudaGraphExecDestroy(p->gexec);
     p->gexec = nullptr;
     // make sure buffers exist before capture (allocation is not capturable)
-    const int ncta = field_ctas_for(p, p->m1 - p->m0, batch);
+    const int ncta = decomp_field_ctas(p, batch);
     if ((rc = ensure_cand(p, batch, ncta))) return rc;
     cudaStream_t cap;
     CU(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
@@ -1252,12 +1288,16 @@ int afd_time_field(afd_plan* p, const double* ghat, int64_t batch, int reps, dou
   }
   // back-to-back launches (PDL-chained, as inside a decomposition) between
   // two events: the average launch duration in a stream of field launches
-  const int ncta = field_ctas_for(p, p->m1 - p->m0, batch);
+  // (the decomposition's launch configuration, dynamic rows included)
+  const int ncta = decomp_field_ctas(p, batch);
+  const bool dyn = field_dyn_ctas(p, p->m1 - p->m0, batch) > 0;
   if ((rc = ensure_cand(p, batch, ncta))) return rc;
+  if (dyn) CU(cudaMemsetAsync(p->row_ctr, 0, sizeof(unsigned) * 2 * (size_t)batch, st));
+  int launch_id = 0;
   auto one = [&]() -> int {
     AFD_DISPATCH(p->K, {
       return launch_field<KK>(p, (const double2*)ghat, p->m0, p->m1, batch, p->cand, ncta,
-                              nullptr, nullptr, st);
+                              nullptr, nullptr, st, dyn ? p->row_ctr : nullptr, launch_id++);
     });
     return fail(AFD_E_UNSUPPORTED, "transform length");
   };

@@ -78,6 +78,12 @@ struct FieldHook {
   int count;       // threads of both groups
   long long* st;   // timing stamps of this row (timing builds) or null
   bool tm_fence;   // TMEM written before the release (gh spectrum, TM variant)
+  // dynamic rows: the group leader publishes its claim of the next row after
+  // the first exchange (the atomic has long returned; the second exchange's
+  // barriers make the slot visible to the group)
+  int* claim_slot;           // null: not the leader / static rows
+  const unsigned* claim;     // the leader's atomicAdd result
+  int claim_base;
   __device__ __forceinline__ void before(int) const {}
   __device__ __forceinline__ void after(int pass) const {
     if (pass == 0 && arrive) {
@@ -89,6 +95,7 @@ struct FieldHook {
 #endif
   }
   __device__ __forceinline__ void exch(int pass) const {
+    if (pass == 0 && claim_slot != nullptr) *claim_slot = claim_base + (int)*claim;
 #ifdef AFD_FIELD_TIMING
     if (st) st[4 + 2 * pass] = ftime();
 #endif
@@ -112,7 +119,9 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
              double2* __restrict__ field_out,      // [row1-row0][N] (MATERIALIZE)
              const State* __restrict__ state,      // per-signal stop flags or null
              const double2* __restrict__ tw_img,   // SmemTw<K,RB> image (one bulk copy)
-             int pp) {                             // 1: offset the row-groups (FieldHook)
+             int pp,                               // 1: offset the row-groups (FieldHook)
+             unsigned* __restrict__ row_ctr,       // dynamic rows: [batch][2] counters or null
+             int launch_id) {                      // selects / resets the counter pair
   using Gm = Geo<K, RB>;
   constexpr int N = Gm::N, T = Gm::T, P = Gm::P;
   extern __shared__ double2 smem[];
@@ -189,7 +198,7 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   // '>' keeps the lowest flat index among equal magnitudes; the flat index is
   // formed once at the end.
   double best_mag = -1.0, best_re = 0.0, best_im = 0.0;
-  int best_rd = -1, best_i = 0;
+  int best_sl = -1, best_i = 0;
 
   // row counts fit 32 bits (M <= 2^31); 32-bit loop state keeps registers
   // for the butterflies
@@ -206,6 +215,13 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   // (always for TM: group 1 reads the spectrum group 0 put in TMEM)
   const bool offset = kGroupSync && Gr == 2 && (pp > 0 || TM) &&
                       (int)blockIdx.x * Gr + 1 < rows;
+  // Dynamic rows (row_ctr): each group's first row is static, later rows are
+  // claimed from a per-launch counter (atomicAdd one row ahead), so groups
+  // that start late or run slow take fewer rows.  Rows of a group still
+  // increase, which the first-maximum tracking below relies on.
+  const bool dyn = kGroupSync && row_ctr != nullptr;
+  unsigned* ctr = dyn ? row_ctr + 2 * sig + (launch_id & 1) : nullptr;
+  __shared__ int next_sl[2][2];  // [group][row parity]
   // First row: its r^l values are step-independent and are loaded before the
   // PDL wait; the spectrum and the stop flags come from the previous kernel.
   double2 v[P];
@@ -260,11 +276,17 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     }
     pdl_trigger();
     FSTAMP(0, 1);
+    // the previous launch is complete: clear the next launch's counter
+    if (dyn && threadIdx.x == 0 && blockIdx.x == 0) row_ctr[2 * sig + ((launch_id + 1) & 1)] = 0;
   }
-  for (int rd = 0; rd < rounds; ++rd) {
-    const int sl = rd * per_round + (int)blockIdx.x * Gr + g;  // row within [row0, row1)
+  // row within [row0, row1); groups that share warps (no kGroupSync) step
+  // through `rounds` together with inactive tails masked
+  int sl = (int)blockIdx.x * Gr + g;
+  for (int rd = 0; kGroupSync ? sl < rows : rd < rounds; ++rd) {
     const long long s = row0 + sl;
-    const bool active = s < row1;
+    const bool active = kGroupSync || sl < rows;
+    unsigned claim = 0;
+    if (dyn && tp == 0) claim = atomicAdd(ctr, 1u);
     if (rd > 0 && active) {
       // prologue: y = powers * c[rev] (transform.py:198), per component
       if constexpr (TM) {
@@ -308,11 +330,13 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
         asm volatile("bar.sync 3, %0;" ::"r"(2 * T) : "memory");
         if constexpr (TM) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       }
-      const FieldHook hook{offset && rd == 0 && g == 0, 2 * T, st, TM};
+      const FieldHook hook{offset && rd == 0 && g == 0, 2 * T, st, TM,
+                           (dyn && tp == 0) ? &next_sl[g][rd & 1] : nullptr, &claim, per_round};
       fft_passes<K, true, RB>(v, tp, active, sm, tw, GroupSync{1 + g, T}, hook);
     } else {
       fft_passes<K, true, RB>(v, tp, active, sm, tw);
     }
+    const int sl_next = dyn ? next_sl[g][rd & 1] : sl + per_round;
     if (active) {
       const double sc = __ldg(scales + s);
 #pragma unroll
@@ -327,13 +351,14 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
             best_mag = mg;
             best_re = f.x;
             best_im = f.y;
-            best_rd = rd;
+            best_sl = sl;
             best_i = i;
           }
         }
       }
     }
     FSTAMP(rd, 14);
+    sl = sl_next;
   }
   if constexpr (TM) {  // all TMEM reads done: release the columns
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -346,9 +371,8 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   __syncthreads();  // all groups done before the block-wide reduction
   Cand best;
   best.mag = best_mag;
-  const long long best_s = row0 + (long long)best_rd * per_round + (long long)blockIdx.x * Gr + g;
-  best.flat =
-      best_rd >= 0 ? best_s * (long long)N + out_pos<K, RB>(tp, best_i) : 0x7fffffffffffffffLL;
+  best.flat = best_sl >= 0 ? (row0 + best_sl) * (long long)N + out_pos<K, RB>(tp, best_i)
+                           : 0x7fffffffffffffffLL;
   best.re = best_re;
   best.im = best_im;
   // CTA reduction of the candidates (first maximum).
