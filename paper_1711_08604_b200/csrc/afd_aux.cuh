@@ -72,6 +72,27 @@ __global__ void cand_reduce_kernel(const Cand* __restrict__ in, int n_per, Cand*
   if (threadIdx.x == 0) out[blockIdx.x] = b;
 }
 
+// First stage of a large candidate reduction: CTA b reduces in[b*per ..
+// min((b+1)*per, n)) -> out[b] (loads issued 4 at a time; the first-maximum
+// merge is order-free, so any split gives the same result).
+__global__ void cand_partial_kernel(const Cand* __restrict__ in, int n, int per,
+                                    Cand* __restrict__ out) {
+  Cand b = cand_none();
+  const int lo = blockIdx.x * per, hi = min(n, lo + per);
+  for (int i = lo + threadIdx.x; i < hi; i += 4 * blockDim.x) {
+    Cand c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = i + u * blockDim.x;
+      c[u] = k < hi ? in[k] : cand_none();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cand_merge(b, c[u]);
+  }
+  b = block_argmax(b);
+  if (threadIdx.x == 0) out[blockIdx.x] = b;
+}
+
 __global__ void neutral_cand_kernel(Cand* out, int batch) {
   for (int i = threadIdx.x; i < batch; i += blockDim.x) out[i] = cand_none();
 }

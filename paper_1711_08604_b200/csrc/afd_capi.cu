@@ -51,6 +51,7 @@ constexpr int kMaxK = 22;
 // way up (fewer launches and launch tails; L2 residency matters less): c2
 // field 3.34 ms at 148 rows -> 2.59 ms with all 4096 rows (4 GiB).
 constexpr size_t kBigBatchBytes = 4ull << 30;
+constexpr int kBigParts = 256;  // first-stage candidate partials (large N)
 
 }  // namespace
 
@@ -96,6 +97,7 @@ struct afd_plan {
   int64_t big_rows = 0;        // rows per batch
   double2* Y = nullptr;        // [big_rows][N]
   Cand* big_cand = nullptr;    // [big_rows][N/16/256]
+  Cand* big_part = nullptr;    // [kBigParts] first-stage reduction of big_cand
   unsigned* row_ctr = nullptr; // [max_batch][2] field row counters (dynamic rows)
   double* nodes = nullptr;     // [2 * N / kNodeLen]
   BigSel* sel = nullptr;
@@ -615,6 +617,21 @@ int big_launch_cols(afd_plan* p, bool inv, int last_mode, int scale_n, int64_t r
   return 0;
 }
 
+// The field's per-CTA candidates (big_rows x col CTAs, up to 65536) reduced
+// in two stages: kBigParts CTAs, then one (a single CTA over all of them was
+// 147 us per c2 step).  Returns the partials and their count for big_select.
+int big_reduce_cands(afd_plan* p, cudaStream_t st, const Cand** parts, int* nparts) {
+  const int n = (int)(p->big_rows * big_col_ctas(p));
+  const int np = std::min(kBigParts, (n + 255) / 256);
+  const int per = (n + np - 1) / np;
+  cand_partial_kernel<<<np, 256, 0, st>>>(p->big_cand, n, per, p->big_part);
+  p->launches++;
+  CU(cudaGetLastError());
+  *parts = p->big_part;
+  *nparts = np;
+  return 0;
+}
+
 // Field rows [r0, r1) of one spectrum: argmax into big_cand (fout == null,
 // slots initialised here) or materialised rows into fout.
 int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, double2* fout,
@@ -672,8 +689,7 @@ int big_step(afd_plan* p, int sig, int k, int max_terms, double thr, int dc_firs
   } else {
     if (!cands) {
       if ((rc = big_field(p, ghat_rev, p->m0, p->m1, nullptr, stopped, st))) return rc;
-      cands = p->big_cand;
-      ncand = (int)(p->big_rows * big_col_ctas(p));
+      if ((rc = big_reduce_cands(p, st, &cands, &ncand))) return rc;
     }
     big_select_kernel<<<1, 256, 0, st>>>(k, dc_first, p->K, cands, ncand, nullptr, 0, p->radii,
                                          p->circle, state, p->sel);
@@ -807,6 +823,7 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
     }
     ALLOC2(p->Y, sizeof(double2) * N * p->big_rows);
     ALLOC2(p->big_cand, sizeof(Cand) * p->big_rows * big_col_ctas(p));
+    ALLOC2(p->big_part, sizeof(Cand) * kBigParts);
     ALLOC2(p->nodes, sizeof(double) * 2 * (N / kNodeLen));
     ALLOC2(p->sel, sizeof(BigSel));
     ALLOC2(p->amb, sizeof(int));
@@ -842,6 +859,7 @@ int afd_plan_destroy(afd_plan* p) {
   cudaFree(p->scratch);
   cudaFree(p->Y);
   cudaFree(p->big_cand);
+  cudaFree(p->big_part);
   cudaFree(p->nodes);
   cudaFree(p->sel);
   cudaFree(p->amb);
@@ -943,13 +961,15 @@ int afd_field_argmax(afd_plan* p, const double* ghat, afd_candidate* out, int64_
   if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   if (p->big) {
-    const int nc = (int)(p->big_rows * big_col_ctas(p));
     for (int64_t b = 0; b < batch; ++b) {
       bitrev_copy_kernel<<<256, 256, 0, st>>>(p->K, p->ka, (const double2*)ghat + b * p->n,
                                               p->tmp);
       p->launches++;
       if ((rc = big_field(p, p->tmp, p->m0, p->m1, nullptr, nullptr, st))) return rc;
-      cand_reduce_kernel<<<1, 256, 0, st>>>(p->big_cand, nc, (Cand*)out + b);
+      const Cand* parts;
+      int np;
+      if ((rc = big_reduce_cands(p, st, &parts, &np))) return rc;
+      cand_reduce_kernel<<<1, 256, 0, st>>>(parts, np, (Cand*)out + b);
       p->launches++;
     }
     CU(cudaGetLastError());
@@ -1179,11 +1199,13 @@ int afd_select_local(afd_plan* p, int k, int dc_first, afd_candidate* cand, int6
     return 0;
   }
   if (p->big) {
-    const int nc = (int)(p->big_rows * big_col_ctas(p));
     for (int64_t b = 0; b < batch; ++b) {
       if ((rc = big_field(p, p->ghat + b * p->n, p->m0, p->m1, nullptr, &p->state[b].stopped, st)))
         return rc;
-      cand_reduce_kernel<<<1, 256, 0, st>>>(p->big_cand, nc, (Cand*)cand + b);
+      const Cand* parts;
+      int np;
+      if ((rc = big_reduce_cands(p, st, &parts, &np))) return rc;
+      cand_reduce_kernel<<<1, 256, 0, st>>>(parts, np, (Cand*)cand + b);
       p->launches++;
     }
     CU(cudaGetLastError());
