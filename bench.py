@@ -46,6 +46,23 @@ def flops_per_eval(n):
     return 5 * (int(n).bit_length() - 1) + 7
 
 
+def bytes_per_eval(n):
+    """Algorithmic HBM bytes per grid eval of the field: 0 for
+    N <= 8192 (on-chip transform, the r^l table and spectrum stay in L2); for
+    larger N the row-batch intermediate is written and read once (32 B) and
+    the r^l table no longer fits in L2 (8 B)."""
+    return 0 if n <= 8192 else 40
+
+
+def hbm_peak_gbs():
+    """MEASURED_PEAKS.json (driver-written) else the profiling guide's fallback."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(p))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, ValueError, KeyError):
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
 def fp64_instr_per_eval(n):
     """FP64-pipe instructions per grid eval of the exact field kernel: prologue
     2 DMUL, stage 0 2 DADD, each later stage 4 (2 DMUL + 2 DFMA + 4 DADD per
@@ -312,20 +329,38 @@ def run_ours(args):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get("field_kernel_%s" % w.name)
-    roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": traffic,
-                "kernel": "field_kernel (fused prologue + inverse DIT + scale + |.|^2 + argmax)",
-                "flops_per_eval": fpe, "evals_per_launch": w.batch * w.m * w.n,
-                "launch_ms": field_ms,
-                "peak_source": "measured in-run DFMA microbenchmark (afd_fp64_peak); "
-                               "MEASURED_PEAKS.json has no FP64 entry",
-                "field_share_of_step": (field_ms * (w.steps) / (total_ms / args.steps)),
-                # bit-exact radix-2 arithmetic is mostly unfused: per eval the kernel
-                # issues fp64_instr_per_eval FP64-pipe instructions for F(N) flops, so
-                # even a saturated FP64 pipe reaches only this fraction of the DFMA peak
-                "fp64_instr_per_eval": fp64_instr_per_eval(w.n),
-                "frac_ceiling_at_this_instruction_mix":
-                    fpe / (2.0 * fp64_instr_per_eval(w.n))}
+    # the binding roofline: FP64 for N <= 8192 (0 algorithmic HBM bytes), HBM
+    # for the large-N path (r^l table + row-batch intermediate)
+    evals = w.batch * w.m * w.n
+    bpe = bytes_per_eval(w.n)
+    hbm_peak, hbm_src = hbm_peak_gbs()
+    t_fp64 = evals * fpe / (peak * 1e12)
+    t_hbm = evals * bpe / (hbm_peak * 1e9)
+    if t_hbm > t_fp64:
+        hbm_achieved = evals * bpe / (field_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": hbm_achieved / hbm_peak, "traffic": traffic,
+                    "bytes_per_eval": bpe, "peak_source": hbm_src,
+                    "fp64": {"achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                             "frac": achieved / peak}}
+    else:
+        roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": traffic,
+                    "peak_source": "measured in-run DFMA microbenchmark (afd_fp64_peak); "
+                                   "MEASURED_PEAKS.json has no FP64 entry",
+                    # bit-exact radix-2 arithmetic is mostly unfused: per eval the
+                    # kernel issues fp64_instr_per_eval FP64-pipe instructions for
+                    # F(N) flops, so even a saturated FP64 pipe reaches only this
+                    # fraction of the DFMA peak
+                    "fp64_instr_per_eval": fp64_instr_per_eval(w.n),
+                    "frac_ceiling_at_this_instruction_mix":
+                        fpe / (2.0 * fp64_instr_per_eval(w.n))}
+    roofline.update({
+        "kernel": ("field_kernel (fused prologue + inverse DIT + scale + |.|^2 + argmax)"
+                   if w.n <= 8192 else
+                   "large-N field: big_pass_a + column pass(es) over the row batches"),
+        "flops_per_eval": fpe, "evals_per_launch": evals, "launch_ms": field_ms,
+        "field_share_of_step": (field_ms * (w.steps) / (total_ms / args.steps))})
 
     # e2e through the public API, host buffers, pinned H2D + D2H in the region
     grid = core.ParameterGrid(radii, w.n)
@@ -481,6 +516,14 @@ def run_sharded(args, w, radii, sig, mode, world, rank, local, dev):
                 "flops_per_eval": fpe, "evals_per_launch": (m1 - m0) * w.n,
                 "launch_ms": field_ms,
                 "peak_source": "measured in-run DFMA microbenchmark (afd_fp64_peak)"}
+    bpe = bytes_per_eval(w.n)
+    hbm_peak, hbm_src = hbm_peak_gbs()
+    if bpe and bpe / (hbm_peak * 1e9) > fpe / (peak * 1e12):  # HBM-bound (large N)
+        hbm = (m1 - m0) * w.n * bpe / (field_ms * 1e-3) / 1e9
+        roofline.update({"bound": "hbm", "achieved": hbm, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": hbm / hbm_peak, "bytes_per_eval": bpe, "peak_source": hbm_src,
+                         "fp64": {"achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                                  "frac": achieved / peak}})
 
     # e2e through the public API with host buffers
     grid = core.ParameterGrid(radii, w.n)
