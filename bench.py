@@ -46,12 +46,21 @@ def flops_per_eval(n):
     return 5 * (int(n).bit_length() - 1) + 7
 
 
-def bytes_per_eval(n):
+def bytes_per_eval(n, radii=None):
     """Algorithmic HBM bytes per grid eval of the field: 0 for
     N <= 8192 (on-chip transform, the r^l table and spectrum stay in L2); for
     larger N the row-batch intermediate is written and read once (32 B) and
-    the r^l table no longer fits in L2 (8 B)."""
-    return 0 if n <= 8192 else 40
+    the r^l table no longer fits in L2: 8 B per entry that is not an
+    underflowed zero (r^l == +0 from l ~ 745/ln(1/r) on, never loaded)."""
+    if n <= 8192:
+        return 0.0
+    if radii is None:
+        return 40.0
+    import math
+    live = 0
+    for r in radii:
+        live += 1 if r <= 0.0 else min(n, int(math.ceil(745.14 / -math.log(r))))
+    return 32.0 + 8.0 * live / (len(radii) * n)
 
 
 def hbm_peak_gbs():
@@ -332,7 +341,7 @@ def run_ours(args):
     # the binding roofline: FP64 for N <= 8192 (0 algorithmic HBM bytes), HBM
     # for the large-N path (r^l table + row-batch intermediate)
     evals = w.batch * w.m * w.n
-    bpe = bytes_per_eval(w.n)
+    bpe = bytes_per_eval(w.n, radii)
     hbm_peak, hbm_src = hbm_peak_gbs()
     t_fp64 = evals * fpe / (peak * 1e12)
     t_hbm = evals * bpe / (hbm_peak * 1e9)
@@ -516,7 +525,7 @@ def run_sharded(args, w, radii, sig, mode, world, rank, local, dev):
                 "flops_per_eval": fpe, "evals_per_launch": (m1 - m0) * w.n,
                 "launch_ms": field_ms,
                 "peak_source": "measured in-run DFMA microbenchmark (afd_fp64_peak)"}
-    bpe = bytes_per_eval(w.n)
+    bpe = bytes_per_eval(w.n, radii[m0:m1])
     hbm_peak, hbm_src = hbm_peak_gbs()
     if bpe and bpe / (hbm_peak * 1e9) > fpe / (peak * 1e12):  # HBM-bound (large N)
         hbm = (m1 - m0) * w.n * bpe / (field_ms * 1e-3) / 1e9

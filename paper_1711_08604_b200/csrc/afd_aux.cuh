@@ -16,17 +16,21 @@ namespace afd {
 // cumprod over [1, r, r, ...].  One warp = 32 radii; each lane runs its
 // radius' chain, a 32x32 shared tile turns the lane-per-row values into
 // coalesced row writes.
+// pw_len[row] = the first l with r^l == 0 (the fold has underflowed and stays
+// +0 from there on), or n: the large-N prologue skips loading the zero tail.
 __global__ void power_table_kernel(const double* __restrict__ radii, long long m0, long long m1,
-                                   long long n, double* __restrict__ pw) {
+                                   long long n, double* __restrict__ pw, int* __restrict__ pw_len) {
   __shared__ double tile[32][33];
   const int lane = threadIdx.x;
   const long long row = m0 + (long long)blockIdx.x * 32 + lane;
   const double r = row < m1 ? radii[row] : 0.0;
   double v = 1.0;
+  long long len = n;
   for (long long c0 = 0; c0 < n; c0 += 32) {
 #pragma unroll 8
     for (int i = 0; i < 32; ++i) {
       if (c0 + i > 0) v = v * r;
+      if (v == 0.0 && len == n) len = c0 + i;
       tile[lane][i] = v;
     }
     __syncwarp();
@@ -36,6 +40,7 @@ __global__ void power_table_kernel(const double* __restrict__ radii, long long m
     }
     __syncwarp();
   }
+  if (pw_len != nullptr && row < m1) pw_len[row - m0] = (int)len;
 }
 
 __device__ __forceinline__ Cand cand_none() {

@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(Geo<KA, 4>::T * kBigGroups, 1)
 big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0,
            const double2* __restrict__ ghat_rev, const double2* __restrict__ x,
            const double2* __restrict__ twst, long long row0, long long row1,
-           double2* __restrict__ Y, const int* __restrict__ stopped) {
+           double2* __restrict__ Y, const int* __restrict__ stopped,
+           const int* __restrict__ pw_len) {
   using GA = Geo<KA, 4>;
   using TwA = SmemTw<KA, 4>;
   constexpr int BLK = 1 << KA, T = GA::T;
@@ -126,11 +127,16 @@ big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0
     if (mode == 0) {
       // prologue y = powers * c[rev] (transform.py:198) straight from the
       // register-layout tables (coalesced over t)
+      // r^l is exactly +0 from pw_len on (underflow): those entries are not
+      // loaded (at c2/c4 well over 90% of the table), the product with the
+      // spectrum still forms the same signed zeros
       const double* __restrict__ pr = pw_rev + (size_t)(row0 + rl - pw_row0) * N + base;
       const double2* __restrict__ gr = ghat_rev + base;
+      const int L = pw_len[row0 + rl - pw_row0];
 #pragma unroll
       for (int i = 0; i < GA::P; ++i) {
-        const double p = __ldg(pr + i * T + tid);
+        const int l = brev_rt((int)(base + ((t0 << 4) | i)), K);  // natural index
+        const double p = l < L ? __ldg(pr + i * T + tid) : 0.0;
         const double2 c = __ldg(gr + i * T + tid);
         v[i] = make_double2(p * c.x, p * c.y);
       }

@@ -99,6 +99,7 @@ struct afd_plan {
   Cand* big_cand = nullptr;    // [big_rows][N/16/256]
   Cand* big_part = nullptr;    // [kBigParts] first-stage reduction of big_cand
   unsigned* row_ctr = nullptr; // [max_batch][2] field row counters (dynamic rows)
+  int* pw_len = nullptr;       // [m1-m0] first l with r^l == 0 (or N)
   double* nodes = nullptr;     // [2 * N / kNodeLen]
   BigSel* sel = nullptr;
   int* amb = nullptr;
@@ -559,13 +560,16 @@ int big_launch_a(afd_plan* p, bool inv, int mode, const double2* ghat_rev, const
     const int block = Geo<KA, 4>::T * kBigGroups;
     if (inv && mode == 0 && KA == 12 && field_tmem_enabled())
       big_pass_a<KA, true, KA == 12><<<grid, block, big_a_smem_g<KA>(), st>>>(
-          p->K, mode, p->pw, p->m0, ghat_rev, x, p->twst, r0, r0 + rows, p->Y, stopped);
+          p->K, mode, p->pw, p->m0, ghat_rev, x, p->twst, r0, r0 + rows, p->Y, stopped,
+          p->pw_len);
     else if (inv)
       big_pass_a<KA, true><<<grid, block, big_a_smem_g<KA>(), st>>>(
-          p->K, mode, p->pw, p->m0, ghat_rev, x, p->twst, r0, r0 + rows, p->Y, stopped);
+          p->K, mode, p->pw, p->m0, ghat_rev, x, p->twst, r0, r0 + rows, p->Y, stopped,
+          p->pw_len);
     else
       big_pass_a<KA, false><<<grid, block, big_a_smem_g<KA>(), st>>>(
-          p->K, mode, p->pw, p->m0, ghat_rev, x, p->twst, r0, r0 + rows, p->Y, stopped);
+          p->K, mode, p->pw, p->m0, ghat_rev, x, p->twst, r0, r0 + rows, p->Y, stopped,
+          p->pw_len);
     p->launches++;
     CU(cudaGetLastError());
     return 0;
@@ -774,6 +778,7 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
   ALLOC(p->gin, sizeof(double2) * N * max_batch);
   ALLOC(p->state, sizeof(State) * max_batch);
   ALLOC(p->row_ctr, sizeof(unsigned) * 2 * max_batch);
+  ALLOC(p->pw_len, sizeof(int) * (size_t)(m1 - m0));
 #undef ALLOC
 #define ALLOC2(ptr, bytes)                                                         \
   do {                                                                             \
@@ -789,7 +794,8 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
   // r^l power rows (np.cumprod, transform.py:147-150), once per plan
   {
     const int64_t rows = m1 - m0;
-    power_table_kernel<<<(unsigned)((rows + 31) / 32), 32>>>(p->radii, m0, m1, n, p->pw);
+    power_table_kernel<<<(unsigned)((rows + 31) / 32), 32>>>(p->radii, m0, m1, n, p->pw,
+                                                             p->pw_len);
     p->launches++;
     if (cudaGetLastError() != cudaSuccess) return cleanup(fail(AFD_E_CUDA, "power table launch"));
   }
@@ -856,6 +862,7 @@ int afd_plan_destroy(afd_plan* p) {
   cudaFree(p->cand);
   cudaFree(p->steps);
   cudaFree(p->row_ctr);
+  cudaFree(p->pw_len);
   cudaFree(p->scratch);
   cudaFree(p->Y);
   cudaFree(p->big_cand);
