@@ -507,3 +507,24 @@ def test_c1_decomposition_bitwise_vs_oracle(afd):
         assert st.coefficient == complex(ref["c_re"], ref["c_im"])
         assert st.residual_energy == ref["residual"]
     assert np.array_equal(d.remainder.view(np.uint64), o.remainder.view(np.uint64))
+
+
+@pytest.mark.parametrize("n,m,dc,thr", [(4096, 96, True, None), (4096, 64, False, 0.02),
+                                        (8192, 1100, True, 0.05), (2048, 40, True, None)])
+def test_cluster_step_options_vs_oracle(afd, n, m, dc, thr):
+    """dc_first / threshold through the 16-CTA cluster step kernel (N = 2048..8192; at
+    N = 8192 with > 1024 radii the pole lookup reads the radii from global memory)."""
+    core, _ = afd
+    from paper_1711_08604_b200 import workloads as W
+    g = W.pole_sum(n, 20, 0.95, n + m)
+    radii = tuple(k / m for k in range(m))
+    d = core.decompose(g, core.ParameterGrid(radii, n), max_terms=12, threshold=thr,
+                       dc_first=dc)
+    o = O.decompose(g, np.array(radii), max_terms=12, threshold=thr, dc_first=dc)
+    assert len(d.steps) == len(o.steps)
+    assert [s.point.angle_index for s in d.steps] == list(o.steps["j"])
+    assert [s.point.radius for s in d.steps] == list(o.steps["radius"])
+    assert [s.coefficient for s in d.steps] == list(o.steps["c_re"] + 1j * o.steps["c_im"])
+    assert [s.residual_energy for s in d.steps] == list(o.steps["residual"])
+    assert d.initial_energy == o.initial_energy
+    assert np.array_equal(d.remainder.view(np.uint64), o.remainder.view(np.uint64))
