@@ -299,8 +299,25 @@ _PLANS_LOCK = threading.Lock()
 _MAX_PLANS = 16
 
 
+_LAST = [None, None]  # (key of the last lookup with this radii object, plan)
+
+
 def get_plan(radii, n, batch=1, m0=0, m1=None, device=None, engine=0):
     """Cached plan for (device, N, radii, shard, engine) with max_batch >= batch."""
+    # fast path: the same radii tuple object as the previous call (a grid's
+    # radii) skips hashing M floats
+    last_key, last_plan = _LAST
+    if (last_key is not None and last_key[0] is radii and last_key[1:] ==
+            (n, m0, m1, device, engine) and last_plan.max_batch >= batch and
+            last_plan.handle is not None and
+            (device is not None or last_plan.device.index == torch.cuda.current_device())):
+        return last_plan
+    p = _get_plan(radii, n, batch, m0, m1, device, engine)
+    _LAST[0], _LAST[1] = (radii, n, m0, m1, device, engine), p
+    return p
+
+
+def _get_plan(radii, n, batch, m0, m1, device, engine):
     dev = require_cuda(device)
     if not (type(radii) is tuple and all(type(r) is float for r in radii[:1])):
         radii = tuple(float(r) for r in radii)
