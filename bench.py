@@ -340,13 +340,13 @@ def run_ours(args):
         traffic = json.load(open(tpath)).get("field_kernel_%s" % w.name)
     # the binding roofline: FP64 for N <= 8192 (0 algorithmic HBM bytes), HBM
     # for the large-N path (r^l table + row-batch intermediate)
-    evals = w.batch * w.m * w.n
+    launch_evals = w.batch * w.m * w.n
     bpe = bytes_per_eval(w.n, radii)
     hbm_peak, hbm_src = hbm_peak_gbs()
-    t_fp64 = evals * fpe / (peak * 1e12)
-    t_hbm = evals * bpe / (hbm_peak * 1e9)
+    t_fp64 = launch_evals * fpe / (peak * 1e12)
+    t_hbm = launch_evals * bpe / (hbm_peak * 1e9)
     if t_hbm > t_fp64:
-        hbm_achieved = evals * bpe / (field_ms * 1e-3) / 1e9
+        hbm_achieved = launch_evals * bpe / (field_ms * 1e-3) / 1e9
         roofline = {"bound": "hbm", "achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
                     "frac": hbm_achieved / hbm_peak, "traffic": traffic,
                     "bytes_per_eval": bpe, "peak_source": hbm_src,
@@ -368,7 +368,7 @@ def run_ours(args):
         "kernel": ("field_kernel (fused prologue + inverse DIT + scale + |.|^2 + argmax)"
                    if w.n <= 8192 else
                    "large-N field: big_pass_a + column pass(es) over the row batches"),
-        "flops_per_eval": fpe, "evals_per_launch": evals, "launch_ms": field_ms,
+        "flops_per_eval": fpe, "evals_per_launch": launch_evals, "launch_ms": field_ms,
         "field_share_of_step": (field_ms * (w.steps) / (total_ms / args.steps))})
 
     # e2e through the public API, host buffers, pinned H2D + D2H in the region
