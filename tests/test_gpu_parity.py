@@ -528,3 +528,25 @@ def test_cluster_step_options_vs_oracle(afd, n, m, dc, thr):
     assert [s.residual_energy for s in d.steps] == list(o.steps["residual"])
     assert d.initial_energy == o.initial_energy
     assert np.array_equal(d.remainder.view(np.uint64), o.remainder.view(np.uint64))
+
+
+def test_bench_line_contract(afd):
+    """bench.py's JSON line: keys of the driver contract, parity, sane e2e/value/roofline."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3",
+                          "--warmup", "3", "--no-cpu-baseline", "--e2e-reps", "3"],
+                         capture_output=True, text=True, cwd=ROOT, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+                "roofline", "e2e", "gpu_launches", "clocks", "cpu_baseline"):
+        assert key in d, key
+    assert d["parity_vs_oracle"] is True
+    assert d["gpu_launches"] > 0
+    assert 0.3 * d["value"] < d["e2e"]["value"] < 1.05 * d["value"]
+    assert 0.0 < d["roofline"]["frac"] < 1.0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
