@@ -136,7 +136,12 @@ big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0
 #pragma unroll
       for (int i = 0; i < GA::P; ++i) {
         const int l = brev_rt((int)(base + ((t0 << 4) | i)), K);  // natural index
-        const double p = l < L ? __ldg(pr + i * T + tid) : 0.0;
+        // a predicated load in PTX: the compiler must not turn it into an
+        // unconditional load + select (the address is valid either way)
+        double p = 0.0;
+        asm volatile("{ .reg .pred q; setp.lt.s32 q, %1, %2; @q ld.global.nc.f64 %0, [%3]; }"
+                     : "+d"(p)
+                     : "r"(l), "r"(L), "l"(pr + i * T + tid));
         const double2 c = __ldg(gr + i * T + tid);
         v[i] = make_double2(p * c.x, p * c.y);
       }
