@@ -75,9 +75,11 @@ def hbm_peak_gbs():
 def fp64_instr_per_eval(n):
     """FP64-pipe instructions per grid eval of the exact field kernel: prologue
     2 DMUL, stage 0 2 DADD, each later stage 4 (2 DMUL + 2 DFMA + 4 DADD per
-    butterfly), epilogue 2 DMUL scale + 3 for |.|^2 + 1 DSETP."""
+    butterfly) except the twiddle-index-0 butterflies of stages 1-3 (pass 0:
+    1.75 per eval skipped), epilogue 2 DMUL scale + 3 for |.|^2 + 1 DSETP
+    (DESIGN.md §4)."""
     k = int(n).bit_length() - 1
-    return 2 + 2 + 4 * (k - 1) + 6
+    return 2 + 2 + 4 * (k - 1) - 1.75 + 6
 
 
 def parse():
