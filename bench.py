@@ -46,21 +46,41 @@ def flops_per_eval(n):
     return 5 * (int(n).bit_length() - 1) + 7
 
 
+def r_power_live(n, radii):
+    """Per radius, the first l with r^l == +0 in the reference's sequential fold
+    (np.cumprod, transform.py:147-150), else n — the entries the large-N
+    prologue must load.  Only r <= 0.5 ever reaches zero: for r > 0.5 the fold
+    sticks at a subnormal (k * 2^-1074 * r rounds back to k * 2^-1074), so
+    those rows are live to the end."""
+    import numpy as np
+    r = np.asarray(radii, dtype=np.float64)
+    live = np.full(r.shape, n, dtype=np.int64)
+    idx = np.nonzero(r <= 0.5)[0]
+    v = np.ones(idx.size)
+    rr = r[idx]
+    for l in range(1, n):
+        if idx.size == 0:
+            break
+        v = v * rr
+        z = v == 0.0
+        if z.any():
+            live[idx[z]] = l
+            keep = ~z
+            idx, v, rr = idx[keep], v[keep], rr[keep]
+    return live
+
+
 def bytes_per_eval(n, radii=None):
     """Algorithmic HBM bytes per grid eval of the field: 0 for
     N <= 8192 (on-chip transform, the r^l table and spectrum stay in L2); for
     larger N the row-batch intermediate is written and read once (32 B) and
-    the r^l table no longer fits in L2: 8 B per entry that is not an
-    underflowed zero (r^l == +0 from l ~ 745/ln(1/r) on, never loaded)."""
+    the r^l table no longer fits in L2: 8 B per entry that is not an exact
+    zero of the fold (those are never loaded, `r_power_live`)."""
     if n <= 8192:
         return 0.0
     if radii is None:
         return 40.0
-    import math
-    live = 0
-    for r in radii:
-        live += 1 if r <= 0.0 else min(n, int(math.ceil(745.14 / -math.log(r))))
-    return 32.0 + 8.0 * live / (len(radii) * n)
+    return 32.0 + 8.0 * float(r_power_live(n, radii).sum()) / (len(radii) * n)
 
 
 def hbm_peak_gbs():

@@ -128,7 +128,8 @@ big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0
       // prologue y = powers * c[rev] (transform.py:198) straight from the
       // register-layout tables (coalesced over t)
       // r^l is exactly +0 from pw_len on (underflow): those entries are not
-      // loaded (at c2/c4 well over 90% of the table), the product with the
+      // loaded (only radii <= 0.5 reach zero — larger ones stick at a
+      // subnormal — so about half of the c2/c4 table), the product with the
       // spectrum still forms the same signed zeros
       const double* __restrict__ pr = pw_rev + (size_t)(row0 + rl - pw_row0) * N + base;
       const double2* __restrict__ gr = ghat_rev + base;
@@ -139,9 +140,13 @@ big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0
         // a predicated load in PTX: the compiler must not turn it into an
         // unconditional load + select (the address is valid either way)
         double p = 0.0;
+#ifdef AFD_EXP_NOPW
+        p = l < L ? 0.5 : 0.0;
+#else
         asm volatile("{ .reg .pred q; setp.lt.s32 q, %1, %2; @q ld.global.nc.f64 %0, [%3]; }"
                      : "+d"(p)
                      : "r"(l), "r"(L), "l"(pr + i * T + tid));
+#endif
         const double2 c = __ldg(gr + i * T + tid);
         v[i] = make_double2(p * c.x, p * c.y);
       }

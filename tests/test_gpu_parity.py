@@ -251,6 +251,25 @@ def test_c4_length_decompose_matches_oracle(afd):
     assert np.array_equal(d.remainder, o.remainder)
 
 
+@pytest.mark.parametrize("m", [100, 163])
+def test_field_n65536_matches_oracle(afd, m):
+    """N = 2^16 (c2's length) over M = 100 / 163 radii: the large-N field
+    (pass A + column pass, all rows in one batch) — selections, coefficients,
+    energies and remainder vs the oracle."""
+    core, _ = afd
+    from paper_1711_08604_b200 import workloads as W
+    n = 1 << 16
+    g = W.pole_sum(n, 32, 0.97, 7)
+    radii = tuple(i / m for i in range(m))
+    d = core.decompose(g, core.ParameterGrid(radii, n), max_terms=3)
+    o = O.decompose(g, np.array(radii), max_terms=3)
+    assert [s.point.angle_index for s in d.steps] == list(o.steps["j"])
+    assert [s.point.radius for s in d.steps] == list(o.steps["radius"])
+    assert [s.coefficient for s in d.steps] == list(o.steps["c_re"] + 1j * o.steps["c_im"])
+    assert [s.residual_energy for s in d.steps] == list(o.steps["residual"])
+    assert np.array_equal(d.remainder, o.remainder)
+
+
 @pytest.mark.parametrize("k", [17, 18, 19])
 def test_fused_column_pass_lengths_match_oracle(afd, k):
     """N = 2^17..2^19: pass A of 2^9..2^11 points then the 8-stage fused
