@@ -140,13 +140,9 @@ big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0
         // a predicated load in PTX: the compiler must not turn it into an
         // unconditional load + select (the address is valid either way)
         double p = 0.0;
-#ifdef AFD_EXP_NOPW
-        p = l < L ? 0.5 : 0.0;
-#else
         asm volatile("{ .reg .pred q; setp.lt.s32 q, %1, %2; @q ld.global.nc.f64 %0, [%3]; }"
                      : "+d"(p)
                      : "r"(l), "r"(L), "l"(pr + i * T + tid));
-#endif
         const double2 c = __ldg(gr + i * T + tid);
         v[i] = make_double2(p * c.x, p * c.y);
       }
