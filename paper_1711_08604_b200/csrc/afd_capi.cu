@@ -13,6 +13,7 @@
 #include "../../include/afd_capi.h"
 #include "afd_kernels.cuh"
 #include "afd_aux.cuh"
+#include "afd_col_tma.cuh"
 #include "afd_step_cluster.cuh"
 #include "afd_big.cuh"
 #include "afd_direct.cuh"
@@ -100,6 +101,8 @@ struct afd_plan {
   Cand* big_part = nullptr;    // [kBigParts] first-stage reduction of big_cand
   unsigned* row_ctr = nullptr; // [max_batch][2] field row counters (dynamic rows)
   int* pw_len = nullptr;       // [m1-m0] first l with r^l == 0 (or N)
+  CUtensorMap ymap;            // Y as [big_rows][256][2^ka complex] (8-stage TMA column pass)
+  bool ymap_ok = false;
   double* nodes = nullptr;     // [2 * N / kNodeLen]
   BigSel* sel = nullptr;
   int* amb = nullptr;
@@ -546,6 +549,31 @@ int big_setup(afd_plan* p) {
                             (int)(sizeof(double2) * 16 * kCol8Pad)));
     CU(cudaFuncSetAttribute(big_pass_col8<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double2) * 16 * kCol8Pad)));
+    CU(cudaFuncSetAttribute(col_tma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)ColTma<4>::SMEM));
+    if (p->K - p->ka == 8) {
+      // Y as float64 [big_rows][256 positions u][2 * 2^ka] (position u of
+      // column q at q + (u << ka)), boxes of 16 columns x 256 positions
+      using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult qr;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) ==
+              cudaSuccess &&
+          qr == cudaDriverEntryPointSuccess && fn) {
+        const cuuint64_t dims[3] = {2ull << p->ka, 256, (cuuint64_t)p->big_rows};
+        const cuuint64_t strides[2] = {16ull << p->ka, 16ull * (cuuint64_t)p->n};
+        const cuuint32_t box[3] = {32, 256, 1}, estr[3] = {1, 1, 1};
+        p->ymap_ok = ((EncodeFn)fn)(&p->ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, p->Y, dims,
+                                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+      }
+    }
+    CU(cudaFuncSetAttribute(col_tma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)ColTma<8>::SMEM));
     return 0;
   });
 }
@@ -578,10 +606,31 @@ int big_launch_a(afd_plan* p, bool inv, int mode, const double2* ghat_rev, const
 
 static const bool kCol8Enabled = !(getenv("AFD_COL8") && atoi(getenv("AFD_COL8")) == 0);
 
+// The field's last column stages as the persistent TMA-pipelined kernel
+// (afd_col_tma.cuh); AFD_COL_TMA=0 keeps the one-tile-per-CTA kernels.
+static const bool kColTmaEnabled = !(getenv("AFD_COL_TMA") && atoi(getenv("AFD_COL_TMA")) == 0);
+
 int big_launch_cols(afd_plan* p, bool inv, int last_mode, int scale_n, int64_t r0, int64_t rows,
                     double2* fout, const int* stopped, cudaStream_t st) {
   dim3 grid((unsigned)big_col_ctas(p), (unsigned)rows);
   for (int b0 = p->ka; b0 < p->K; b0 += 4) {
+    const int left = p->K - b0;
+    if (inv && last_mode == 1 && kColTmaEnabled &&
+        (left == 4 || (left == 8 && kCol8Enabled && p->ymap_ok))) {
+      const int64_t tiles = rows * ((int64_t)1 << b0) / (left == 8 ? 16 : 256);
+      const unsigned g = (unsigned)std::min<int64_t>(p->sms, tiles);
+      if (left == 8)
+        col_tma_kernel<8><<<g, 256, ColTma<8>::SMEM, st>>>(p->K, b0, p->Y, p->twst, p->scales,
+                                                           r0, r0 + rows, p->big_cand, stopped,
+                                                           p->ymap);
+      else
+        col_tma_kernel<4><<<g, 256, ColTma<4>::SMEM, st>>>(p->K, b0, p->Y, p->twst, p->scales,
+                                                           r0, r0 + rows, p->big_cand, stopped,
+                                                           p->ymap);
+      p->launches++;
+      CU(cudaGetLastError());
+      break;
+    }
     // 8 stages at once (big_pass_col8) where they are the field's last eight
     // or are followed by more column stages (in-place)
     if (inv && b0 + 8 <= p->K && (last_mode == 1 || b0 + 8 < p->K) && kCol8Enabled) {

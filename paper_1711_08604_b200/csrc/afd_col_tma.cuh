@@ -1,0 +1,226 @@
+// afd_col_tma.cuh — the field's last column stages for large N as a
+// persistent, TMA-pipelined kernel (replaces big_pass_col<..,1> and
+// big_pass_col8<1> in the field, transform.py:199-200 + core.py:298-299).
+//
+// The column pass streams the row-batch intermediate from HBM once.  The
+// one-tile-per-CTA kernels issue their 16 loads per thread, then compute,
+// with two CTAs per SM: the SM alternates between waiting and computing
+// (c4: 3.0 TB/s, FP64 39% busy).  Here one CTA per SM walks a contiguous
+// range of tiles; while it computes tile n, tile n+1 is already in flight
+// into shared memory by bulk copies (cp.async.bulk, completion on an
+// mbarrier), so HBM streams continuously.
+//
+// Tile = 4096 evaluations of one row.  KC = 8 (the last eight stages,
+// N = 2^17..2^20): 16 columns q0..q0+15 x 256 positions q + (u << b0), landed
+// as smem[u][c] by one tensor copy (a 3-d tensor map over the row batch:
+// 256-B inner box x 256 positions x 1 row); thread (c, h) runs stages b0..b0+3
+// on u = 16h + i, writes back in place, and stages b0+4..b0+7 on u = h + 16i
+// (the transpose is the change of index, conflict-free both ways).  KC = 4
+// (N = 2^14..2^16): 256 columns x 16 positions (16 copies of 4 KiB), one
+// column per thread.  Tiles run column-chunk-major, so a CTA's tiles share
+// their columns and the stage twiddles (they depend on the column only) stay
+// in shared memory, conjugated once.  Butterflies, scale and |.|^2 are the
+// reference's own operations, so the field and its first maximum are
+// bit-identical to the two-kernel form.
+#pragma once
+
+#include <cuda.h>  // CUtensorMap
+
+#include "afd_big.cuh"
+
+namespace afd {
+
+template <int KC>
+struct ColTma {
+  static constexpr int COLS = KC == 8 ? 16 : 256;     // columns per tile
+  static constexpr int U = 1 << KC;                    // positions per column
+  static constexpr int TILE = COLS * U;                // double2 per tile (4096)
+  static constexpr int STAGES = 2;
+  static constexpr int TWA = 15 * COLS;                // stage b0..b0+3 twiddles [slot][c]
+  static constexpr int TWB = KC == 8 ? 15 * 256 : 0;   // stage b0+4.. [slot][h][c]
+  static constexpr size_t SMEM = sizeof(double2) * (STAGES * TILE + TWA + TWB);
+};
+
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, unsigned bytes,
+                                         unsigned long long* mbar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const unsigned m = (unsigned)__cvta_generic_to_shared(mbar);
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(d), "l"(gsrc), "r"(bytes), "r"(m)
+      : "memory");
+}
+
+template <int KC>
+__global__ void __launch_bounds__(256, 1)
+col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __restrict__ twst,
+               const double* __restrict__ scales, long long row0, long long row1,
+               Cand* __restrict__ cand, const int* __restrict__ stopped,
+               const __grid_constant__ CUtensorMap ymap) {
+  using C = ColTma<KC>;
+  constexpr int COLS = C::COLS, U = C::U, TILE = C::TILE;
+  extern __shared__ __align__(128) double2 csm[];
+  __shared__ __align__(8) unsigned long long full[C::STAGES];
+  if (stopped && *stopped) return;
+  double2* tw_a = csm + C::STAGES * TILE;
+  double2* tw_b = tw_a + C::TWA;
+  const long long N = 1LL << K;
+  const int rows = (int)(row1 - row0);
+  const int chunks = (1 << b0) / COLS;
+  const long long tiles = (long long)rows * chunks;
+  // contiguous tile range of this CTA, tile = chunk * rows + row
+  const long long t0 = tiles * blockIdx.x / gridDim.x;
+  const long long t1 = tiles * (blockIdx.x + 1) / gridDim.x;
+  const int ntile = (int)(t1 - t0);
+  const int tid = threadIdx.x, lane = tid & 31;
+
+  if (tid == 0) {
+    for (int s = 0; s < C::STAGES; ++s) mbar_init(&full[s], 1);
+  }
+  __syncthreads();
+  // warp 0 issues the copies of local tile n into stage n % STAGES
+  auto issue = [&](int n) {
+    const long long t = t0 + n;
+    const int chunk = (int)(t / rows), row = (int)(t % rows);
+    const double2* src = Y + (size_t)row * N + (size_t)chunk * COLS;
+    double2* dst = csm + (n % C::STAGES) * TILE;
+    unsigned long long* mb = &full[n % C::STAGES];
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(mb)),
+                   "r"((unsigned)(sizeof(double2) * TILE))
+                   : "memory");
+    __syncwarp();
+    if constexpr (KC == 8) {
+      // box {32 doubles, 256 positions, 1 row} at (2 q0, 0, row)
+      if (lane == 0)
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+            "l"(reinterpret_cast<unsigned long long>(&ymap)), "r"(2 * chunk * COLS), "r"(0),
+            "r"(row), "r"((unsigned)__cvta_generic_to_shared(mb))
+            : "memory");
+    } else {
+      for (int u = lane; u < U; u += 32)
+        bulk_g2s(dst + u * COLS, src + ((size_t)u << b0), sizeof(double2) * COLS, mb);
+    }
+  };
+  if (tid < 32) {
+    for (int n = 0; n < C::STAGES && n < ntile; ++n) issue(n);
+  }
+
+  Cand best;
+  best.mag = -1.0;
+  best.flat = 0x7fffffffffffffffLL;
+  best.re = best.im = 0.0;
+  int tw_chunk = -1;
+  const int c = KC == 8 ? (tid & 15) : tid;
+  const int h = KC == 8 ? (tid >> 4) : 0;
+  for (int n = 0; n < ntile; ++n) {
+    const long long t = t0 + n;
+    const int chunk = (int)(t / rows), rl = (int)(t % rows);
+    const long long row = row0 + rl;
+    const int q0 = chunk * COLS;
+    if (chunk != tw_chunk) {
+      // stage twiddles of this chunk's columns, conjugated (transform.py:199):
+      // S_b[q + (k << b0)] for stage b = b0 + e
+      __syncthreads();  // previous chunk's twiddles no longer read
+      for (int x = tid; x < C::TWA; x += blockDim.x) {
+        const int slot = x / COLS, cc = x % COLS;  // slot = 2^e - 1 + kk
+        const int e = 31 - __clz(slot + 1), kk = slot + 1 - (1 << e);
+        double2 w = __ldg(twst + ((1LL << (b0 + e)) - 1) + q0 + cc + ((long long)kk << b0));
+        w.y = -w.y;
+        tw_a[x] = w;
+      }
+      if constexpr (KC == 8) {
+        for (int x = tid; x < C::TWB; x += blockDim.x) {
+          const int slot = x / 256, hc = x % 256, hh = hc / 16, cc = hc % 16;
+          const int ib = 31 - __clz(slot + 1), kk = slot + 1 - (1 << ib);
+          double2 w = __ldg(twst + ((1LL << (b0 + 4 + ib)) - 1) + q0 + cc +
+                            ((long long)(hh + 16 * kk) << b0));
+          w.y = -w.y;
+          tw_b[x] = w;
+        }
+      }
+      __syncthreads();
+      tw_chunk = chunk;
+    }
+    const int s = n % C::STAGES;
+    double2* tile = csm + s * TILE;
+    mbar_wait(&full[s], (unsigned)((n / C::STAGES) & 1));
+    const double sc = __ldg(scales + row);
+    const int q = q0 + c;
+    double2 v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = tile[(16 * h + i) * COLS + c];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+#pragma unroll
+      for (int kk = 0; kk < (1 << e); ++kk) {
+        const double2 w = tw_a[((1 << e) - 1 + kk) * COLS + c];
+#pragma unroll
+        for (int hh = 0; hh < (16 >> (e + 1)); ++hh) {
+          const int i = kk | (hh << (e + 1));
+          bfly(v[i], v[i | (1 << e)], w);
+        }
+      }
+    }
+    if constexpr (KC == 8) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) tile[(16 * h + i) * COLS + c] = v[i];
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = tile[(h + 16 * i) * COLS + c];
+#pragma unroll
+      for (int ib = 0; ib < 4; ++ib) {
+#pragma unroll
+        for (int kk = 0; kk < (1 << ib); ++kk) {
+          const double2 w = tw_b[((1 << ib) - 1 + kk) * 256 + h * 16 + c];
+#pragma unroll
+          for (int hh = 0; hh < (16 >> (ib + 1)); ++hh) {
+            const int i = kk | (hh << (ib + 1));
+            bfly(v[i], v[i | (1 << ib)], w);
+          }
+        }
+      }
+    }
+    // this tile's stage is free once every thread has read it: refill it
+    // with tile n + STAGES (generic-proxy writes above precede the async
+    // proxy's overwrite)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid < 32 && n + C::STAGES < ntile) issue(n + C::STAGES);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const long long j = q + ((long long)(KC == 8 ? h + 16 * i : i) << b0);
+      const double2 f = make_double2(v[i].x * sc, v[i].y * sc);  // transform.py:200
+      const double mg = np_mag2(f);                              // core.py:298
+      const long long flat = row * N + j;
+      if (mg >= best.mag && cand_better(mg, flat, best.mag, best.flat)) {
+        best.mag = mg;
+        best.flat = flat;
+        best.re = f.x;
+        best.im = f.y;
+      }
+    }
+  }
+  // merge this CTA's first maximum into its slot (slots persist over the
+  // row batches of one step; the (mag, flat) order makes merging order-free)
+  __shared__ Cand red[8];
+  best = warp_argmax(best);
+  const int wid = tid >> 5;
+  if (lane == 0) red[wid] = best;
+  __syncthreads();
+  if (wid == 0) {
+    Cand cc = lane < 8 ? red[lane] : best;
+    cc = warp_argmax(cc);
+    if (lane == 0) {
+      Cand& slot = cand[blockIdx.x];
+      Cand o = slot;
+      cand_merge(o, cc);
+      slot = o;
+    }
+  }
+}
+
+}  // namespace afd
