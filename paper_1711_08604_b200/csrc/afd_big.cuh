@@ -30,6 +30,7 @@
 namespace afd {
 
 constexpr int kNodeLen = 2048;             // samples per energy node
+constexpr int kMaxNodes = (1 << 22) / kNodeLen;  // node sums at the largest N (2^22)
 constexpr int kColThreads = 256;
 
 // Pass-A bits: K = KA + 4 c with 9 <= KA <= 12 (K = 14..22).
@@ -451,7 +452,7 @@ big_select_kernel(int k, int dc_first, int K, const Cand* __restrict__ cand, int
                   const double* __restrict__ nodes, int nnodes,
                   const double* __restrict__ radii, const double2* __restrict__ circle,
                   const State* __restrict__ state, BigSel* __restrict__ sel) {
-  __shared__ double re[1024], im[1024];
+  __shared__ double re[kMaxNodes], im[kMaxNodes];
   if (state->stopped) return;
   const long long N = 1LL << K;
   BigSel out;
@@ -549,7 +550,7 @@ __global__ void __launch_bounds__(256)
 big_finalize_kernel(int k, int K, int max_terms, double threshold, const double* __restrict__ nodes,
                     int nnodes, const BigSel* __restrict__ sel, const int* __restrict__ amb,
                     State* __restrict__ state, Step* __restrict__ steps) {
-  __shared__ double v[1024];
+  __shared__ double v[kMaxNodes];
   if (k >= 0 && state->stopped) return;
   const double N = (double)(1LL << K);
   for (int i = threadIdx.x; i < nnodes; i += blockDim.x) v[i] = nodes[i];

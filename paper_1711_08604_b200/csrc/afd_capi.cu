@@ -264,7 +264,10 @@ int setup_kernels(afd_plan* p) {
   return 0;
 }
 
-// Number of CTAs per signal for `rows` rows: minimise waves x rows-per-CTA.
+// Number of CTAs per signal for `rows` rows: minimise waves x (units per CTA
+// + one unit of per-CTA setup: TMEM allocation and twiddle fill, first-row
+// loads, the closing reduction — measured ~1 row-pair; c3 with 16-row CTAs
+// ran 10% slower than with whole-signal CTAs, 128 signals with 2-row CTAs 1.9x).
 int field_ctas(const afd_plan* p, int64_t rows, int G, int64_t batch, int block = 0) {
   const int64_t units = (rows + G - 1) / G;
   // a reduced block (fewer row-groups) fits proportionally more CTAs per SM
@@ -278,7 +281,7 @@ int field_ctas(const afd_plan* p, int64_t rows, int G, int64_t batch, int block 
     if (x > 1 && (units + x - 2) / (x - 1) == per) continue;  // same per-CTA load, more CTAs
     const int64_t ctas = x * batch;
     const int64_t waves = (ctas + slots - 1) / slots;
-    const double t = (double)waves * (double)per + 1e-3 * (double)ctas / (double)slots;
+    const double t = (double)waves * (double)(per + 1) + 1e-3 * (double)ctas / (double)slots;
     if (t < best_t) {
       best_t = t;
       best_x = x;
@@ -406,6 +409,10 @@ int launch_direct(afd_plan* p, const double2* g, int64_t r0, int64_t r1, int64_t
 // CTAs per signal of a field launch over `rows` rows (what launch_field uses).
 int field_ctas_for(const afd_plan* p, int64_t rows, int64_t batch) {
   if (p->engine == 1) return (int)rows;
+  if (const char* e = getenv("AFD_FIELD_CTAS")) {  // experiments
+    const int x = atoi(e);
+    if (x > 0) return (int)std::min<int64_t>(x, rows);
+  }
   AFD_DISPATCH(p->K, {
     constexpr int G = groups_for<KK>();
     const int ge = groups_eff<KK>(p, rows, batch);

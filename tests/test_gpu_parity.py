@@ -270,6 +270,25 @@ def test_field_n65536_matches_oracle(afd, m):
     assert np.array_equal(d.remainder, o.remainder)
 
 
+@pytest.mark.parametrize("k,m", [(15, 40), (21, 3), (22, 2)])
+def test_large_n_column_pass_lengths_match_oracle(afd, k, m):
+    """N = 2^15 (pass A of 2^11 points + the 4-stage TMA column pass) and
+    N = 2^21 / 2^22 (pass A of 2^9 / 2^10, an in-place 8-stage column pass,
+    then the 4-stage TMA column pass): decomposition vs the CPU oracle."""
+    core, _ = afd
+    from paper_1711_08604_b200 import workloads as W
+    n = 1 << k
+    g = W.pole_sum(n, 16, 0.97, k)
+    radii = tuple(0.999 * i / m for i in range(m))
+    d = core.decompose(g, core.ParameterGrid(radii, n), max_terms=2)
+    o = O.decompose(g, np.array(radii), max_terms=2)
+    assert [s.point.angle_index for s in d.steps] == list(o.steps["j"])
+    assert [s.point.radius for s in d.steps] == list(o.steps["radius"])
+    assert [s.coefficient for s in d.steps] == list(o.steps["c_re"] + 1j * o.steps["c_im"])
+    assert [s.residual_energy for s in d.steps] == list(o.steps["residual"])
+    assert np.array_equal(d.remainder, o.remainder)
+
+
 @pytest.mark.parametrize("k", [17, 18, 19])
 def test_fused_column_pass_lengths_match_oracle(afd, k):
     """N = 2^17..2^19: pass A of 2^9..2^11 points then the 8-stage fused
