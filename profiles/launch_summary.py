@@ -15,19 +15,22 @@ def summarise(path):
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h, data = rows[hi], rows[hi + 1:]
     ik, iv, iu = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    ig = h.index("Grid Size") if "Grid Size" in h else None
     agg = collections.defaultdict(list)
     for r in data:
         if len(r) <= iv:
             continue
-        name = r[ik].split("(")[0].replace("void ", "")
+        # launches of one kernel with different grids (e.g. the bench's
+        # decomposition vs its saturated steady-state probe) listed apart
+        name = r[ik].split("(")[0].replace("void ", "") + (" grid" + r[ig] if ig is not None else "")
         v = float(r[iv].replace(",", ""))
         v = v / 1000 if r[iu] == "ns" else (v * 1000 if r[iu] == "ms" else v)
         agg[name].append(v)
     tot = sum(sum(v) for v in agg.values())
     out = []
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
-        out.append("%-70s n=%5d mean=%9.2f us total=%10.1f us share=%5.1f%%"
-                   % (k[:70], len(v), sum(v) / len(v), sum(v), 100 * sum(v) / tot))
+        out.append("%-86s n=%5d mean=%9.2f us total=%10.1f us share=%5.1f%%"
+                   % (k[:86], len(v), sum(v) / len(v), sum(v), 100 * sum(v) / tot))
     return "\n".join(out)
 
 
