@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/afd_capi.h"
@@ -1179,6 +1180,27 @@ int afd_decompose(afd_plan* p, const double* g0, int64_t batch, int max_terms, d
   return 0;
 }
 
+// Host memcpy on up to 8 threads for large buffers (the pinned staging copies
+// of a batch run at one core's bandwidth otherwise: 64 MiB ~6 ms).
+static void par_memcpy(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kMin = (size_t)8 << 20;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int nt = (int)std::min<size_t>(std::min(8u, hw), bytes / kMin);
+  if (nt <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t per = ((bytes + nt - 1) / nt + 63) & ~(size_t)63;
+  std::vector<std::thread> th;
+  for (int i = 1; i < nt; ++i) {
+    const size_t o = per * i;
+    if (o >= bytes) break;
+    th.emplace_back([=] { std::memcpy((char*)dst + o, (const char*)src + o, std::min(per, bytes - o)); });
+  }
+  std::memcpy(dst, src, std::min(per, bytes));
+  for (auto& t : th) t.join();
+}
+
 int afd_decompose_host(afd_plan* p, const double* g0_host, int64_t batch, int max_terms,
                        double threshold, int dc_first, afd_step* steps_host,
                        int32_t* n_steps_host, double* initial_host, double* remainder_host,
@@ -1212,7 +1234,7 @@ int afd_decompose_host(afd_plan* p, const double* g0_host, int64_t batch, int ma
     CU(cudaHostAlloc(&p->pin, need_pin, cudaHostAllocDefault));
     p->pin_bytes = need_pin;
   }
-  std::memcpy(p->pin, g0_host, sig);
+  par_memcpy(p->pin, g0_host, sig);
   CU(cudaMemcpyAsync(p->gin, p->pin, sig, cudaMemcpyHostToDevice, st));
   unsigned char* d = p->packed;
   if ((rc = afd_decompose(p, (const double*)p->gin, batch, max_terms, threshold, dc_first,
@@ -1225,7 +1247,7 @@ int afd_decompose_host(afd_plan* p, const double* g0_host, int64_t batch, int ma
   std::memcpy(steps_host, hp, stp);
   std::memcpy(n_steps_host, hp + o_ns, sizeof(int32_t) * batch);
   std::memcpy(initial_host, hp + o_in, sizeof(double) * batch);
-  std::memcpy(remainder_host, hp + o_rm, sig);
+  par_memcpy(remainder_host, hp + o_rm, sig);
   if (h2d_bytes) *h2d_bytes = (int64_t)sig;
   if (d2h_bytes) *d2h_bytes = (int64_t)need_pack;
   return 0;
