@@ -120,6 +120,12 @@ big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0
   const int t0 = brev_bits(tid, GA::TB);
   const bool offset = TM && (long long)blockIdx.x * kBigGroups + 1 < items;
   bool first = true;
+#ifndef AFD_PASSA_NO_BULK
+  constexpr bool kBulkOut = TM;  // field mode (TM is only instantiated for it)
+#else
+  constexpr bool kBulkOut = false;
+#endif
+  bool bulk_pending = false;
   for (long long it = (long long)blockIdx.x * kBigGroups + g; it < items;
        it += (long long)gridDim.x * kBigGroups) {
     const long long rl = it / nblk;               // row within the batch
@@ -155,6 +161,14 @@ big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0
       for (int i = 0; i < GA::P; ++i) v[i] = buf[GA::sw(GA::pos(0, t0, i))];
       sync();
     }
+    if constexpr (kBulkOut) {
+      // the previous item's bulk store has read the buffer out
+      if (bulk_pending) {
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        sync();
+        bulk_pending = false;
+      }
+    }
     if constexpr (TM) {
       if (offset && first && g == 1) asm volatile("bar.sync 3, %0;" ::"r"(2 * T) : "memory");
       const FieldHook hook{offset && first && g == 0, 2 * T, nullptr, false};
@@ -164,9 +178,30 @@ big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0
       fft_passes<KA, INV, 4>(v, tid, true, buf, tw, sync);
     }
     double2* __restrict__ y = Y + (size_t)rl * N + base;
+    if constexpr (kBulkOut) {
+      // field blocks: staged in natural order in the group's buffer and
+      // written by one bulk copy (TMA) — off the load/store pipe the next
+      // item's prologue loads need
 #pragma unroll
-    for (int i = 0; i < GA::P; ++i) y[out_pos<KA, 4>(tid, i)] = v[i];
-    sync();  // buffer reuse by the next item
+      for (int i = 0; i < GA::P; ++i) buf[out_pos<KA, 4>(tid, i)] = v[i];
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      sync();
+      if (tid == 0) {
+        asm volatile(
+            "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+            "cp.async.bulk.commit_group;" ::"l"(y),
+            "r"((unsigned)__cvta_generic_to_shared(buf)), "r"((unsigned)(sizeof(double2) * BLK))
+            : "memory");
+      }
+      bulk_pending = true;
+    } else {
+#pragma unroll
+      for (int i = 0; i < GA::P; ++i) y[out_pos<KA, 4>(tid, i)] = v[i];
+      sync();  // buffer reuse by the next item
+    }
+  }
+  if constexpr (kBulkOut) {
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   if constexpr (TM) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
