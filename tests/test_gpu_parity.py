@@ -346,6 +346,45 @@ def test_sharded_step_api_on_one_gpu(afd, case):
         assert np.array_equal(rem.cpu().numpy()[0], g["remainder"])
 
 
+@pytest.mark.parametrize("k", [16, 18])
+def test_sharded_large_n_matches_oracle(afd, k):
+    """Three radius shards of a large-N grid (N = 2^16: TMA 4-stage column
+    pass; 2^18: tensor-map 8-stage column pass) through afd_select_local /
+    afd_apply_step with the all-gather emulated: every shard's records and
+    remainder equal the CPU oracle's decomposition."""
+    core, engine = afd
+    import torch
+    from paper_1711_08604_b200 import _capi, workloads as W
+    from paper_1711_08604_b200.distributed import shard_bounds
+    n = 1 << k
+    g = W.pole_sum(n, 20, 0.97, 100 + k)
+    radii = tuple(0.998 * i / 7 for i in range(7))
+    max_terms, world = 3, 3
+    o = O.decompose(g, np.array(radii), max_terms=max_terms)
+    plans = [engine.Plan(radii, n, *shard_bounds(len(radii), r, world), max_batch=1)
+             for r in range(world)]
+    x = torch.from_numpy(g[None, :]).cuda()
+    steps = [torch.zeros((1, max_terms, _capi.STEP_DTYPE.itemsize), dtype=torch.uint8,
+                         device="cuda") for _ in plans]
+    for p in plans:
+        p.sharded_begin(x)
+    for kk in range(max_terms):
+        cands = torch.stack([p.select_local(kk, False, 1) for p in plans], 1).contiguous()
+        for p, s in zip(plans, steps):
+            p.apply_step(kk, max_terms, None, False, cands, s)
+    for p, s in zip(plans, steps):
+        n_steps, initial, rem, _ = p.sharded_finish(1)
+        count = int(n_steps.cpu()[0])
+        rec = s.cpu().numpy().view(_capi.STEP_DTYPE)[0, :count, 0]
+        assert count == len(o.steps)
+        assert np.array_equal(rec["j"], o.steps["j"])
+        assert np.array_equal(rec["radius"], o.steps["radius"])
+        assert np.array_equal(rec["c_re"], o.steps["c_re"])
+        assert np.array_equal(rec["c_im"], o.steps["c_im"])
+        assert np.array_equal(rec["residual"], o.steps["residual"])
+        assert np.array_equal(rem.cpu().numpy()[0], o.remainder)
+
+
 # ---------------------------------------------------------------------------
 # size-independent properties at BASELINE sizes (reference acceptance
 # criteria 2, 7, 8: tests/test_acceptance.py:66-76, 135-166)
