@@ -213,6 +213,145 @@ big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0
 }
 
 // ---------------------------------------------------------------------------
+// Field pass A for 4096-point blocks (N = 2^16, 2^20: KA = 12), block-major.
+// The two row-groups of a CTA always work on the same block index of two
+// rows (a "pair"), and each CTA walks a contiguous range of pairs in
+// block-major order, so the block's 64 KiB of spectrum is loaded into tensor
+// memory once per block change (a few per CTA and launch) instead of from L2
+// for every item — the field kernel's spectrum-in-TMEM, with its TMEM
+// twiddles, one-pass row-group offset and the bulk-stored outputs of
+// big_pass_a.  Same butterflies, same bits.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(Geo<12, 4>::T * kBigGroups, 1)
+big_field_a(int K, const double* __restrict__ pw_rev, long long pw_row0,
+            const double2* __restrict__ ghat_rev, const double2* __restrict__ twst,
+            long long row0, long long row1, double2* __restrict__ Y,
+            const int* __restrict__ stopped, const int* __restrict__ pw_len) {
+  constexpr int KA = 12;
+  using GA = Geo<KA, 4>;
+  using TwA = SmemTw<KA, 4>;
+  constexpr int BLK = 1 << KA, T = GA::T, P = GA::P;
+  extern __shared__ double2 smem[];
+  if (stopped && *stopped) return;
+  const long long N = 1LL << K;
+  const int nblk = (int)(N >> KA);
+  const int rows = (int)(row1 - row0);
+  const int rpairs = (rows + 1) / 2;
+  const long long pairs = (long long)nblk * rpairs;
+  const long long p0 = pairs * blockIdx.x / gridDim.x, p1 = pairs * (blockIdx.x + 1) / gridDim.x;
+  __shared__ uint32_t tm_base;
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&tm_base))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  TwA::load(smem, twst);  // N-table stage twiddles S_b, b < 12 (for the TMEM fill)
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int g = threadIdx.x / T, tid = threadIdx.x % T;
+  const int warp = threadIdx.x >> 5;
+  TmemTw tw;
+  tw.base = tm_base + ((uint32_t)((warp & 3) * 32) << 16) +
+            (uint32_t)(((warp & 7) >> 2) * TmemTw::kSetCols);
+  // spectrum of the current block: 16 values per thread, shared by the two
+  // groups (same thread index, same values), as in field_kernel
+  const uint32_t gh_tm = tm_base + ((uint32_t)((warp & 3) * 32) << 16) +
+                         (uint32_t)TmemTw::kGhCol + (uint32_t)(((warp & 7) >> 2) * (4 * P));
+  if (g == 0) {
+    tw.fill<KA, 4, true>(tid, TwA{smem});
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  double2* buf = smem + TwA::ENTRIES + g * GA::SMEM;
+  const GroupSync sync{1 + g, T};
+  const int t0 = brev_bits(tid, GA::TB);
+  int cur_blk = -1;
+  bool first = true, bulk_pending = false;
+  for (long long ip = p0; ip < p1; ++ip) {
+    const int blk = (int)(ip / rpairs);
+    const int rl = 2 * (int)(ip % rpairs) + g;  // row within the batch
+    const bool live = rl < rows;               // odd row count: last pair half empty
+    const int base = blk * BLK;
+    if (blk != cur_blk) {
+      // block change: both groups done with the old spectrum (and, the
+      // first time, the twiddle fill visible), group 0 loads the new one
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (g == 0) {
+        const double2* __restrict__ gr = ghat_rev + base;
+#pragma unroll
+        for (int i = 0; i < P; ++i) tm_st4(gh_tm + 4 * i, __ldg(gr + i * T + tid));
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      cur_blk = blk;
+      first = true;  // re-establish the one-pass group offset
+    }
+    double2 v[P];
+    if (live) {
+      // prologue y = powers * c[rev] (transform.py:198); r^l from the
+      // register-layout table (predicated past the underflow, see big_pass_a)
+      const double* __restrict__ pr = pw_rev + (size_t)(row0 + rl - pw_row0) * N + base;
+      const int L = pw_len[row0 + rl - pw_row0];
+#pragma unroll
+      for (int i0 = 0; i0 < P; i0 += 4) {
+        uint32_t r[16];
+        tm_ld<16>(gh_tm + 4 * i0, r);
+        tm_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = i0 + j;
+          const int l = brev_rt(base + ((t0 << 4) | i), K);  // natural index
+          double p = 0.0;
+          asm volatile("{ .reg .pred q; setp.lt.s32 q, %1, %2; @q ld.global.nc.f64 %0, [%3]; }"
+                       : "+d"(p)
+                       : "r"(l), "r"(L), "l"(pr + i * T + tid));
+          const double2 c = make_double2(__hiloint2double(r[4 * j + 1], r[4 * j]),
+                                         __hiloint2double(r[4 * j + 3], r[4 * j + 2]));
+          v[i] = make_double2(p * c.x, p * c.y);
+        }
+      }
+    }
+    if (bulk_pending) {  // the previous block's bulk store has read the buffer
+      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      sync();
+      bulk_pending = false;
+    }
+    if (first && g == 1) asm volatile("bar.sync 3, %0;" ::"r"(2 * T) : "memory");
+    if (live) {
+      const FieldHook hook{first && g == 0, 2 * T, nullptr, false};
+      fft_passes<KA, true, 4>(v, tid, true, buf, tw, sync, hook);
+      double2* __restrict__ y = Y + (size_t)rl * N + base;
+#pragma unroll
+      for (int i = 0; i < P; ++i) buf[out_pos<KA, 4>(tid, i)] = v[i];
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      sync();
+      if (tid == 0) {
+        asm volatile(
+            "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+            "cp.async.bulk.commit_group;" ::"l"(y),
+            "r"((unsigned)__cvta_generic_to_shared(buf)), "r"((unsigned)(sizeof(double2) * BLK))
+            : "memory");
+      }
+      bulk_pending = true;
+    } else if (first && g == 0) {
+      asm volatile("bar.arrive 3, %0;" ::"r"(2 * T) : "memory");  // (never: group 0 is live)
+    }
+    first = false;
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm_base)
+                 : "memory");
+}
+
+// ---------------------------------------------------------------------------
 // Column pass over stage bits [b0, b0+4).  Thread = column q (bits b0..b0+3
 // of q clear); blockIdx.y = row within the batch.
 //   out_mode 0: write back to Y in place

@@ -553,6 +553,8 @@ int big_setup(afd_plan* p) {
                             (int)big_a_smem_g<KA>()));
     CU(cudaFuncSetAttribute(big_pass_a<KA, true, KA == 12>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_a_smem_g<KA>()));
+    CU(cudaFuncSetAttribute(big_field_a, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)big_a_smem_g<12>()));
     CU(cudaFuncSetAttribute(big_pass_col8<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double2) * 16 * kCol8Pad)));
     CU(cudaFuncSetAttribute(big_pass_col8<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -586,6 +588,10 @@ int big_setup(afd_plan* p) {
   });
 }
 
+// Block-major field pass A with the spectrum in TMEM (big_field_a);
+// AFD_FIELD_A=0 keeps big_pass_a's item order (experiments).
+static const bool kFieldAEnabled = !(getenv("AFD_FIELD_A") && atoi(getenv("AFD_FIELD_A")) == 0);
+
 // Pass A over rows [r0, r0+rows) (mode 0: field prologue) or one signal (mode 1).
 int big_launch_a(afd_plan* p, bool inv, int mode, const double2* ghat_rev, const double2* x,
                  int64_t r0, int64_t rows, const int* stopped, cudaStream_t st) {
@@ -594,7 +600,11 @@ int big_launch_a(afd_plan* p, bool inv, int mode, const double2* ghat_rev, const
     // persistent: one CTA per SM (2 row-groups each), work items strided
     const unsigned grid = (unsigned)std::min<int64_t>(p->sms, (items + kBigGroups - 1) / kBigGroups);
     const int block = Geo<KA, 4>::T * kBigGroups;
-    if (inv && mode == 0 && KA == 12 && field_tmem_enabled())
+    if (inv && mode == 0 && KA == 12 && field_tmem_enabled() && kFieldAEnabled)
+      big_field_a<<<(unsigned)std::min<int64_t>(p->sms, (items + kBigGroups - 1) / kBigGroups),
+                    block, big_a_smem_g<KA>(), st>>>(p->K, p->pw, p->m0, ghat_rev, p->twst, r0,
+                                                     r0 + rows, p->Y, stopped, p->pw_len);
+    else if (inv && mode == 0 && KA == 12 && field_tmem_enabled())
       big_pass_a<KA, true, KA == 12><<<grid, block, big_a_smem_g<KA>(), st>>>(
           p->K, mode, p->pw, p->m0, ghat_rev, x, p->twst, r0, r0 + rows, p->Y, stopped,
           p->pw_len);
