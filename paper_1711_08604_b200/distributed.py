@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _capi
 
-__all__ = ["shard_bounds", "decompose_sharded"]
+__all__ = ["shard_bounds", "decompose_sharded", "decompose_batch_sharded"]
 
 
 def shard_bounds(count, rank, world):
@@ -94,3 +94,37 @@ def decompose_sharded(signals, grid, max_terms=10, threshold=None, dc_first=Fals
     remh = rem.cpu().numpy()
     return [core._build(grid, n, engine_name, rec[i], int(counts[i]), init[i], remh[i].copy())
             for i in range(b)]
+
+
+def decompose_batch_sharded(signals, grid, max_terms=10, threshold=None, dc_first=False,
+                            group=None, engine_name="fft", gather=True, decompose_fn=None):
+    """Signal-sharded ``core.decompose_batch`` (BASELINE c3).
+
+    Rank p decomposes the contiguous block ``shard_bounds(B, p, P)`` of the
+    batch on its own GPU — no collective inside the loop.  With ``gather``
+    the per-signal Decompositions are all-gathered once at the end, so every
+    rank returns the whole batch in order (identical to the single-GPU
+    result); otherwise each rank returns its own block.
+    ``decompose_fn(signals, grid, max_terms, threshold, dc_first)`` replaces
+    the CUDA decomposition (tests inject a CPU stand-in).
+    """
+    import torch.distributed as dist
+
+    from . import core
+
+    sig = np.asarray(signals, dtype=np.complex128)
+    if sig.ndim != 2:
+        raise ValueError("signals must be 2-d [batch, N], got shape %r" % (sig.shape,))
+    core._check_decompose_args(sig, grid, max_terms, threshold, engine_name)
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    lo, hi = shard_bounds(sig.shape[0], rank, world)
+    if decompose_fn is None:
+        def decompose_fn(x, gr, mt, thr, dc):
+            return core.decompose_batch(x, gr, mt, thr, engine_name, dc) if len(x) else []
+    local = decompose_fn(sig[lo:hi], grid, max_terms, threshold, dc_first)
+    if not gather:
+        return local
+    parts = [None] * world
+    dist.all_gather_object(parts, local, group=group)
+    return [d for part in parts for d in part]

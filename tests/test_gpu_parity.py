@@ -385,6 +385,33 @@ def test_sharded_large_n_matches_oracle(afd, k):
         assert np.array_equal(rem.cpu().numpy()[0], o.remainder)
 
 
+def test_signal_sharded_batch_one_nccl_rank(afd):
+    """distributed.decompose_batch_sharded on a one-rank NCCL group equals
+    core.decompose_batch (the c3 multi-GPU entry point, gather included)."""
+    core, _ = afd
+    import socket
+    import torch.distributed as dist
+    from paper_1711_08604_b200 import distributed, workloads as W
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    dist.init_process_group("nccl", init_method="tcp://127.0.0.1:%d" % port, rank=0,
+                            world_size=1)
+    try:
+        n, radii = 1024, tuple(i / 64 for i in range(64))
+        sig = np.stack([W.pole_sum(n, 8, 0.9, 200 + s) for s in range(5)])
+        grid = core.ParameterGrid(radii, n)
+        got = distributed.decompose_batch_sharded(sig, grid, max_terms=6)
+        want = core.decompose_batch(sig, grid, max_terms=6)
+        assert len(got) == len(want) == 5
+        for a, b in zip(got, want):
+            assert a.steps == b.steps
+            assert np.array_equal(a.remainder, b.remainder)
+    finally:
+        dist.destroy_process_group()
+
+
 # ---------------------------------------------------------------------------
 # size-independent properties at BASELINE sizes (reference acceptance
 # criteria 2, 7, 8: tests/test_acceptance.py:66-76, 135-166)

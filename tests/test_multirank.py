@@ -81,3 +81,55 @@ def test_shard_bounds():
             assert blocks[0][0] == 0 and blocks[-1][1] == m
             assert all(a[1] == b[0] for a, b in zip(blocks, blocks[1:]))
             assert max(h - l for l, h in blocks) - min(h - l for l, h in blocks) <= 1
+
+
+def _batch_worker(rank, world, port, out_q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1711_08604_b200 import core, distributed, workloads as W
+        n, radii = 128, tuple(i / 16 for i in range(16))
+        sig = np.stack([W.pole_sum(n, 4, 0.9, 50 + s) for s in range(7)])
+        grid = core.ParameterGrid(radii, n)
+
+        def oracle_batch(x, gr, mt, thr, dc):
+            # CPU stand-in for core.decompose_batch: the oracle's records
+            out = []
+            for row in x:
+                o = O.decompose(row, np.array(gr.radii), max_terms=mt)
+                out.append((list(o.steps["j"]), list(o.steps["radius"]),
+                            list(o.steps["c_re"] + 1j * o.steps["c_im"]), o.remainder))
+            return out
+
+        res = distributed.decompose_batch_sharded(sig, grid, max_terms=4,
+                                                  decompose_fn=oracle_batch)
+        out_q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_signal_sharded_batch_gathers_in_order(world):
+    """7 signals over 2 / 3 ranks: every rank gets all 7 results, in batch
+    order, each equal to the single-process oracle decomposition."""
+    from paper_1711_08604_b200 import workloads as W
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n, radii = 128, np.array([i / 16 for i in range(16)])
+    want = [O.decompose(W.pole_sum(n, 4, 0.9, 50 + s), radii, max_terms=4) for s in range(7)]
+    for rank, got in res:
+        assert len(got) == 7, rank
+        for (j, r, c, rem), o in zip(got, want):
+            assert j == list(o.steps["j"]) and r == list(o.steps["radius"])
+            assert c == list(o.steps["c_re"] + 1j * o.steps["c_im"])
+            assert np.array_equal(rem, o.remainder)
