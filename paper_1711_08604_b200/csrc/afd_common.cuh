@@ -37,6 +37,38 @@ __device__ __forceinline__ double2 np_cdiv(double2 a, double2 b) {
   return o;
 }
 
+// np_cdiv split in two: the divisor-only part (branch, ratio, reciprocal —
+// both divisions) and the numerator part; np_cdiv_fin(a, np_cdiv_pre(b)) is
+// np_cdiv(a, b) operation for operation.  Lets a caller issue the divisions
+// before the numerator is known.
+struct CdivPre {
+  double rat, scl;
+  bool xbig;
+};
+__device__ __forceinline__ CdivPre np_cdiv_pre(double2 b) {
+  CdivPre p;
+  p.xbig = fabs(b.x) >= fabs(b.y);
+  if (p.xbig) {
+    p.rat = b.y / b.x;
+    p.scl = 1.0 / (b.x + b.y * p.rat);
+  } else {
+    p.rat = b.x / b.y;
+    p.scl = 1.0 / (b.y + b.x * p.rat);
+  }
+  return p;
+}
+__device__ __forceinline__ double2 np_cdiv_fin(double2 a, const CdivPre& p) {
+  double2 o;
+  if (p.xbig) {
+    o.x = (a.x + a.y * p.rat) * p.scl;
+    o.y = (a.y - a.x * p.rat) * p.scl;
+  } else {
+    o.x = (a.x * p.rat + a.y) * p.scl;
+    o.y = (a.y * p.rat - a.x) * p.scl;
+  }
+  return o;
+}
+
 // |z|^2 as core.py:298 evaluates it: re**2 + im**2, two roundings + add.
 __device__ __forceinline__ double np_mag2(double2 v) { return v.x * v.x + v.y * v.y; }
 

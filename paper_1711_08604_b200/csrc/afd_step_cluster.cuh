@@ -315,6 +315,21 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   // ---- update this CTA's samples (or copy g0 at init) -------------------------
   int amb = 0;
   {
+    // the divisions of both complex quotients depend only on a and z: they
+    // are issued first and run under kernel_norm's dependency chain
+    double2 dd[PER];
+    CdivPre q1[PER], q2[PER];
+    if (k >= 0) {
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int i = tid + u * CG::THREADS;
+        const int l = C * (i < NC ? i : 0) + rc;
+        const double2 z = circ[l];
+        dd[u] = one_minus_conja_z(a, z);
+        q1[u] = np_cdiv_pre(dd[u]);
+        q2[u] = np_cdiv_pre(make_double2(z.x - a.x, z.y - a.y));
+      }
+    }
     double kn = 0.0;
     if (k >= 0) kn = kernel_norm(a, &amb);
     const double2 sc = make_double2(kn, 0.0);
@@ -326,14 +341,13 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
         const int l = C * i + rc;
         double2 out = gs[u];
         if (k >= 0) {
-          const double2 z = circ[l];
-          const double2 d = one_minus_conja_z(a, z);
-          const double2 e = np_cdiv(sc, d);
+          const double2 d = dd[u];
+          const double2 e = np_cdiv_fin(sc, q1[u]);  // np_cdiv(sc, d)
           const double2 ce = np_cmul(coeff, e);  // N <= 8192: no numpy elision
           const double2 g = gs[u];
           const double2 stp = make_double2(g.x - ce.x, g.y - ce.y);
           const double2 num = np_cmul(stp, d);
-          out = np_cdiv(num, make_double2(z.x - a.x, z.y - a.y));
+          out = np_cdiv_fin(num, q2[u]);  // np_cdiv(num, z - a)
         }
         slice[i] = out;
         // |G|^2 to the CTA whose natural slice holds l (a pairwise-sum node)
