@@ -289,6 +289,30 @@ def test_large_n_column_pass_lengths_match_oracle(afd, k, m):
     assert np.array_equal(d.remainder, o.remainder)
 
 
+@pytest.mark.parametrize("k", [16, 18])
+def test_large_n_multi_batch_matches_oracle(afd, k, monkeypatch):
+    """Row batches forced to 2 rows (AFD_BIG_ROWS, read at plan creation):
+    7 radii = 4 batches, the last one partial, through the block-major pass A
+    and the TMA column pass (N = 2^18: tensor map over 2-row batches)."""
+    core, engine = afd
+    from paper_1711_08604_b200 import workloads as W
+    monkeypatch.setenv("AFD_BIG_ROWS", "2")
+    n = 1 << k
+    g = W.pole_sum(n, 16, 0.96, 300 + k)
+    radii = tuple(0.997 * i / 7 for i in range(7))
+    plan = engine.Plan(radii, n, max_batch=1)  # private plan: built with 2-row batches
+    rec, counts, initial, rem, _, _ = plan.decompose_host(g[None, :], 3)
+    o = O.decompose(g, np.array(radii), max_terms=3)
+    c = int(counts[0])
+    assert c == len(o.steps)
+    assert np.array_equal(rec[0]["j"][:c], o.steps["j"])
+    assert np.array_equal(rec[0]["radius"][:c], o.steps["radius"])
+    assert np.array_equal(rec[0]["c_re"][:c], o.steps["c_re"])
+    assert np.array_equal(rec[0]["c_im"][:c], o.steps["c_im"])
+    assert np.array_equal(rec[0]["residual"][:c], o.steps["residual"])
+    assert np.array_equal(rem[0], o.remainder)
+
+
 @pytest.mark.parametrize("k", [17, 18, 19])
 def test_fused_column_pass_lengths_match_oracle(afd, k):
     """N = 2^17..2^19: pass A of 2^9..2^11 points then the 8-stage fused
