@@ -212,6 +212,24 @@ big_pass_a(int K, int mode, const double* __restrict__ pw_rev, long long pw_row0
   }
 }
 
+// FieldHook plus: the previous item's bulk store must have read the group's
+// buffer before the first exchange overwrites it — waited for after pass 0
+// (not before it: the store is still draining when the prologue ends).
+struct BulkWaitHook {
+  FieldHook fh;
+  bool pending, leader;
+  GroupSync sync;
+  __device__ __forceinline__ void before(int pass) const { fh.before(pass); }
+  __device__ __forceinline__ void after(int pass) const {
+    if (pass == 0 && pending) {
+      if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      sync();
+    }
+    fh.after(pass);
+  }
+  __device__ __forceinline__ void exch(int pass) const { fh.exch(pass); }
+};
+
 // ---------------------------------------------------------------------------
 // Field pass A for 4096-point blocks (N = 2^16, 2^20: KA = 12), block-major.
 // The two row-groups of a CTA always work on the same block index of two
@@ -316,15 +334,12 @@ big_field_a(int K, const double* __restrict__ pw_rev, long long pw_row0,
         }
       }
     }
-    if (bulk_pending) {  // the previous block's bulk store has read the buffer
-      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      sync();
-      bulk_pending = false;
-    }
     if (first && g == 1) asm volatile("bar.sync 3, %0;" ::"r"(2 * T) : "memory");
     if (live) {
-      const FieldHook hook{first && g == 0, 2 * T, nullptr, false};
+      const BulkWaitHook hook{{first && g == 0, 2 * T, nullptr, false}, bulk_pending, tid == 0,
+                              sync};
       fft_passes<KA, true, 4>(v, tid, true, buf, tw, sync, hook);
+      bulk_pending = false;
       double2* __restrict__ y = Y + (size_t)rl * N + base;
 #pragma unroll
       for (int i = 0; i < P; ++i) buf[out_pos<KA, 4>(tid, i)] = v[i];
@@ -338,8 +353,13 @@ big_field_a(int K, const double* __restrict__ pw_rev, long long pw_row0,
             : "memory");
       }
       bulk_pending = true;
-    } else if (first && g == 0) {
-      asm volatile("bar.arrive 3, %0;" ::"r"(2 * T) : "memory");  // (never: group 0 is live)
+    } else {
+      if (first && g == 0) asm volatile("bar.arrive 3, %0;" ::"r"(2 * T) : "memory");  // (never)
+      if (bulk_pending) {  // a dead item: drain the pending store here
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        sync();
+        bulk_pending = false;
+      }
     }
     first = false;
   }
