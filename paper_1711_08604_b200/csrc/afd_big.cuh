@@ -315,6 +315,18 @@ big_field_a(int K, const double* __restrict__ pw_rev, long long pw_row0,
       // register-layout table (predicated past the underflow, see big_pass_a)
       const double* __restrict__ pr = pw_rev + (size_t)(row0 + rl - pw_row0) * N + base;
       const int L = pw_len[row0 + rl - pw_row0];
+      // all sixteen HBM loads in flight before the first use (the volatile
+      // loads keep program order, so interleaving them with the TMEM reads
+      // below serialised four round trips)
+      double pv[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const int l = brev_rt(base + ((t0 << 4) | i), K);  // natural index
+        pv[i] = 0.0;
+        asm volatile("{ .reg .pred q; setp.lt.s32 q, %1, %2; @q ld.global.nc.f64 %0, [%3]; }"
+                     : "+d"(pv[i])
+                     : "r"(l), "r"(L), "l"(pr + i * T + tid));
+      }
 #pragma unroll
       for (int i0 = 0; i0 < P; i0 += 4) {
         uint32_t r[16];
@@ -323,11 +335,7 @@ big_field_a(int K, const double* __restrict__ pw_rev, long long pw_row0,
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int i = i0 + j;
-          const int l = brev_rt(base + ((t0 << 4) | i), K);  // natural index
-          double p = 0.0;
-          asm volatile("{ .reg .pred q; setp.lt.s32 q, %1, %2; @q ld.global.nc.f64 %0, [%3]; }"
-                       : "+d"(p)
-                       : "r"(l), "r"(L), "l"(pr + i * T + tid));
+          const double p = pv[i];
           const double2 c = make_double2(__hiloint2double(r[4 * j + 1], r[4 * j]),
                                          __hiloint2double(r[4 * j + 3], r[4 * j + 2]));
           v[i] = make_double2(p * c.x, p * c.y);

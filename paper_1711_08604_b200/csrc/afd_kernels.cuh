@@ -291,6 +291,12 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
       // prologue: y = powers * c[rev] (transform.py:198), per component
       if constexpr (TM) {
         const double* __restrict__ pr = pw + (size_t)(s - pw_row0) * N;
+        // all r^l loads issued before the TMEM reads (tcgen05.wait::ld is a
+        // memory barrier to the compiler: loads placed after one cannot be
+        // hoisted above it)
+        double pv[P];
+#pragma unroll
+        for (int i = 0; i < P; ++i) pv[i] = __ldg(pr + Gm::l0(tp, i));
 #pragma unroll
         for (int i0 = 0; i0 < P; i0 += 4) {
           uint32_t r[16];
@@ -298,10 +304,9 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
           tm_wait_ld();
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const int l = Gm::l0(tp, i0 + j);
             const double2 c = make_double2(__hiloint2double(r[4 * j + 1], r[4 * j]),
                                            __hiloint2double(r[4 * j + 3], r[4 * j + 2]));
-            const double p = __ldg(pr + l);
+            const double p = pv[i0 + j];
             v[i0 + j] = make_double2(p * c.x, p * c.y);
           }
         }
