@@ -313,6 +313,43 @@ def test_large_n_multi_batch_matches_oracle(afd, k, monkeypatch):
     assert np.array_equal(rem[0], o.remainder)
 
 
+def test_c4_full_size_first_step(afd):
+    """BASELINE c4 at full size (N = 2^20, M = 16384: a 128 GiB r^l table, 74
+    row batches), first AFD step on the GPU.  The oracle cannot evaluate the
+    whole 2^34-point grid here, so the check is row-local: the selected point
+    is, bit for bit, the first maximum of its own row as the oracle computes
+    it; no row of a seeded sample (plus the neighbours) beats it under the
+    reference's order; the coefficient, remainder and energy equal the
+    oracle's update with that atom."""
+    core, engine = afd
+    from paper_1711_08604_b200 import workloads as W
+    w = W.CONFIGS["c4"]
+    g = W.signal_for("c4")
+    radii = np.array(W.radii_for(w.m))
+    plan = engine.Plan(tuple(radii), w.n, max_batch=1)
+    try:
+        rec, counts, initial, rem, _, _ = plan.decompose_host(g[None, :], 1)
+    finally:
+        del plan
+    r = rec[0][0]
+    s, j = int(r["s"]), int(r["j"])
+    flat = s * w.n + j
+    ghat = O.dft_forward(g)
+    own = O.field_argmax(ghat, radii, s, s + 1)
+    assert int(own["flat"]) == flat
+    assert own["re"] == r["c_re"] and own["im"] == r["c_im"]
+    rng = np.random.default_rng(44)
+    rows = sorted(set(rng.integers(0, w.m, 20).tolist()) | {max(s - 1, 0), min(s + 1, w.m - 1),
+                                                            w.m - 1})
+    for row in rows:
+        c = O.field_argmax(ghat, radii, row, row + 1)
+        assert c["mag"] < own["mag"] or (c["mag"] == own["mag"] and c["flat"] >= flat), row
+    a = complex(r["a_re"], r["a_im"])
+    want = O.remainder_update(g, a, complex(r["c_re"], r["c_im"]))
+    assert np.array_equal(rem[0], want)
+    assert r["residual"] == O.energy(want)
+
+
 @pytest.mark.parametrize("k", [17, 18, 19])
 def test_fused_column_pass_lengths_match_oracle(afd, k):
     """N = 2^17..2^19: pass A of 2^9..2^11 points then the 8-stage fused
