@@ -350,6 +350,25 @@ def test_c4_full_size_first_step(afd):
     assert r["residual"] == O.energy(want)
 
 
+@pytest.mark.parametrize("k,dc,thr", [(14, True, None), (16, True, 0.3), (18, False, 0.6)])
+def test_large_n_dc_first_and_threshold(afd, k, dc, thr):
+    """Large N with the numpy-mean atom first (pairwise complex sum over N on
+    the device) and/or the energy-threshold stop, vs the oracle."""
+    core, _ = afd
+    from paper_1711_08604_b200 import workloads as W
+    n = 1 << k
+    g = W.pole_sum(n, 12, 0.95, 400 + k) + 0.25
+    radii = tuple(0.99 * i / 6 for i in range(6))
+    d = core.decompose(g, core.ParameterGrid(radii, n), max_terms=5, threshold=thr,
+                       dc_first=dc)
+    o = O.decompose(g, np.array(radii), max_terms=5, threshold=thr, dc_first=dc)
+    assert len(d.steps) == len(o.steps)
+    assert [s.point.angle_index for s in d.steps] == list(o.steps["j"])
+    assert [s.coefficient for s in d.steps] == list(o.steps["c_re"] + 1j * o.steps["c_im"])
+    assert [s.residual_energy for s in d.steps] == list(o.steps["residual"])
+    assert np.array_equal(d.remainder, o.remainder)
+
+
 @pytest.mark.parametrize("k", [17, 18, 19])
 def test_fused_column_pass_lengths_match_oracle(afd, k):
     """N = 2^17..2^19: pass A of 2^9..2^11 points then the 8-stage fused
