@@ -12,9 +12,10 @@ warnings.simplefilter("ignore")
 os.environ["AFD_LIB_PATH"] = "paper_1711_08604_b200/lib/libafd_b200_timing.so"
 from paper_1711_08604_b200 import engine, workloads as W, _capi  # noqa: E402
 
-w = W.CONFIGS["c1"]
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c1"
+w = W.CONFIGS[cfg]
 plan = engine.get_plan(W.radii_for(w.m), w.n)
-g = torch.from_numpy(W.signal_for("c1")[None, :]).cuda()
+g = torch.from_numpy(W.signal_for(cfg)[None, :]).cuda()
 for _ in range(3):
     plan.decompose(g, w.steps)
 torch.cuda.synchronize()
@@ -24,7 +25,7 @@ lib.afd_debug_step_stamps.argtypes = [C.c_void_p]
 assert lib.afd_debug_step_stamps(out.ctypes.data) == 0
 names = ["start", "tables", "pdl_wait", "select", "update", "node", "csync1", "energy+rec",
          "fft_in", "fft_local", "csync2", "radix8", "csync3"]
-rows = out[1:29].astype(np.int64)
+rows = out[1:w.steps - 1].astype(np.int64)
 d = np.diff(rows[:, :13], axis=1)
 print("phase (ns, median over steps 1..28):")
 for i in range(12):

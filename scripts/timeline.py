@@ -1,5 +1,6 @@
-"""Per-step hand-off timeline (c1): field and step kernels of the last AFD
-step, from the AFD_FIELD_TIMING + AFD_STEP_TIMING build (globaltimer, ns)."""
+"""Per-step hand-off timeline (c1, or the config given as argv[1]): field and
+step kernels of the last AFD step, from the AFD_FIELD_TIMING + AFD_STEP_TIMING
+build (globaltimer, ns)."""
 import ctypes as C
 import os
 import sys
@@ -13,9 +14,10 @@ warnings.simplefilter("ignore")
 os.environ.setdefault("AFD_LIB_PATH", "paper_1711_08604_b200/lib/libafd_b200_both.so")
 from paper_1711_08604_b200 import engine, workloads as W, _capi  # noqa: E402
 
-w = W.CONFIGS["c1"]
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c1"
+w = W.CONFIGS[cfg]
 plan = engine.get_plan(W.radii_for(w.m), w.n)
-g = torch.from_numpy(W.signal_for("c1")[None, :]).cuda()
+g = torch.from_numpy(W.signal_for(cfg)[None, :]).cuda()
 for _ in range(3):
     plan.decompose(g, w.steps)
 torch.cuda.synchronize()
