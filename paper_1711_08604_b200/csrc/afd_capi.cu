@@ -1472,6 +1472,10 @@ extern "C" int afd_debug_step_stamps(unsigned long long* host_out) {
   CU(cudaMemcpyFromSymbol(host_out, afd::g_step_stamps, sizeof(afd::g_step_stamps)));
   return 0;
 }
+extern "C" int afd_debug_step_cta_start(unsigned long long* host_out) {
+  CU(cudaMemcpyFromSymbol(host_out, afd::g_step_cta_start, sizeof(afd::g_step_cta_start)));
+  return 0;
+}
 #endif
 
 #ifdef AFD_FIELD_TIMING

@@ -34,6 +34,7 @@ __host__ __device__ constexpr int cluster_ctas(int K) { return K >= 11 ? 16 : 8;
 
 #ifdef AFD_STEP_TIMING
 __device__ unsigned long long g_step_stamps[64][24];
+__device__ unsigned long long g_step_cta_start[64][16];  // per-CTA start, signal 0
 // stamp row of this step, resolved once (opaque register) so that a stamp
 // never waits on a constant-bank load
 #define STAMP(i)                                                                       \
@@ -154,6 +155,13 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   }
 #endif
   STAMP(0);
+#ifdef AFD_STEP_TIMING
+  if (threadIdx.x == 0 && blockIdx.x < 16 && k >= 0 && k < 64) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    g_step_cta_start[k][blockIdx.x] = t_;
+  }
+#endif
 
   // The whole circle z_m (step-independent) lands in shared memory by bulk
   // copy: the pole lookup circle[j] and this CTA's update slice read it there.
@@ -224,6 +232,7 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   pdl_wait();
   STAMP(2);
   asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  STAMP(18);
   if (k == 0 && dc_first) {
     // this kernel's PDL predecessor is the init step kernel itself (no field
     // launch in between), so G_0 is only final after the wait
@@ -276,17 +285,31 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
     b.flat = 0x7fffffffffffffffLL;
     b.re = b.im = 0.0;
     const int lane = tid & 31;
-    for (int i = lane; i < ncand; i += 32) {
-      const Cand* cp = cand + (size_t)sig * ncand + i;
+    // up to 4 candidates per lane loaded before any is merged: one L2 round
+    // trip (a plain loop issued each lane's loads one merge apart)
+    const Cand* cs = cand + (size_t)sig * ncand;
+    auto load_cand = [&](int i) {
       Cand x;
-      const double2 lo = __ldcg(reinterpret_cast<const double2*>(cp));
-      const double2 hi = __ldcg(reinterpret_cast<const double2*>(cp) + 1);
+      const double2 lo = __ldcg(reinterpret_cast<const double2*>(cs + i));
+      const double2 hi = __ldcg(reinterpret_cast<const double2*>(cs + i) + 1);
       x.mag = lo.x;
       x.flat = __double_as_longlong(lo.y);
       x.re = hi.x;
       x.im = hi.y;
-      cand_merge(b, x);
+      return x;
+    };
+    {
+      Cand xs[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = lane + 32 * u;
+        if (i < ncand) xs[u] = load_cand(i);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (lane + 32 * u < ncand) cand_merge(b, xs[u]);
     }
+    for (int i = lane + 128; i < ncand; i += 32) cand_merge(b, load_cand(i));
     STAMP(16);
     if (stopped) {
       mbar_wait(&circ_bar, 0);  // no bulk copy may target an exited CTA

@@ -38,3 +38,15 @@ print("  select detail: wait -> cand loop done %.0f -> stop tested+trigger %.0f 
     np.median(rows[:, 13] - rows[:, 17])))
 print("  total %.0f ns; gap step k start -> step k+1 start %.0f ns" %
       (np.median(rows[:, 12] - rows[:, 0]), np.median(np.diff(rows[:, 0]))))
+
+# per-CTA start of the cluster (debug builds with afd_debug_step_cta_start)
+if hasattr(lib, "afd_debug_step_cta_start"):
+    cs = np.zeros((64, 16), np.uint64)
+    lib.afd_debug_step_cta_start.argtypes = [C.c_void_p]
+    lib.afd_debug_step_cta_start(cs.ctypes.data)
+    cs = cs.astype(np.int64)[1:w.steps - 1]
+    ncl = int((cs[0] != 0).sum())
+    rel = cs[:, :ncl] - cs[:, :1]
+    print("  cluster CTA start vs CTA 0 (ns, median over steps):", np.median(rel, axis=0).astype(int))
+    print("  pdl_wait -> cluster wait done %.0f" % np.median(out[1:w.steps - 1, 18].astype(np.int64) -
+                                                            out[1:w.steps - 1, 2].astype(np.int64)))
