@@ -250,14 +250,21 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     // trips on the critical path); the flag is tested once v is formed
     const int stopped = state != nullptr ? __ldcg(&state[sig].stopped) : 0;
     if (act0) {
+      // all sixteen spectrum loads in flight before the first TMEM store (a
+      // tcgen05.st is a memory barrier to the compiler: loads after one are
+      // not hoisted above it)
+#pragma unroll
+      for (int i = 0; i < P; ++i) v[i] = __ldg(gh + Gm::l0(tp, i));
+      if constexpr (TM) {
+        if (g == 0) {
+#pragma unroll
+          for (int i = 0; i < P; ++i) tm_st4(gh_tm + 4 * i, v[i]);
+        }
+      }
 #pragma unroll
       for (int i = 0; i < P; ++i) {
-        const double2 c = __ldg(gh + Gm::l0(tp, i));
-        v[i] = make_double2(pv[i] * c.x, pv[i] * c.y);  // transform.py:198
+        v[i] = make_double2(pv[i] * v[i].x, pv[i] * v[i].y);  // transform.py:198
         asm volatile("" ::"d"(v[i].x), "d"(v[i].y));  // formed before the test
-        if constexpr (TM) {
-          if (g == 0) tm_st4(gh_tm + 4 * i, c);
-        }
       }
       if constexpr (TM) {
         if (g == 0) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
