@@ -298,9 +298,14 @@ big_field_a(int K, const double* __restrict__ pw_rev, long long pw_row0,
       __syncthreads();
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (g == 0) {
+        // all loads before the first TMEM store (a tcgen05.st is a memory
+        // barrier to the compiler: loads after one are not hoisted)
         const double2* __restrict__ gr = ghat_rev + base;
+        double2 gv[P];
 #pragma unroll
-        for (int i = 0; i < P; ++i) tm_st4(gh_tm + 4 * i, __ldg(gr + i * T + tid));
+        for (int i = 0; i < P; ++i) gv[i] = __ldg(gr + i * T + tid);
+#pragma unroll
+        for (int i = 0; i < P; ++i) tm_st4(gh_tm + 4 * i, gv[i]);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
