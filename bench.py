@@ -1,23 +1,26 @@
 """AFD grid-evaluation throughput on B200 (BASELINE.json metric), one JSON line.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl reference]
 
-Workload (BASELINE.json configs[1], "c1"): one analytic signal (32-pole sum,
-|b| < 0.95, seeded), N = 4096 samples, M = 512 radii r_m = m/M, 30 AFD steps.
-A bench step is one full decomposition (30 AFD steps = M*N*30 grid evals)
-through the device-resident decomposition (CUDA graph of fused field+argmax
-and step kernels, input resident in HBM).  `value` = whole-job grid evals/s;
-`e2e` = the same through the public API `core.decompose` with the signal in
-host memory (pinned H2D + D2H of the result inside the timed region).
+Workload (default; BASELINE.json configs[4], "c4", the largest configuration
+and the one north_star sets its targets on): one analytic signal (128-pole
+sum, |b| < 0.99, seeded), N = 2^20 samples, M = 16384 radii r_m = m/M,
+20 AFD steps: 2^34 grid points per step.  A bench step is one full
+decomposition (M*N*20 grid evals) with the input resident in HBM; `value` =
+whole-job grid evals/s; `e2e` = the same through the public API
+(`core.decompose`, host numpy in, host results out: pinned H2D + D2H inside
+the timed region).  `--config c0..c3` selects the other BASELINE workloads
+(parity cases; their lines are kept under profiles/).
 
-Multi-GPU (torchrun, one rank per GPU): c1 does not shard (SURVEY.md §8(e):
-"replicas only"); every rank decomposes its own replica, time = max over
-ranks, value = all ranks' evals / that time, scaling "weak".
+Multi-GPU: `--gpus N` without a torchrun environment re-launches itself
+under `torch.distributed.run` with N ranks (one per GPU).  c4/c2 shard the
+radius grid (one 32-byte candidate all-gather per AFD step), c3 shards the
+signals, c0/c1 run replicas; time = max over ranks.
 
 --impl reference times the reference's CPU implementation: the oracle port
 (oracle/afd_oracle.c, a bit-exact C restatement of the reference; the
 reference itself is pure Python and cannot travel to the GPU box) on all
-host threads, on a bounded sample of the same workload.
+host threads, on a bounded sample of the same workload, rank 0 only.
 """
 
 from __future__ import annotations
@@ -105,9 +108,12 @@ def fp64_instr_per_eval(n):
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="c1")
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=["c0", "c1", "c2", "c3", "c4"])
+    ap.add_argument("--mode", default="exact", choices=["exact", "fast"],
+                    help="exact: bit-identical to the reference; fast: FP64 radix-16/fused "
+                         "butterflies, r^l on chip (identical indices, 1e-9 relative)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -116,6 +122,22 @@ def parse():
     ap.add_argument("--shard", default="auto", choices=["auto", "replicas", "signals", "radii"],
                     help="multi-GPU mode (auto: c3 signals, c2/c4 radii, else replicas)")
     return ap.parse_args()
+
+
+def maybe_spawn(args):
+    """`--gpus N` (N > 1) outside torchrun: re-launch under torch.distributed.run
+    with N ranks on this node (rendezvous on 127.0.0.1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 def dist_env():
@@ -231,6 +253,67 @@ def cpu_baseline(w, radii, g, seconds):
 
 
 # ---------------------------------------------------------------------------
+# shared pieces of both arms
+# ---------------------------------------------------------------------------
+def shard_mode(args, w, world):
+    """Multi-GPU mode of the workload: radius sharding for the
+    single huge signals (c2, c4), signal sharding for the batch (c3),
+    replicas for the small configs (c0, c1); 'single' on one GPU."""
+    if args.shard != "auto":
+        return args.shard
+    if world == 1:
+        return "single"
+    return {"c3": "signals", "c2": "radii", "c4": "radii"}.get(w.name, "replicas")
+
+
+def config_dict(args, w, world):
+    """The `config` object of the JSON line — identical for both arms."""
+    mode = shard_mode(args, w, world)
+    par = {"single": "single", "replicas": "replicas x%d" % world}.get(
+        mode, "dp%d over %s" % (world, mode))
+    return {"workload": w.name, "n": w.n, "m": w.m, "afd_steps": w.steps, "signals": w.batch,
+            "radii": "r_m = m/M", "parallelism": par,
+            "l2": "flushed (512 MiB write) between timed iterations",
+            "mode": ("exact (bit-identical to reference)" if args.mode == "exact" else
+                     "fast (FP64 fused butterflies, r^l on chip; identical indices, 1e-9)")}
+
+
+def scaling_of(mode):
+    return "strong" if mode in ("radii", "signals") else "weak"
+
+
+def check_parity(w, radii, sig0, rec0, count0, exact):
+    """Signal 0 of the benchmarked output against the CPU oracle: the whole
+    decomposition where the oracle finishes in seconds (<= 2^31 grid evals),
+    else a replay of the GPU's selections (oracle.replay_check: the selected
+    row's first maximum, neighbouring and sampled rows, coefficient and
+    residual of every step).  exact: bitwise; fast: identical
+    indices, 1e-9 relative."""
+    import oracle as O
+    rtol = 0.0 if exact else 1e-9
+    radii = np.array(radii)
+    t0 = time.perf_counter()
+    if w.m * w.n * w.steps <= (1 << 31):
+        o = O.decompose(sig0, radii, max_terms=w.steps)
+        c = min(int(count0), w.steps)
+        ok = c == len(o.steps) and np.array_equal(rec0["j"][:c], o.steps["j"]) and \
+            np.array_equal(rec0["radius"][:c], o.steps["radius"])
+        for key in ("c_re", "c_im", "residual"):
+            a, b = rec0[key][:c], o.steps[key]
+            ok = ok and (np.array_equal(a, b) if exact else
+                         bool(np.all(np.abs(a - b) <= rtol * np.maximum(np.abs(b), 1e-300))))
+        return {"ok": bool(ok), "method": "full oracle decomposition of signal 0 (%d steps)" % c,
+                "seconds": round(time.perf_counter() - t0, 1)}
+    r = O.replay_check(sig0, radii, rec0, int(count0), rows_per_step=6, rtol=rtol,
+                       threads=O.max_threads())
+    ok = r["ok"] and int(count0) == w.steps
+    return {"ok": bool(ok), "method": "oracle replay of the GPU's %d selections: selected row, "
+            "rows s+-2, last row and 6 seeded rows per step (%d rows of %d-point field in total)"
+            % (int(count0), r["rows"], w.n), "why": r["why"],
+            "seconds": round(time.perf_counter() - t0, 1)}
+
+
+# ---------------------------------------------------------------------------
 # reference arm
 # ---------------------------------------------------------------------------
 def run_reference(args):
@@ -260,16 +343,16 @@ def run_reference(args):
     evals = len(r) * w.n * afd  # one signal
     value = evals * args.steps / total
     sample = ("oracle port (bit-exact C restatement of the reference) decomposing %s signal 0: "
-              "first %d of %d AFD steps (M=%d%s, N=%d) per step, %d threads"
+              "first %d of %d AFD steps (M=%d%s, N=%d) per bench step, %d threads"
               % (w.name, afd, w.steps, len(r),
                  "" if stride == 1 else " of %d radii, every %d-th" % (w.m, stride), w.n, threads))
+    mode = shard_mode(args, w, world)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded BASELINE generator)", "impl": "reference",
-        "config": {"workload": w.name, "n": w.n, "m": w.m, "afd_steps": w.steps,
-                   "signals": w.batch, "sampled_afd_steps_per_bench_step": afd},
+        "higher_is_better": True, "scaling": scaling_of(mode), "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded BASELINE generator, SURVEY.md §8(d))",
+        "impl": "reference", "config": config_dict(args, w, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -280,9 +363,56 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def field_roofline(plan, w, radii_rows, ghat, exact, local):
+    """Roofline of the field (the dominant kernel): CUDA-event launch time of
+    one field evaluation over the plan's rows for `ghat` (on this stream),
+    against FP64 (N <= 8192) or HBM (large N: the row-batch intermediate and,
+    in exact mode, the live r^l table)."""
+    from paper_1711_08604_b200 import engine
+    rows = len(radii_rows)
+    batch = ghat.shape[0]
+    plan.time_field(ghat, reps=2)
+    field_ms = plan.time_field(ghat, reps=5 if w.n > 8192 else 50)
+    fpe = flops_per_eval(w.n)
+    launch_evals = batch * rows * w.n
+    achieved = launch_evals * fpe / (field_ms * 1e-3) / 1e12
+    peak = engine.fp64_peak_tflops(local)
+    bpe = bytes_per_eval(w.n, radii_rows) if exact else (32.0 if w.n > 8192 else 0.0)
+    hbm_peak, hbm_src = hbm_peak_gbs()
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get("field_%s_%s" % (
+            "exact" if exact else "fast", w.name))
+    instr = fp64_instr_per_eval(w.n) if exact else None
+    fp64 = {"achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "peak_source": "builder-measured in-run DFMA microbenchmark (afd_fp64_peak); "
+                           "MEASURED_PEAKS.json has no FP64 entry"}
+    if bpe and launch_evals * bpe / (hbm_peak * 1e9) > launch_evals * fpe / (peak * 1e12):
+        hbm = launch_evals * bpe / (field_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": hbm, "peak": hbm_peak, "unit": "GB/s",
+                "frac": hbm / hbm_peak, "traffic": traffic, "bytes_per_eval": bpe,
+                "peak_source": hbm_src, "fp64": fp64}
+    else:
+        roof = dict(fp64, bound="fp64", traffic=traffic)
+        if instr:
+            # bit-exact radix-2 arithmetic is mostly unfused: per eval the
+            # kernel issues `instr` FP64-pipe instructions for F(N) flops
+            roof["fp64_instr_per_eval"] = instr
+            roof["frac_ceiling_at_this_instruction_mix"] = fpe / (2.0 * instr)
+    roof.update({
+        "kernel": ("field_kernel (fused prologue + inverse DIT + scale + |.|^2 + argmax)"
+                   if w.n <= 8192 else
+                   "large-N field: pass A (big_field_a) + TMA column pass (col_tma_kernel)"),
+        "flops_per_eval": fpe, "evals_per_launch": launch_evals, "launch_ms": field_ms})
+    return roof
+
+
 def run_ours(args):
     import torch
     world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE=%d" % (args.gpus, world))
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
@@ -290,27 +420,19 @@ def run_ours(args):
     from paper_1711_08604_b200 import core, engine
     dev = torch.device("cuda", local)
     w, radii = workload(args.config)
-    plan = engine.get_plan(radii, w.n, batch=w.batch)
+    exact = args.mode == "exact"
+    fast = 0 if exact else 1
 
     def project(sig):
         p = engine.get_plan((0.0,), w.n, batch=len(sig))
-        return plan_to_np(p.analytic_projection(torch.from_numpy(sig.astype(np.complex128))
-                                                .to(dev)))
-
-    def plan_to_np(t):
-        return t.cpu().numpy()
+        return p.analytic_projection(torch.from_numpy(sig.astype(np.complex128)).to(dev)) \
+            .cpu().numpy()
 
     sig = host_signals(w, args.config, project=project)
-    # multi-GPU mode: replicas of the whole workload (c0/c1,
-    # weak scaling), the signals of a batch split over the ranks (c3), or the
-    # radius grid split over the ranks with one all-gather per step (c2/c4);
-    # the last two are strong scaling.  One GPU: the single-plan path.
-    mode = args.shard if args.shard != "auto" else {
-        "c3": "signals", "c2": "radii", "c4": "radii"}.get(w.name, "replicas")
-    if world == 1 and args.shard == "auto":
-        mode = "single"
+    mode = shard_mode(args, w, world)
     if mode in ("signals", "radii"):
         return run_sharded(args, w, radii, sig, mode, world, rank, local, dev)
+    plan = engine.get_plan(radii, w.n, batch=w.batch, fast=fast)
     g_dev = torch.from_numpy(sig).to(dev)
     out = plan.alloc_outputs(w.batch, w.steps)
     stream = torch.cuda.current_stream()
@@ -339,8 +461,7 @@ def run_ours(args):
     launches = plan.launch_count() - l0
     barrier()
     torch.cuda.synchronize()
-    per = [a.elapsed_time(b) for a, b in ev]
-    total_ms = float(sum(per))
+    total_ms = float(sum(a.elapsed_time(b) for a, b in ev))
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([total_ms], device=dev)
@@ -348,100 +469,50 @@ def run_ours(args):
         total_ms = float(t.item())
     evals = w.batch * w.m * w.n * w.steps
     value = world * evals * args.steps / (total_ms * 1e-3)
+    step_ms = total_ms / args.steps
 
-    # parity of the benchmarked output against the oracle (first signal;
-    # for the big configs only the first `check` steps, replayed by the oracle)
-    import oracle as O
     recs, counts = out.host_steps()
-    check = w.steps if w.m * w.n * w.steps <= (1 << 31) else 2
     parity = None
-    if not args.no_parity:
-        o = O.decompose(sig[0], np.array(radii), max_terms=check)
-        c = min(int(counts[0]), check)
-        parity = bool(c == len(o.steps) and
-                      np.array_equal(recs[0]["j"][:c], o.steps["j"]) and
-                      np.array_equal(recs[0]["radius"][:c], o.steps["radius"]) and
-                      np.array_equal(recs[0]["c_re"][:c], o.steps["c_re"]) and
-                      np.array_equal(recs[0]["residual"][:c], o.steps["residual"]))
+    if not args.no_parity and rank == 0:
+        parity = check_parity(w, radii, sig[0], recs[0], counts[0], exact)
 
-    # roofline: the fused field+argmax kernel, CUDA events on this stream
     ghat = plan.dft_forward(g_dev)
-    plan.time_field(ghat, reps=5)
-    field_ms = plan.time_field(ghat, reps=50)
-    fpe = flops_per_eval(w.n)
-    field_flops = w.batch * w.m * w.n * fpe
-    achieved = field_flops / (field_ms * 1e-3) / 1e12
-    peak = engine.fp64_peak_tflops(local)
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get("field_kernel_%s" % w.name)
-    # the binding roofline: FP64 for N <= 8192 (0 algorithmic HBM bytes), HBM
-    # for the large-N path (r^l table + row-batch intermediate)
-    launch_evals = w.batch * w.m * w.n
-    bpe = bytes_per_eval(w.n, radii)
-    hbm_peak, hbm_src = hbm_peak_gbs()
-    t_fp64 = launch_evals * fpe / (peak * 1e12)
-    t_hbm = launch_evals * bpe / (hbm_peak * 1e9)
-    if t_hbm > t_fp64:
-        hbm_achieved = launch_evals * bpe / (field_ms * 1e-3) / 1e9
-        roofline = {"bound": "hbm", "achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
-                    "frac": hbm_achieved / hbm_peak, "traffic": traffic,
-                    "bytes_per_eval": bpe, "peak_source": hbm_src,
-                    "fp64": {"achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                             "frac": achieved / peak}}
-    else:
-        roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": traffic,
-                    "peak_source": "measured in-run DFMA microbenchmark (afd_fp64_peak); "
-                                   "MEASURED_PEAKS.json has no FP64 entry",
-                    # bit-exact radix-2 arithmetic is mostly unfused: per eval the
-                    # kernel issues fp64_instr_per_eval FP64-pipe instructions for
-                    # F(N) flops, so even a saturated FP64 pipe reaches only this
-                    # fraction of the DFMA peak
-                    "fp64_instr_per_eval": fp64_instr_per_eval(w.n),
-                    "frac_ceiling_at_this_instruction_mix":
-                        fpe / (2.0 * fp64_instr_per_eval(w.n))}
-        if w.batch * w.m < 16384:
-            # the same kernel with enough rows to fill the GPU many times over
-            # (c3's regime: 128 spectra x 1024 radii r_m = m/1024): the
-            # workload's own launch is two rows per row-group, latency-bound
-            sb, sm_ = 128, 1024
-            # a private plan: the cached one keeps serving the e2e leg below
-            splan = engine.Plan(tuple(m / sm_ for m in range(sm_)), w.n, max_batch=sb,
-                                device=g_dev.device.index)
-            rng = np.random.default_rng(5)
-            sx = torch.from_numpy(rng.standard_normal((sb, w.n)) +
-                                  1j * rng.standard_normal((sb, w.n))).to(g_dev.device)
-            sgh = splan.dft_forward(sx)
-            splan.time_field(sgh, reps=2)
-            sms = splan.time_field(sgh, reps=10)
-            sach = sb * sm_ * w.n * fpe / (sms * 1e-3) / 1e12
-            roofline["steady_state"] = {
-                "evals_per_launch": sb * sm_ * w.n, "launch_ms": sms, "achieved": sach,
-                "frac": sach / peak,
-                "note": "same field kernel at N=%d, %d signals x M=%d radii" % (w.n, sb, sm_)}
-            del splan, sx, sgh
-    roofline.update({
-        "kernel": ("field_kernel (fused prologue + inverse DIT + scale + |.|^2 + argmax)"
-                   if w.n <= 8192 else
-                   "large-N field: big_pass_a + column pass(es) over the row batches"),
-        "flops_per_eval": fpe, "evals_per_launch": launch_evals, "launch_ms": field_ms,
-        "field_share_of_step": (field_ms * (w.steps) / (total_ms / args.steps))})
+    roofline = field_roofline(plan, w, radii, ghat, exact, local)
+    if exact and w.n <= 8192 and w.batch * w.m < 16384:
+        # the same kernel with enough rows to fill the GPU many times over
+        # (c3's regime: 128 spectra x 1024 radii r_m = m/1024): the small
+        # workloads' own launch is two rows per row-group, latency-bound
+        sb, sm_ = 128, 1024
+        splan = engine.Plan(tuple(m / sm_ for m in range(sm_)), w.n, max_batch=sb,
+                            device=local, fast=fast)
+        rng = np.random.default_rng(5)
+        sx = torch.from_numpy(rng.standard_normal((sb, w.n)) +
+                              1j * rng.standard_normal((sb, w.n))).to(dev)
+        sgh = splan.dft_forward(sx)
+        splan.time_field(sgh, reps=2)
+        sms = splan.time_field(sgh, reps=10)
+        fpe = flops_per_eval(w.n)
+        sach = sb * sm_ * w.n * fpe / (sms * 1e-3) / 1e12
+        roofline["steady_state"] = {
+            "evals_per_launch": sb * sm_ * w.n, "launch_ms": sms, "achieved": sach,
+            "frac": sach / roofline["peak"],
+            "note": "same field kernel at N=%d, %d signals x M=%d radii" % (w.n, sb, sm_)}
+        del splan, sx, sgh
+    roofline["field_share_of_step"] = roofline["launch_ms"] * w.steps / step_ms
 
     # e2e through the public API, host buffers, pinned H2D + D2H in the region
     grid = core.ParameterGrid(radii, w.n)
-    e2e_reps = args.e2e_reps or max(3, min(args.steps, 200))
-    for _ in range(min(3, e2e_reps)):
-        plan.decompose_host(sig, w.steps)
+    engine_name = "fft" if exact else "fft-fast"
+    e2e_reps = args.e2e_reps or max(2, min(args.steps, int(20e3 / max(step_ms, 1e-3))))
+    plan.decompose_host(sig, w.steps)
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(e2e_reps):
         if w.batch == 1:
-            core.decompose(sig[0], grid, max_terms=w.steps)
+            core.decompose(sig[0], grid, max_terms=w.steps, engine=engine_name)
         else:
-            core.decompose_batch(sig, grid, max_terms=w.steps)
+            core.decompose_batch(sig, grid, max_terms=w.steps, engine=engine_name)
     e2e_s = time.perf_counter() - t0
     if world > 1:
         import torch.distributed as dist
@@ -450,7 +521,9 @@ def run_ours(args):
         e2e_s = float(t.item())
     _, _, _, _, h2d, d2h = plan.decompose_host(sig, w.steps)
     e2e = {"value": world * evals * e2e_reps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
-           "d2h_bytes_per_step": d2h, "api": "paper_1711_08604_b200.core.decompose"}
+           "d2h_bytes_per_step": d2h, "reps": e2e_reps,
+           "api": "paper_1711_08604_b200.core.decompose%s(engine=%r)"
+                  % ("" if w.batch == 1 else "_batch", engine_name)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -459,16 +532,13 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded BASELINE generator, SURVEY.md §8(d))",
-            "config": {"workload": w.name, "n": w.n, "m": w.m, "afd_steps": w.steps,
-                       "signals": w.batch, "radii": "r_m = m/M",
-                       "parallelism": "replicas" if world > 1 else "single",
-                       "l2": "flushed (512 MiB write) between timed iterations",
-                       "mode": "exact (bit-identical to reference)"},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": scaling_of(mode), "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded BASELINE generator, SURVEY.md §8(d))",
+            "config": config_dict(args, w, world),
             "gpu_launches": launches,
-            "parity_vs_oracle": parity,
+            "parity_vs_oracle": None if parity is None else parity["ok"],
+            "parity": parity,
             "roofline": roofline,
             "e2e": e2e,
             "clocks": clk.summary(),
@@ -487,8 +557,10 @@ def run_sharded(args, w, radii, sig, mode, world, rank, local, dev):
     then every rank applies the same update: distributed.py)."""
     import torch
     import torch.distributed as dist
-    from paper_1711_08604_b200 import _capi, core, distributed as D, engine
+    from paper_1711_08604_b200 import core, distributed as D, engine
 
+    exact = args.mode == "exact"
+    fast = 0 if exact else 1
     if not dist.is_initialized():  # explicit --shard on one GPU without torchrun
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29517")
@@ -496,10 +568,11 @@ def run_sharded(args, w, radii, sig, mode, world, rank, local, dev):
                                 device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    lo, hi = 0, w.batch
     if mode == "signals":
         lo, hi = D.shard_bounds(w.batch, rank, world)
         m0, m1, b = 0, w.m, hi - lo
-        plan = engine.get_plan(radii, w.n, batch=max(b, 1))
+        plan = engine.get_plan(radii, w.n, batch=max(b, 1), fast=fast)
         g_dev = torch.from_numpy(sig[lo:hi]).to(dev)
         out = plan.alloc_outputs(max(b, 1), w.steps)
 
@@ -513,25 +586,16 @@ def run_sharded(args, w, radii, sig, mode, world, rank, local, dev):
     else:
         m0, m1 = D.shard_bounds(w.m, rank, world)
         b = w.batch
-        plan = engine.get_plan(radii, w.n, batch=b, m0=m0, m1=m1)
+        plan = engine.get_plan(radii, w.n, batch=b, m0=m0, m1=m1, fast=fast)
         g_dev = torch.from_numpy(sig).to(dev)
-        steps_buf = torch.zeros((b, w.steps, _capi.STEP_DTYPE.itemsize), dtype=torch.uint8,
-                                device=dev)
-        gathered = torch.empty((world, b, 32), dtype=torch.uint8, device=dev)
-        state = {}
+        runner = D.ShardedRunner(plan, b, w.steps, None, False, group=None)
 
         def run():
-            plan.sharded_begin(g_dev)
-            for k in range(w.steps):
-                local_c = plan.select_local(k, False, b)
-                dist.all_gather_into_tensor(gathered, local_c.contiguous())
-                plan.apply_step(k, w.steps, None, False,
-                                gathered.permute(1, 0, 2).contiguous(), steps_buf)
-            state["fin"] = plan.sharded_finish(b)
+            runner.run(g_dev)
 
         def records():
-            rec = steps_buf.cpu().numpy().view(_capi.STEP_DTYPE)[..., 0]
-            return rec[0], int(state["fin"][0].cpu().numpy()[0])
+            rec, counts = runner.host_records()
+            return rec[0], int(counts[0])
 
     for _ in range(args.warmup):
         run()
@@ -556,74 +620,51 @@ def run_sharded(args, w, radii, sig, mode, world, rank, local, dev):
     total_ms = float(t.item())
     evals = w.batch * w.m * w.n * w.steps
     value = evals * args.steps / (total_ms * 1e-3)
+    step_ms = total_ms / args.steps
 
-    import oracle as O
     parity = None
-    if rank == 0 and not args.no_parity:
+    if rank == 0 and not args.no_parity and (mode == "radii" or hi > lo):
         rec, count = records()
-        check = w.steps if w.m * w.n * w.steps <= (1 << 31) else 2
-        o = O.decompose(sig[0], np.array(radii), max_terms=check)
-        c = min(count, check)
-        parity = bool(c == len(o.steps) and np.array_equal(rec["j"][:c], o.steps["j"]) and
-                      np.array_equal(rec["radius"][:c], o.steps["radius"]) and
-                      np.array_equal(rec["c_re"][:c], o.steps["c_re"]) and
-                      np.array_equal(rec["residual"][:c], o.steps["residual"]))
+        parity = check_parity(w, radii, sig[lo], rec, count, exact)
 
-    # roofline of this rank's field launches (its rows / signals)
-    gh = plan.dft_forward(torch.from_numpy(sig[:1] if mode == "radii" else sig[lo:lo + 1])
-                          .to(dev))
-    plan.time_field(gh, reps=3)
-    field_ms = plan.time_field(gh, reps=10)
-    fpe = flops_per_eval(w.n)
-    achieved = (m1 - m0) * w.n * fpe / (field_ms * 1e-3) / 1e12
-    peak = engine.fp64_peak_tflops(local)
-    roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None,
-                "kernel": "field_kernel / big_pass_a+big_pass_col (this rank's rows, one signal)",
-                "flops_per_eval": fpe, "evals_per_launch": (m1 - m0) * w.n,
-                "launch_ms": field_ms,
-                "peak_source": "measured in-run DFMA microbenchmark (afd_fp64_peak)"}
-    bpe = bytes_per_eval(w.n, radii[m0:m1])
-    hbm_peak, hbm_src = hbm_peak_gbs()
-    if bpe and bpe / (hbm_peak * 1e9) > fpe / (peak * 1e12):  # HBM-bound (large N)
-        hbm = (m1 - m0) * w.n * bpe / (field_ms * 1e-3) / 1e9
-        roofline.update({"bound": "hbm", "achieved": hbm, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": hbm / hbm_peak, "bytes_per_eval": bpe, "peak_source": hbm_src,
-                         "fp64": {"achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                                  "frac": achieved / peak}})
+    # roofline of this rank's field launches (its rows, one signal)
+    gh = plan.dft_forward(torch.from_numpy(sig[lo:lo + 1]).to(dev))
+    roofline = field_roofline(plan, w, radii[m0:m1], gh, exact, local)
+    roofline["field_share_of_step"] = roofline["launch_ms"] * w.steps * (
+        1 if mode == "radii" else b) / step_ms
 
     # e2e through the public API with host buffers
     grid = core.ParameterGrid(radii, w.n)
+    engine_name = "fft" if exact else "fft-fast"
     reps = args.e2e_reps or 2
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(reps):
         if mode == "signals":
             if hi > lo:
-                core.decompose_batch(sig[lo:hi], grid, max_terms=w.steps)
+                core.decompose_batch(sig[lo:hi], grid, max_terms=w.steps, engine=engine_name)
         else:
-            D.decompose_sharded(sig, grid, max_terms=w.steps)
+            D.decompose_sharded(sig, grid, max_terms=w.steps, engine_name=engine_name)
     torch.cuda.synchronize()
     tt = torch.tensor([time.perf_counter() - t0], device=dev)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     e2e = {"value": evals * reps / float(tt.item()), "unit": UNIT,
            "h2d_bytes_per_step": int(sig.nbytes if mode == "radii" else sig[lo:hi].nbytes),
-           "d2h_bytes_per_step": None,
+           "d2h_bytes_per_step": int((sig.nbytes if mode == "radii" else sig[lo:hi].nbytes) +
+                                     72 * w.steps * (b if mode == "signals" else w.batch)),
+           "reps": reps,
            "api": ("paper_1711_08604_b200.core.decompose_batch" if mode == "signals" else
                    "paper_1711_08604_b200.distributed.decompose_sharded")}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded BASELINE generator, SURVEY.md §8(d))",
-            "config": {"workload": w.name, "n": w.n, "m": w.m, "afd_steps": w.steps,
-                       "signals": w.batch, "radii": "r_m = m/M",
-                       "parallelism": "dp%d over %s" % (world, mode),
-                       "l2": "flushed (512 MiB write) between timed iterations",
-                       "mode": "exact (bit-identical to reference)"},
-            "gpu_launches": launches, "parity_vs_oracle": parity, "roofline": roofline,
-            "e2e": e2e, "clocks": clk.summary(), "cpu_baseline": None,
+            "config": config_dict(args, w, world),
+            "gpu_launches": launches,
+            "parity_vs_oracle": None if parity is None else parity["ok"], "parity": parity,
+            "roofline": roofline, "e2e": e2e, "clocks": clk.summary(), "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
@@ -631,6 +672,7 @@ def run_sharded(args, w, radii, sig, mode, world, rank, local, dev):
 
 def main():
     args = parse()
+    maybe_spawn(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -20,8 +20,9 @@
  *    NULL = legacy default stream).
  *  - A plan binds one device, one transform length N = 2^K (8 <= N), the
  *    radius grid (M radii, of which this plan evaluates rows [m0, m1)) and
- *    a maximum batch of independent signals.  Plans are not thread-safe;
- *    use one plan per host thread.
+ *    a maximum batch of independent signals.  A plan's buffers are shared by
+ *    its calls: calls on one plan must not overlap (the Python layer holds a
+ *    per-plan lock); use one plan per concurrent caller.
  *  - Host tables are taken from the caller so both sides start from the
  *    same bits: twiddles exp(-2 pi i k/N), k < N/2 (transform.py:65),
  *    circle exp(2 pi i m/N) (core.py:87), scales
@@ -69,6 +70,18 @@ typedef struct afd_plan afd_plan;
 const char *afd_last_error(void);
 int afd_version(void);
 
+/* Plan flags.
+ * AFD_PLAN_FAST: the field (the M x N grid of weighted inverse transforms,
+ *   transform.py:185-201) is computed with FMA-fused FP64 butterflies,
+ *   exact trivial rotations and r^l generated on chip from per-radius
+ *   factor tables instead of the reference's radix-2 numpy arithmetic and
+ *   M x N cumprod table: the selected indices are identical to the
+ *   reference's and coefficients, remainders and errors agree to ~1e-14
+ *   relative (the parity contract is 1e-9), not bit for bit.  Everything
+ *   after the argmax (update, energy, forward transform, records) stays
+ *   bit-exact arithmetic.  Default (0): bit-identical to the reference. */
+#define AFD_PLAN_FAST 1
+
 /* Create a plan.  radii_host/scales_host hold all M radii/scales
  * (core.ParameterGrid.radii, core.py:115-145); the plan evaluates global
  * rows [m0, m1) (radius sharding across GPUs).
@@ -77,7 +90,7 @@ int afd_version(void);
 int afd_plan_create(afd_plan **out, int device, int64_t n, int64_t m, int64_t m0, int64_t m1,
                     int64_t max_batch, const double *radii_host, const double *scales_host,
                     const double *twiddle_host /* N/2 complex */,
-                    const double *circle_host /* N complex */);
+                    const double *circle_host /* N complex */, int flags /* AFD_PLAN_* */);
 int afd_plan_destroy(afd_plan *plan);
 
 /* transform.dft_forward / dft_inverse (transform.py:106-134), batch rows. */

@@ -30,6 +30,7 @@ CAND_DTYPE = np.dtype([("mag2", np.float64), ("flat", np.int64),
                        ("re", np.float64), ("im", np.float64)])
 
 STEP_FLAG_POW_AMBIGUOUS = 1
+PLAN_FAST = 1  # AFD_PLAN_FAST
 
 # (name, restype, argtypes) for every symbol include/afd_capi.h declares
 _VP = C.c_void_p
@@ -40,7 +41,7 @@ SIGNATURES = [
     ("afd_last_error", C.c_char_p, []),
     ("afd_version", _I, []),
     ("afd_plan_create", _I, [C.POINTER(_VP), _I, _I64, _I64, _I64, _I64, _I64, _VP, _VP, _VP,
-                             _VP]),
+                             _VP, _I]),
     ("afd_plan_destroy", _I, [_VP]),
     ("afd_dft_forward", _I, [_VP, _VP, _VP, _I64, _VP]),
     ("afd_dft_inverse", _I, [_VP, _VP, _VP, _I64, _VP]),

@@ -17,6 +17,11 @@ is the reference's O(M N^2) quadrature baseline (``oracle.field_direct``),
 also on the device (``csrc/afd_direct.cuh``, N <= 8192); its sums are
 ordered differently from np.correlate, so it agrees with the reference to
 the reference's own engine tolerance (identical poles, 1e-9), not bitwise.
+``engine="fft-fast"`` (an addition; the reference has no such engine) is
+the transform engine with the field computed in fast FP64 arithmetic
+(AFD_PLAN_FAST: FMA-fused butterflies, r^l formed on chip): the selected
+poles are identical to the reference's and coefficients, remainders and
+errors agree to ~1e-14 relative (the north-star contract is 1e-9).
 ``parallel`` is accepted for signature compatibility; the device path is
 always parallel and, like the reference's threaded path, produces
 identical results.
@@ -42,7 +47,7 @@ __all__ = [
 ]
 
 RADIUS_WARN_LIMIT = 0.95  # core.py:59
-ENGINES = ("fft", "direct")
+ENGINES = ("fft", "direct", "fft-fast")
 
 
 def _engine():
@@ -292,7 +297,7 @@ def _check_decompose_args(g, grid, max_terms, threshold, engine):
         raise ValueError("grid angular_count %d does not match signal length %d"
                          % (grid.angular_count, g.shape[-1]))
     if engine not in ENGINES:
-        raise ValueError("engine must be 'fft' or 'direct', got %r" % (engine,))
+        raise ValueError("engine must be 'fft' or 'direct', got %r" % (engine,))  # core.py:357-358
     if max_terms < 1:
         raise ValueError("max_terms must be >= 1")
     if threshold is not None and not 0.0 < threshold <= 1.0:
@@ -357,7 +362,8 @@ def decompose_batch(signals, grid, max_terms=10, threshold=None, engine="fft", d
             raise ValueError("signal contains non-finite samples")
         _check_decompose_args(sig, grid, max_terms, threshold, engine)
     b, n = sig.shape
-    plan = _engine().get_plan(grid.radii, n, batch=b, engine=1 if engine == "direct" else 0)
+    plan = _engine().get_plan(grid.radii, n, batch=b, engine=1 if engine == "direct" else 0,
+                              fast=engine == "fft-fast")
     rec, counts, initial, rem, _, _ = plan.decompose_host(sig, int(max_terms), threshold,
                                                           dc_first)
     if b == 1:

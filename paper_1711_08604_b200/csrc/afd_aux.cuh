@@ -43,6 +43,32 @@ __global__ void power_table_kernel(const double* __restrict__ radii, long long m
   if (pw_len != nullptr && row < m1) pw_len[row - m0] = (int)len;
 }
 
+// Fast-mode weight factor tables (AFD_PLAN_FAST), one row per plan radius:
+// section j (j = 0, 1, 2; n_j entries, exponent step 2^e_j, e_0 = 0) holds
+// r^(k 2^e_j), section 0 times the row's scale sqrt(1-r^2)/(N(1-r^N)) (the
+// reference's own scales, transform.py:153).  The kernels weight position l
+// by the product of one entry per section (its bit fields), so r^l is never
+// tabulated: ~2 ulp per pow, a few ulp per product, against the reference's
+// cumprod (transform.py:147-150), which itself drifts by up to 6e-14.
+__global__ void fast_weight_kernel(const double* __restrict__ radii,
+                                   const double* __restrict__ scales, long long m0,
+                                   long long rows, int stride, int n0, int n1, int e1, int n2,
+                                   int e2, double* __restrict__ fw) {
+  const long long total = rows * stride;
+  for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+       x += (long long)gridDim.x * blockDim.x) {
+    const long long row = x / stride;
+    const int k = (int)(x % stride);
+    const double r = radii[m0 + row];
+    double v;
+    if (k < n0) v = scales[m0 + row] * pow(r, (double)k);
+    else if (k < n0 + n1) v = pow(r, ldexp((double)(k - n0), e1));
+    else v = pow(r, ldexp((double)(k - n0 - n1), e2));
+    (void)n2;
+    fw[x] = v;
+  }
+}
+
 __device__ __forceinline__ Cand cand_none() {
   Cand c;
   c.mag = -1.0;

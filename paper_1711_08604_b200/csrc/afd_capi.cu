@@ -67,8 +67,15 @@ struct afd_plan {
   double* scales = nullptr;   // [M]
   double2* twst = nullptr;    // stage tables [N-1]
   double2* circle = nullptr;  // [N]
-  double* pw = nullptr;       // [m1-m0][N] cumprod r^l
+  double* pw = nullptr;       // [m1-m0][N] cumprod r^l (exact mode)
   double2* tw_img = nullptr;  // field kernel's shared-memory twiddle image
+  // fast mode (AFD_PLAN_FAST): (c, t) stage tables, their shared-memory
+  // image, and per-row weight factor tables instead of pw
+  bool fast = false;
+  double2* twct = nullptr;     // [N-1] (cos, tan) of the conjugated stage twiddles
+  double2* tw_img_ct = nullptr;
+  double* fw = nullptr;        // [m1-m0][fw_stride]
+  int fw_stride = 0;
   // per-signal working buffers
   double2* ghat = nullptr;    // [max_batch][N]
   double2* rem = nullptr;     // [max_batch][N]
@@ -220,8 +227,13 @@ template <int K, bool MAT>
 int setup_field_kernel(int* occ) {
   auto kern = field_kernel<K, kFieldRB, groups_for<K>(), MAT>;
   CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem<K>()));
+  CU(cudaFuncSetAttribute(field_kernel<K, kFieldRB, groups_for<K>(), MAT, false, true>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem<K>()));
   if constexpr (field_tmem_capable<K>()) {
     CU(cudaFuncSetAttribute(field_kernel<K, kFieldRB, groups_for<K>(), MAT, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)field_smem<K>()));
+    CU(cudaFuncSetAttribute(field_kernel<K, kFieldRB, groups_for<K>(), MAT, true, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)field_smem<K>()));
   }
@@ -247,6 +259,11 @@ int setup_kernels(afd_plan* p) {
   CU(cudaMalloc(&p->tw_img, sizeof(double2) * SmemTw<K, kFieldRB>::ENTRIES));
   build_tw_image_kernel<K><<<32, 256>>>(p->tw_img, p->twst);
   p->launches++;
+  if (p->fast) {
+    CU(cudaMalloc(&p->tw_img_ct, sizeof(double2) * SmemTw<K, kFieldRB>::ENTRIES));
+    build_tw_image_kernel<K><<<32, 256>>>(p->tw_img_ct, p->twct);
+    p->launches++;
+  }
   CU(cudaGetLastError());
   p->field_block = field_block<K>();
   if ((rc = setup_field_kernel<K, false>(&p->field_occ))) return rc;
@@ -315,23 +332,27 @@ int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64
   // TMEM twiddles need the whole TMEM of the SM: only for one full-size CTA
   // (both row-groups) per SM
   const bool tm = field_tmem_capable<K>() && ge == G && field_tmem_enabled();
+  constexpr bool TMC = field_tmem_capable<K>();
+  // exact: the cumprod table and the numpy twiddle image; fast: the weight
+  // factor tables and the (c, t) image
+  const double* tab = p->fast ? p->fw : p->pw;
+  const double2* img = p->fast ? p->tw_img_ct : p->tw_img;
   if (field_out) {
-    if (tm) {
-      field_kernel<K, kFieldRB, G, true, field_tmem_capable<K>()><<<grid, block, smem, st>>>(
-          ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, nullptr, field_out, nullptr,
-          p->tw_img, field_pp(), (unsigned*)nullptr, 0);
-    } else {
-      field_kernel<K, kFieldRB, G, true><<<grid, block, smem, st>>>(
-          ghat, p->pw, p->scales, p->twst, r0, r1, p->m0, nullptr, field_out, nullptr,
-          p->tw_img, field_pp(), (unsigned*)nullptr, 0);
-    }
+    auto kern = p->fast ? (tm ? field_kernel<K, kFieldRB, G, true, TMC, true>
+                              : field_kernel<K, kFieldRB, G, true, false, true>)
+                        : (tm ? field_kernel<K, kFieldRB, G, true, TMC>
+                              : field_kernel<K, kFieldRB, G, true>);
+    kern<<<grid, block, smem, st>>>(ghat, tab, p->scales, p->twst, r0, r1, p->m0, nullptr,
+                                    field_out, nullptr, img, field_pp(), (unsigned*)nullptr, 0);
   } else {
-    auto kern = tm ? field_kernel<K, kFieldRB, G, false, field_tmem_capable<K>()>
-                   : field_kernel<K, kFieldRB, G, false>;
-    CU(launch_pdl(kern, grid, dim3(block), smem, st, ghat, (const double*)p->pw,
+    auto kern = p->fast ? (tm ? field_kernel<K, kFieldRB, G, false, TMC, true>
+                              : field_kernel<K, kFieldRB, G, false, false, true>)
+                        : (tm ? field_kernel<K, kFieldRB, G, false, TMC>
+                              : field_kernel<K, kFieldRB, G, false>);
+    CU(launch_pdl(kern, grid, dim3(block), smem, st, ghat, tab,
                   (const double*)p->scales, (const double2*)p->twst, (long long)r0,
                   (long long)r1, (long long)p->m0, cand, (double2*)nullptr, state,
-                  (const double2*)p->tw_img, field_pp(), row_ctr, launch_id));
+                  img, field_pp(), row_ctr, launch_id));
   }
   p->launches++;
   CU(cudaGetLastError());
@@ -453,8 +474,21 @@ int decomp_field_ctas(const afd_plan* p, int64_t batch) {
   return d ? d : field_ctas_for(p, rows, batch);
 }
 
+// The decomposition graph bakes in the addresses of the plan's buffers:
+// any reallocation must drop it (it is re-captured on the next call).
+void invalidate_graph(afd_plan* p) {
+  if (p->gexec) cudaGraphExecDestroy(p->gexec);
+  p->gexec = nullptr;
+  p->g_max_terms = -1;
+  p->g_dc_first = -1;
+  p->g_threshold = -2;
+  p->g_batch = -1;
+  p->g_stream = nullptr;
+}
+
 int ensure_cand(afd_plan* p, int64_t batch, int ncta) {
   if (ncta > p->ncand_cap) {
+    invalidate_graph(p);
     if (p->cand) cudaFree(p->cand);
     p->cand = nullptr;
     p->ncand_cap = 0;
@@ -467,6 +501,7 @@ int ensure_cand(afd_plan* p, int64_t batch, int ncta) {
 
 int ensure_steps(afd_plan* p, int max_terms) {
   if (max_terms > p->steps_cap) {
+    invalidate_graph(p);
     if (p->steps) cudaFree(p->steps);
     p->steps = nullptr;
     p->steps_cap = 0;
@@ -788,7 +823,7 @@ int afd_version(void) { return 1; }
 
 int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0, int64_t m1,
                     int64_t max_batch, const double* radii_host, const double* scales_host,
-                    const double* twiddle_host, const double* circle_host) {
+                    const double* twiddle_host, const double* circle_host, int flags) {
   if (!out) return fail(AFD_E_INVALID, "out is NULL");
   *out = nullptr;
   if (n < 8 || (n & (n - 1)))
@@ -804,6 +839,9 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
   if (max_batch < 1) return fail(AFD_E_INVALID, "max_batch must be >= 1");
   if (!radii_host || !scales_host || !twiddle_host || !circle_host)
     return fail(AFD_E_INVALID, "NULL host table");
+  if (flags & ~AFD_PLAN_FAST) return fail(AFD_E_INVALID, "unknown plan flags 0x%x", flags);
+  if ((flags & AFD_PLAN_FAST) && K > kMaxOnChipK && K != 16 && K != 20)
+    return fail(AFD_E_UNSUPPORTED, "fast mode for N = 2^%d not built (2^3..2^13, 2^16, 2^20)", K);
   for (int64_t i = 0; i < m; ++i) {
     if (!(radii_host[i] >= 0.0 && radii_host[i] < 1.0))
       return fail(AFD_E_INVALID, "grid radii must lie in [0, 1), got %g", radii_host[i]);
@@ -816,6 +854,7 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
   p->m0 = m0;
   p->m1 = m1;
   p->max_batch = max_batch;
+  p->fast = (flags & AFD_PLAN_FAST) != 0;
   auto cleanup = [&](int rc) {
     afd_plan_destroy(p);
     return rc;
@@ -839,13 +878,35 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
   ALLOC(p->scales, sizeof(double) * m);
   ALLOC(p->twst, sizeof(double2) * (N - 1));
   ALLOC(p->circle, sizeof(double2) * N);
-  ALLOC(p->pw, sizeof(double) * N * (size_t)(m1 - m0));
+  // fast mode: per-row weight factor tables (fast_weight_kernel) instead of
+  // the M x N cumprod table
+  int fw_sec[3] = {0, 0, 0}, fw_exp[3] = {0, 0, 0};
+  if (p->fast) {
+    if (K <= kMaxOnChipK) {
+      const int rb = K >= 4 ? 4 : K;  // Geo<K, kFieldRB>
+      fw_sec[0] = 1 << (K - rb);      // scale r^t, t < T
+      fw_sec[1] = 1 << rb;            // r^(T m), m < P
+      fw_exp[1] = K - rb;
+    } else {
+      const int ka = big_ka(K);
+      fw_sec[0] = 1 << (K - ka);  // scale r^c, c < N / 2^ka (the block's low bits)
+      fw_sec[1] = 1 << (ka - 4);  // r^(t 2^(K-ka)), t < 2^(ka-4)
+      fw_exp[1] = K - ka;
+      fw_sec[2] = 16;             // r^(m 2^(K-4)), m < 16
+      fw_exp[2] = K - 4;
+    }
+    p->fw_stride = fw_sec[0] + fw_sec[1] + fw_sec[2];
+    ALLOC(p->fw, sizeof(double) * (size_t)p->fw_stride * (size_t)(m1 - m0));
+    ALLOC(p->twct, sizeof(double2) * (N - 1));
+  } else {
+    ALLOC(p->pw, sizeof(double) * N * (size_t)(m1 - m0));
+    ALLOC(p->pw_len, sizeof(int) * (size_t)(m1 - m0));
+  }
   ALLOC(p->ghat, sizeof(double2) * N * max_batch);
   ALLOC(p->rem, sizeof(double2) * N * max_batch);
   ALLOC(p->gin, sizeof(double2) * N * max_batch);
   ALLOC(p->state, sizeof(State) * max_batch);
   ALLOC(p->row_ctr, sizeof(unsigned) * 2 * max_batch);
-  ALLOC(p->pw_len, sizeof(int) * (size_t)(m1 - m0));
 #undef ALLOC
 #define ALLOC2(ptr, bytes)                                                         \
   do {                                                                             \
@@ -858,8 +919,28 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
       cudaMemcpy(p->circle, circle_host, sizeof(double2) * N, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemset(p->state, 0, sizeof(State) * max_batch) != cudaSuccess)
     return cleanup(fail(AFD_E_CUDA, "table upload failed"));
-  // r^l power rows (np.cumprod, transform.py:147-150), once per plan
-  {
+  if (p->fast) {
+    // (c, t) of the conjugated stage twiddles W = conj(w) = c (1 + i t),
+    // c = Re W, t = Im W / Re W (numpy's table never has Re W == 0 exactly:
+    // W_4 = 6.12e-17 + 1j keeps t finite; guarded anyway)
+    std::vector<double2> ct(N - 1);
+    for (size_t i = 0; i < N - 1; ++i) {
+      const double wr = st[i].x, wi = -st[i].y;
+      const double c = wr != 0.0 ? wr : 0x1p-60;
+      ct[i] = make_double2(c, wi / c);
+    }
+    if (cudaMemcpy(p->twct, ct.data(), sizeof(double2) * (N - 1), cudaMemcpyHostToDevice) !=
+        cudaSuccess)
+      return cleanup(fail(AFD_E_CUDA, "table upload failed"));
+    const int64_t rows = m1 - m0;
+    const int64_t total = rows * p->fw_stride;
+    fast_weight_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256>>>(
+        p->radii, p->scales, m0, rows, p->fw_stride, fw_sec[0], fw_sec[1], fw_exp[1], fw_sec[2],
+        fw_exp[2], p->fw);
+    p->launches++;
+    if (cudaGetLastError() != cudaSuccess) return cleanup(fail(AFD_E_CUDA, "weight table launch"));
+  } else {
+    // r^l power rows (np.cumprod, transform.py:147-150), once per plan
     const int64_t rows = m1 - m0;
     power_table_kernel<<<(unsigned)((rows + 31) / 32), 32>>>(p->radii, m0, m1, n, p->pw,
                                                              p->pw_len);
@@ -871,11 +952,13 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
     // large N: bit-reversed power rows (transform.py:151) and batch buffers
     p->big = true;
     p->ka = big_ka(K);
-    bitrev_rows_kernel<<<dim3(1u << (K - 10), (unsigned)(m1 - m0)), dim3(32, 32)>>>(p->pw, K);
-    perm_blocks_kernel<<<dim3(1u << (K - p->ka), (unsigned)(m1 - m0)), 256,
-                         sizeof(double) << p->ka>>>(p->pw, K, p->ka);
-    p->launches += 2;
-    if (cudaGetLastError() != cudaSuccess) return cleanup(fail(AFD_E_CUDA, "bitrev launch"));
+    if (!p->fast) {
+      bitrev_rows_kernel<<<dim3(1u << (K - 10), (unsigned)(m1 - m0)), dim3(32, 32)>>>(p->pw, K);
+      perm_blocks_kernel<<<dim3(1u << (K - p->ka), (unsigned)(m1 - m0)), 256,
+                           sizeof(double) << p->ka>>>(p->pw, K, p->ka);
+      p->launches += 2;
+      if (cudaGetLastError() != cudaSuccess) return cleanup(fail(AFD_E_CUDA, "bitrev launch"));
+    }
     {
       // Rows per batch: all of them if kBigBatchBytes allows, else as many as
       // it allows rounded down to a whole number of pass-A rounds.
@@ -922,6 +1005,9 @@ int afd_plan_destroy(afd_plan* p) {
   cudaFree(p->circle);
   cudaFree(p->pw);
   cudaFree(p->tw_img);
+  cudaFree(p->twct);
+  cudaFree(p->tw_img_ct);
+  cudaFree(p->fw);
   cudaFree(p->ghat);
   cudaFree(p->rem);
   cudaFree(p->gin);
@@ -1020,10 +1106,7 @@ int afd_plan_set_engine(afd_plan* p, int engine) {
   if (!p) return fail(AFD_E_INVALID, "NULL plan");
   if (engine != 0 && engine != 1) return fail(AFD_E_INVALID, "engine must be 0 (fft) or 1 (direct)");
   if (engine == 1 && p->big) return fail(AFD_E_UNSUPPORTED, "direct engine supports N <= 8192");
-  if (engine != p->engine && p->gexec) {
-    cudaGraphExecDestroy(p->gexec);
-    p->gexec = nullptr;
-  }
+  if (engine != p->engine) invalidate_graph(p);
   p->engine = engine;
   return 0;
 }
@@ -1153,8 +1236,7 @@ int afd_decompose(afd_plan* p, const double* g0, int64_t batch, int max_terms, d
   const bool reuse = p->gexec && p->g_max_terms == max_terms && p->g_dc_first == dc_first &&
                      p->g_threshold == thr && p->g_batch == batch && p->g_stream == st;
   if (!reuse) {
-    if (p->gexec) cudaGraphExecDestroy(p->gexec);
-    p->gexec = nullptr;
+    invalidate_graph(p);
     // make sure buffers exist before capture (allocation is not capturable)
     const int ncta = decomp_field_ctas(p, batch);
     if ((rc = ensure_cand(p, batch, ncta))) return rc;

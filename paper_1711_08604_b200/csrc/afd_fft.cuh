@@ -28,6 +28,8 @@
 // across lanes later.  (Shared-memory slots are padded, see Geo::sw.)
 #pragma once
 
+#include <type_traits>
+
 #include "afd_common.cuh"
 
 namespace afd {
@@ -365,6 +367,150 @@ __device__ __forceinline__ void fft_pass_tm(double2 (&v)[Geo<K, RB>::P], const T
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fast mode (AFD_PLAN_FAST).  The same DIT dataflow, but each butterfly is
+// FMA-fused: a twiddle is held as (c, t) with W = c (1 + i t) (c = cos,
+// t = tan of the conjugated numpy twiddle, built once per plan), so
+//     u  = hi (1 + i t)          2 DFMA
+//     lo, hi = lo +- c u         4 DFMA
+// is 6 FP64 instructions instead of the reference's 2 DMUL + 2 DFMA + 4 DADD,
+// and is exact to a few ulp for every angle (t is large only where c is
+// small; numpy's W_4 = 6.12e-17 - 1j keeps t finite).  Pass 0's twiddles
+// are the 16th roots of unity, applied as compile-time constants: W = 1 and
+// W = +i are exact add/sub butterflies (no multiply at all).  The weighting
+// r^l and the scale are formed on chip and fused into stage 0 (see
+// fast_prologue), so stage 0 is skipped here.  Results agree with the
+// reference to ~1e-14 relative, not bit for bit.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void bfly_ct(double2& lo, double2& hi, double c, double t) {
+  const double ur = fma(-t, hi.y, hi.x);
+  const double ui = fma(t, hi.x, hi.y);
+  hi = make_double2(fma(-c, ur, lo.x), fma(-c, ui, lo.y));
+  lo = make_double2(fma(c, ur, lo.x), fma(c, ui, lo.y));
+}
+// W = +i (inverse transform, quarter turn): lo +- (-hi.y, hi.x)
+__device__ __forceinline__ void bfly_pi(double2& lo, double2& hi) {
+  const double2 l = lo;
+  lo = make_double2(l.x - hi.y, l.y + hi.x);
+  hi = make_double2(l.x + hi.y, l.y - hi.x);
+}
+// exact (re, im) twiddle or (c, t) twiddle, by mode
+template <bool FAST>
+__device__ __forceinline__ void bfly_any(double2& lo, double2& hi, double2 w) {
+  if constexpr (FAST) bfly_ct(lo, hi, w.x, w.y);
+  else bfly(lo, hi, w);
+}
+
+// (c, t) of exp(+i pi a / 8), a = 0..7 (correctly rounded); a = 0, 4 are the
+// exact W = 1, W = +i butterflies.
+__device__ __forceinline__ constexpr double ct_c8(int a) {
+  return a == 1 ? 0x1.d906bcf328d46p-1 : a == 2 ? 0x1.6a09e667f3bcdp-1 :
+         a == 3 ? 0x1.87de2a6aea963p-2 : a == 5 ? -0x1.87de2a6aea963p-2 :
+         a == 6 ? -0x1.6a09e667f3bcdp-1 : a == 7 ? -0x1.d906bcf328d46p-1 : 1.0;
+}
+__device__ __forceinline__ constexpr double ct_t8(int a) {
+  return a == 1 ? 0x1.a827999fcef32p-2 : a == 2 ? 1.0 : a == 3 ? 0x1.3504f333f9de6p+1 :
+         a == 5 ? -0x1.3504f333f9de6p+1 : a == 6 ? -1.0 : a == 7 ? -0x1.a827999fcef32p-2 : 0.0;
+}
+template <int A>
+__device__ __forceinline__ void bfly_root16(double2& lo, double2& hi) {
+  if constexpr (A == 0) bfly1(lo, hi);
+  else if constexpr (A == 4) bfly_pi(lo, hi);
+  else bfly_ct(lo, hi, ct_c8(A), ct_t8(A));
+}
+
+// Fast twiddle sources: the (c, t) stage tables in the SmemTw layout
+// (shared memory) or in the TmemTw layout (tensor memory).
+template <int K, int RB = 4>
+struct SmemTwCT : SmemTw<K, RB> {};
+struct TmemTwCT : TmemTw {};
+template <class Tw>
+struct IsFastTw {
+  static constexpr bool value = false;
+};
+template <int K, int RB>
+struct IsFastTw<SmemTwCT<K, RB>> {
+  static constexpr bool value = true;
+};
+template <>
+struct IsFastTw<TmemTwCT> {
+  static constexpr bool value = true;
+};
+
+// Pass 0, stages 1..RB-1 (stage 0 is fused into the prologue): the
+// twiddle of register pair kk at stage b is exp(+i pi kk / 2^b).
+template <int RB, int B = 1>
+__device__ __forceinline__ void fast_pass0(double2 (&v)[1 << RB]) {
+  if constexpr (B < RB) {
+    constexpr int P = 1 << RB;
+#pragma unroll
+    for (int kk = 0; kk < (1 << B); ++kk) {
+#pragma unroll
+      for (int h = 0; h < (P >> (B + 1)); ++h) {
+        const int i = kk | (h << (B + 1));
+        // angle kk / 2^B of pi, in eighths
+        switch (kk << (3 - B)) {
+          case 0: bfly_root16<0>(v[i], v[i | (1 << B)]); break;
+          case 1: bfly_root16<1>(v[i], v[i | (1 << B)]); break;
+          case 2: bfly_root16<2>(v[i], v[i | (1 << B)]); break;
+          case 3: bfly_root16<3>(v[i], v[i | (1 << B)]); break;
+          case 4: bfly_root16<4>(v[i], v[i | (1 << B)]); break;
+          case 5: bfly_root16<5>(v[i], v[i | (1 << B)]); break;
+          case 6: bfly_root16<6>(v[i], v[i | (1 << B)]); break;
+          default: bfly_root16<7>(v[i], v[i | (1 << B)]); break;
+        }
+      }
+    }
+    fast_pass0<RB, B + 1>(v);
+  }
+}
+
+// Passes >= 1 with (c, t) twiddles of logical thread t.
+template <int K, int RB, int PASS, int B, class Tw>
+__device__ __forceinline__ void fast_stage(double2 (&v)[Geo<K, RB>::P], int t, const Tw& tw) {
+  using G = Geo<K, RB>;
+  constexpr int c = G::c_of(PASS);
+  constexpr int q = B - c;
+  if constexpr (std::is_same<Tw, TmemTwCT>::value) {
+    // one tcgen05.ld of the stage's 2^q (c, t) pairs (stored by fill<.., false>)
+    uint32_t r[4 << q];
+    tm_ld<(4 << q)>(tw.base + TmemTw::col(PASS, (1 << q) - 1), r);
+    tm_wait_ld();
+#pragma unroll
+    for (int kk = 0; kk < (1 << q); ++kk) {
+      const double cc = __hiloint2double(r[4 * kk + 1], r[4 * kk]);
+      const double tt = __hiloint2double(r[4 * kk + 3], r[4 * kk + 2]);
+#pragma unroll
+      for (int h = 0; h < (G::P >> (q + 1)); ++h) {
+        const int i = kk | (h << (q + 1));
+        bfly_ct(v[i], v[i | (1 << q)], cc, tt);
+      }
+    }
+  } else {
+    const int tlow = t & ((1 << c) - 1);
+#pragma unroll
+    for (int kk = 0; kk < (1 << q); ++kk) {
+      const double2 w = tw(B, tlow | (kk << c));
+#pragma unroll
+      for (int h = 0; h < (G::P >> (q + 1)); ++h) {
+        const int i = kk | (h << (q + 1));
+        bfly_ct(v[i], v[i | (1 << q)], w.x, w.y);
+      }
+    }
+  }
+}
+
+template <int K, int RB, int PASS, class Tw, int B = Geo<K, RB>::RB * PASS>
+__device__ __forceinline__ void fast_pass(double2 (&v)[Geo<K, RB>::P], int t, const Tw& tw) {
+  using G = Geo<K, RB>;
+  static_assert(PASS > 0, "pass 0 is fast_pass0");
+  constexpr int b1 = (G::RB * PASS + G::RB) < K ? (G::RB * PASS + G::RB) : K;
+  if constexpr (B < b1) {
+    fast_stage<K, RB, PASS, B>(v, t, tw);
+    fast_pass<K, RB, PASS, Tw, B + 1>(v, t, tw);
+  }
+}
+
 // Store the registers of pass PASS to shared memory (swizzled positions).
 template <int K, int RB, int PASS>
 __device__ __forceinline__ void pass_store(const double2 (&v)[Geo<K, RB>::P], int t, double2* sm) {
@@ -418,7 +564,12 @@ __device__ __forceinline__ void fft_passes(double2 (&v)[Geo<K, RB>::P], int tp, 
   using G = Geo<K, RB>;
   const int t = PASS == 0 ? brev_bits(tp, G::TB) : tp;
   hook.before(PASS);
-  if constexpr (IsTmemTw<Tw>::value) {
+  if constexpr (IsFastTw<Tw>::value) {
+    if (active) {
+      if constexpr (PASS == 0) fast_pass0<G::RB>(v);
+      else fast_pass<K, RB, PASS, Tw>(v, t, tw);
+    }
+  } else if constexpr (IsTmemTw<Tw>::value) {
     static_assert(INV, "TMEM twiddles are stored conjugated (inverse transform)");
     if (active) fft_pass_tm<K, RB, PASS>(v, tw);
   } else {

@@ -107,10 +107,44 @@ struct FieldHook {
 // each group evaluates one radius row per round; rows are strided over the
 // CTAs of a signal (blockIdx.y).
 // ---------------------------------------------------------------------------
-template <int K, int RB, int G, bool MATERIALIZE, bool TM = false>
+// Fast weights (AFD_PLAN_FAST): row s of `pw` is then the factor table
+// fw[s] = { scale_s r_s^t (t < T), r_s^(T m) (m < P) }, so register i of
+// thread t (natural l = (rev(i) << TB) | t) is weighted by
+// w = fw[t] * fw[T + rev(i)] = scale r^l, formed on chip (1 DMUL) instead of
+// read from the M x N cumprod table, and the weighting is fused into
+// stage 0: z = w_b y_b, lo/hi = fma(w_a, y_a, +-z).
+template <int K, int RB>
+struct FastW {
+  static constexpr int T = Geo<K, RB>::T, P = Geo<K, RB>::P;
+  static constexpr int STRIDE = T + P;
+  // weights of thread tp's P registers for table row `fr`
+  __device__ __forceinline__ static void load(const double* __restrict__ fr, int tp,
+                                              double (&w)[P]) {
+    const double a = __ldg(fr + tp);
+    double b[P];
+#pragma unroll
+    for (int m = 0; m < P; ++m) b[m] = __ldg(fr + T + m);
+#pragma unroll
+    for (int i = 0; i < P; ++i) w[i] = a * b[brev_bits(i, Geo<K, RB>::RB)];
+  }
+};
+// y_i = w_i x_i followed by the stage-0 butterflies (pairs 2h, 2h+1; W = 1)
+template <int P>
+__device__ __forceinline__ void fast_prologue(double2 (&v)[P], const double (&w)[P]) {
+#pragma unroll
+  for (int h = 0; h < P / 2; ++h) {
+    const double2 a = v[2 * h], b = v[2 * h + 1];
+    const double zr = w[2 * h + 1] * b.x, zi = w[2 * h + 1] * b.y;
+    v[2 * h] = make_double2(fma(w[2 * h], a.x, zr), fma(w[2 * h], a.y, zi));
+    v[2 * h + 1] = make_double2(fma(w[2 * h], a.x, -zr), fma(w[2 * h], a.y, -zi));
+  }
+}
+__device__ __forceinline__ double fast_mag2(double2 f) { return fma(f.x, f.x, f.y * f.y); }
+
+template <int K, int RB, int G, bool MATERIALIZE, bool TM = false, bool FAST = false>
 __global__ void __launch_bounds__(Geo<K, RB>::T * G, (RB <= 3 && Geo<K, RB>::T * G <= 512) ? 2 : 1)
 field_kernel(const double2* __restrict__ ghat,     // [batch][N]
-             const double* __restrict__ pw,        // [rows of plan][N], r^l natural l
+             const double* __restrict__ pw,        // [rows of plan][N], r^l natural l (FAST: fw)
              const double* __restrict__ scales,    // [M] (global radius index)
              const double2* __restrict__ twst,     // stage twiddle tables (N-1)
              long long row0, long long row1,       // global rows to evaluate
@@ -170,7 +204,8 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     }
   }
   bool tw_ready = false;
-  using TwSrc = std::conditional_t<TM, TmemTw, TwT>;
+  using TwSrc = std::conditional_t<TM, std::conditional_t<FAST, TmemTwCT, TmemTw>,
+                                   std::conditional_t<FAST, SmemTwCT<K, RB>, TwT>>;
   TwSrc tw;
   if constexpr (TM) {
     const int warp = threadIdx.x >> 5;
@@ -225,20 +260,25 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   // First row: its r^l values are step-independent and are loaded before the
   // PDL wait; the spectrum and the stop flags come from the previous kernel.
   double2 v[P];
+  constexpr int PWS = FAST ? FastW<K, RB>::STRIDE : N;  // table row stride
   {
     const long long s0 = row0 + (long long)blockIdx.x * Gr + g;
     const bool act0 = rounds > 0 && s0 < row1;
     double pv[P];
     if (act0) {
-      const double* __restrict__ pr = pw + (size_t)(s0 - pw_row0) * N;
+      const double* __restrict__ pr = pw + (size_t)(s0 - pw_row0) * PWS;
+      if constexpr (FAST) {
+        FastW<K, RB>::load(pr, tp, pv);
+      } else {
 #pragma unroll
-      for (int i = 0; i < P; ++i) pv[i] = __ldg(pr + Gm::l0(tp, i));
+        for (int i = 0; i < P; ++i) pv[i] = __ldg(pr + Gm::l0(tp, i));
+      }
     }
     if constexpr (TM) {  // step-independent: fill TMEM before the PDL wait
       mbar_wait(&tw_bar, 0);
       tw_ready = true;
       if (g == 0) {
-        tw.template fill<K, RB, true>(tp, TwT{smem});
+        tw.template fill<K, RB, !FAST>(tp, TwT{smem});
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -261,11 +301,14 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
           for (int i = 0; i < P; ++i) tm_st4(gh_tm + 4 * i, v[i]);
         }
       }
+      if constexpr (FAST) {
+        fast_prologue(v, pv);
+      } else {
 #pragma unroll
-      for (int i = 0; i < P; ++i) {
-        v[i] = make_double2(pv[i] * v[i].x, pv[i] * v[i].y);  // transform.py:198
-        asm volatile("" ::"d"(v[i].x), "d"(v[i].y));  // formed before the test
+        for (int i = 0; i < P; ++i) v[i] = make_double2(pv[i] * v[i].x, pv[i] * v[i].y);  // transform.py:198
       }
+#pragma unroll
+      for (int i = 0; i < P; ++i) asm volatile("" ::"d"(v[i].x), "d"(v[i].y));  // formed before the test
       if constexpr (TM) {
         if (g == 0) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
@@ -297,13 +340,17 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     if (rd > 0 && active) {
       // prologue: y = powers * c[rev] (transform.py:198), per component
       if constexpr (TM) {
-        const double* __restrict__ pr = pw + (size_t)(s - pw_row0) * N;
+        const double* __restrict__ pr = pw + (size_t)(s - pw_row0) * PWS;
         // all r^l loads issued before the TMEM reads (tcgen05.wait::ld is a
         // memory barrier to the compiler: loads placed after one cannot be
         // hoisted above it)
         double pv[P];
+        if constexpr (FAST) {
+          FastW<K, RB>::load(pr, tp, pv);
+        } else {
 #pragma unroll
-        for (int i = 0; i < P; ++i) pv[i] = __ldg(pr + Gm::l0(tp, i));
+          for (int i = 0; i < P; ++i) pv[i] = __ldg(pr + Gm::l0(tp, i));
+        }
 #pragma unroll
         for (int i0 = 0; i0 < P; i0 += 4) {
           uint32_t r[16];
@@ -313,18 +360,31 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
           for (int j = 0; j < 4; ++j) {
             const double2 c = make_double2(__hiloint2double(r[4 * j + 1], r[4 * j]),
                                            __hiloint2double(r[4 * j + 3], r[4 * j + 2]));
-            const double p = pv[i0 + j];
-            v[i0 + j] = make_double2(p * c.x, p * c.y);
+            if constexpr (FAST) {
+              v[i0 + j] = c;
+            } else {
+              const double p = pv[i0 + j];
+              v[i0 + j] = make_double2(p * c.x, p * c.y);
+            }
           }
         }
+        if constexpr (FAST) fast_prologue(v, pv);
       } else {
-        const double* __restrict__ pr = pw + (size_t)(s - pw_row0) * N;
+        const double* __restrict__ pr = pw + (size_t)(s - pw_row0) * PWS;
+        if constexpr (FAST) {
+          double pv[P];
+          FastW<K, RB>::load(pr, tp, pv);
 #pragma unroll
-        for (int i = 0; i < P; ++i) {
-          const int l = Gm::l0(tp, i);
-          const double p = __ldg(pr + l);
-          const double2 c = __ldg(gh + l);
-          v[i] = make_double2(p * c.x, p * c.y);
+          for (int i = 0; i < P; ++i) v[i] = __ldg(gh + Gm::l0(tp, i));
+          fast_prologue(v, pv);
+        } else {
+#pragma unroll
+          for (int i = 0; i < P; ++i) {
+            const int l = Gm::l0(tp, i);
+            const double p = __ldg(pr + l);
+            const double2 c = __ldg(gh + l);
+            v[i] = make_double2(p * c.x, p * c.y);
+          }
         }
       }
     }
@@ -350,15 +410,15 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     }
     const int sl_next = dyn ? next_sl[g][rd & 1] : sl + per_round;
     if (active) {
-      const double sc = __ldg(scales + s);
+      const double sc = FAST ? 1.0 : __ldg(scales + s);  // FAST: scale is in the weights
 #pragma unroll
       for (int i = 0; i < P; ++i) {
         // y *= scales[:, None] (transform.py:200)
-        const double2 f = make_double2(v[i].x * sc, v[i].y * sc);
+        const double2 f = FAST ? v[i] : make_double2(v[i].x * sc, v[i].y * sc);
         if (MATERIALIZE) {
           field_out[(size_t)(s - row0) * N + out_pos<K, RB>(tp, i)] = f;
         } else {
-          const double mg = np_mag2(f);  // core.py:298
+          const double mg = FAST ? fast_mag2(f) : np_mag2(f);  // core.py:298
           if (__builtin_expect(mg > best_mag, 0)) {
             best_mag = mg;
             best_re = f.x;

@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _capi
 
-__all__ = ["shard_bounds", "decompose_sharded", "decompose_batch_sharded"]
+__all__ = ["shard_bounds", "decompose_sharded", "decompose_batch_sharded", "ShardedRunner"]
 
 
 def shard_bounds(count, rank, world):
@@ -36,17 +36,68 @@ def shard_bounds(count, rank, world):
 
 
 def _all_gather(out, t, group):
-    """all_gather_into_tensor where the backend has it (NCCL), else the list form (gloo)."""
+    """One all-gather of every rank's candidates, chosen by backend (every
+    rank issues the same collective): all_gather_into_tensor on NCCL, the
+    list form elsewhere (gloo)."""
     import torch.distributed as dist
-    try:
+    if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, t, group=group)
-    except (RuntimeError, NotImplementedError, ValueError):
+    else:
         dist.all_gather(list(out.unbind(0)), t, group=group)
 
 
-def _default_plan(radii, n, batch, m0, m1, device):
+def _default_plan(radii, n, batch, m0, m1, device, engine_name="fft"):
     from . import engine
-    return engine.get_plan(radii, n, batch=batch, m0=m0, m1=m1, device=device)
+    return engine.get_plan(radii, n, batch=batch, m0=m0, m1=m1, device=device,
+                           engine=1 if engine_name == "direct" else 0,
+                           fast=engine_name == "fft-fast")
+
+
+class ShardedRunner:
+    """The radius-sharded decomposition loop of one rank.
+
+    Per AFD step: the rank's field + argmax over its rows (select_local), an
+    all-gather of the 32-byte candidates of all ranks (rank-major, so the
+    lowest flat index still wins ties), then the identical replicated
+    update + energy + next spectrum (apply_step).  The host issues the steps
+    without ever synchronising; once a signal's stop rule fires its kernels
+    are no-ops.  Reusable: ``run`` may be called repeatedly (benchmarks)."""
+
+    def __init__(self, plan, batch, max_terms, threshold=None, dc_first=False, group=None):
+        import torch
+        import torch.distributed as dist
+        self.plan, self.batch, self.max_terms = plan, int(batch), int(max_terms)
+        self.threshold, self.dc_first, self.group = threshold, bool(dc_first), group
+        self.world = dist.get_world_size(group)
+        dev = plan.device
+        self.steps = torch.zeros((self.batch, self.max_terms, _capi.STEP_DTYPE.itemsize),
+                                 dtype=torch.uint8, device=dev)
+        self.gathered = torch.empty((self.world, self.batch, 32), dtype=torch.uint8,
+                                    device=dev)
+        self.cpu = dist.get_backend(group) != "nccl" and dev.type == "cuda"
+        self.fin = None
+
+    def run(self, g):
+        """Decompose g ([batch, N], on the plan's device) over all ranks."""
+        p = self.plan
+        p.sharded_begin(g)
+        for k in range(self.max_terms):
+            local = p.select_local(k, self.dc_first, self.batch)           # [B, 32]
+            if self.cpu:  # gloo: exchange through host memory
+                host = self.gathered.cpu()
+                _all_gather(host, local.cpu().contiguous(), self.group)
+                self.gathered.copy_(host)
+            else:
+                _all_gather(self.gathered, local.contiguous(), self.group)
+            cands = self.gathered.permute(1, 0, 2).contiguous()           # [B, P, 32]
+            p.apply_step(k, self.max_terms, self.threshold, self.dc_first, cands, self.steps)
+        self.fin = p.sharded_finish(self.batch)
+        return self.fin
+
+    def host_records(self):
+        """(step records [batch, max_terms], n_steps [batch]) of the last run."""
+        rec = self.steps.cpu().numpy().view(_capi.STEP_DTYPE)[..., 0]
+        return rec, self.fin[0].cpu().numpy()
 
 
 def decompose_sharded(signals, grid, max_terms=10, threshold=None, dc_first=False, group=None,
@@ -76,19 +127,15 @@ def decompose_sharded(signals, grid, max_terms=10, threshold=None, dc_first=Fals
     if world > m:
         raise ValueError("more ranks (%d) than radii (%d)" % (world, m))
     m0, m1 = shard_bounds(m, rank, world)
-    plan = (plan_factory or _default_plan)(grid.radii, n, b, m0, m1, device)
+    if plan_factory is None:
+        plan = _default_plan(grid.radii, n, b, m0, m1, device, engine_name)
+    else:
+        plan = plan_factory(grid.radii, n, b, m0, m1, device)
     dev = plan.device
     g = torch.from_numpy(sig).to(dev)
-    plan.sharded_begin(g)
-    steps = torch.zeros((b, max_terms, _capi.STEP_DTYPE.itemsize), dtype=torch.uint8, device=dev)
-    gathered = torch.empty((world, b, 32), dtype=torch.uint8, device=dev)
-    for k in range(max_terms):
-        local = plan.select_local(k, dc_first, b)                    # [B, 32]
-        _all_gather(gathered, local.contiguous(), group)
-        cands = gathered.permute(1, 0, 2).contiguous()               # [B, P, 32] rank-major
-        plan.apply_step(k, max_terms, threshold, dc_first, cands, steps)
-    n_steps, initial, rem, _ = plan.sharded_finish(b)
-    rec = steps.cpu().numpy().view(_capi.STEP_DTYPE)[..., 0]
+    runner = ShardedRunner(plan, b, max_terms, threshold, dc_first, group)
+    n_steps, initial, rem, _ = runner.run(g)
+    rec = runner.steps.cpu().numpy().view(_capi.STEP_DTYPE)[..., 0]
     counts = n_steps.cpu().numpy()
     init = initial.cpu().numpy()
     remh = rem.cpu().numpy()

@@ -45,6 +45,26 @@ def host_tables(radii, n):
     return tw, circle, scales
 
 
+def _locked(fn):
+    """Run a Plan method under the plan's lock (the plan's device buffers and
+    cached graph are shared by all its entry points).  Work is stream-ordered,
+    so a call on a different stream than the previous one first waits for
+    the previous call's work (an event recorded after every call)."""
+    def wrapper(self, *a, **kw):
+        with self.lock:
+            st = kw.get("stream") or torch.cuda.current_stream(self.device)
+            if self._last_stream is not None and st != self._last_stream:
+                st.wait_event(self._done)
+            out = fn(self, *a, **kw)
+            if self._done is None:
+                self._done = torch.cuda.Event()
+            self._done.record(st)
+            self._last_stream = st
+            return out
+    wrapper.__name__, wrapper.__doc__ = fn.__name__, fn.__doc__
+    return wrapper
+
+
 def _ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None else None
 
@@ -68,9 +88,15 @@ class DeviceDecomposition:
 
 
 class Plan:
-    """One afd_plan: device tables for (N, radii, radius shard, batch)."""
+    """One afd_plan: device tables for (N, radii, radius shard, batch).
 
-    def __init__(self, radii, n, m0=0, m1=None, max_batch=1, device=None, engine=0):
+    ``fast=1`` builds an AFD_PLAN_FAST plan (FMA-fused field arithmetic, r^l
+    on chip; identical selections, ~1e-14 relative instead of bit-exact).
+    A plan's device buffers are shared by all its entry points, so every
+    call holds the plan's lock (concurrent callers serialise instead of
+    corrupting each other's state)."""
+
+    def __init__(self, radii, n, m0=0, m1=None, max_batch=1, device=None, engine=0, fast=0):
         self.device = require_cuda(device)
         self.lib = _capi.load()
         self.radii = tuple(float(r) for r in radii)
@@ -79,6 +105,9 @@ class Plan:
         self.m0 = int(m0)
         self.m1 = self.m if m1 is None else int(m1)
         self.max_batch = int(max_batch)
+        self.fast = int(bool(fast))
+        self.lock = threading.RLock()
+        self._last_stream, self._done = None, None
         tw, circle, scales = host_tables(self.radii, self.n)
         r = np.ascontiguousarray(self.radii, dtype=np.float64)
         handle = C.c_void_p()
@@ -86,7 +115,7 @@ class Plan:
             _capi.check(self.lib.afd_plan_create(
                 C.byref(handle), self.device.index, self.n, self.m, self.m0, self.m1,
                 self.max_batch, r.ctypes.data, scales.ctypes.data, tw.ctypes.data,
-                circle.ctypes.data))
+                circle.ctypes.data, _capi.PLAN_FAST if self.fast else 0))
         self.handle = handle
         self._keep = (tw, circle, scales, r)
         self.engine = int(engine)
@@ -116,6 +145,7 @@ class Plan:
     def launch_count(self):
         return int(self.lib.afd_launch_count(self.handle))
 
+    @_locked
     def time_field(self, ghat, reps=20, stream=None):
         """Mean CUDA-event time (ms) of one fused field+argmax launch."""
         ghat = self._signal(ghat)
@@ -125,6 +155,7 @@ class Plan:
         return ms.value
 
     # -- transforms -----------------------------------------------------------
+    @_locked
     def _fft(self, fn, x, stream=None):
         x = self._signal(x)
         out = torch.empty_like(x)
@@ -140,6 +171,7 @@ class Plan:
     def analytic_projection(self, x, stream=None):
         return self._fft(self.lib.afd_analytic_projection, x, stream)
 
+    @_locked
     def field(self, ghat, r0=None, r1=None, stream=None):
         ghat = self._signal(ghat)[0]
         r0 = self.m0 if r0 is None else int(r0)
@@ -149,6 +181,7 @@ class Plan:
                                        _stream(stream)))
         return out
 
+    @_locked
     def field_direct(self, g, r0=None, r1=None, stream=None):
         """oracle.field_direct rows (direct engine) of one signal g (not its spectrum)."""
         g = self._signal(g)[0]
@@ -159,6 +192,7 @@ class Plan:
                                               _stream(stream)))
         return out
 
+    @_locked
     def field_argmax(self, ghat, stream=None):
         ghat = self._signal(ghat)
         out = torch.empty((ghat.shape[0], 32), dtype=torch.uint8, device=self.device)
@@ -166,6 +200,7 @@ class Plan:
                                               _stream(stream)))
         return out
 
+    @_locked
     def argmax(self, field, stream=None):
         field = field.to(device=self.device, dtype=torch.complex128).contiguous()
         if field.dim() != 2 or field.shape[1] != self.n:
@@ -175,6 +210,7 @@ class Plan:
                                         _stream(stream)))
         return out
 
+    @_locked
     def atom(self, kind, a, c=0j, g=None, stream=None):
         a = complex(a)
         c = complex(c)
@@ -185,6 +221,7 @@ class Plan:
                                       _ptr(out), _stream(stream)))
         return out
 
+    @_locked
     def energy(self, g, stream=None):
         g = self._signal(g)
         out = torch.empty(g.shape[0], dtype=torch.float64, device=self.device)
@@ -192,6 +229,7 @@ class Plan:
                                         _stream(stream)))
         return out
 
+    @_locked
     def energy_diff(self, g, s, stream=None):
         g = self._signal(g)
         s = self._signal(s)
@@ -201,6 +239,7 @@ class Plan:
         return out
 
     # -- the hot path -----------------------------------------------------------
+    @_locked
     def decompose(self, g, max_terms, threshold=None, dc_first=False, stream=None, out=None):
         """Device-resident decomposition of g ([batch, N] CUDA complex128)."""
         g = self._signal(g)
@@ -214,6 +253,7 @@ class Plan:
             _stream(stream)))
         return out
 
+    @_locked
     def decompose_host(self, signals, max_terms, threshold=None, dc_first=False, stream=None):
         """Host numpy [batch, N] in -> host results out (afd_decompose_host).
 
@@ -244,6 +284,7 @@ class Plan:
             initial=torch.empty(batch, dtype=torch.float64, device=dev),
             remainder=torch.empty((batch, self.n), dtype=torch.complex128, device=dev))
 
+    @_locked
     def error_trace(self, g, dec, stream=None):
         """errors [batch, max_terms] and reconstructions [batch, N] (device)."""
         g = self._signal(g)
@@ -256,17 +297,20 @@ class Plan:
         return errors, recon
 
     # -- radius-sharded stepping (multi-GPU) ---------------------------------------
+    @_locked
     def sharded_begin(self, g, stream=None):
         g = self._signal(g)
         _capi.check(self.lib.afd_sharded_begin(self.handle, _ptr(g), g.shape[0], _stream(stream)))
         return g.shape[0]
 
+    @_locked
     def select_local(self, k, dc_first, batch, stream=None):
         out = torch.empty((batch, 32), dtype=torch.uint8, device=self.device)
         _capi.check(self.lib.afd_select_local(self.handle, int(k), int(bool(dc_first)), _ptr(out),
                                               batch, _stream(stream)))
         return out
 
+    @_locked
     def apply_step(self, k, max_terms, threshold, dc_first, cands, steps, stream=None):
         """cands: uint8 [batch, ncand, 32] (rank-major), steps: uint8 [batch, max_terms, 72]."""
         cands = cands.contiguous()
@@ -275,6 +319,7 @@ class Plan:
             int(bool(dc_first)), _ptr(cands), cands.shape[1], cands.shape[0], _ptr(steps),
             _stream(stream)))
 
+    @_locked
     def sharded_finish(self, batch, stream=None):
         dev = self.device
         n_steps = torch.empty(batch, dtype=torch.int32, device=dev)
@@ -302,26 +347,27 @@ _MAX_PLANS = 16
 _LAST = [None, None]  # (key of the last lookup with this radii object, plan)
 
 
-def get_plan(radii, n, batch=1, m0=0, m1=None, device=None, engine=0):
-    """Cached plan for (device, N, radii, shard, engine) with max_batch >= batch."""
+def get_plan(radii, n, batch=1, m0=0, m1=None, device=None, engine=0, fast=0):
+    """Cached plan for (device, N, radii, shard, engine, fast) with max_batch >= batch."""
     # fast path: the same radii tuple object as the previous call (a grid's
     # radii) skips hashing M floats
     last_key, last_plan = _LAST
+    fast = int(bool(fast))
     if (last_key is not None and last_key[0] is radii and last_key[1:] ==
-            (n, m0, m1, device, engine) and last_plan.max_batch >= batch and
+            (n, m0, m1, device, engine, fast) and last_plan.max_batch >= batch and
             last_plan.handle is not None and
             (device is not None or last_plan.device.index == torch.cuda.current_device())):
         return last_plan
-    p = _get_plan(radii, n, batch, m0, m1, device, engine)
-    _LAST[0], _LAST[1] = (radii, n, m0, m1, device, engine), p
+    p = _get_plan(radii, n, batch, m0, m1, device, engine, fast)
+    _LAST[0], _LAST[1] = (radii, n, m0, m1, device, engine, fast), p
     return p
 
 
-def _get_plan(radii, n, batch, m0, m1, device, engine):
+def _get_plan(radii, n, batch, m0, m1, device, engine, fast):
     dev = require_cuda(device)
     if not (type(radii) is tuple and all(type(r) is float for r in radii[:1])):
         radii = tuple(float(r) for r in radii)
-    key = (dev.index, int(n), radii, int(m0), m1, int(engine))
+    key = (dev.index, int(n), radii, int(m0), m1, int(engine), fast)
     with _PLANS_LOCK:
         p = _PLANS.get(key)
         if p is None or p.max_batch < batch:
@@ -330,6 +376,6 @@ def _get_plan(radii, n, batch, m0, m1, device, engine):
             if len(_PLANS) >= _MAX_PLANS:
                 _PLANS.pop(next(iter(_PLANS)))
             p = Plan(radii, n, m0=m0, m1=m1, max_batch=max(int(batch), 1), device=dev.index,
-                     engine=engine)
+                     engine=engine, fast=fast)
             _PLANS[key] = p
         return p

@@ -734,3 +734,66 @@ def test_bench_line_contract(afd):
     assert 0.3 * d["value"] < d["e2e"]["value"] < 1.05 * d["value"]
     assert 0.0 < d["roofline"]["frac"] < 1.0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+
+
+# ---------------------------------------------------------------------------
+# fast mode (AFD_PLAN_FAST / engine "fft-fast"): FMA-fused butterflies and
+# on-chip r^l.  Contract (BASELINE north_star): identical selected indices,
+# coefficients / remainders / errors within 1e-9 relative.  The field itself
+# is checked much tighter (1e-12 of the row's largest value).
+# ---------------------------------------------------------------------------
+FAST_TOL = 1e-9
+
+
+@pytest.mark.parametrize("n", [8, 16, 64, 256, 1024, 4096, 8192])
+def test_fast_field_rows_close_to_reference(afd, tr, n):
+    core, engine = afd
+    import torch
+    c = tr["fwd_%d" % n]
+    radii = tuple(tr["radii_%d" % n])
+    ref = tr["field_%d" % n]
+    plan = engine.Plan(radii, n, fast=1)
+    got = plan.field(torch.from_numpy(c).cuda()).cpu().numpy()
+    for row in range(len(radii)):
+        scale = np.abs(ref[row]).max()
+        assert np.abs(got[row] - ref[row]).max() <= 1e-12 * scale, (n, row)
+
+
+@pytest.mark.parametrize("case", ["c0", "c1", "c3_s0", "c3_s1", "rand3", "rand11", "rand42",
+                                  "atom", "f1_thr", "const"])
+def test_fast_decompose_matches_reference(afd, case):
+    core, _ = afd
+    g = load_golden("decomp_%s.npz" % case)
+    thr = float(g["threshold"])
+    grid = core.ParameterGrid(tuple(g["radii"]), g["g"].shape[0])
+    d = core.decompose(g["g"], grid, max_terms=int(g["max_terms"]),
+                       threshold=None if np.isnan(thr) else thr,
+                       dc_first=bool(g["dc_first"]), engine="fft-fast")
+    assert d.engine == "fft-fast"
+    assert len(d.steps) == len(g["j"])
+    for k, s in enumerate(d.steps):
+        assert s.point.angle_index == g["j"][k], (case, k)
+        assert s.point.radius == g["radius"][k], (case, k)
+        assert abs(s.coefficient - g["coeff"][k]) <= FAST_TOL * abs(g["coeff"][k]), (case, k)
+        assert abs(s.residual_energy - g["residual"][k]) <= FAST_TOL * max(
+            abs(g["residual"][k]), 1e-300 + FAST_TOL * g["initial"]), (case, k)
+    scale = np.abs(g["remainder"]).max() + 1e-300
+    assert np.abs(d.remainder - g["remainder"]).max() <= FAST_TOL * scale
+
+
+def test_fast_c3_batch_matches_oracle(afd):
+    """Batched fast decompositions (c3 shape, 8 signals): identical selections."""
+    core, _ = afd
+    from paper_1711_08604_b200 import workloads as W
+    w = W.CONFIGS["c3"]
+    sig = np.stack([W.signal_for("c3", i) for i in range(8)])
+    radii = W.radii_for(w.m)
+    grid = core.ParameterGrid(radii, w.n)
+    ds = core.decompose_batch(sig, grid, max_terms=w.steps, engine="fft-fast")
+    for i in (0, 5):
+        o = O.decompose(sig[i], np.array(radii), max_terms=w.steps)
+        assert [s.point.angle_index for s in ds[i].steps] == list(o.steps["j"])
+        assert [s.point.radius for s in ds[i].steps] == list(o.steps["radius"])
+        c = np.array([s.coefficient for s in ds[i].steps])
+        oc = o.steps["c_re"] + 1j * o.steps["c_im"]
+        assert np.all(np.abs(c - oc) <= FAST_TOL * np.abs(oc))
