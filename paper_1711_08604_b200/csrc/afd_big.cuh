@@ -240,6 +240,12 @@ struct BulkWaitHook {
 // twiddles, one-pass row-group offset and the bulk-stored outputs of
 // big_pass_a.  Same butterflies, same bits.
 // ---------------------------------------------------------------------------
+// FAST (AFD_PLAN_FAST): pw_rev is the weight factor table fw (row stride
+// 2^(K-12) + 256 + 16; fast_weight_kernel) and twst the (c, t) stage table.
+// Register i of thread t in block blk holds natural index
+//   l = rev_{K-12}(blk) + (t << (K-12)) + (rev4(i) << (K-4)),
+// so its weight scale r^l = fw[rev(blk)] * fw[2^(K-12) + t] * fw[2^(K-12) + 256 + rev4(i)].
+template <bool FAST = false>
 __global__ void __launch_bounds__(Geo<12, 4>::T * kBigGroups, 1)
 big_field_a(int K, const double* __restrict__ pw_rev, long long pw_row0,
             const double2* __restrict__ ghat_rev, const double2* __restrict__ twst,
@@ -270,15 +276,17 @@ big_field_a(int K, const double* __restrict__ pw_rev, long long pw_row0,
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const int g = threadIdx.x / T, tid = threadIdx.x % T;
   const int warp = threadIdx.x >> 5;
-  TmemTw tw;
+  std::conditional_t<FAST, TmemTwCT, TmemTw> tw;
   tw.base = tm_base + ((uint32_t)((warp & 3) * 32) << 16) +
             (uint32_t)(((warp & 7) >> 2) * TmemTw::kSetCols);
   // spectrum of the current block: 16 values per thread, shared by the two
   // groups (same thread index, same values), as in field_kernel
   const uint32_t gh_tm = tm_base + ((uint32_t)((warp & 3) * 32) << 16) +
                          (uint32_t)TmemTw::kGhCol + (uint32_t)(((warp & 7) >> 2) * (4 * P));
+  const int kb = K - KA;                 // FAST: bits of the block index
+  const int fws = (1 << kb) + 256 + 16;  // FAST: weight table row stride
   if (g == 0) {
-    tw.fill<KA, 4, true>(tid, TwA{smem});
+    tw.template fill<KA, 4, !FAST>(tid, TwA{smem});
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
   double2* buf = smem + TwA::ENTRIES + g * GA::SMEM;
@@ -315,7 +323,29 @@ big_field_a(int K, const double* __restrict__ pw_rev, long long pw_row0,
       first = true;  // re-establish the one-pass group offset
     }
     double2 v[P];
-    if (live) {
+    if (live && FAST) {
+      const double* __restrict__ fr = pw_rev + (size_t)(row0 + rl - pw_row0) * fws;
+      const double a = __ldg(fr + brev_rt(blk, kb)) * __ldg(fr + (1 << kb) + tid);
+      double w[P];
+#pragma unroll
+      for (int m = 0; m < P; ++m) w[m] = __ldg(fr + (1 << kb) + 256 + m);
+#pragma unroll
+      for (int i = 0; i < P; ++i) w[i] = a * w[i];  // now indexed by rev4(i) below
+      double wi[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) wi[i] = w[brev_bits(i, 4)];
+#pragma unroll
+      for (int i0 = 0; i0 < P; i0 += 4) {
+        uint32_t r[16];
+        tm_ld<16>(gh_tm + 4 * i0, r);
+        tm_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          v[i0 + j] = make_double2(__hiloint2double(r[4 * j + 1], r[4 * j]),
+                                   __hiloint2double(r[4 * j + 3], r[4 * j + 2]));
+      }
+      fast_prologue(v, wi);
+    } else if (live) {
       // prologue y = powers * c[rev] (transform.py:198); r^l from the
       // register-layout table (predicated past the underflow, see big_pass_a)
       const double* __restrict__ pr = pw_rev + (size_t)(row0 + rl - pw_row0) * N + base;
@@ -396,7 +426,8 @@ big_field_a(int K, const double* __restrict__ pw_rev, long long pw_row0,
 // MODE >= 0 fixes out_mode at compile time (the field pass, MODE = 1: fewer
 // live registers than the all-modes kernel, no spills); MODE = -1 dispatches
 // on out_mode at run time.
-template <bool INV, int MODE = -1>
+// FAST (field modes 0-2 only): (c, t) twiddles, no scale (see col_tma_kernel).
+template <bool INV, int MODE = -1, bool FAST = false>
 __global__ void __launch_bounds__(kColThreads, 2)
 big_pass_col(int K, int ka, int b0, int out_mode_rt, int scale_n, double2* __restrict__ Y,
              const double2* __restrict__ twst, const double* __restrict__ scales,
@@ -427,11 +458,11 @@ big_pass_col(int K, int ka, int b0, int out_mode_rt, int scale_n, double2* __res
 #pragma unroll
       for (int kk = 0; kk < (1 << e); ++kk) {
         double2 w = __ldg(sb + qlow + ((long long)kk << b0));
-        if (INV) w.y = -w.y;
+        if (INV && !FAST) w.y = -w.y;
 #pragma unroll
         for (int h = 0; h < (16 >> (e + 1)); ++h) {
           const int i = kk | (h << (e + 1));
-          bfly(v[i], v[i | (1 << e)], w);
+          bfly_any<FAST>(v[i], v[i | (1 << e)], w);
         }
       }
     }
@@ -439,15 +470,15 @@ big_pass_col(int K, int ka, int b0, int out_mode_rt, int scale_n, double2* __res
 #pragma unroll
       for (int u = 0; u < 16; ++u) y[q + ((long long)u << b0)] = v[u];
     } else if (out_mode == 1 || out_mode == 2) {
-      const double sc = __ldg(scales + row);
+      const double sc = FAST ? 1.0 : __ldg(scales + row);
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const long long j = q + ((long long)u << b0);
-        const double2 f = make_double2(v[u].x * sc, v[u].y * sc);  // transform.py:200
+        const double2 f = FAST ? v[u] : make_double2(v[u].x * sc, v[u].y * sc);  // transform.py:200
         if (out_mode == 2) {
           fout[(size_t)(row - row0) * N + j] = f;
         } else {
-          const double mg = np_mag2(f);
+          const double mg = FAST ? fast_mag2(f) : np_mag2(f);
           if (mg > best.mag) {  // j increases with u: first maximum
             best.mag = mg;
             best.flat = row * N + j;

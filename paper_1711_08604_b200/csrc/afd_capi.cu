@@ -588,8 +588,14 @@ int big_setup(afd_plan* p) {
                             (int)big_a_smem_g<KA>()));
     CU(cudaFuncSetAttribute(big_pass_a<KA, true, KA == 12>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_a_smem_g<KA>()));
-    CU(cudaFuncSetAttribute(big_field_a, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CU(cudaFuncSetAttribute(big_field_a<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)big_a_smem_g<12>()));
+    CU(cudaFuncSetAttribute(big_field_a<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)big_a_smem_g<12>()));
+    CU(cudaFuncSetAttribute(col_tma_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)ColTma<4>::SMEM));
+    CU(cudaFuncSetAttribute(col_tma_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)ColTma<8>::SMEM));
     CU(cudaFuncSetAttribute(big_pass_col8<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(sizeof(double2) * 16 * kCol8Pad)));
     CU(cudaFuncSetAttribute(big_pass_col8<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -635,10 +641,14 @@ int big_launch_a(afd_plan* p, bool inv, int mode, const double2* ghat_rev, const
     // persistent: one CTA per SM (2 row-groups each), work items strided
     const unsigned grid = (unsigned)std::min<int64_t>(p->sms, (items + kBigGroups - 1) / kBigGroups);
     const int block = Geo<KA, 4>::T * kBigGroups;
-    if (inv && mode == 0 && KA == 12 && field_tmem_enabled() && kFieldAEnabled)
-      big_field_a<<<(unsigned)std::min<int64_t>(p->sms, (items + kBigGroups - 1) / kBigGroups),
-                    block, big_a_smem_g<KA>(), st>>>(p->K, p->pw, p->m0, ghat_rev, p->twst, r0,
-                                                     r0 + rows, p->Y, stopped, p->pw_len);
+    if (p->fast && inv && mode == 0) {
+      // fast field: weights from the factor tables, (c, t) twiddles
+      if (KA != 12) return fail(AFD_E_UNSUPPORTED, "fast pass A needs 4096-point blocks");
+      big_field_a<true><<<grid, block, big_a_smem_g<KA>(), st>>>(
+          p->K, p->fw, p->m0, ghat_rev, p->twct, r0, r0 + rows, p->Y, stopped, nullptr);
+    } else if (inv && mode == 0 && KA == 12 && field_tmem_enabled() && kFieldAEnabled)
+      big_field_a<false><<<grid, block, big_a_smem_g<KA>(), st>>>(
+          p->K, p->pw, p->m0, ghat_rev, p->twst, r0, r0 + rows, p->Y, stopped, p->pw_len);
     else if (inv && mode == 0 && KA == 12 && field_tmem_enabled())
       big_pass_a<KA, true, KA == 12><<<grid, block, big_a_smem_g<KA>(), st>>>(
           p->K, mode, p->pw, p->m0, ghat_rev, x, p->twst, r0, r0 + rows, p->Y, stopped,
@@ -666,23 +676,46 @@ static const bool kColTmaEnabled = !(getenv("AFD_COL_TMA") && atoi(getenv("AFD_C
 int big_launch_cols(afd_plan* p, bool inv, int last_mode, int scale_n, int64_t r0, int64_t rows,
                     double2* fout, const int* stopped, cudaStream_t st) {
   dim3 grid((unsigned)big_col_ctas(p), (unsigned)rows);
+  // fast arithmetic for the field's column stages only (the transforms of
+  // the step bookkeeping stay exact)
+  const bool fastf = p->fast && inv && (last_mode == 1 || last_mode == 2);
   for (int b0 = p->ka; b0 < p->K; b0 += 4) {
     const int left = p->K - b0;
     if (inv && last_mode == 1 && kColTmaEnabled &&
         (left == 4 || (left == 8 && kCol8Enabled && p->ymap_ok))) {
       const int64_t tiles = rows * ((int64_t)1 << b0) / (left == 8 ? 16 : 256);
       const unsigned g = (unsigned)std::min<int64_t>(p->sms, tiles);
+      auto k8 = fastf ? col_tma_kernel<8, true> : col_tma_kernel<8>;
+      auto k4 = fastf ? col_tma_kernel<4, true> : col_tma_kernel<4>;
+      const double2* tws = fastf ? p->twct : p->twst;
       if (left == 8)
-        col_tma_kernel<8><<<g, 256, ColTma<8>::SMEM, st>>>(p->K, b0, p->Y, p->twst, p->scales,
-                                                           r0, r0 + rows, p->big_cand, stopped,
-                                                           p->ymap);
+        k8<<<g, 256, ColTma<8>::SMEM, st>>>(p->K, b0, p->Y, tws, p->scales, r0, r0 + rows,
+                                            p->big_cand, stopped, p->ymap);
       else
-        col_tma_kernel<4><<<g, 256, ColTma<4>::SMEM, st>>>(p->K, b0, p->Y, p->twst, p->scales,
-                                                           r0, r0 + rows, p->big_cand, stopped,
-                                                           p->ymap);
+        k4<<<g, 256, ColTma<4>::SMEM, st>>>(p->K, b0, p->Y, tws, p->scales, r0, r0 + rows,
+                                            p->big_cand, stopped, p->ymap);
       p->launches++;
       CU(cudaGetLastError());
       break;
+    }
+    if (fastf) {
+      // materialised fast field rows / fallback: one 4-stage pass at a time
+      const int mode = (b0 + 4 >= p->K) ? last_mode : 0;
+      if (mode == 0)
+        big_pass_col<true, 0, true><<<grid, kColThreads, 0, st>>>(
+            p->K, p->ka, b0, mode, scale_n, p->Y, p->twct, p->scales, r0, r0 + rows,
+            p->big_cand, fout, stopped);
+      else if (mode == 1)
+        big_pass_col<true, 1, true><<<grid, kColThreads, 0, st>>>(
+            p->K, p->ka, b0, mode, scale_n, p->Y, p->twct, p->scales, r0, r0 + rows,
+            p->big_cand, fout, stopped);
+      else
+        big_pass_col<true, -1, true><<<grid, kColThreads, 0, st>>>(
+            p->K, p->ka, b0, mode, scale_n, p->Y, p->twct, p->scales, r0, r0 + rows,
+            p->big_cand, fout, stopped);
+      p->launches++;
+      CU(cudaGetLastError());
+      continue;
     }
     // 8 stages at once (big_pass_col8) where they are the field's last eight
     // or are followed by more column stages (in-place)

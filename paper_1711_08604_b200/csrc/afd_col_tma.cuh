@@ -51,7 +51,9 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, unsig
       : "memory");
 }
 
-template <int KC>
+// FAST (AFD_PLAN_FAST): twst is the (c, t) table (already conjugated), the
+// butterflies are bfly_ct and the scale is already in pass A's weights.
+template <int KC, bool FAST = false>
 __global__ void __launch_bounds__(256, 1)
 col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __restrict__ twst,
                const double* __restrict__ scales, long long row0, long long row1,
@@ -129,7 +131,7 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
         const int slot = x / COLS, cc = x % COLS;  // slot = 2^e - 1 + kk
         const int e = 31 - __clz(slot + 1), kk = slot + 1 - (1 << e);
         double2 w = __ldg(twst + ((1LL << (b0 + e)) - 1) + q0 + cc + ((long long)kk << b0));
-        w.y = -w.y;
+        if (!FAST) w.y = -w.y;
         tw_a[x] = w;
       }
       if constexpr (KC == 8) {
@@ -138,7 +140,7 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
           const int ib = 31 - __clz(slot + 1), kk = slot + 1 - (1 << ib);
           double2 w = __ldg(twst + ((1LL << (b0 + 4 + ib)) - 1) + q0 + cc +
                             ((long long)(hh + 16 * kk) << b0));
-          w.y = -w.y;
+          if (!FAST) w.y = -w.y;
           tw_b[x] = w;
         }
       }
@@ -148,7 +150,7 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
     const int s = n % C::STAGES;
     double2* tile = csm + s * TILE;
     mbar_wait(&full[s], (unsigned)((n / C::STAGES) & 1));
-    const double sc = __ldg(scales + row);
+    const double sc = FAST ? 1.0 : __ldg(scales + row);
     const int q = q0 + c;
     double2 v[16];
 #pragma unroll
@@ -161,7 +163,7 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
 #pragma unroll
         for (int hh = 0; hh < (16 >> (e + 1)); ++hh) {
           const int i = kk | (hh << (e + 1));
-          bfly(v[i], v[i | (1 << e)], w);
+          bfly_any<FAST>(v[i], v[i | (1 << e)], w);
         }
       }
     }
@@ -179,7 +181,7 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
 #pragma unroll
           for (int hh = 0; hh < (16 >> (ib + 1)); ++hh) {
             const int i = kk | (hh << (ib + 1));
-            bfly(v[i], v[i | (1 << ib)], w);
+            bfly_any<FAST>(v[i], v[i | (1 << ib)], w);
           }
         }
       }
@@ -193,8 +195,8 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const long long j = q + ((long long)(KC == 8 ? h + 16 * i : i) << b0);
-      const double2 f = make_double2(v[i].x * sc, v[i].y * sc);  // transform.py:200
-      const double mg = np_mag2(f);                              // core.py:298
+      const double2 f = FAST ? v[i] : make_double2(v[i].x * sc, v[i].y * sc);  // transform.py:200
+      const double mg = FAST ? fast_mag2(f) : np_mag2(f);                     // core.py:298
       const long long flat = row * N + j;
       if (mg >= best.mag && cand_better(mg, flat, best.mag, best.flat)) {
         best.mag = mg;

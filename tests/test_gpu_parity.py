@@ -797,3 +797,75 @@ def test_fast_c3_batch_matches_oracle(afd):
         c = np.array([s.coefficient for s in ds[i].steps])
         oc = o.steps["c_re"] + 1j * o.steps["c_im"]
         assert np.all(np.abs(c - oc) <= FAST_TOL * np.abs(oc))
+
+
+@pytest.mark.parametrize("k,m", [(16, 100), (20, 5)])
+def test_fast_big_field_rows_close_to_oracle(afd, k, m):
+    """Fast large-N field (pass A with on-chip weights + (c, t) column pass):
+    materialised rows vs the oracle's bit-exact rows, 1e-12 of each row's max."""
+    core, engine = afd
+    import torch
+    from paper_1711_08604_b200 import workloads as W
+    n = 1 << k
+    g = W.pole_sum(n, 32, 0.98, 50 + k)
+    radii = tuple(0.999 * i / (m - 1) for i in range(m))
+    ghat = O.dft_forward(g)
+    plan = engine.Plan(radii, n, fast=1)
+    rows = [0, 1, m // 2, m - 1] if m > 4 else list(range(m))
+    got = plan.field(torch.from_numpy(ghat).cuda()).cpu().numpy()
+    for r in rows:
+        ref = O.field(ghat, np.array(radii), r, r + 1)[0]
+        assert np.abs(got[r] - ref).max() <= 1e-12 * np.abs(ref).max(), r
+
+
+@pytest.mark.parametrize("k,m", [(16, 163), (20, 7)])
+def test_fast_big_decompose_matches_oracle(afd, k, m):
+    core, _ = afd
+    from paper_1711_08604_b200 import workloads as W
+    n = 1 << k
+    g = W.pole_sum(n, 32, 0.97, 7 + k)
+    radii = tuple(i / m for i in range(m))
+    d = core.decompose(g, core.ParameterGrid(radii, n), max_terms=3, engine="fft-fast")
+    o = O.decompose(g, np.array(radii), max_terms=3)
+    assert [s.point.angle_index for s in d.steps] == list(o.steps["j"])
+    assert [s.point.radius for s in d.steps] == list(o.steps["radius"])
+    oc = o.steps["c_re"] + 1j * o.steps["c_im"]
+    c = np.array([s.coefficient for s in d.steps])
+    assert np.all(np.abs(c - oc) <= FAST_TOL * np.abs(oc))
+    res = np.array([s.residual_energy for s in d.steps])
+    assert np.all(np.abs(res - o.steps["residual"]) <= FAST_TOL * o.steps["residual"])
+    assert np.abs(d.remainder - o.remainder).max() <= FAST_TOL * np.abs(o.remainder).max()
+
+
+def test_fast_c2_first_steps(afd):
+    """BASELINE c2 (N=65536, M=4096) in fast mode: the reference's own first
+    selections (golden fixture) with coefficients / residuals within 1e-9."""
+    core, _ = afd
+    g = load_golden("c2_step.npz")
+    grid = core.ParameterGrid(tuple(g["radii"]), g["g"].shape[0])
+    d = core.decompose(g["g"], grid, max_terms=len(g["s"]), engine="fft-fast")
+    for k, st in enumerate(d.steps):
+        assert grid.radii.index(st.point.radius) == g["s"][k]
+        assert st.point.angle_index == g["j"][k]
+        assert abs(st.coefficient - g["coeff"][k]) <= FAST_TOL * abs(g["coeff"][k])
+        assert abs(st.residual_energy - g["residual"][k]) <= FAST_TOL * g["residual"][k]
+
+
+def test_fast_c4_full_size_replay(afd):
+    """BASELINE c4 at full size (N = 2^20, M = 16384) in fast mode, 3 AFD
+    steps, replayed by the oracle (selected row's first maximum, neighbouring
+    and sampled rows, coefficient and residual within 1e-9 per step)."""
+    core, engine = afd
+    from paper_1711_08604_b200 import workloads as W
+    w = W.CONFIGS["c4"]
+    g = W.signal_for("c4")
+    radii = np.array(W.radii_for(w.m))
+    plan = engine.Plan(tuple(radii), w.n, max_batch=1, fast=1)
+    try:
+        rec, counts, initial, rem, _, _ = plan.decompose_host(g[None, :], 3)
+    finally:
+        del plan
+    r = O.replay_check(g, radii, rec[0], int(counts[0]), rows_per_step=4, rtol=FAST_TOL,
+                       threads=O.max_threads())
+    assert r["ok"], r["why"]
+    assert np.abs(rem[0] - r["remainder"]).max() <= FAST_TOL * np.abs(r["remainder"]).max()
