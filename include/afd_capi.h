@@ -182,6 +182,31 @@ int afd_apply_step(afd_plan *plan, int k, int max_terms, double threshold, int d
 int afd_sharded_finish(afd_plan *plan, int64_t batch, int32_t *n_steps, double *initial,
                        double *remainder, int32_t *stopped, void *stream);
 
+/* Device-resident radius-sharded decomposition (SURVEY.md §8(b)'s
+ * afd_decompose(..., nccl_comm)).  A communicator is an NCCL communicator
+ * over the ranks that share the radius grid (one process per GPU); the
+ * library loads libnccl.so.2 at run time (the copy already in the process,
+ * e.g. torch's, else the system's).  Rank 0 calls afd_comm_unique_id and
+ * the caller distributes the 128 bytes to every rank (any side channel:
+ * torch.distributed, MPI, a file), then each rank calls afd_comm_init.
+ *
+ * afd_decompose_sharded: every rank passes the same g0 and a plan over its
+ * own rows [m0, m1); the whole loop — local field + argmax, an ncclAllGather
+ * of one 32-byte candidate per rank and signal, the replicated update,
+ * energy and next spectrum — is captured once into a CUDA graph (per comm,
+ * max_terms, threshold, dc_first, batch, stream) and replayed, so no step
+ * returns to the host.  Outputs as afd_decompose, identical on every rank
+ * and identical to the unsharded result.  Replaces the reference's only
+ * parallelism, the radius-row thread pool (core.py:253-282). */
+typedef struct afd_comm afd_comm;
+int afd_comm_unique_id(void *id_out /* 128 bytes */);
+int afd_comm_init(afd_comm **out, const void *id /* 128 bytes */, int world, int rank,
+                  int device);
+int afd_comm_destroy(afd_comm *comm);
+int afd_decompose_sharded(afd_plan *plan, afd_comm *comm, const double *g0, int64_t batch,
+                          int max_terms, double threshold, int dc_first, afd_step *steps,
+                          int32_t *n_steps, double *initial, double *remainder, void *stream);
+
 /* core.error_trace + core.reconstruct (core.py:411-460) for `batch` signals:
  * errors[batch][max_terms] (entry k = relative error of the (k+1)-term
  * partial sum), recon[batch][N] = S_{n_steps} (may be NULL). */

@@ -61,6 +61,10 @@ SIGNATURES = [
     ("afd_select_local", _I, [_VP, _I, _I, _VP, _I64, _VP]),
     ("afd_apply_step", _I, [_VP, _I, _I, _D, _I, _VP, _I, _I64, _VP, _VP]),
     ("afd_sharded_finish", _I, [_VP, _I64, _VP, _VP, _VP, _VP, _VP]),
+    ("afd_comm_unique_id", _I, [_VP]),
+    ("afd_comm_init", _I, [C.POINTER(_VP), _VP, _I, _I, _I]),
+    ("afd_comm_destroy", _I, [_VP]),
+    ("afd_decompose_sharded", _I, [_VP, _VP, _VP, _I64, _I, _D, _I, _VP, _VP, _VP, _VP, _VP]),
     ("afd_error_trace", _I, [_VP, _VP, _VP, _I, _VP, _I64, _VP, _VP, _VP]),
     ("afd_launch_count", _I64, [_VP]),
     ("afd_time_field", _I, [_VP, _VP, _I64, _I, _VP, _VP]),

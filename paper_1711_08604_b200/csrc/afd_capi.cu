@@ -2,6 +2,8 @@
 // tables), kernel dispatch by transform length, the device-resident
 // decomposition loop captured as a CUDA graph, and the sharded step API.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl.so.2 is loaded at run time (nccl())
 
 #include <cmath>
 #include <cstdarg>
@@ -115,6 +117,18 @@ struct afd_plan {
   BigSel* sel = nullptr;
   int* amb = nullptr;
   double2* tmp = nullptr;      // [N] projection spectrum
+  // radius-sharded decomposition graph (afd_decompose_sharded)
+  Cand* loc_cand = nullptr;    // [max_batch] this rank's candidates
+  Cand* gath_cand = nullptr;   // [world][max_batch] all-gathered
+  Cand* gath_t = nullptr;      // [max_batch][world] transposed
+  int gath_world = 0;
+  cudaGraphExec_t sgexec = nullptr;
+  const void* sg_comm = nullptr;
+  int sg_max_terms = -1, sg_dc_first = -1;
+  double sg_threshold = -2;
+  int64_t sg_batch = -1;
+  cudaStream_t sg_stream = nullptr;
+  int64_t sgraph_launches = 0;
   // host-buffer entry point: pinned staging + packed device output
   void* pin = nullptr;
   size_t pin_bytes = 0;
@@ -479,6 +493,9 @@ int decomp_field_ctas(const afd_plan* p, int64_t batch) {
 void invalidate_graph(afd_plan* p) {
   if (p->gexec) cudaGraphExecDestroy(p->gexec);
   p->gexec = nullptr;
+  if (p->sgexec) cudaGraphExecDestroy(p->sgexec);
+  p->sgexec = nullptr;
+  p->sg_comm = nullptr;
   p->g_max_terms = -1;
   p->g_dc_first = -1;
   p->g_threshold = -2;
@@ -843,7 +860,67 @@ int big_step(afd_plan* p, int sig, int k, int max_terms, double thr, int dc_firs
   return big_fft(p, rem, ghat_rev, false, 0, 4, stopped, st);
 }
 
+// ---------------------------------------------------------------------------
+// NCCL, loaded at run time (the single-GPU library has no NCCL dependency):
+// the process's already-loaded libnccl.so.2 (e.g. torch's) if there is one,
+// else the system's.  Only the five entry points the sharded loop needs.
+// ---------------------------------------------------------------------------
+struct Nccl {
+  bool ok = false;
+  std::string err;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+
+const Nccl& nccl() {
+  static Nccl n = [] {
+    Nccl x;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      x.err = std::string("libnccl.so.2 not found: ") + dlerror();
+      return x;
+    }
+    x.getUniqueId = (decltype(x.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    x.commInitRank = (decltype(x.commInitRank))dlsym(h, "ncclCommInitRank");
+    x.commDestroy = (decltype(x.commDestroy))dlsym(h, "ncclCommDestroy");
+    x.allGather = (decltype(x.allGather))dlsym(h, "ncclAllGather");
+    x.getErrorString = (decltype(x.getErrorString))dlsym(h, "ncclGetErrorString");
+    x.ok = x.getUniqueId && x.commInitRank && x.commDestroy && x.allGather && x.getErrorString;
+    if (!x.ok) x.err = "libnccl.so.2 lacks a required symbol";
+    return x;
+  }();
+  return n;
+}
+
+#define NC(call)                                                                        \
+  do {                                                                                  \
+    ncclResult_t r_ = (call);                                                           \
+    if (r_ != ncclSuccess)                                                              \
+      return fail(AFD_E_CUDA, "%s: %s", #call, nccl().getErrorString(r_));              \
+  } while (0)
+
+// [world][batch] candidates (all-gather order) -> [batch][world] (rank-major
+// per signal: the step kernels' merge keeps the lowest flat index on ties)
+__global__ void cand_transpose_kernel(const Cand* __restrict__ in, int world, int batch,
+                                      Cand* __restrict__ out) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < world * batch;
+       x += gridDim.x * blockDim.x) {
+    const int r = x / batch, b = x % batch;
+    out[(size_t)b * world + r] = in[x];
+  }
+}
+
 }  // namespace
+
+struct afd_comm {
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0, device = 0;
+};
 
 // ---------------------------------------------------------------------------
 // C ABI
@@ -1032,6 +1109,10 @@ int afd_plan_destroy(afd_plan* p) {
   if (!p) return AFD_OK;
   cudaSetDevice(p->device);
   if (p->gexec) cudaGraphExecDestroy(p->gexec);
+  if (p->sgexec) cudaGraphExecDestroy(p->sgexec);
+  cudaFree(p->loc_cand);
+  cudaFree(p->gath_cand);
+  cudaFree(p->gath_t);
   cudaFree(p->radii);
   cudaFree(p->scales);
   cudaFree(p->twst);
@@ -1378,13 +1459,11 @@ int afd_decompose_host(afd_plan* p, const double* g0_host, int64_t batch, int ma
   return 0;
 }
 
-int afd_sharded_begin(afd_plan* p, const double* g0, int64_t batch, void* stream) {
-  if (!p || !g0) return fail(AFD_E_INVALID, "NULL argument");
+static int enqueue_sharded_begin(afd_plan* p, const double* g0, int64_t batch, cudaStream_t st) {
   int rc;
-  if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
-  CU(cudaMemcpyAsync(p->gin, g0, sizeof(double2) * (size_t)p->n * batch,
-                     cudaMemcpyDeviceToDevice, st));
+  if ((const void*)g0 != (const void*)p->gin)
+    CU(cudaMemcpyAsync(p->gin, g0, sizeof(double2) * (size_t)p->n * batch,
+                       cudaMemcpyDeviceToDevice, st));
   if (p->big) {
     for (int64_t b = 0; b < batch; ++b)
       if ((rc = big_step(p, (int)b, -1, 1, 0.0, 0, p->gin + b * p->n, nullptr, 0, p->steps, st)))
@@ -1395,15 +1474,14 @@ int afd_sharded_begin(afd_plan* p, const double* g0, int64_t batch, void* stream
                                             st));
 }
 
-int afd_select_local(afd_plan* p, int k, int dc_first, afd_candidate* cand, int64_t batch,
-                     void* stream) {
-  if (!p || !cand) return fail(AFD_E_INVALID, "NULL argument");
+// Field + argmax over the plan's rows -> cand[batch] (neutral at a dc_first
+// step 0).  ensure_cand must have run (capture cannot allocate).
+static int enqueue_select_local(afd_plan* p, int k, int dc_first, Cand* cand, int64_t batch,
+                                cudaStream_t st) {
   int rc;
-  if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
   if (k == 0 && dc_first) {
     // the pinned mean atom needs no field; emit a neutral candidate
-    neutral_cand_kernel<<<1, 128, 0, st>>>((Cand*)cand, (int)batch);
+    neutral_cand_kernel<<<1, 128, 0, st>>>(cand, (int)batch);
     p->launches++;
     CU(cudaGetLastError());
     return 0;
@@ -1415,14 +1493,14 @@ int afd_select_local(afd_plan* p, int k, int dc_first, afd_candidate* cand, int6
       const Cand* parts;
       int np;
       if ((rc = big_reduce_cands(p, st, &parts, &np))) return rc;
-      cand_reduce_kernel<<<1, 256, 0, st>>>(parts, np, (Cand*)cand + b);
+      cand_reduce_kernel<<<1, 256, 0, st>>>(parts, np, cand + b);
       p->launches++;
     }
     CU(cudaGetLastError());
     return 0;
   }
   const int ncta = field_ctas_for(p, p->m1 - p->m0, batch);
-  if ((rc = ensure_cand(p, batch, ncta))) return rc;
+  if (ncta > p->ncand_cap) return fail(AFD_E_INVALID, "candidate buffer not sized");
   if (p->engine == 1) {
     if ((rc = launch_direct(p, p->rem, p->m0, p->m1, batch, p->cand, nullptr, p->state, st)))
       return rc;
@@ -1434,10 +1512,43 @@ int afd_select_local(afd_plan* p, int k, int dc_first, afd_candidate* cand, int6
       break;
     });
   }
-  cand_reduce_kernel<<<(unsigned)batch, 128, 0, st>>>(p->cand, ncta, (Cand*)cand);
+  cand_reduce_kernel<<<(unsigned)batch, 128, 0, st>>>(p->cand, ncta, cand);
   p->launches++;
   CU(cudaGetLastError());
   return 0;
+}
+
+static int enqueue_apply_step(afd_plan* p, int k, int max_terms, double thr, int dc_first,
+                              const Cand* cands, int ncand, int64_t batch, Step* steps,
+                              cudaStream_t st) {
+  int rc;
+  if (p->big) {
+    for (int64_t b = 0; b < batch; ++b)
+      if ((rc = big_step(p, (int)b, k, max_terms, thr, dc_first, nullptr, cands + b * ncand,
+                         ncand, steps, st)))
+        return rc;
+    return 0;
+  }
+  AFD_DISPATCH(p->K, return launch_step<KK>(p, k, max_terms, thr, dc_first, nullptr, cands,
+                                            ncand, batch, steps, st));
+}
+
+int afd_sharded_begin(afd_plan* p, const double* g0, int64_t batch, void* stream) {
+  if (!p || !g0) return fail(AFD_E_INVALID, "NULL argument");
+  int rc;
+  if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
+  return enqueue_sharded_begin(p, g0, batch, (cudaStream_t)stream);
+}
+
+int afd_select_local(afd_plan* p, int k, int dc_first, afd_candidate* cand, int64_t batch,
+                     void* stream) {
+  if (!p || !cand) return fail(AFD_E_INVALID, "NULL argument");
+  int rc;
+  if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
+  if (!p->big && !(k == 0 && dc_first) &&
+      (rc = ensure_cand(p, batch, field_ctas_for(p, p->m1 - p->m0, batch))))
+    return rc;
+  return enqueue_select_local(p, k, dc_first, (Cand*)cand, batch, (cudaStream_t)stream);
 }
 
 int afd_apply_step(afd_plan* p, int k, int max_terms, double threshold, int dc_first,
@@ -1448,17 +1559,136 @@ int afd_apply_step(afd_plan* p, int k, int max_terms, double threshold, int dc_f
   int rc;
   if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
   const double thr = threshold > 0.0 ? threshold : 0.0;
-  if (p->big) {
-    for (int64_t b = 0; b < batch; ++b)
-      if ((rc = big_step(p, (int)b, k, max_terms, thr, dc_first, nullptr,
-                         (const Cand*)cands + b * ncand, ncand, (Step*)steps,
-                         (cudaStream_t)stream)))
-        return rc;
-    return 0;
+  return enqueue_apply_step(p, k, max_terms, thr, dc_first, (const Cand*)cands, ncand, batch,
+                            (Step*)steps, (cudaStream_t)stream);
+}
+
+// The radius-sharded loop with its all-gathers: init + max_terms x (local
+// field + argmax -> NCCL all-gather of the 32-byte candidates -> replicated
+// update), all stream-ordered on st (captured into a graph by the caller).
+static int enqueue_decompose_sharded(afd_plan* p, afd_comm* c, int64_t batch, int max_terms, double thr,
+                              int dc_first, cudaStream_t st) {
+  int rc;
+  if ((rc = enqueue_sharded_begin(p, (const double*)p->gin, batch, st))) return rc;
+  const size_t bytes = sizeof(Cand) * (size_t)batch;
+  for (int k = 0; k < max_terms; ++k) {
+    if ((rc = enqueue_select_local(p, k, dc_first, p->loc_cand, batch, st))) return rc;
+    NC(nccl().allGather(p->loc_cand, p->gath_cand, bytes, ncclUint8, c->comm, st));
+    const Cand* cands = p->gath_cand;
+    if (batch > 1 && c->world > 1) {
+      cand_transpose_kernel<<<1, 256, 0, st>>>(p->gath_cand, c->world, (int)batch, p->gath_t);
+      p->launches++;
+      cands = p->gath_t;
+    }
+    if ((rc = enqueue_apply_step(p, k, max_terms, thr, dc_first, cands, c->world, batch,
+                                 p->steps, st)))
+      return rc;
   }
-  AFD_DISPATCH(p->K, return launch_step<KK>(p, k, max_terms, thr, dc_first, nullptr,
-                                            (const Cand*)cands, ncand, batch, (Step*)steps,
-                                            (cudaStream_t)stream));
+  CU(cudaGetLastError());
+  return 0;
+}
+
+int afd_comm_unique_id(void* id_out) {
+  if (!id_out) return fail(AFD_E_INVALID, "NULL argument");
+  if (!nccl().ok) return fail(AFD_E_UNSUPPORTED, "%s", nccl().err.c_str());
+  ncclUniqueId id;
+  NC(nccl().getUniqueId(&id));
+  std::memcpy(id_out, &id, sizeof id);
+  return 0;
+}
+
+int afd_comm_init(afd_comm** out, const void* id, int world, int rank, int device) {
+  if (!out || !id) return fail(AFD_E_INVALID, "NULL argument");
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(AFD_E_INVALID, "rank %d outside world of %d", rank, world);
+  if (!nccl().ok) return fail(AFD_E_UNSUPPORTED, "%s", nccl().err.c_str());
+  CU(cudaSetDevice(device));
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof uid);
+  afd_comm* c = new afd_comm();
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  const ncclResult_t r = nccl().commInitRank(&c->comm, world, uid, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(AFD_E_CUDA, "ncclCommInitRank: %s", nccl().getErrorString(r));
+  }
+  *out = c;
+  return 0;
+}
+
+int afd_comm_destroy(afd_comm* c) {
+  if (!c) return 0;
+  if (c->comm) nccl().commDestroy(c->comm);
+  delete c;
+  return 0;
+}
+
+int afd_decompose_sharded(afd_plan* p, afd_comm* c, const double* g0, int64_t batch,
+                          int max_terms, double threshold, int dc_first, afd_step* steps,
+                          int32_t* n_steps, double* initial, double* remainder, void* stream) {
+  if (!p || !c || !g0 || !steps || !n_steps || !initial || !remainder)
+    return fail(AFD_E_INVALID, "NULL argument");
+  if (max_terms < 1) return fail(AFD_E_INVALID, "max_terms must be >= 1");
+  if (c->device != p->device) return fail(AFD_E_INVALID, "communicator and plan on different devices");
+  int rc;
+  if ((rc = check_batch(p, batch)) || (rc = set_device(p))) return rc;
+  if ((rc = ensure_steps(p, max_terms))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const double thr = threshold > 0.0 ? threshold : 0.0;
+  if (!p->big && (rc = ensure_cand(p, batch, field_ctas_for(p, p->m1 - p->m0, batch)))) return rc;
+  if (p->gath_world < c->world) {
+    invalidate_graph(p);
+    cudaFree(p->loc_cand);
+    cudaFree(p->gath_cand);
+    cudaFree(p->gath_t);
+    p->loc_cand = p->gath_cand = p->gath_t = nullptr;
+    p->gath_world = 0;
+    CU(cudaMalloc(&p->loc_cand, sizeof(Cand) * (size_t)p->max_batch));
+    CU(cudaMalloc(&p->gath_cand, sizeof(Cand) * (size_t)p->max_batch * c->world));
+    CU(cudaMalloc(&p->gath_t, sizeof(Cand) * (size_t)p->max_batch * c->world));
+    p->gath_world = c->world;
+  }
+  CU(cudaMemcpyAsync(p->gin, g0, sizeof(double2) * (size_t)p->n * batch, cudaMemcpyDeviceToDevice,
+                     st));
+  const bool reuse = p->sgexec && p->sg_comm == (const void*)c && p->sg_max_terms == max_terms &&
+                     p->sg_dc_first == dc_first && p->sg_threshold == thr &&
+                     p->sg_batch == batch && p->sg_stream == st;
+  if (!reuse) {
+    if (p->sgexec) cudaGraphExecDestroy(p->sgexec);
+    p->sgexec = nullptr;
+    cudaStream_t cap;
+    CU(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    cudaGraph_t graph;
+    const int64_t before = p->launches;
+    CU(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    rc = enqueue_decompose_sharded(p, c, batch, max_terms, thr, dc_first, cap);
+    cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+    cudaStreamDestroy(cap);
+    if (rc) return rc;
+    if (ce != cudaSuccess) return fail(AFD_E_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+    p->sgraph_launches = p->launches - before;
+    p->launches = before;
+    ce = cudaGraphInstantiate(&p->sgexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) return fail(AFD_E_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+    p->sg_comm = c;
+    p->sg_max_terms = max_terms;
+    p->sg_dc_first = dc_first;
+    p->sg_threshold = thr;
+    p->sg_batch = batch;
+    p->sg_stream = st;
+  }
+  CU(cudaGraphLaunch(p->sgexec, st));
+  p->launches += p->sgraph_launches;
+  gather_outputs_kernel<<<(unsigned)batch, 256, 0, st>>>(
+      (int)p->n, max_terms, p->steps, p->state, p->rem, (Step*)steps, n_steps, initial,
+      (double2*)remainder, nullptr);
+  p->launches++;
+  CU(cudaGetLastError());
+  return 0;
 }
 
 int afd_sharded_finish(afd_plan* p, int64_t batch, int32_t* n_steps, double* initial,

@@ -53,6 +53,26 @@ def _default_plan(radii, n, batch, m0, m1, device, engine_name="fft"):
                            fast=engine_name == "fft-fast")
 
 
+_COMMS = {}
+
+
+def library_comm(group, device):
+    """The library's own NCCL communicator over `group` (cached per group):
+    rank 0 draws the NCCL unique id, torch.distributed broadcasts it."""
+    import torch.distributed as dist
+    from . import engine
+    key = (id(group), str(device))
+    c = _COMMS.get(key)
+    if c is None:
+        obj = [engine.Comm.unique_id() if dist.get_rank(group) == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0,
+                                   group=group)
+        c = engine.Comm(obj[0], dist.get_world_size(group), dist.get_rank(group),
+                        device.index)
+        _COMMS[key] = c
+    return c
+
+
 class ShardedRunner:
     """The radius-sharded decomposition loop of one rank.
 
@@ -61,7 +81,12 @@ class ShardedRunner:
     lowest flat index still wins ties), then the identical replicated
     update + energy + next spectrum (apply_step).  The host issues the steps
     without ever synchronising; once a signal's stop rule fires its kernels
-    are no-ops.  Reusable: ``run`` may be called repeatedly (benchmarks)."""
+    are no-ops.  Reusable: ``run`` may be called repeatedly (benchmarks).
+
+    On an NCCL group with CUDA plans the whole loop is device-resident: the
+    library captures it, all-gathers included, into one CUDA graph
+    (afd_decompose_sharded over the library's own communicator).  Otherwise
+    (gloo, CPU stand-in plans) the host issues it step by step."""
 
     def __init__(self, plan, batch, max_terms, threshold=None, dc_first=False, group=None):
         import torch
@@ -76,10 +101,21 @@ class ShardedRunner:
                                     device=dev)
         self.cpu = dist.get_backend(group) != "nccl" and dev.type == "cuda"
         self.fin = None
+        self.device_loop = (dist.get_backend(group) == "nccl" and dev.type == "cuda" and
+                            hasattr(plan, "decompose_sharded"))
+        if self.device_loop:
+            self.comm = library_comm(group, dev)
+            self.out = plan.alloc_outputs(self.batch, self.max_terms)
 
     def run(self, g):
         """Decompose g ([batch, N], on the plan's device) over all ranks."""
         p = self.plan
+        if self.device_loop:
+            o = p.decompose_sharded(self.comm, g, self.max_terms, self.threshold,
+                                    self.dc_first, out=self.out)
+            self.steps = o.steps
+            self.fin = (o.n_steps, o.initial, o.remainder, None)
+            return self.fin
         p.sharded_begin(g)
         for k in range(self.max_terms):
             local = p.select_local(k, self.dc_first, self.batch)           # [B, 32]

@@ -25,7 +25,7 @@ try:  # torch is plumbing only; the product cannot run without it and a GPU
 except ImportError as exc:  # pragma: no cover
     raise _capi.AfdCudaUnavailable("torch is required for device memory") from exc
 
-__all__ = ["Plan", "get_plan", "host_tables", "DeviceDecomposition", "require_cuda"]
+__all__ = ["Plan", "Comm", "get_plan", "host_tables", "DeviceDecomposition", "require_cuda"]
 
 
 def require_cuda(device=None):
@@ -298,6 +298,23 @@ class Plan:
 
     # -- radius-sharded stepping (multi-GPU) ---------------------------------------
     @_locked
+    def decompose_sharded(self, comm, g, max_terms, threshold=None, dc_first=False, stream=None,
+                          out=None):
+        """Device-resident radius-sharded decomposition over `comm` (a Comm):
+        the plan's rows are this rank's shard; one CUDA graph per call shape,
+        NCCL all-gathers inside it (afd_decompose_sharded)."""
+        g = self._signal(g)
+        b = g.shape[0]
+        if out is None:
+            out = self.alloc_outputs(b, max_terms)
+        _capi.check(self.lib.afd_decompose_sharded(
+            self.handle, comm.handle, _ptr(g), b, int(max_terms),
+            0.0 if threshold is None else float(threshold), int(bool(dc_first)),
+            _ptr(out.steps), _ptr(out.n_steps), _ptr(out.initial), _ptr(out.remainder),
+            _stream(stream)))
+        return out
+
+    @_locked
     def sharded_begin(self, g, stream=None):
         g = self._signal(g)
         _capi.check(self.lib.afd_sharded_begin(self.handle, _ptr(g), g.shape[0], _stream(stream)))
@@ -329,6 +346,34 @@ class Plan:
         _capi.check(self.lib.afd_sharded_finish(self.handle, batch, _ptr(n_steps), _ptr(initial),
                                                 _ptr(rem), _ptr(stopped), _stream(stream)))
         return n_steps, initial, rem, stopped
+
+
+class Comm:
+    """An afd_comm (NCCL communicator of the library) for `world` ranks."""
+
+    def __init__(self, uid, world, rank, device=None):
+        self.device = require_cuda(device)
+        self.lib = _capi.load()
+        h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(uid), 128)
+        _capi.check(self.lib.afd_comm_init(C.byref(h), buf, int(world), int(rank),
+                                           self.device.index))
+        self.handle, self.world, self.rank = h, int(world), int(rank)
+
+    @staticmethod
+    def unique_id():
+        buf = C.create_string_buffer(128)
+        _capi.check(_capi.load().afd_comm_unique_id(buf))
+        return buf.raw
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self.lib.afd_comm_destroy(h)
+            except Exception:  # pragma: no cover - interpreter teardown
+                pass
+            self.handle = None
 
 
 def fp64_peak_tflops(device=None, stream=None):
