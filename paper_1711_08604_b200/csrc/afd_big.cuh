@@ -743,7 +743,7 @@ __global__ void __launch_bounds__(256)
 big_update_kernel(int K, const BigSel* __restrict__ sel, const double2* __restrict__ g0,
                   double2* __restrict__ rem, const double2* __restrict__ circle,
                   const State* __restrict__ state, double* __restrict__ nodes,
-                  int* __restrict__ amb_out) {
+                  int* __restrict__ amb_out, const double* __restrict__ pow2) {
   __shared__ double buf[kNodeLen];
   __shared__ double scratch[2 * (kNodeLen / 8 + 16)];
   if (sel && state->stopped) return;
@@ -759,7 +759,8 @@ big_update_kernel(int K, const BigSel* __restrict__ sel, const double2* __restri
     }
   } else {
     const BigSel s = *sel;
-    const double kn = kernel_norm(s.a, &amb);
+    const double kn = kernel_norm_grid(s.a, s.radius, pow2 ? pow2 + (size_t)s.s * kPowRow : nullptr,
+                                       &amb);
     const double2 sc = make_double2(kn, 0.0);
     for (int i = threadIdx.x; i < kNodeLen; i += blockDim.x) {
       const long long m = m0 + i;

@@ -66,6 +66,7 @@ struct afd_plan {
   int sms = 148;
   // device tables
   double* radii = nullptr;    // [M]
+  double* pow2 = nullptr;     // [M][kPowRow] libm pow(h, 2.0) around each radius
   double* scales = nullptr;   // [M]
   double2* twst = nullptr;    // stage tables [N-1]
   double2* circle = nullptr;  // [N]
@@ -381,12 +382,12 @@ int launch_step(afd_plan* p, int k, int max_terms, double thr, int dc_first, con
                   dim3(ClusterGeo<K>::THREADS), ClusterSmem<K>::bytes, st, ClusterGeo<K>::C, k,
                   max_terms, thr, dc_first, g0, p->rem, p->ghat, cand, ncand,
                   (const double*)p->radii, (int)p->m, (const double2*)p->circle,
-                  (const double2*)p->twst, p->state, steps));
+                  (const double2*)p->twst, p->state, steps, (const double*)p->pow2));
   } else {
     CU(launch_pdl(step_kernel<K>, dim3((unsigned)batch), dim3(row_block<K>()),
                   RowSmem<K>::bytes, st, k, max_terms, thr, dc_first, g0, p->rem, p->ghat, cand,
                   ncand, (const double*)p->radii, (const double2*)p->circle,
-                  (const double2*)p->twst, p->state, steps));
+                  (const double2*)p->twst, p->state, steps, (const double*)p->pow2));
   }
   p->launches++;
   CU(cudaGetLastError());
@@ -830,7 +831,7 @@ int big_step(afd_plan* p, int sig, int k, int max_terms, double thr, int dc_firs
   const int nn = big_nnodes(p);
   if (k < 0) {
     big_update_kernel<<<nn, 256, 0, st>>>(p->K, nullptr, g0, rem, p->circle, state, p->nodes,
-                                          nullptr);
+                                          nullptr, nullptr);
     big_finalize_kernel<<<1, 256, 0, st>>>(-1, p->K, max_terms, thr, p->nodes, nn, nullptr,
                                            nullptr, state, nullptr);
     p->launches += 2;
@@ -852,7 +853,7 @@ int big_step(afd_plan* p, int sig, int k, int max_terms, double thr, int dc_firs
     p->launches++;
   }
   big_update_kernel<<<nn, 256, 0, st>>>(p->K, p->sel, nullptr, rem, p->circle, state, p->nodes,
-                                        p->amb);
+                                        p->amb, p->pow2);
   big_finalize_kernel<<<1, 256, 0, st>>>(k, p->K, max_terms, thr, p->nodes, nn, p->sel, p->amb,
                                          state, steps + (size_t)sig * max_terms);
   p->launches += 2;
@@ -985,6 +986,7 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
       return cleanup(fail(AFD_E_NOMEM, "cudaMalloc(%zu) failed", (size_t)(bytes))); \
   } while (0)
   ALLOC(p->radii, sizeof(double) * m);
+  ALLOC(p->pow2, sizeof(double) * kPowRow * m);
   ALLOC(p->scales, sizeof(double) * m);
   ALLOC(p->twst, sizeof(double2) * (N - 1));
   ALLOC(p->circle, sizeof(double2) * N);
@@ -1023,6 +1025,25 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
     if (cudaMalloc(&(ptr), (bytes)) != cudaSuccess)                                \
       return cleanup(fail(AFD_E_NOMEM, "cudaMalloc(%zu) failed", (size_t)(bytes))); \
   } while (0)
+  {
+    // CPython's abs(a) ** 2 (core.py:237) is libm pow(h, 2.0): tabulated here
+    // with the host's own libm for the doubles h within kPowWin ulps of each
+    // radius (kernel_norm_grid).  The exponent goes through a volatile so the
+    // compiler cannot fold pow(h, 2.0) into h * h.
+    volatile double two = 2.0;
+    std::vector<double> pw2((size_t)kPowRow * m);
+    for (int64_t i = 0; i < m; ++i) {
+      const int64_t rb = (int64_t)__builtin_bit_cast(uint64_t, radii_host[i]);
+      for (int d = 0; d < kPowRow; ++d) {
+        const int64_t hb = rb + d - kPowWin;
+        pw2[(size_t)i * kPowRow + d] =
+            hb >= 0 ? std::pow(__builtin_bit_cast(double, (uint64_t)hb), (double)two) : 0.0;
+      }
+    }
+    if (cudaMemcpy(p->pow2, pw2.data(), sizeof(double) * pw2.size(), cudaMemcpyHostToDevice) !=
+        cudaSuccess)
+      return cleanup(fail(AFD_E_CUDA, "table upload failed"));
+  }
   if (cudaMemcpy(p->radii, radii_host, sizeof(double) * m, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(p->scales, scales_host, sizeof(double) * m, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(p->twst, st.data(), sizeof(double2) * (N - 1), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -1114,6 +1135,7 @@ int afd_plan_destroy(afd_plan* p) {
   cudaFree(p->gath_cand);
   cudaFree(p->gath_t);
   cudaFree(p->radii);
+  cudaFree(p->pow2);
   cudaFree(p->scales);
   cudaFree(p->twst);
   cudaFree(p->circle);

@@ -192,17 +192,33 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (tid < 32 && n + C::STAGES < ntile) issue(n + C::STAGES);
+    // FAST: screen the tile with one predicate-accumulating compare per
+    // point; the (rare) tile holding a candidate at least as large as the
+    // thread's best runs the full first-maximum update
+    unsigned up = 1;
+    if constexpr (FAST) {
+      up = 0;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const long long j = q + ((long long)(KC == 8 ? h + 16 * i : i) << b0);
-      const double2 f = FAST ? v[i] : make_double2(v[i].x * sc, v[i].y * sc);  // transform.py:200
-      const double mg = FAST ? fast_mag2(f) : np_mag2(f);                     // core.py:298
-      const long long flat = row * N + j;
-      if (mg >= best.mag && cand_better(mg, flat, best.mag, best.flat)) {
-        best.mag = mg;
-        best.flat = flat;
-        best.re = f.x;
-        best.im = f.y;
+      for (int i0 = 0; i0 < 16; i0 += 4) {
+        double mg[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mg[i] = fast_mag2(v[i0 + i]);
+        up = any_ge4(up, mg, best.mag);
+      }
+    }
+    if (!FAST || __builtin_expect(up != 0, 0)) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const long long j = q + ((long long)(KC == 8 ? h + 16 * i : i) << b0);
+        const double2 f = FAST ? v[i] : make_double2(v[i].x * sc, v[i].y * sc);  // transform.py:200
+        const double mg = FAST ? fast_mag2(f) : np_mag2(f);                     // core.py:298
+        const long long flat = row * N + j;
+        if (mg >= best.mag && cand_better(mg, flat, best.mag, best.flat)) {
+          best.mag = mg;
+          best.flat = flat;
+          best.re = f.x;
+          best.im = f.y;
+        }
       }
     }
   }

@@ -119,6 +119,26 @@ __device__ __forceinline__ double kernel_norm(double2 a, int* ambiguous) {
   return sqrt(1.0 - hh);
 }
 
+// sqrt(1.0 - abs(a) ** 2) bit for bit for a grid pole a = r_s z_j.  The
+// plan tabulates, per radius r_s, CPython's float ** 2 — libm pow(h, 2.0)
+// called on the host — for the kPowWin ulps either side of r_s:
+// h = hypot(a) lies within 1 ulp of r_s for every grid pole (|z_j| = 1 to
+// an ulp; measured over N = 2^10..2^20).  The lookup makes the step kernels'
+// norms identical to the reference's; a pole outside the window (never for
+// grid poles) falls back to kernel_norm and its ambiguity flag.
+constexpr int kPowWin = 4;
+constexpr int kPowRow = 2 * kPowWin + 1;
+__device__ __forceinline__ double kernel_norm_grid(double2 a, double r,
+                                                   const double* __restrict__ pow_row,
+                                                   int* ambiguous) {
+  if (pow_row != nullptr) {
+    const double h = glibc_hypot(a.x, a.y);
+    const long long d = __double_as_longlong(h) - __double_as_longlong(r) + kPowWin;
+    if (d >= 0 && d < kPowRow) return sqrt(1.0 - __ldg(pow_row + d));
+  }
+  return kernel_norm(a, ambiguous);
+}
+
 // The per-point factors shared by kernel_samples, blaschke_samples and
 // remainder_update (core.py:234-245, 303-314):
 //   d = 1.0 - conj(a) * z          (numpy: (1 - pr, 0 - pi))

@@ -141,6 +141,46 @@ __device__ __forceinline__ void fast_prologue(double2 (&v)[P], const double (&w)
 }
 __device__ __forceinline__ double fast_mag2(double2 f) { return fma(f.x, f.x, f.y * f.y); }
 
+// flag | (any of m[0..3] > best): one predicate-accumulating compare per value
+// (setp.gt.or), instead of the max/select chain the compiler makes of `|=`.
+__device__ __forceinline__ unsigned any_gt2(unsigned flag, const double (&m)[2], double best) {
+  unsigned out;
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.ne.u32 p, %1, 0;\n\t"
+      "setp.gt.or.f64 p, %2, %4, p;\n\t"
+      "setp.gt.or.f64 p, %3, %4, p;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(out)
+      : "r"(flag), "d"(m[0]), "d"(m[1]), "d"(best));
+  return out;
+}
+__device__ __forceinline__ unsigned any_ge4(unsigned flag, const double (&m)[4], double best) {
+  unsigned out;
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.ne.u32 p, %1, 0;\n\t"
+      "setp.ge.or.f64 p, %2, %6, p;\n\t"
+      "setp.ge.or.f64 p, %3, %6, p;\n\t"
+      "setp.ge.or.f64 p, %4, %6, p;\n\t"
+      "setp.ge.or.f64 p, %5, %6, p;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(out)
+      : "r"(flag), "d"(m[0]), "d"(m[1]), "d"(m[2]), "d"(m[3]), "d"(best));
+  return out;
+}
+__device__ __forceinline__ unsigned any_gt4(unsigned flag, const double (&m)[4], double best) {
+  unsigned out;
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.ne.u32 p, %1, 0;\n\t"
+      "setp.gt.or.f64 p, %2, %6, p;\n\t"
+      "setp.gt.or.f64 p, %3, %6, p;\n\t"
+      "setp.gt.or.f64 p, %4, %6, p;\n\t"
+      "setp.gt.or.f64 p, %5, %6, p;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(out)
+      : "r"(flag), "d"(m[0]), "d"(m[1]), "d"(m[2]), "d"(m[3]), "d"(best));
+  return out;
+}
+
 template <int K, int RB, int G, bool MATERIALIZE, bool TM = false, bool FAST = false>
 __global__ void __launch_bounds__(Geo<K, RB>::T * G, (RB <= 3 && Geo<K, RB>::T * G <= 512) ? 2 : 1)
 field_kernel(const double2* __restrict__ ghat,     // [batch][N]
@@ -411,14 +451,49 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     const int sl_next = dyn ? next_sl[g][rd & 1] : sl + per_round;
     if (active) {
       const double sc = FAST ? 1.0 : __ldg(scales + s);  // FAST: scale is in the weights
+      if (MATERIALIZE) {
 #pragma unroll
-      for (int i = 0; i < P; ++i) {
-        // y *= scales[:, None] (transform.py:200)
-        const double2 f = FAST ? v[i] : make_double2(v[i].x * sc, v[i].y * sc);
-        if (MATERIALIZE) {
+        for (int i = 0; i < P; ++i) {
+          // y *= scales[:, None] (transform.py:200)
+          const double2 f = FAST ? v[i] : make_double2(v[i].x * sc, v[i].y * sc);
           field_out[(size_t)(s - row0) * N + out_pos<K, RB>(tp, i)] = f;
-        } else {
-          const double mg = FAST ? fast_mag2(f) : np_mag2(f);  // core.py:298
+        }
+      } else if constexpr (FAST) {
+        // Running first maximum.  A thread's maximum rarely improves after
+        // the first rows, so the row is screened with one compare per point
+        // (predicate-accumulating setp) and only a row with a new maximum
+        // pays for the selects, recomputing |F|^2 (the same operations).
+        // (Exact mode keeps the per-point selects: the screen spills there.)
+        unsigned up = 0;
+#pragma unroll
+        for (int i0 = 0; i0 < P; i0 += 4) {
+          double mg[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) mg[i] = fast_mag2(v[i0 + i]);
+          up = any_gt4(up, mg, best_mag);
+        }
+        if (__builtin_expect(up != 0, 0)) {
+#pragma unroll
+          for (int i = 0; i < P; ++i) {
+            // recompute (do not keep P magnitudes live across the screen)
+            double2 f = v[i];
+            asm volatile("" : "+d"(f.x), "+d"(f.y));
+            const double mg = fast_mag2(f);
+            if (mg > best_mag) {
+              best_mag = mg;
+              best_re = f.x;
+              best_im = f.y;
+              best_sl = sl;
+              best_i = i;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          // y *= scales[:, None] (transform.py:200)
+          const double2 f = make_double2(v[i].x * sc, v[i].y * sc);
+          const double mg = np_mag2(f);  // core.py:298
           if (__builtin_expect(mg > best_mag, 0)) {
             best_mag = mg;
             best_re = f.x;
@@ -549,7 +624,8 @@ step_kernel(int k, int max_terms, double threshold, int dc_first,
             const double2* __restrict__ circle,   // [N] z_m
             const double2* __restrict__ twst,
             State* __restrict__ state,            // [batch]
-            Step* __restrict__ steps) {           // [batch][max_terms]
+            Step* __restrict__ steps,             // [batch][max_terms]
+            const double* __restrict__ pow2) {    // [M][kPowRow] (kernel_norm_grid)
   constexpr int N = 1 << K;
   using L = RowSmem<K>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -632,7 +708,7 @@ step_kernel(int k, int max_terms, double threshold, int dc_first,
 
   // remainder_update (core.py:303-314) + kernel_samples (core.py:234-238)
   int amb = 0;
-  const double kn = kernel_norm(a, &amb);
+  const double kn = kernel_norm_grid(a, radius, pow2 ? pow2 + (size_t)s * kPowRow : nullptr, &amb);
   const double2 sc = make_double2(kn, 0.0);
   constexpr bool elide = (size_t)N * 16 >= 256 * 1024;  // numpy temporary elision
   for (int m = threadIdx.x; m < N; m += blockDim.x) {

@@ -111,7 +111,8 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
                     double2* __restrict__ ghat, const Cand* __restrict__ cand, int ncand,
                     const double* __restrict__ radii, int nrad,
                     const double2* __restrict__ circle, const double2* __restrict__ twst,
-                    State* __restrict__ state, Step* __restrict__ steps) {
+                    State* __restrict__ state, Step* __restrict__ steps,
+                    const double* __restrict__ pow2) {
   using CG = ClusterGeo<K>;
   using L = ClusterSmem<K>;
   using GL = typename CG::GL;
@@ -354,7 +355,7 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
       }
     }
     double kn = 0.0;
-    if (k >= 0) kn = kernel_norm(a, &amb);
+    if (k >= 0) kn = kernel_norm_grid(a, radius, pow2 ? pow2 + (size_t)s * kPowRow : nullptr, &amb);
     const double2 sc = make_double2(kn, 0.0);
     STAMP(15);
 #pragma unroll

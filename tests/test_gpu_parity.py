@@ -759,10 +759,13 @@ def test_fast_field_rows_close_to_reference(afd, tr, n):
         assert np.abs(got[row] - ref[row]).max() <= 1e-12 * scale, (n, row)
 
 
-# not "atom": after the exact one-atom recovery the residual is rounding
-# noise (~1e-31) and the next selection is decided by that noise alone
+# Not the tie-prone cases: "atom" (after the exact one-atom recovery the
+# residual is rounding noise, ~1e-31, and the next selection is decided by
+# that noise) and the paper's f1/f2 signals (real Taylor coefficients: the
+# field is conjugate-symmetric, so j and N - j tie up to the last bits and
+# only the bit-exact engine reproduces the reference's pick).
 @pytest.mark.parametrize("case", ["c0", "c1", "c3_s0", "c3_s1", "rand3", "rand11", "rand42",
-                                  "f1_thr", "const"])
+                                  "const"])
 def test_fast_decompose_matches_reference(afd, case):
     core, _ = afd
     g = load_golden("decomp_%s.npz" % case)
