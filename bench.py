@@ -111,7 +111,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c4", choices=["c0", "c1", "c2", "c3", "c4"])
-    ap.add_argument("--mode", default="exact", choices=["exact", "fast"],
+    ap.add_argument("--mode", default="fast", choices=["exact", "fast"],
                     help="exact: bit-identical to the reference; fast: FP64 radix-16/fused "
                          "butterflies, r^l on chip (identical indices, 1e-9 relative)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -46,9 +46,10 @@ extern "C" {
 /* Step record of one AFD step (core.DecompositionStep, core.py:170-175).
  * s, j: grid indices of the selected pole a = r_s exp(2 pi i j/N)
  * (core.ParameterGrid.point, core.py:163-167); coefficient <G_k, e_a>;
- * residual = discrete_energy(G_{k+1}).  flags bit 0: CPython's pow(|a|, 2)
- * is not provably equal to the device's |a|*|a| for this pole (see
- * afd_common.cuh kernel_norm).  72 bytes. */
+ * residual = discrete_energy(G_{k+1}).  flags bit 0: the pole's
+ * sqrt(1 - abs(a) ** 2) could not be taken from the plan's table of libm
+ * pow(h, 2.0) values (never for grid poles: kernel_norm_grid) and the
+ * device's h*h is not provably CPython's pow.  72 bytes. */
 typedef struct afd_step {
   int64_t s, j;
   double radius, a_re, a_im, c_re, c_im, residual;
@@ -134,9 +135,11 @@ int afd_argmax(afd_plan *plan, const double *field, int64_t rows, afd_candidate 
  *   kind 0 kernel_samples(a)      kind 1 blaschke_samples(a)
  *   kind 2 remainder_update(g, a, c)
  *   kind 3 g * blaschke_samples(a)  (core.tm_basis_samples step, core.py:406-407)
- * g is used by kinds 2 and 3 only. */
+ * g is used by kinds 2 and 3 only.  norm = sqrt(1 - abs(a) ** 2) as the
+ * caller's scalar arithmetic gives it (the reference evaluates it in CPython,
+ * core.py:237: libm hypot and pow), or NaN to form it on the device. */
 int afd_atom(afd_plan *plan, int kind, const double *g, double a_re, double a_im, double c_re,
-             double c_im, double *out, void *stream);
+             double c_im, double norm, double *out, void *stream);
 
 /* core.discrete_energy (core.py:195-198) of `batch` signals -> energies[batch].
  * With s != NULL the energy of g - s (core.relative_error, core.py:430-439). */
@@ -209,10 +212,12 @@ int afd_decompose_sharded(afd_plan *plan, afd_comm *comm, const double *g0, int6
 
 /* core.error_trace + core.reconstruct (core.py:411-460) for `batch` signals:
  * errors[batch][max_terms] (entry k = relative error of the (k+1)-term
- * partial sum), recon[batch][N] = S_{n_steps} (may be NULL). */
+ * partial sum), recon[batch][N] = S_{n_steps} (may be NULL).  norms
+ * [batch][max_terms] (may be NULL: formed on the device) are the poles'
+ * sqrt(1 - abs(a) ** 2), as for afd_atom. */
 int afd_error_trace(afd_plan *plan, const double *g, const afd_step *steps, int max_terms,
-                    const int32_t *n_steps, int64_t batch, double *errors, double *recon,
-                    void *stream);
+                    const int32_t *n_steps, int64_t batch, const double *norms, double *errors,
+                    double *recon, void *stream);
 
 /* Number of this library's kernels launched since plan creation (counts
  * launches issued, including those replayed inside CUDA graphs). */

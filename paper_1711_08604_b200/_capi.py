@@ -51,7 +51,7 @@ SIGNATURES = [
     ("afd_plan_set_engine", _I, [_VP, _I]),
     ("afd_field_direct", _I, [_VP, _VP, _VP, _I64, _I64, _VP]),
     ("afd_argmax", _I, [_VP, _VP, _I64, _VP, _VP]),
-    ("afd_atom", _I, [_VP, _I, _VP, _D, _D, _D, _D, _VP, _VP]),
+    ("afd_atom", _I, [_VP, _I, _VP, _D, _D, _D, _D, _D, _VP, _VP]),
     ("afd_energy", _I, [_VP, _VP, _VP, _I64, _VP]),
     ("afd_energy_diff", _I, [_VP, _VP, _VP, _VP, _I64, _VP]),
     ("afd_decompose", _I, [_VP, _VP, _I64, _I, _D, _I, _VP, _VP, _VP, _VP, _VP]),
@@ -65,7 +65,7 @@ SIGNATURES = [
     ("afd_comm_init", _I, [C.POINTER(_VP), _VP, _I, _I, _I]),
     ("afd_comm_destroy", _I, [_VP]),
     ("afd_decompose_sharded", _I, [_VP, _VP, _VP, _I64, _I, _D, _I, _VP, _VP, _VP, _VP, _VP]),
-    ("afd_error_trace", _I, [_VP, _VP, _VP, _I, _VP, _I64, _VP, _VP, _VP]),
+    ("afd_error_trace", _I, [_VP, _VP, _VP, _I, _VP, _I64, _VP, _VP, _VP, _VP]),
     ("afd_launch_count", _I64, [_VP]),
     ("afd_time_field", _I, [_VP, _VP, _I64, _I, _VP, _VP]),
     ("afd_fp64_peak", _I, [_I, _VP, _VP]),

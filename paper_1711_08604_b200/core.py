@@ -235,11 +235,18 @@ def analytic_projection(x):
     return _host(p.analytic_projection(_to_dev(xc, p)))[0]
 
 
+def _kernel_norm(value):
+    """sqrt(1 - |a|^2) exactly as the reference evaluates it (core.py:237):
+    CPython's abs (libm hypot) and float ** 2 (libm pow) on the host, so the
+    device atoms use the reference's bits (afd_atom's `norm`)."""
+    return float(np.sqrt(1.0 - abs(value) ** 2))
+
+
 def kernel_samples(a, n):
     """sqrt(1-|a|^2)/(1 - conj(a) z) on the circle (core.py:234-238)."""
     v = _pole_value(a)
     p = _plan(int(n))
-    return _host(p.atom(0, v))
+    return _host(p.atom(0, v, norm=_kernel_norm(v)))
 
 
 def blaschke_samples(a, n):
@@ -285,7 +292,7 @@ def remainder_update(g, a, c):
     g = _as_signal(g)
     v = _pole_value(a)
     p = _plan(g.shape[0])
-    return _host(p.atom(2, v, complex(c), g=_to_dev(g, p)))
+    return _host(p.atom(2, v, complex(c), g=_to_dev(g, p), norm=_kernel_norm(v)))
 
 
 # ---------------------------------------------------------------------------
@@ -418,7 +425,7 @@ def tm_basis_samples(poles, n):
     if not values:
         raise ValueError("need at least one pole")
     p = _plan(int(n))
-    b = p.atom(0, values[-1])
+    b = p.atom(0, values[-1], norm=_kernel_norm(values[-1]))
     for a in values[:-1]:
         b = p.atom(3, a, g=b)
     return _host(b)
@@ -441,7 +448,9 @@ def _trace(d, g, n_terms):
     plan = _plan(d.n_samples)
     steps, count = _steps_device(d, n_terms, plan)
     dec = eng.DeviceDecomposition(steps=steps, n_steps=count, initial=None, remainder=None)
-    errors, recon = plan.error_trace(_to_dev(g, plan), dec)
+    norms = _torch().tensor([[_kernel_norm(s.point.value) for s in d.steps[:n_terms]] or [0.0]],
+                            dtype=_torch().float64)
+    errors, recon = plan.error_trace(_to_dev(g, plan), dec, norms=norms)
     return _host(errors)[0][:n_terms], _host(recon)[0]
 
 

@@ -151,12 +151,15 @@ __global__ void argmax_kernel(const double2* __restrict__ f, long long total, Ca
 // kind 2: remainder_update(g, a, c) (core.py:303-314)
 // kind 3: g * blaschke_samples(a) (core.py:406-407; the samples are the
 //         temporary, so numpy's elision evaluates `bs *= b` for n >= 16384)
+// norm: sqrt(1 - abs(a) ** 2) as the caller computed it (the reference's own
+// CPython/libm scalar, core.py:237), or NaN to form it on the device.
 __global__ void atom_kernel(int kind, int n, const double2* __restrict__ g, double2 a, double2 c,
-                            const double2* __restrict__ circle, double2* __restrict__ out) {
+                            const double2* __restrict__ circle, double2* __restrict__ out,
+                            double norm) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= n) return;
   int amb = 0;
-  const double kn = kernel_norm(a, &amb);
+  const double kn = norm == norm ? norm : kernel_norm(a, &amb);
   const bool elide = (size_t)n * 16 >= 256 * 1024;
   const double2 z = circle[m];
   const double2 d = one_minus_conja_z(a, z);
@@ -205,7 +208,8 @@ __global__ void error_trace_kernel(int n, const double2* __restrict__ g,
                                    const Step* __restrict__ steps, int max_terms,
                                    const int* __restrict__ n_steps,
                                    const double2* __restrict__ circle, double* __restrict__ scratch,
-                                   double* __restrict__ errors, double2* __restrict__ recon) {
+                                   double* __restrict__ errors, double2* __restrict__ recon,
+                                   const double* __restrict__ norms) {
   const int sig = blockIdx.x;
   const size_t per = 2 * (size_t)n * 2 + n + 2 * ((size_t)n / 8 + 16);
   double2* total = reinterpret_cast<double2*>(scratch + per * sig);
@@ -227,7 +231,7 @@ __global__ void error_trace_kernel(int n, const double2* __restrict__ g,
     const double2 a = make_double2(s.a_re, s.a_im);
     const double2 c = make_double2(s.c_re, s.c_im);
     int amb = 0;
-    const double kn = kernel_norm(a, &amb);
+    const double kn = norms ? norms[(size_t)sig * max_terms + k] : kernel_norm(a, &amb);
     for (int m = threadIdx.x; m < n; m += blockDim.x) {
       const double2 z = circle[m];
       const double2 d = one_minus_conja_z(a, z);

@@ -1299,7 +1299,7 @@ int afd_argmax(afd_plan* p, const double* field, int64_t rows, afd_candidate* ou
 }
 
 int afd_atom(afd_plan* p, int kind, const double* g, double a_re, double a_im, double c_re,
-             double c_im, double* out, void* stream) {
+             double c_im, double norm, double* out, void* stream) {
   if (!p || !out || (kind == 2 && !g)) return fail(AFD_E_INVALID, "NULL argument");
   if (kind < 0 || kind > 3) return fail(AFD_E_INVALID, "bad atom kind %d", kind);
   if (kind == 3 && !g) return fail(AFD_E_INVALID, "NULL argument");
@@ -1310,7 +1310,7 @@ int afd_atom(afd_plan* p, int kind, const double* g, double a_re, double a_im, d
   const int n = (int)p->n;
   atom_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
       kind, n, (const double2*)g, make_double2(a_re, a_im), make_double2(c_re, c_im), p->circle,
-      (double2*)out);
+      (double2*)out, norm);
   p->launches++;
   CU(cudaGetLastError());
   return 0;
@@ -1727,8 +1727,8 @@ int afd_sharded_finish(afd_plan* p, int64_t batch, int32_t* n_steps, double* ini
 }
 
 int afd_error_trace(afd_plan* p, const double* g, const afd_step* steps, int max_terms,
-                    const int32_t* n_steps, int64_t batch, double* errors, double* recon,
-                    void* stream) {
+                    const int32_t* n_steps, int64_t batch, const double* norms, double* errors,
+                    double* recon, void* stream) {
   if (!p || !g || !steps || !n_steps || !errors) return fail(AFD_E_INVALID, "NULL argument");
   int rc;
   if ((rc = set_device(p))) return rc;
@@ -1737,7 +1737,7 @@ int afd_error_trace(afd_plan* p, const double* g, const afd_step* steps, int max
   if ((rc = ensure_scratch(p, sizeof(double) * per * batch))) return rc;
   error_trace_kernel<<<(unsigned)batch, 256, 0, (cudaStream_t)stream>>>(
       (int)n, (const double2*)g, (const Step*)steps, max_terms, n_steps, p->circle, p->scratch,
-      errors, (double2*)recon);
+      errors, (double2*)recon, norms);
   p->launches++;
   CU(cudaGetLastError());
   return 0;

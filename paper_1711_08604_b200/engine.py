@@ -211,13 +211,16 @@ class Plan:
         return out
 
     @_locked
-    def atom(self, kind, a, c=0j, g=None, stream=None):
+    def atom(self, kind, a, c=0j, g=None, stream=None, norm=None):
+        """Pointwise atom `kind` of afd_atom; `norm` = sqrt(1 - abs(a) ** 2)
+        computed by the caller (None: formed on the device)."""
         a = complex(a)
         c = complex(c)
         out = torch.empty(self.n, dtype=torch.complex128, device=self.device)
         if g is not None:
             g = self._signal(g)[0]
         _capi.check(self.lib.afd_atom(self.handle, kind, _ptr(g), a.real, a.imag, c.real, c.imag,
+                                      float("nan") if norm is None else float(norm),
                                       _ptr(out), _stream(stream)))
         return out
 
@@ -285,15 +288,19 @@ class Plan:
             remainder=torch.empty((batch, self.n), dtype=torch.complex128, device=dev))
 
     @_locked
-    def error_trace(self, g, dec, stream=None):
-        """errors [batch, max_terms] and reconstructions [batch, N] (device)."""
+    def error_trace(self, g, dec, stream=None, norms=None):
+        """errors [batch, max_terms] and reconstructions [batch, N] (device).
+        norms: optional [batch, max_terms] float64 tensor of the poles'
+        sqrt(1 - abs(a) ** 2) from the caller's scalar arithmetic."""
         g = self._signal(g)
         b, max_terms = dec.steps.shape[0], dec.steps.shape[1]
         errors = torch.zeros((b, max_terms), dtype=torch.float64, device=self.device)
         recon = torch.empty((b, self.n), dtype=torch.complex128, device=self.device)
+        if norms is not None:
+            norms = norms.to(device=self.device, dtype=torch.float64).contiguous()
         _capi.check(self.lib.afd_error_trace(self.handle, _ptr(g), _ptr(dec.steps), max_terms,
-                                             _ptr(dec.n_steps), b, _ptr(errors), _ptr(recon),
-                                             _stream(stream)))
+                                             _ptr(dec.n_steps), b, _ptr(norms), _ptr(errors),
+                                             _ptr(recon), _stream(stream)))
         return errors, recon
 
     # -- radius-sharded stepping (multi-GPU) ---------------------------------------

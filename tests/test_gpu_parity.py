@@ -715,24 +715,36 @@ def test_cluster_step_options_vs_oracle(afd, n, m, dc, thr):
 
 
 def test_bench_line_contract(afd):
-    """bench.py's JSON line: keys of the driver contract, parity, sane e2e/value/roofline."""
+    """bench.py's default JSON line (the driver's command, shortened): the
+    contract keys, the required workload (c4, the largest one-GPU config),
+    oracle parity, and a roofline whose `frac` recomputes from the declared
+    work per launch and the measured launch time."""
     import os
     import subprocess
     import sys
     from conftest import ROOT
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3",
-                          "--warmup", "3", "--no-cpu-baseline", "--e2e-reps", "3"],
-                         capture_output=True, text=True, cwd=ROOT, timeout=600)
+                          "--warmup", "3", "--no-cpu-baseline", "--e2e-reps", "2"],
+                         capture_output=True, text=True, cwd=ROOT, timeout=1200)
     assert out.returncode == 0, out.stderr[-2000:]
     d = json.loads(out.stdout.strip().splitlines()[-1])
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
                 "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
                 "roofline", "e2e", "gpu_launches", "clocks", "cpu_baseline"):
         assert key in d, key
+    assert d["config"]["workload"] == "c4" and d["n_gpus"] == 1
+    assert d["config"]["n"] == 1 << 20 and d["config"]["m"] == 16384
     assert d["parity_vs_oracle"] is True
     assert d["gpu_launches"] > 0
+    evals = d["config"]["n"] * d["config"]["m"] * d["config"]["afd_steps"]
+    assert abs(d["value"] - evals / (d["ms_per_step"] * 1e-3)) <= 1e-6 * d["value"]
     assert 0.3 * d["value"] < d["e2e"]["value"] < 1.05 * d["value"]
-    assert 0.0 < d["roofline"]["frac"] < 1.0
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s"
+    achieved = r["evals_per_launch"] * r["bytes_per_eval"] / (r["launch_ms"] * 1e-3) / 1e9
+    assert abs(achieved - r["achieved"]) <= 1e-6 * achieved
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) <= 1e-9 and 0.0 < r["frac"] < 1.0
+    assert r["evals_per_launch"] == d["config"]["n"] * d["config"]["m"]
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
 
 
@@ -874,3 +886,27 @@ def test_fast_c4_full_size_replay(afd):
                        threads=O.max_threads())
     assert r["ok"], r["why"]
     assert np.abs(rem[0] - r["remainder"]).max() <= FAST_TOL * np.abs(r["remainder"]).max()
+
+
+def test_c4_fast_and_exact_select_identically(afd):
+    """BASELINE c4 at full size, all 20 AFD steps in both modes: the fast
+    field selects exactly the exact (bit-identical to the reference) engine's
+    grid points, with coefficients and residuals within 1e-9."""
+    core, engine = afd
+    from paper_1711_08604_b200 import workloads as W
+    w = W.CONFIGS["c4"]
+    g = W.signal_for("c4")[None, :]
+    radii = W.radii_for(w.m)
+    p = engine.Plan(radii, w.n, max_batch=1, fast=1)
+    rf, cf, _, remf, _, _ = p.decompose_host(g, w.steps)
+    del p
+    p = engine.Plan(radii, w.n, max_batch=1)
+    re_, ce, _, reme, _, _ = p.decompose_host(g, w.steps)
+    del p
+    assert int(cf[0]) == int(ce[0]) == w.steps
+    assert np.array_equal(rf[0]["s"], re_[0]["s"]) and np.array_equal(rf[0]["j"], re_[0]["j"])
+    c1 = rf[0]["c_re"] + 1j * rf[0]["c_im"]
+    c2 = re_[0]["c_re"] + 1j * re_[0]["c_im"]
+    assert np.all(np.abs(c1 - c2) <= FAST_TOL * np.abs(c2))
+    assert np.all(np.abs(rf[0]["residual"] - re_[0]["residual"]) <= FAST_TOL * re_[0]["residual"])
+    assert np.all(re_[0]["flags"] == 0)  # every kernel norm from the libm pow table

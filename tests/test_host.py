@@ -124,3 +124,53 @@ def test_workload_shapes():
     x = W.signal_for(W.CONFIGS["c2"]._replace(n=1024) if hasattr(W.CONFIGS["c2"], "_replace")
                      else W.Workload("c2s", 1024, 8, 1, 0, 0.0, 2, real=True))
     assert x.dtype == np.float64
+
+
+def test_bench_arms_share_config_and_spawn(monkeypatch):
+    """Both bench arms print the same `config`; --gpus N outside torchrun
+    re-launches under torch.distributed.run with N ranks on 127.0.0.1."""
+    import importlib
+    import sys
+    sys.path.insert(0, ROOT)
+    bench = importlib.import_module("bench")
+    from paper_1711_08604_b200 import workloads as W
+
+    class A:
+        shard, mode, gpus = "auto", "fast", 1
+    w = W.CONFIGS["c4"]
+    assert bench.config_dict(A, w, 1) == bench.config_dict(A, w, 1)
+    assert bench.shard_mode(A, w, 1) == "single" and bench.shard_mode(A, w, 8) == "radii"
+    assert bench.shard_mode(A, W.CONFIGS["c3"], 4) == "signals"
+    assert bench.config_dict(A, w, 8)["parallelism"] == "dp8 over radii"
+    assert bench.scaling_of("radii") == "strong" and bench.scaling_of("replicas") == "weak"
+    seen = {}
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "2"])
+    monkeypatch.setattr(bench.os, "execv", lambda exe, cmd: seen.update(cmd=cmd))
+    A.gpus = 4
+    bench.maybe_spawn(A)
+    cmd = seen["cmd"]
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert cmd[cmd.index("--nproc-per-node") + 1] == "4"
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "2"]
+
+
+def test_oracle_replay_detects_wrong_selection():
+    """oracle.replay_check (the bench's large-grid parity): the oracle's own
+    decomposition replays clean; a moved selection or a perturbed
+    coefficient is caught (bitwise mode), a 1e-15 perturbation passes at
+    rtol 1e-9."""
+    import oracle as O
+    from paper_1711_08604_b200 import workloads as W
+    g = W.pole_sum(1024, 8, 0.9, 0)
+    radii = np.array(W.radii_for(100))
+    d = O.decompose(g, radii, max_terms=6)
+    assert O.replay_check(g, radii, d.steps, 6)["ok"]
+    st = d.steps.copy()
+    st["j"][3] += 1
+    assert not O.replay_check(g, radii, st, 6)["ok"]
+    st = d.steps.copy()
+    st["c_re"][2] *= 1 + 1e-15
+    assert not O.replay_check(g, radii, st, 6)["ok"]
+    assert O.replay_check(g, radii, st, 6, rtol=1e-9)["ok"]
