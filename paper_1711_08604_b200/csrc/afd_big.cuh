@@ -250,7 +250,8 @@ __global__ void __launch_bounds__(Geo<12, 4>::T * kBigGroups, 1)
 big_field_a(int K, const double* __restrict__ pw_rev, long long pw_row0,
             const double2* __restrict__ ghat_rev, const double2* __restrict__ twst,
             long long row0, long long row1, double2* __restrict__ Y,
-            const int* __restrict__ stopped, const int* __restrict__ pw_len) {
+            const int* __restrict__ stopped, const int* __restrict__ pw_len,
+            int direct_out) {
   constexpr int KA = 12;
   using GA = Geo<KA, 4>;
   using TwA = SmemTw<KA, 4>;
@@ -384,6 +385,14 @@ big_field_a(int K, const double* __restrict__ pw_rev, long long pw_row0,
       fft_passes<KA, true, 4>(v, tid, true, buf, tw, sync, hook);
       bulk_pending = false;
       double2* __restrict__ y = Y + (size_t)rl * N + base;
+      if (direct_out) {
+        // straight from registers (lanes hold consecutive positions: every
+        // store is a coalesced 512-B warp write), no shared-memory staging
+#pragma unroll
+        for (int i = 0; i < P; ++i) __stcs(y + out_pos<KA, 4>(tid, i), v[i]);
+        first = false;
+        continue;
+      }
 #pragma unroll
       for (int i = 0; i < P; ++i) buf[out_pos<KA, 4>(tid, i)] = v[i];
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -651,6 +651,10 @@ int big_setup(afd_plan* p) {
 // AFD_FIELD_A=0 keeps big_pass_a's item order (experiments).
 static const bool kFieldAEnabled = !(getenv("AFD_FIELD_A") && atoi(getenv("AFD_FIELD_A")) == 0);
 
+// Field pass A writes its blocks straight from registers (1) or stages them
+// in shared memory for one TMA bulk store (0); AFD_PASSA_DIRECT selects.
+static const int kPassADirect = getenv("AFD_PASSA_DIRECT") ? atoi(getenv("AFD_PASSA_DIRECT")) : 0;
+
 // Pass A over rows [r0, r0+rows) (mode 0: field prologue) or one signal (mode 1).
 int big_launch_a(afd_plan* p, bool inv, int mode, const double2* ghat_rev, const double2* x,
                  int64_t r0, int64_t rows, const int* stopped, cudaStream_t st) {
@@ -663,10 +667,12 @@ int big_launch_a(afd_plan* p, bool inv, int mode, const double2* ghat_rev, const
       // fast field: weights from the factor tables, (c, t) twiddles
       if (KA != 12) return fail(AFD_E_UNSUPPORTED, "fast pass A needs 4096-point blocks");
       big_field_a<true><<<grid, block, big_a_smem_g<KA>(), st>>>(
-          p->K, p->fw, p->m0, ghat_rev, p->twct, r0, r0 + rows, p->Y, stopped, nullptr);
+          p->K, p->fw, p->m0, ghat_rev, p->twct, r0, r0 + rows, p->Y, stopped, nullptr,
+          kPassADirect);
     } else if (inv && mode == 0 && KA == 12 && field_tmem_enabled() && kFieldAEnabled)
       big_field_a<false><<<grid, block, big_a_smem_g<KA>(), st>>>(
-          p->K, p->pw, p->m0, ghat_rev, p->twst, r0, r0 + rows, p->Y, stopped, p->pw_len);
+          p->K, p->pw, p->m0, ghat_rev, p->twst, r0, r0 + rows, p->Y, stopped, p->pw_len,
+          kPassADirect);
     else if (inv && mode == 0 && KA == 12 && field_tmem_enabled())
       big_pass_a<KA, true, KA == 12><<<grid, block, big_a_smem_g<KA>(), st>>>(
           p->K, mode, p->pw, p->m0, ghat_rev, x, p->twst, r0, r0 + rows, p->Y, stopped,

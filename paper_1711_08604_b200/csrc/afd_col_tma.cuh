@@ -36,9 +36,13 @@ struct ColTma {
   static constexpr int U = 1 << KC;                    // positions per column
   static constexpr int TILE = COLS * U;                // double2 per tile (4096)
   static constexpr int STAGES = 2;
-  static constexpr int TWA = 15 * COLS;                // stage b0..b0+3 twiddles [slot][c]
-  static constexpr int TWB = KC == 8 ? 15 * 256 : 0;   // stage b0+4.. [slot][h][c]
-  static constexpr size_t SMEM = sizeof(double2) * (STAGES * TILE + TWA + TWB);
+  // twiddles live in tensor memory, per thread: 15 slots per 4-stage group
+  // (slot 2^e - 1 + kk), 4 words each; one column set per pair of warps
+  // sharing a lane quadrant
+  static constexpr int NSLOT = KC == 8 ? 30 : 15;
+  static constexpr int SET_COLS = 4 * NSLOT;                       // 120 / 60
+  static constexpr unsigned TM_COLS = KC == 8 ? 256 : 128;         // >= 2 sets, power of 2
+  static constexpr size_t SMEM = sizeof(double2) * (STAGES * TILE);
 };
 
 __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, unsigned bytes,
@@ -53,6 +57,30 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, unsig
 
 // FAST (AFD_PLAN_FAST): twst is the (c, t) table (already conjugated), the
 // butterflies are bfly_ct and the scale is already in pass A's weights.
+// Four radix-2 stages on the thread's 16 registers (stage e pairs bit e)
+// with the twiddles of slots SLOT0 + 2^e - 1 + kk from tensor memory: one
+// tcgen05.ld per stage (a separate data path from the shared-memory traffic
+// of the tile and the transpose).
+template <bool FAST, int SLOT0, int E = 0>
+__device__ __forceinline__ void col_stages4(double2 (&v)[16], uint32_t twm) {
+  if constexpr (E < 4) {
+    uint32_t r[4 << E];
+    tm_ld<(4 << E)>(twm + 4 * (SLOT0 + (1 << E) - 1), r);
+    tm_wait_ld();
+#pragma unroll
+    for (int kk = 0; kk < (1 << E); ++kk) {
+      const double2 w = make_double2(__hiloint2double(r[4 * kk + 1], r[4 * kk]),
+                                     __hiloint2double(r[4 * kk + 3], r[4 * kk + 2]));
+#pragma unroll
+      for (int hh = 0; hh < (16 >> (E + 1)); ++hh) {
+        const int i = kk | (hh << (E + 1));
+        bfly_any<FAST>(v[i], v[i | (1 << E)], w);
+      }
+    }
+    col_stages4<FAST, SLOT0, E + 1>(v, twm);
+  }
+}
+
 template <int KC, bool FAST = false>
 __global__ void __launch_bounds__(256, 1)
 col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __restrict__ twst,
@@ -64,8 +92,7 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
   extern __shared__ __align__(128) double2 csm[];
   __shared__ __align__(8) unsigned long long full[C::STAGES];
   if (stopped && *stopped) return;
-  double2* tw_a = csm + C::STAGES * TILE;
-  double2* tw_b = tw_a + C::TWA;
+  __shared__ uint32_t tm_base_s;
   const long long N = 1LL << K;
   const int rows = (int)(row1 - row0);
   const int chunks = (1 << b0) / COLS;
@@ -79,7 +106,19 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
   if (tid == 0) {
     for (int s = 0; s < C::STAGES; ++s) mbar_init(&full[s], 1);
   }
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&tm_base_s)),
+                 "r"(C::TM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // this thread's twiddle cells: its lane of the warp's quadrant, its set
+  const uint32_t twm = tm_base_s + ((uint32_t)(((tid >> 5) & 3) * 32) << 16) +
+                       (uint32_t)((tid >> 7) * C::SET_COLS);
   // warp 0 issues the copies of local tile n into stage n % STAGES
   auto issue = [&](int n) {
     const long long t = t0 + n;
@@ -124,27 +163,32 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
     const long long row = row0 + rl;
     const int q0 = chunk * COLS;
     if (chunk != tw_chunk) {
-      // stage twiddles of this chunk's columns, conjugated (transform.py:199):
-      // S_b[q + (k << b0)] for stage b = b0 + e
-      __syncthreads();  // previous chunk's twiddles no longer read
-      for (int x = tid; x < C::TWA; x += blockDim.x) {
-        const int slot = x / COLS, cc = x % COLS;  // slot = 2^e - 1 + kk
-        const int e = 31 - __clz(slot + 1), kk = slot + 1 - (1 << e);
-        double2 w = __ldg(twst + ((1LL << (b0 + e)) - 1) + q0 + cc + ((long long)kk << b0));
-        if (!FAST) w.y = -w.y;
-        tw_a[x] = w;
-      }
-      if constexpr (KC == 8) {
-        for (int x = tid; x < C::TWB; x += blockDim.x) {
-          const int slot = x / 256, hc = x % 256, hh = hc / 16, cc = hc % 16;
-          const int ib = 31 - __clz(slot + 1), kk = slot + 1 - (1 << ib);
-          double2 w = __ldg(twst + ((1LL << (b0 + 4 + ib)) - 1) + q0 + cc +
-                            ((long long)(hh + 16 * kk) << b0));
+      // this thread's stage twiddles for the chunk's column q0 + c, straight
+      // from the stage tables into its tensor-memory cells (no other thread
+      // reads them: no barrier), conjugated (transform.py:199) unless FAST
+      // (already the (c, t) form): S_b[q + (k << b0)], b = b0 + e
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+#pragma unroll
+        for (int kk = 0; kk < (1 << e); ++kk) {
+          double2 w = __ldg(twst + ((1LL << (b0 + e)) - 1) + q0 + c + ((long long)kk << b0));
           if (!FAST) w.y = -w.y;
-          tw_b[x] = w;
+          tm_st4(twm + 4 * ((1 << e) - 1 + kk), w);
         }
       }
-      __syncthreads();
+      if constexpr (KC == 8) {
+#pragma unroll
+        for (int ib = 0; ib < 4; ++ib) {
+#pragma unroll
+          for (int kk = 0; kk < (1 << ib); ++kk) {
+            double2 w = __ldg(twst + ((1LL << (b0 + 4 + ib)) - 1) + q0 + c +
+                              ((long long)(h + 16 * kk) << b0));
+            if (!FAST) w.y = -w.y;
+            tm_st4(twm + 4 * (15 + (1 << ib) - 1 + kk), w);
+          }
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tw_chunk = chunk;
     }
     const int s = n % C::STAGES;
@@ -155,36 +199,14 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
     double2 v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = tile[(16 * h + i) * COLS + c];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-#pragma unroll
-      for (int kk = 0; kk < (1 << e); ++kk) {
-        const double2 w = tw_a[((1 << e) - 1 + kk) * COLS + c];
-#pragma unroll
-        for (int hh = 0; hh < (16 >> (e + 1)); ++hh) {
-          const int i = kk | (hh << (e + 1));
-          bfly_any<FAST>(v[i], v[i | (1 << e)], w);
-        }
-      }
-    }
+    col_stages4<FAST, 0>(v, twm);
     if constexpr (KC == 8) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) tile[(16 * h + i) * COLS + c] = v[i];
       __syncthreads();
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = tile[(h + 16 * i) * COLS + c];
-#pragma unroll
-      for (int ib = 0; ib < 4; ++ib) {
-#pragma unroll
-        for (int kk = 0; kk < (1 << ib); ++kk) {
-          const double2 w = tw_b[((1 << ib) - 1 + kk) * 256 + h * 16 + c];
-#pragma unroll
-          for (int hh = 0; hh < (16 >> (ib + 1)); ++hh) {
-            const int i = kk | (hh << (ib + 1));
-            bfly_any<FAST>(v[i], v[i | (1 << ib)], w);
-          }
-        }
-      }
+      col_stages4<FAST, 15>(v, twm);
     }
     // this tile's stage is free once every thread has read it: refill it
     // with tile n + STAGES (generic-proxy writes above precede the async
@@ -222,6 +244,12 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
       }
     }
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (tid < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_base_s),
+                 "r"(C::TM_COLS)
+                 : "memory");
   // merge this CTA's first maximum into its slot (slots persist over the
   // row batches of one step; the (mag, flat) order makes merging order-free)
   __shared__ Cand red[8];
