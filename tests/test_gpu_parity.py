@@ -910,3 +910,43 @@ def test_c4_fast_and_exact_select_identically(afd):
     assert np.all(np.abs(c1 - c2) <= FAST_TOL * np.abs(c2))
     assert np.all(np.abs(rf[0]["residual"] - re_[0]["residual"]) <= FAST_TOL * re_[0]["residual"])
     assert np.all(re_[0]["flags"] == 0)  # every kernel norm from the libm pow table
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_c2_all_steps_replayed_by_oracle(afd, mode):
+    """BASELINE c2 in full (N = 2^16, M = 4096, 50 AFD steps, projected real
+    input): every step replayed by the oracle (selected row's first maximum,
+    neighbouring and sampled rows, coefficient and residual) — bitwise for
+    the exact engine, 1e-9 for the fast one."""
+    core, engine = afd
+    from paper_1711_08604_b200 import workloads as W
+    w = W.CONFIGS["c2"]
+    g = O.analytic_projection(W.signal_for("c2"))
+    radii = np.array(W.radii_for(w.m))
+    plan = engine.Plan(tuple(radii), w.n, max_batch=1, fast=int(mode == "fast"))
+    rec, counts, _, rem, _, _ = plan.decompose_host(g[None, :], w.steps)
+    del plan
+    assert int(counts[0]) == w.steps
+    tol = 0.0 if mode == "exact" else FAST_TOL
+    r = O.replay_check(g, radii, rec[0], w.steps, rows_per_step=4, rtol=tol,
+                       threads=O.max_threads())
+    assert r["ok"], r["why"]
+    if mode == "exact":
+        assert np.array_equal(rem[0], r["remainder"])
+        assert np.all(rec[0]["flags"] == 0)
+
+
+def test_c4_exact_all_steps_replayed_by_oracle(afd):
+    """BASELINE c4 in full, exact engine, all 20 AFD steps replayed bitwise."""
+    core, engine = afd
+    from paper_1711_08604_b200 import workloads as W
+    w = W.CONFIGS["c4"]
+    g = W.signal_for("c4")
+    radii = np.array(W.radii_for(w.m))
+    plan = engine.Plan(tuple(radii), w.n, max_batch=1)
+    rec, counts, _, rem, _, _ = plan.decompose_host(g[None, :], w.steps)
+    del plan
+    assert int(counts[0]) == w.steps
+    r = O.replay_check(g, radii, rec[0], w.steps, rows_per_step=3, threads=O.max_threads())
+    assert r["ok"], r["why"]
+    assert np.array_equal(rem[0], r["remainder"])
