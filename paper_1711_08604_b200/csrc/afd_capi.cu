@@ -643,6 +643,14 @@ int big_setup(afd_plan* p) {
     }
     CU(cudaFuncSetAttribute(col_tma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)ColTma<8>::SMEM));
+    CU(cudaFuncSetAttribute(col_tma_kernel<8, true, 2>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ColTma<8, 2>::SMEM));
+    CU(cudaFuncSetAttribute(col_tma_kernel<8, false, 2>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ColTma<8, 2>::SMEM));
+    CU(cudaFuncSetAttribute(col_tma_kernel<4, true, 2>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ColTma<4, 2>::SMEM));
+    CU(cudaFuncSetAttribute(col_tma_kernel<4, false, 2>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ColTma<4, 2>::SMEM));
     return 0;
   });
 }
@@ -697,6 +705,10 @@ static const bool kCol8Enabled = !(getenv("AFD_COL8") && atoi(getenv("AFD_COL8")
 // (afd_col_tma.cuh); AFD_COL_TMA=0 keeps the one-tile-per-CTA kernels.
 static const bool kColTmaEnabled = !(getenv("AFD_COL_TMA") && atoi(getenv("AFD_COL_TMA")) == 0);
 
+// Thread groups of the TMA column pass (ColTma): 2 = two 256-thread groups
+// on a three-stage ring; AFD_COL_GROUPS selects (experiments).
+static const int kColGroups = getenv("AFD_COL_GROUPS") ? atoi(getenv("AFD_COL_GROUPS")) : 2;
+
 int big_launch_cols(afd_plan* p, bool inv, int last_mode, int scale_n, int64_t r0, int64_t rows,
                     double2* fout, const int* stopped, cudaStream_t st) {
   dim3 grid((unsigned)big_col_ctas(p), (unsigned)rows);
@@ -709,15 +721,26 @@ int big_launch_cols(afd_plan* p, bool inv, int last_mode, int scale_n, int64_t r
         (left == 4 || (left == 8 && kCol8Enabled && p->ymap_ok))) {
       const int64_t tiles = rows * ((int64_t)1 << b0) / (left == 8 ? 16 : 256);
       const unsigned g = (unsigned)std::min<int64_t>(p->sms, tiles);
-      auto k8 = fastf ? col_tma_kernel<8, true> : col_tma_kernel<8>;
-      auto k4 = fastf ? col_tma_kernel<4, true> : col_tma_kernel<4>;
       const double2* tws = fastf ? p->twct : p->twst;
-      if (left == 8)
-        k8<<<g, 256, ColTma<8>::SMEM, st>>>(p->K, b0, p->Y, tws, p->scales, r0, r0 + rows,
-                                            p->big_cand, stopped, p->ymap);
-      else
-        k4<<<g, 256, ColTma<4>::SMEM, st>>>(p->K, b0, p->Y, tws, p->scales, r0, r0 + rows,
-                                            p->big_cand, stopped, p->ymap);
+      if (kColGroups == 2) {
+        auto k8 = fastf ? col_tma_kernel<8, true, 2> : col_tma_kernel<8, false, 2>;
+        auto k4 = fastf ? col_tma_kernel<4, true, 2> : col_tma_kernel<4, false, 2>;
+        if (left == 8)
+          k8<<<g, 512, ColTma<8, 2>::SMEM, st>>>(p->K, b0, p->Y, tws, p->scales, r0, r0 + rows,
+                                                 p->big_cand, stopped, p->ymap);
+        else
+          k4<<<g, 512, ColTma<4, 2>::SMEM, st>>>(p->K, b0, p->Y, tws, p->scales, r0, r0 + rows,
+                                                 p->big_cand, stopped, p->ymap);
+      } else {
+        auto k8 = fastf ? col_tma_kernel<8, true> : col_tma_kernel<8>;
+        auto k4 = fastf ? col_tma_kernel<4, true> : col_tma_kernel<4>;
+        if (left == 8)
+          k8<<<g, 256, ColTma<8>::SMEM, st>>>(p->K, b0, p->Y, tws, p->scales, r0, r0 + rows,
+                                              p->big_cand, stopped, p->ymap);
+        else
+          k4<<<g, 256, ColTma<4>::SMEM, st>>>(p->K, b0, p->Y, tws, p->scales, r0, r0 + rows,
+                                              p->big_cand, stopped, p->ymap);
+      }
       p->launches++;
       CU(cudaGetLastError());
       break;
@@ -795,6 +818,10 @@ int big_reduce_cands(afd_plan* p, cudaStream_t st, const Cand** parts, int* npar
   return 0;
 }
 
+// Timing experiments only (wrong results): AFD_BIG_SKIP=1 skips pass A of
+// the field, 2 its column pass.
+static const int kBigSkip = getenv("AFD_BIG_SKIP") ? atoi(getenv("AFD_BIG_SKIP")) : 0;
+
 // Field rows [r0, r1) of one spectrum: argmax into big_cand (fout == null,
 // slots initialised here) or materialised rows into fout.
 int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, double2* fout,
@@ -807,7 +834,10 @@ int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, doub
   }
   for (int64_t b = r0; b < r1; b += p->big_rows) {
     const int64_t rows = std::min<int64_t>(p->big_rows, r1 - b);
-    if ((rc = big_launch_a(p, true, 0, ghat_rev, nullptr, b, rows, stopped, st))) return rc;
+    if (!(kBigSkip & 1) &&
+        (rc = big_launch_a(p, true, 0, ghat_rev, nullptr, b, rows, stopped, st)))
+      return rc;
+    if (kBigSkip & 2) continue;
     if ((rc = big_launch_cols(p, true, fout ? 2 : 1, 0, b, rows,
                               fout ? fout + (size_t)(b - r0) * p->n : nullptr, stopped, st)))
       return rc;

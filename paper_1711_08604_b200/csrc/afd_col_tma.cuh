@@ -30,18 +30,25 @@
 
 namespace afd {
 
-template <int KC>
+// GROUPS = 2: two 256-thread groups per CTA take alternate tiles from a
+// ring of three stages (tile n: group n & 1, stage n % 3), so 16 warps
+// compute while a tile is in flight.  The one-group form keeps 8 warps per
+// SM, and its column stages were latency-bound (FP64 pipe ~42% busy, 2
+// warps per scheduler) rather than HBM-bound.
+template <int KC, int GROUPS = 1>
 struct ColTma {
   static constexpr int COLS = KC == 8 ? 16 : 256;     // columns per tile
   static constexpr int U = 1 << KC;                    // positions per column
   static constexpr int TILE = COLS * U;                // double2 per tile (4096)
-  static constexpr int STAGES = 2;
+  static constexpr int STAGES = GROUPS == 2 ? 3 : 2;
+  static constexpr int THREADS = 256 * GROUPS;
   // twiddles live in tensor memory, per thread: 15 slots per 4-stage group
   // (slot 2^e - 1 + kk), 4 words each; one column set per pair of warps
-  // sharing a lane quadrant
+  // sharing a lane quadrant (2 sets per group)
   static constexpr int NSLOT = KC == 8 ? 30 : 15;
   static constexpr int SET_COLS = 4 * NSLOT;                       // 120 / 60
-  static constexpr unsigned TM_COLS = KC == 8 ? 256 : 128;         // >= 2 sets, power of 2
+  static constexpr unsigned TM_COLS =
+      GROUPS == 2 ? (KC == 8 ? 512 : 256) : (KC == 8 ? 256 : 128);  // >= sets, power of 2
   static constexpr size_t SMEM = sizeof(double2) * (STAGES * TILE);
 };
 
@@ -81,16 +88,21 @@ __device__ __forceinline__ void col_stages4(double2 (&v)[16], uint32_t twm) {
   }
 }
 
-template <int KC, bool FAST = false>
-__global__ void __launch_bounds__(256, 1)
+template <int KC, bool FAST = false, int GROUPS = 1>
+__global__ void __launch_bounds__(256 * GROUPS, 1)
 col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __restrict__ twst,
                const double* __restrict__ scales, long long row0, long long row1,
                Cand* __restrict__ cand, const int* __restrict__ stopped,
                const __grid_constant__ CUtensorMap ymap) {
-  using C = ColTma<KC>;
+  using C = ColTma<KC, GROUPS>;
   constexpr int COLS = C::COLS, U = C::U, TILE = C::TILE;
   extern __shared__ __align__(128) double2 csm[];
   __shared__ __align__(8) unsigned long long full[C::STAGES];
+  // GROUPS = 2: rel[s] completes a phase when the group that consumed a
+  // tile of stage s has issued the stage's next copy.  A group waits on it
+  // before its full[s] wait, because the other group may still be on the
+  // stage's previous tile (a parity wait alone would alias to that phase).
+  __shared__ __align__(8) unsigned long long rel[C::STAGES];
   if (stopped && *stopped) return;
   __shared__ uint32_t tm_base_s;
   const long long N = 1LL << K;
@@ -101,12 +113,22 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
   const long long t0 = tiles * blockIdx.x / gridDim.x;
   const long long t1 = tiles * (blockIdx.x + 1) / gridDim.x;
   const int ntile = (int)(t1 - t0);
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int lane = threadIdx.x & 31;
+  const int grp = GROUPS == 2 ? (int)(threadIdx.x >> 8) : 0;
+  const int tid = threadIdx.x & 255;  // thread within its group
+  // group-local barrier (named barrier 1 + group; the whole CTA if one group)
+  auto gsync = [&]() {
+    if constexpr (GROUPS == 2) asm volatile("bar.sync %0, 256;" ::"r"(1 + grp) : "memory");
+    else __syncthreads();
+  };
 
-  if (tid == 0) {
-    for (int s = 0; s < C::STAGES; ++s) mbar_init(&full[s], 1);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&rel[s], 1);
+    }
   }
-  if (tid < 32) {
+  if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      (unsigned)__cvta_generic_to_shared(&tm_base_s)),
                  "r"(C::TM_COLS)
@@ -117,9 +139,9 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // this thread's twiddle cells: its lane of the warp's quadrant, its set
-  const uint32_t twm = tm_base_s + ((uint32_t)(((tid >> 5) & 3) * 32) << 16) +
-                       (uint32_t)((tid >> 7) * C::SET_COLS);
-  // warp 0 issues the copies of local tile n into stage n % STAGES
+  const uint32_t twm = tm_base_s + ((uint32_t)(((threadIdx.x >> 5) & 3) * 32) << 16) +
+                       (uint32_t)((threadIdx.x >> 7) * C::SET_COLS);
+  // one warp issues the copies of local tile n into stage n % STAGES
   auto issue = [&](int n) {
     const long long t = t0 + n;
     const int chunk = (int)(t / rows), row = (int)(t % rows);
@@ -146,7 +168,7 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
         bulk_g2s(dst + u * COLS, src + ((size_t)u << b0), sizeof(double2) * COLS, mb);
     }
   };
-  if (tid < 32) {
+  if (threadIdx.x < 32) {
     for (int n = 0; n < C::STAGES && n < ntile; ++n) issue(n);
   }
 
@@ -157,7 +179,7 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
   int tw_chunk = -1;
   const int c = KC == 8 ? (tid & 15) : tid;
   const int h = KC == 8 ? (tid >> 4) : 0;
-  for (int n = 0; n < ntile; ++n) {
+  for (int n = grp; n < ntile; n += GROUPS) {
     const long long t = t0 + n;
     const int chunk = (int)(t / rows), rl = (int)(t % rows);
     const long long row = row0 + rl;
@@ -193,6 +215,8 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
     }
     const int s = n % C::STAGES;
     double2* tile = csm + s * TILE;
+    if (GROUPS == 2 && n >= C::STAGES)
+      mbar_wait(&rel[s], (unsigned)(((n - C::STAGES) / C::STAGES) & 1));
     mbar_wait(&full[s], (unsigned)((n / C::STAGES) & 1));
     const double sc = FAST ? 1.0 : __ldg(scales + row);
     const int q = q0 + c;
@@ -203,7 +227,7 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
     if constexpr (KC == 8) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) tile[(16 * h + i) * COLS + c] = v[i];
-      __syncthreads();
+      gsync();
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = tile[(h + 16 * i) * COLS + c];
       col_stages4<FAST, 15>(v, twm);
@@ -212,8 +236,14 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
     // with tile n + STAGES (generic-proxy writes above precede the async
     // proxy's overwrite)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (tid < 32 && n + C::STAGES < ntile) issue(n + C::STAGES);
+    gsync();
+    if (tid < 32 && n + C::STAGES < ntile) {
+      issue(n + C::STAGES);
+      if (GROUPS == 2 && lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(&rel[s]))
+                     : "memory");
+    }
     // FAST: screen the tile with one predicate-accumulating compare per
     // point; the (rare) tile holding a candidate at least as large as the
     // thread's best runs the full first-maximum update
@@ -246,19 +276,19 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (tid < 32)
+  if (threadIdx.x < 32)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_base_s),
                  "r"(C::TM_COLS)
                  : "memory");
   // merge this CTA's first maximum into its slot (slots persist over the
   // row batches of one step; the (mag, flat) order makes merging order-free)
-  __shared__ Cand red[8];
+  __shared__ Cand red[8 * GROUPS];
   best = warp_argmax(best);
-  const int wid = tid >> 5;
+  const int wid = threadIdx.x >> 5;
   if (lane == 0) red[wid] = best;
   __syncthreads();
   if (wid == 0) {
-    Cand cc = lane < 8 ? red[lane] : best;
+    Cand cc = lane < 8 * GROUPS ? red[lane] : best;
     cc = warp_argmax(cc);
     if (lane == 0) {
       Cand& slot = cand[blockIdx.x];
