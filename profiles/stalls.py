@@ -13,17 +13,34 @@ NAMES = ['stall_barrier', 'stall_branch_resolving', 'stall_dispatch', 'stall_lg'
          'stall_short_sb', 'stall_wait']
 
 
-def main(rep, top=12):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True).stdout
+def num(x):
+    try:
+        return int(x or 0)
+    except ValueError:
+        return 0
+
+
+def main(rep, kernel=None, top=12):
+    cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"]
+    if kernel:
+        cmd += ["--kernel-name", "regex:" + kernel]
+    txt = subprocess.run(cmd, capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
-    hdr, data = rows[1], rows[2:]
+    hdr = rows[1]
+    # a report with several launches repeats the table: keep the first one
+    data = []
+    for r in rows[2:]:
+        if len(r) != len(hdr) or r[0] == hdr[0]:
+            if data:
+                break
+            continue
+        data.append(r)
     idx = {n: hdr.index(n) for n in NAMES}
     isrc = hdr.index('Source')
     iall = hdr.index('Warp Stall Sampling (All Samples)')
-    tot = sum(int(r[iall] or 0) for r in data)
+    tot = sum(num(r[iall]) for r in data)
     print("samples", tot)
-    print(" ".join("%s=%.1f%%" % (n[6:], 100 * sum(int(r[idx[n]] or 0) for r in data) / max(tot, 1))
+    print(" ".join("%s=%.1f%%" % (n[6:], 100 * sum(num(r[idx[n]]) for r in data) / max(tot, 1))
                    for n in NAMES))
     ops = Counter()
     for r in data:
@@ -33,10 +50,10 @@ def main(rep, top=12):
         op = t[1] if t[0].startswith('@') else t[0]
         ops[op.split('.')[0]] += 1
     print("sass op counts:", ", ".join("%s:%d" % kv for kv in ops.most_common(14)))
-    for r in sorted(data, key=lambda r: -int(r[iall] or 0))[:top]:
-        worst = max(NAMES, key=lambda n: int(r[idx[n]] or 0))
+    for r in sorted(data, key=lambda r: -num(r[iall]))[:top]:
+        worst = max(NAMES, key=lambda n: num(r[idx[n]]))
         print("%5s %-14s %s" % (r[iall], worst[6:], r[isrc][:70]))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None)

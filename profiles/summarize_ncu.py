@@ -1,4 +1,4 @@
-"""One-page text summary of an `ncu --set full` report (first kernel in it).
+"""Text summary of an `ncu --set full` report (every kernel in it).
 
     python profiles/summarize_ncu.py gpurun_out/x.ncu-rep > profiles/r01/x.txt
 """
@@ -27,19 +27,25 @@ def raw(rep):
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
-    return rows[0], rows[1], rows[2]
+    return rows[0], rows[1], rows[2:]
 
 
 def main(rep):
-    h, u, v = raw(rep)
-    name = v[h.index("Kernel Name")] if "Kernel Name" in h else "?"
-    print("kernel:", name)
-    for k in WANT:
-        if k in h:
-            i = h.index(k)
-            print("  %-70s %s %s" % (k, v[i], u[i]))
-    sys.stdout.flush()
-    subprocess.run([sys.executable, __file__.replace("summarize_ncu.py", "stalls.py"), rep])
+    h, u, vs = raw(rep)
+    for v in vs:
+        if len(v) != len(h):
+            continue
+        name = v[h.index("Kernel Name")] if "Kernel Name" in h else "?"
+        print("kernel:", name)
+        for k in WANT:
+            if k in h:
+                i = h.index(k)
+                print("  %-70s %s %s" % (k, v[i], u[i]))
+        sys.stdout.flush()
+        kid = v[h.index("Kernel Name")].split("(")[0].split("<")[0].split()[-1] \
+            if "Kernel Name" in h else None
+        subprocess.run([sys.executable, __file__.replace("summarize_ncu.py", "stalls.py"), rep]
+                       + ([kid] if kid else []))
 
 
 if __name__ == "__main__":

@@ -96,3 +96,27 @@ int main() {
   run("tiles read, round-robin (4 CTA/SM x 256)", G, [&] { tiles_rd<<<sms * 4, 256>>>(a, 256, 1, out); });
   return 0;
 }
+
+// ctypes entry for scripts/micro/power_patterns.py: run pattern `which` reps
+// times on the current stream (buffers allocated on first call).
+extern "C" int hbm_pattern(int which, int reps) {
+  static double2 *a = nullptr, *b = nullptr; static double* out = nullptr;
+  const size_t bytes = 4ULL << 30, n = bytes / 16;
+  if (!a) {
+    if (cudaMalloc(&a, bytes) || cudaMalloc(&b, bytes) || cudaMalloc(&out, 8)) return 1;
+    cudaMemset(a, 0, bytes); cudaMemset(b, 0, bytes);
+    cudaFuncSetAttribute(bulk_wr, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
+  }
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  for (int r = 0; r < reps; ++r) {
+    switch (which) {
+      case 0: rd<<<sms * 8, 512>>>(a, n, out); break;
+      case 1: wr<<<sms * 8, 512>>>(a, n); break;
+      case 2: bulk_wr<<<sms, 256, 131072>>>(a, n / 4096); break;
+      case 3: tiles_rd<<<sms * 4, 256>>>(a, 256, 0, out); break;
+      case 4: tiles_rd<<<sms * 4, 256>>>(a, 256, 1, out); break;
+      default: return 2;
+    }
+  }
+  return cudaGetLastError() != cudaSuccess;
+}
