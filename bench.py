@@ -50,27 +50,9 @@ def flops_per_eval(n):
 
 
 def r_power_live(n, radii):
-    """Per radius, the first l with r^l == +0 in the reference's sequential fold
-    (np.cumprod, transform.py:147-150), else n — the entries the large-N
-    prologue must load.  Only r <= 0.5 ever reaches zero: for r > 0.5 the fold
-    sticks at a subnormal (k * 2^-1074 * r rounds back to k * 2^-1074), so
-    those rows are live to the end."""
-    import numpy as np
-    r = np.asarray(radii, dtype=np.float64)
-    live = np.full(r.shape, n, dtype=np.int64)
-    idx = np.nonzero(r <= 0.5)[0]
-    v = np.ones(idx.size)
-    rr = r[idx]
-    for l in range(1, n):
-        if idx.size == 0:
-            break
-        v = v * rr
-        z = v == 0.0
-        if z.any():
-            live[idx[z]] = l
-            keep = ~z
-            idx, v, rr = idx[keep], v[keep], rr[keep]
-    return live
+    """Live r^l entries per radius (distributed.live_powers)."""
+    from paper_1711_08604_b200.distributed import live_powers
+    return live_powers(radii, n)
 
 
 def bytes_per_eval(n, radii=None):
@@ -584,7 +566,7 @@ def run_sharded(args, w, radii, sig, mode, world, rank, local, dev):
             recs, counts = out.host_steps()
             return recs[0], int(counts[0])
     else:
-        m0, m1 = D.shard_bounds(w.m, rank, world)
+        m0, m1 = D.radius_shard_bounds(radii, w.n, rank, world, exact=exact)
         b = w.batch
         plan = engine.get_plan(radii, w.n, batch=b, m0=m0, m1=m1, fast=fast)
         g_dev = torch.from_numpy(sig).to(dev)

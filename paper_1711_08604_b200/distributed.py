@@ -25,7 +25,8 @@ import numpy as np
 
 from . import _capi
 
-__all__ = ["shard_bounds", "decompose_sharded", "decompose_batch_sharded", "ShardedRunner"]
+__all__ = ["shard_bounds", "radius_shard_bounds", "live_powers", "decompose_sharded",
+           "decompose_batch_sharded", "ShardedRunner"]
 
 
 def shard_bounds(count, rank, world):
@@ -33,6 +34,60 @@ def shard_bounds(count, rank, world):
     if world < 1 or not 0 <= rank < world:
         raise ValueError("rank %d outside world of %d" % (rank, world))
     return (count * rank) // world, (count * (rank + 1)) // world
+
+
+def live_powers(radii, n):
+    """Per radius, the number of leading entries of its r^l row (the
+    reference's sequential np.cumprod fold, transform.py:147-150) that are
+    not exactly +0 — the entries the exact large-N field loads (pw_len on the
+    device).  Only r <= 0.5 ever reaches zero: for r > 0.5 the fold sticks at
+    a subnormal (k 2^-1074 r rounds back to k 2^-1074), so those rows are
+    live to the end."""
+    r = np.asarray(radii, dtype=np.float64)
+    live = np.full(r.shape, int(n), dtype=np.int64)
+    idx = np.nonzero(r <= 0.5)[0]
+    v = np.ones(idx.size)
+    rr = r[idx]
+    for l in range(1, int(n)):
+        if idx.size == 0:
+            break
+        v = v * rr
+        z = v == 0.0
+        if z.any():
+            live[idx[z]] = l
+            keep = ~z
+            idx, v, rr = idx[keep], v[keep], rr[keep]
+    return live
+
+
+def radius_shard_bounds(radii, n, rank, world, exact=True):
+    """Contiguous radius block [m0, m1) of `rank` balanced by field cost.
+
+    For the exact large-N field (N > 8192) a row costs its 32 B per eval of
+    row-batch intermediate plus 8 B per live r^l entry (live_powers), so
+    rows with r <= 0.5 are cheaper and equal row counts leave the low-radius
+    ranks idle at the end of every step; blocks are cut at equal cumulative
+    cost instead.  Otherwise (fast mode: r^l formed on chip; on-chip N)
+    every row costs the same and this is shard_bounds.  Blocks stay
+    rank-ordered and non-empty, so the lowest-flat-index tie rule holds."""
+    m = len(radii)
+    if not exact or n <= 8192 or world == 1:
+        return shard_bounds(m, rank, world)
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("rank %d outside world of %d" % (rank, world))
+    cost = 32.0 + 8.0 * live_powers(radii, n) / float(n)
+    cum = np.concatenate([[0.0], np.cumsum(cost)])
+
+    def cut(p):
+        if p <= 0:
+            return 0
+        if p >= world:
+            return m
+        b = int(np.searchsorted(cum, cum[-1] * p / world))
+        if b > 0 and abs(cum[b - 1] - cum[-1] * p / world) <= abs(cum[b] - cum[-1] * p / world):
+            b -= 1
+        return min(max(b, p), m - (world - p))
+    return cut(rank), cut(rank + 1)
 
 
 def _all_gather(out, t, group):
@@ -162,7 +217,7 @@ def decompose_sharded(signals, grid, max_terms=10, threshold=None, dc_first=Fals
     m = len(grid.radii)
     if world > m:
         raise ValueError("more ranks (%d) than radii (%d)" % (world, m))
-    m0, m1 = shard_bounds(m, rank, world)
+    m0, m1 = radius_shard_bounds(grid.radii, n, rank, world, exact=engine_name != "fft-fast")
     if plan_factory is None:
         plan = _default_plan(grid.radii, n, b, m0, m1, device, engine_name)
     else:

@@ -83,6 +83,45 @@ def test_shard_bounds():
             assert max(h - l for l, h in blocks) - min(h - l for l, h in blocks) <= 1
 
 
+def test_live_powers_match_the_cumprod_fold():
+    """live_powers = count of leading nonzero entries of the reference's
+    np.cumprod rows (transform.py:145-149)."""
+    from paper_1711_08604_b200.distributed import live_powers
+    n = 4096
+    radii = np.array([0.0, 0.01, 0.1, 0.25, 0.3, 0.4999, 0.5, 0.5001, 0.9, 0.99])
+    powers = np.empty((len(radii), n))
+    powers[:, 0] = 1.0
+    powers[:, 1:] = radii[:, None]
+    np.cumprod(powers, axis=1, out=powers)
+    expect = [int(np.argmax(row == 0.0)) if (row == 0.0).any() else n for row in powers]
+    assert list(live_powers(radii, n)) == expect
+    assert all(np.all(row[e:] == 0.0) for row, e in zip(powers, expect))
+
+
+def test_radius_shard_bounds_balance_the_exact_field():
+    """Exact large-N shards: contiguous, rank-ordered, non-empty, covering,
+    and balanced in field cost (32 B + 8 B per live r^l entry per eval) to
+    within a row; fast mode and on-chip N fall back to row counts."""
+    from paper_1711_08604_b200 import workloads as W
+    from paper_1711_08604_b200.distributed import live_powers, radius_shard_bounds, shard_bounds
+    n, m = 1 << 16, 4096
+    radii = W.radii_for(m)
+    cost = 32.0 + 8.0 * live_powers(radii, n) / n
+    for world in (2, 3, 8):
+        blocks = [radius_shard_bounds(radii, n, r, world) for r in range(world)]
+        assert blocks[0][0] == 0 and blocks[-1][1] == m
+        assert all(a[1] == b[0] for a, b in zip(blocks, blocks[1:]))
+        assert all(h > l for l, h in blocks)
+        share = [cost[l:h].sum() for l, h in blocks]
+        assert max(share) - min(share) <= 2 * cost.max()
+        assert [radius_shard_bounds(radii, n, r, world, exact=False) for r in range(world)] == \
+            [shard_bounds(m, r, world) for r in range(world)]
+        assert [radius_shard_bounds(radii, 4096, r, world) for r in range(world)] == \
+            [shard_bounds(m, r, world) for r in range(world)]
+    tiny = (0.1, 0.2, 0.9)
+    assert [radius_shard_bounds(tiny, n, r, 3) for r in range(3)] == [(0, 1), (1, 2), (2, 3)]
+
+
 def _batch_worker(rank, world, port, out_q):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
