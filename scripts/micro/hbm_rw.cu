@@ -65,6 +65,43 @@ __global__ void __launch_bounds__(256) tiles_rd(const double2* __restrict__ y, i
   if (s == 1.2345) out[0] = s;
 }
 
+// strided bulk stores: a CTA-item writes 4096 points as 256 pieces of 256 B
+// at 64 KiB stride (pass A writing a column-tile-contiguous layout:
+// Y[row][chunk][block][16]); items in block-major order per CTA range
+__global__ void __launch_bounds__(256) bulk_wr_strided(double2* __restrict__ y, int rows) {
+  extern __shared__ __align__(128) double2 sm[];
+  for (int i = threadIdx.x; i < 8192; i += 256) sm[i] = make_double2(i, 1.0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  const long long items = (long long)rows * 256;  // (block, row), block-major
+  const long long i0 = items * blockIdx.x / gridDim.x, i1 = items * (blockIdx.x + 1) / gridDim.x;
+  int k = 0;
+  for (long long it = i0; it < i1; ++it, ++k) {
+    const long long blk = it / rows, row = it % rows;
+    // warp 0: lanes issue 8 pieces each
+    if (threadIdx.x < 32) {
+      if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 8;" ::: "memory");
+      __syncwarp();
+      for (int c = threadIdx.x; c < 256; c += 32) {
+        double2* dst = y + row * (1LL << 20) + (long long)c * 4096 + blk * 16;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     :: "l"(dst), "r"((unsigned)__cvta_generic_to_shared(sm + (k & 1) * 4096 + c * 16)), "r"(256u) : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (threadIdx.x < 32) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+// contiguous tile reads: 64 KiB per tile (the col pass on that layout)
+__global__ void __launch_bounds__(256) tiles_rd_contig(const double2* __restrict__ y, size_t n, double* out) {
+  double s = 0;
+  for (size_t t = blockIdx.x; t < n / 4096; t += gridDim.x) {
+#pragma unroll 4
+    for (int u = threadIdx.x; u < 4096; u += 256) { double2 v = __ldcs(y + t * 4096 + u); s += v.x + v.y; }
+  }
+  if (s == 1.2345) out[0] = s;
+}
+
 int main() {
   const size_t bytes = 4ULL << 30, n = bytes / 16;
   double2 *a, *b; double* out;
@@ -106,6 +143,7 @@ extern "C" int hbm_pattern(int which, int reps) {
     if (cudaMalloc(&a, bytes) || cudaMalloc(&b, bytes) || cudaMalloc(&out, 8)) return 1;
     cudaMemset(a, 0, bytes); cudaMemset(b, 0, bytes);
     cudaFuncSetAttribute(bulk_wr, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
+    cudaFuncSetAttribute(bulk_wr_strided, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
   }
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   for (int r = 0; r < reps; ++r) {
@@ -115,6 +153,8 @@ extern "C" int hbm_pattern(int which, int reps) {
       case 2: bulk_wr<<<sms, 256, 131072>>>(a, n / 4096); break;
       case 3: tiles_rd<<<sms * 4, 256>>>(a, 256, 0, out); break;
       case 4: tiles_rd<<<sms * 4, 256>>>(a, 256, 1, out); break;
+      case 5: bulk_wr_strided<<<sms, 256, 131072>>>(a, 256); break;
+      case 6: tiles_rd_contig<<<sms * 4, 256>>>(a, n, out); break;
       default: return 2;
     }
   }
