@@ -234,6 +234,36 @@ def cpu_baseline(w, radii, g, seconds):
                          w.n, el, threads)}
 
 
+def numpy_baseline(w, radii, g, seconds):
+    """The reference's own numpy selection step (oracle/numpy_port.py: the
+    cumprod tables, bit-reversed gather, stage loop, scale and first argmax of
+    transform.py:73-93,137-201 and core.py:285-300 — the same bits as the
+    reference) on one core, on the same radius sample as cpu_baseline: the
+    reference package itself is not on the GPU box.  The tables are built
+    once (the reference caches them per grid) and not timed."""
+    import oracle as O
+    from oracle import numpy_port as NP
+    r, _, stride = cpu_sample(w, radii)
+    t = NP.Tables(r, w.n)
+    c = O.dft_forward(g)
+    NP.select(t, c)
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        NP.select(t, c)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or reps >= 1000:
+            break
+    return {"value": len(r) * w.n * reps / el, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": "%d x the reference's numpy field + argmax (oracle/numpy_port.py, "
+                      "bit-identical to the C oracle) for %s signal 0: M=%d%s x N=%d, "
+                      "%.1f s on one core" % (reps, w.name, len(r),
+                                               "" if stride == 1 else
+                                               " (every %d-th of %d radii)" % (stride, w.m),
+                                               w.n, el)}
+
+
 # ---------------------------------------------------------------------------
 # shared pieces of both arms
 # ---------------------------------------------------------------------------
@@ -507,9 +537,10 @@ def run_ours(args):
            "api": "paper_1711_08604_b200.core.decompose%s(engine=%r)"
                   % ("" if w.batch == 1 else "_batch", engine_name)}
 
-    cpu = None
+    cpu = cpu_np = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(w, radii, sig[0], args.cpu_seconds)
+        cpu_np = numpy_baseline(w, radii, sig[0], args.cpu_seconds)
 
     if rank == 0:
         line = {
@@ -525,6 +556,7 @@ def run_ours(args):
             "e2e": e2e,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "cpu_baseline_numpy": cpu_np,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

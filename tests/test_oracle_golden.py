@@ -107,3 +107,21 @@ def test_big_n_elision_forms(n):
     if n <= 65536:
         f = O.field(O.dft_forward(x), b["radii_%d" % n])
         assert np.array_equal(f[:, sel], b["field_%d" % n])
+
+
+def test_numpy_port_field_matches_the_c_oracle():
+    """oracle/numpy_port.py (the reference's numpy selection step, timed by
+    bench.py as the reference-speed baseline) computes the C oracle's field
+    bit for bit and the same first maximum."""
+    import oracle as O
+    from oracle import numpy_port as NP
+    from paper_1711_08604_b200 import workloads as W
+    for n, m, seed in ((1024, 100, 3), (4096, 64, 4), (1 << 14, 8, 5)):
+        g = W.pole_sum(n, 16, 0.95, seed)
+        radii = W.radii_for(m)
+        c = O.dft_forward(g)
+        t = NP.Tables(radii, n)
+        assert np.array_equal(NP.field(t, c), O.field(c, np.array(radii)))
+        s, j, mag, f = NP.select(t, c)
+        cand = O.field_argmax(c, np.array(radii))
+        assert (s * n + j, mag) == (int(cand["flat"]), float(cand["mag"]))
