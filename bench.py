@@ -387,9 +387,24 @@ def field_roofline(plan, w, radii_rows, ghat, exact, local):
     field_ms = plan.time_field(ghat, reps=5 if w.n > 8192 else 50)
     fpe = flops_per_eval(w.n)
     launch_evals = batch * rows * w.n
+    bpe = bytes_per_eval(w.n, radii_rows) if exact else (32.0 if w.n > 8192 else 0.0)
+    split = None
+    if not exact and w.n > 8192:
+        # pruned fast field (afd_pruned.cuh): on-chip rows are 4096-point
+        # transforms of pre-twiddled spectra (F(4096) flops, no HBM bytes:
+        # the Q spectra and the weight tables are L2-resident), the rest
+        # the two-pass path (F(N) flops, 32 B per eval)
+        onchip, twopass = plan.field_split()
+        f_on = flops_per_eval(4096)
+        fpe = (onchip * f_on + twopass * fpe) / float(rows)
+        bpe = 32.0 * twopass / float(rows)
+        split = {"onchip_rows": onchip, "twopass_rows": twopass,
+                 "flops_per_eval_onchip": f_on, "flops_per_eval_twopass": flops_per_eval(w.n),
+                 "bytes_per_eval_twopass": 32.0,
+                 "note": "rows whose weight tail (l >= 4096) is below 2^-64 of the largest "
+                         "kept term run as N/4096 on-chip 4096-point fields (DESIGN.md §4)"}
     achieved = launch_evals * fpe / (field_ms * 1e-3) / 1e12
     peak = engine.fp64_peak_tflops(local)
-    bpe = bytes_per_eval(w.n, radii_rows) if exact else (32.0 if w.n > 8192 else 0.0)
     hbm_peak, hbm_src = hbm_peak_gbs()
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -406,7 +421,7 @@ def field_roofline(plan, w, radii_rows, ghat, exact, local):
                 "frac": hbm / hbm_peak, "traffic": traffic, "bytes_per_eval": bpe,
                 "peak_source": hbm_src, "fp64": fp64}
     else:
-        roof = dict(fp64, bound="fp64", traffic=traffic)
+        roof = dict(fp64, bound="fp64", traffic=traffic, bytes_per_eval=bpe)
         if instr:
             # bit-exact radix-2 arithmetic is mostly unfused: per eval the
             # kernel issues `instr` FP64-pipe instructions for F(N) flops
@@ -415,8 +430,13 @@ def field_roofline(plan, w, radii_rows, ghat, exact, local):
     roof.update({
         "kernel": ("field_kernel (fused prologue + inverse DIT + scale + |.|^2 + argmax)"
                    if w.n <= 8192 else
-                   "large-N field: pass A (big_field_a) + TMA column pass (col_tma_kernel)"),
+                   "large-N field: pass A (big_field_a) + TMA column pass (col_tma_kernel)"
+                   if split is None else
+                   "pruned large-N field: N/4096 on-chip 4096-point fields "
+                   "(field_kernel<12>) + two-pass rows (big_field_a + col_tma_kernel)"),
         "flops_per_eval": fpe, "evals_per_launch": launch_evals, "launch_ms": field_ms})
+    if split is not None:
+        roof["split"] = split
     return roof
 
 

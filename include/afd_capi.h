@@ -231,6 +231,13 @@ int64_t afd_launch_count(afd_plan *plan);
  * FMA chains on every SM), *tflops counts 2 flops per DFMA. */
 int afd_time_field(afd_plan *plan, const double *ghat, int64_t batch, int reps, double *avg_ms,
                    void *stream);
+/* afd_field_split: how the last large-N fast field evaluation on `stream`
+ * (synchronised here) split the plan's rows: *onchip rows went through the
+ * pruned on-chip 4096-point transforms (their weight tail r^l, l >= 4096,
+ * is below 2^-64 of the largest kept term), *twopass rows through pass A +
+ * the TMA column pass.  Exact plans and N <= 8192: *onchip = 0 and every
+ * row is counted as *twopass (large N) or *onchip = rows (on-chip N). */
+int afd_field_split(afd_plan *plan, int64_t *onchip, int64_t *twopass, void *stream);
 int afd_fp64_peak(int device, double *tflops, void *stream);
 
 #ifdef __cplusplus

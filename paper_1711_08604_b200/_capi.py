@@ -69,6 +69,7 @@ SIGNATURES = [
     ("afd_launch_count", _I64, [_VP]),
     ("afd_time_field", _I, [_VP, _VP, _I64, _I, _VP, _VP]),
     ("afd_fp64_peak", _I, [_I, _VP, _VP]),
+    ("afd_field_split", _I, [_VP, _VP, _VP, _VP]),
 ]
 
 _LIB = None

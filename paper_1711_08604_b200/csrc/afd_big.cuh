@@ -251,13 +251,18 @@ big_field_a(int K, const double* __restrict__ pw_rev, long long pw_row0,
             const double2* __restrict__ ghat_rev, const double2* __restrict__ twst,
             long long row0, long long row1, double2* __restrict__ Y,
             const int* __restrict__ stopped, const int* __restrict__ pw_len,
-            int direct_out) {
+            int direct_out, const int* __restrict__ lim = nullptr) {
   constexpr int KA = 12;
   using GA = Geo<KA, 4>;
   using TwA = SmemTw<KA, 4>;
   constexpr int BLK = 1 << KA, T = GA::T, P = GA::P;
   extern __shared__ double2 smem[];
   if (stopped && *stopped) return;
+  if (lim != nullptr) {  // pruned field: rows below *lim are done on chip (afd_pruned.cuh)
+    const long long l = *lim;
+    if (l > row0) row0 = l < row1 ? l : row1;
+    if (row0 >= row1) return;
+  }
   const long long N = 1LL << K;
   const int nblk = (int)(N >> KA);
   const int rows = (int)(row1 - row0);

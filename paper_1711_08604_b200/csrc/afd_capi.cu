@@ -19,6 +19,7 @@
 #include "afd_col_tma.cuh"
 #include "afd_step_cluster.cuh"
 #include "afd_big.cuh"
+#include "afd_pruned.cuh"
 #include "afd_direct.cuh"
 
 using namespace afd;
@@ -114,6 +115,16 @@ struct afd_plan {
   int* pw_len = nullptr;       // [m1-m0] first l with r^l == 0 (or N)
   CUtensorMap ymap;            // Y as [big_rows][256][2^ka complex] (8-stage TMA column pass)
   bool ymap_ok = false;
+  // pruned fast field (afd_pruned.cuh): rows with a negligible weight tail
+  // as a batch of Q = N / 4096 on-chip 4096-point fields
+  bool pruned = false;
+  double* fw12 = nullptr;      // [m1-m0][FastW<12,4>::STRIDE] weights (this plan's scales)
+  double2* ghq = nullptr;      // [Q][4096] pre-twiddled spectra
+  double2* tw_img12 = nullptr; // SmemTw<12,4> (c, t) image
+  Cand* pr_cand = nullptr;     // [Q][pr_ncta]
+  int pr_ncta = 0;
+  int* mstar = nullptr;        // first row left to the two-pass path
+  unsigned long long* tmax = nullptr;
   double* nodes = nullptr;     // [2 * N / kNodeLen]
   BigSel* sel = nullptr;
   int* amb = nullptr;
@@ -358,7 +369,8 @@ int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64
                         : (tm ? field_kernel<K, kFieldRB, G, true, TMC>
                               : field_kernel<K, kFieldRB, G, true>);
     kern<<<grid, block, smem, st>>>(ghat, tab, p->scales, p->twst, r0, r1, p->m0, nullptr,
-                                    field_out, nullptr, img, field_pp(), (unsigned*)nullptr, 0);
+                                    field_out, nullptr, img, field_pp(), (unsigned*)nullptr, 0,
+                                    SubMap{0, 0, nullptr});
   } else {
     auto kern = p->fast ? (tm ? field_kernel<K, kFieldRB, G, false, TMC, true>
                               : field_kernel<K, kFieldRB, G, false, false, true>)
@@ -367,7 +379,7 @@ int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64
     CU(launch_pdl(kern, grid, dim3(block), smem, st, ghat, tab,
                   (const double*)p->scales, (const double2*)p->twst, (long long)r0,
                   (long long)r1, (long long)p->m0, cand, (double2*)nullptr, state,
-                  img, field_pp(), row_ctr, launch_id));
+                  img, field_pp(), row_ctr, launch_id, SubMap{0, 0, nullptr}));
   }
   p->launches++;
   CU(cudaGetLastError());
@@ -665,7 +677,8 @@ static const int kPassADirect = getenv("AFD_PASSA_DIRECT") ? atoi(getenv("AFD_PA
 
 // Pass A over rows [r0, r0+rows) (mode 0: field prologue) or one signal (mode 1).
 int big_launch_a(afd_plan* p, bool inv, int mode, const double2* ghat_rev, const double2* x,
-                 int64_t r0, int64_t rows, const int* stopped, cudaStream_t st) {
+                 int64_t r0, int64_t rows, const int* stopped, cudaStream_t st,
+                 const int* lim = nullptr) {
   const int64_t items = (p->n >> p->ka) * rows;
   AFD_KA_DISPATCH(p->ka, {
     // persistent: one CTA per SM (2 row-groups each), work items strided
@@ -676,7 +689,7 @@ int big_launch_a(afd_plan* p, bool inv, int mode, const double2* ghat_rev, const
       if (KA != 12) return fail(AFD_E_UNSUPPORTED, "fast pass A needs 4096-point blocks");
       big_field_a<true><<<grid, block, big_a_smem_g<KA>(), st>>>(
           p->K, p->fw, p->m0, ghat_rev, p->twct, r0, r0 + rows, p->Y, stopped, nullptr,
-          kPassADirect);
+          kPassADirect, lim);
     } else if (inv && mode == 0 && KA == 12 && field_tmem_enabled() && kFieldAEnabled)
       big_field_a<false><<<grid, block, big_a_smem_g<KA>(), st>>>(
           p->K, p->pw, p->m0, ghat_rev, p->twst, r0, r0 + rows, p->Y, stopped, p->pw_len,
@@ -709,8 +722,17 @@ static const bool kColTmaEnabled = !(getenv("AFD_COL_TMA") && atoi(getenv("AFD_C
 // on a three-stage ring; AFD_COL_GROUPS selects (experiments).
 static const int kColGroups = getenv("AFD_COL_GROUPS") ? atoi(getenv("AFD_COL_GROUPS")) : 2;
 
+// Pruned fast field (afd_pruned.cuh); AFD_PRUNED=0 keeps the two-pass path
+// for every row (experiments).  It needs the TMA column pass for the rows it
+// leaves to the two-pass path (that kernel honours the device row limit).
+static const bool kPrunedEnabled = !(getenv("AFD_PRUNED") && atoi(getenv("AFD_PRUNED")) == 0);
+bool pruned_col_ok(const afd_plan* p) {
+  const int left = p->K - p->ka;
+  return kColTmaEnabled && (left == 4 || (left == 8 && kCol8Enabled && p->ymap_ok));
+}
+
 int big_launch_cols(afd_plan* p, bool inv, int last_mode, int scale_n, int64_t r0, int64_t rows,
-                    double2* fout, const int* stopped, cudaStream_t st) {
+                    double2* fout, const int* stopped, cudaStream_t st, const int* lim = nullptr) {
   dim3 grid((unsigned)big_col_ctas(p), (unsigned)rows);
   // fast arithmetic for the field's column stages only (the transforms of
   // the step bookkeeping stay exact)
@@ -727,19 +749,19 @@ int big_launch_cols(afd_plan* p, bool inv, int last_mode, int scale_n, int64_t r
         auto k4 = fastf ? col_tma_kernel<4, true, 2> : col_tma_kernel<4, false, 2>;
         if (left == 8)
           k8<<<g, 512, ColTma<8, 2>::SMEM, st>>>(p->K, b0, p->Y, tws, p->scales, r0, r0 + rows,
-                                                 p->big_cand, stopped, p->ymap);
+                                                 p->big_cand, stopped, lim, p->ymap);
         else
           k4<<<g, 512, ColTma<4, 2>::SMEM, st>>>(p->K, b0, p->Y, tws, p->scales, r0, r0 + rows,
-                                                 p->big_cand, stopped, p->ymap);
+                                                 p->big_cand, stopped, lim, p->ymap);
       } else {
         auto k8 = fastf ? col_tma_kernel<8, true> : col_tma_kernel<8>;
         auto k4 = fastf ? col_tma_kernel<4, true> : col_tma_kernel<4>;
         if (left == 8)
           k8<<<g, 256, ColTma<8>::SMEM, st>>>(p->K, b0, p->Y, tws, p->scales, r0, r0 + rows,
-                                              p->big_cand, stopped, p->ymap);
+                                              p->big_cand, stopped, lim, p->ymap);
         else
           k4<<<g, 256, ColTma<4>::SMEM, st>>>(p->K, b0, p->Y, tws, p->scales, r0, r0 + rows,
-                                              p->big_cand, stopped, p->ymap);
+                                              p->big_cand, stopped, lim, p->ymap);
       }
       p->launches++;
       CU(cudaGetLastError());
@@ -832,14 +854,39 @@ int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, doub
     cand_init_kernel<<<(n + 255) / 256, 256, 0, st>>>(p->big_cand, n);
     p->launches++;
   }
+  const int* lim = nullptr;
+  if (!fout && p->pruned) {
+    // rows [r0, mstar) as Q on-chip 4096-point fields; rows [mstar, r1)
+    // through the batches below (their kernels read mstar on the device)
+    const int Q = (int)(p->n >> kPruneK);
+    prune_init_kernel<<<1, 1, 0, st>>>(p->mstar, r1, p->tmax);
+    prune_tail_kernel<<<2 * p->sms, 256, 0, st>>>(ghat_rev, p->n, p->tmax);
+    prune_rows_kernel<<<2 * p->sms, 256, 0, st>>>(p->K, p->ka, ghat_rev, p->radii, r0, r1,
+                                                  p->tmax, stopped, p->mstar);
+    pretwiddle_kernel<<<4 * p->sms, 256, 0, st>>>(p->K, p->ka, ghat_rev, p->circle, p->ghq,
+                                                  stopped);
+    using Gm = Geo<kPruneK, kFieldRB>;
+    const size_t smem = field_smem<kPruneK>();
+    field_kernel<kPruneK, kFieldRB, 2, false, true, true>
+        <<<dim3((unsigned)p->pr_ncta, (unsigned)Q), Gm::T * 2, smem, st>>>(
+            p->ghq, p->fw12, p->scales, p->twct, (long long)r0, (long long)r1, (long long)p->m0,
+            p->pr_cand, nullptr, nullptr, p->tw_img12, field_pp(), (unsigned*)nullptr, 0,
+            SubMap{(long long)p->n, Q, p->mstar});
+    const int n = Q * p->pr_ncta;
+    const int np = std::min(kBigParts, (n + 255) / 256);
+    cand_partial_kernel<<<np, 256, 0, st>>>(p->pr_cand, n, (n + np - 1) / np, p->big_cand);
+    p->launches += 6;
+    CU(cudaGetLastError());
+    lim = p->mstar;
+  }
   for (int64_t b = r0; b < r1; b += p->big_rows) {
     const int64_t rows = std::min<int64_t>(p->big_rows, r1 - b);
     if (!(kBigSkip & 1) &&
-        (rc = big_launch_a(p, true, 0, ghat_rev, nullptr, b, rows, stopped, st)))
+        (rc = big_launch_a(p, true, 0, ghat_rev, nullptr, b, rows, stopped, st, lim)))
       return rc;
     if (kBigSkip & 2) continue;
     if ((rc = big_launch_cols(p, true, fout ? 2 : 1, 0, b, rows,
-                              fout ? fout + (size_t)(b - r0) * p->n : nullptr, stopped, st)))
+                              fout ? fout + (size_t)(b - r0) * p->n : nullptr, stopped, st, lim)))
       return rc;
   }
   return 0;
@@ -1152,6 +1199,35 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
     ALLOC2(p->amb, sizeof(int));
     ALLOC2(p->tmp, sizeof(double2) * N);
     rc = big_setup(p);
+    if (!rc && p->fast && kPrunedEnabled && K > kPruneK && pruned_col_ok(p)) {
+      // pruned fast field: weights {scale r^t, t < 256; r^(256 m), m < 16}
+      // of this plan's radii and N-point scales, the 4096-point (c, t)
+      // twiddle image (the stage tables S_b, b < 12, are the first 4095
+      // entries of the N-point tables), per-CTA candidates
+      constexpr int STR = FastW<kPruneK, kFieldRB>::STRIDE;
+      const int64_t rows = m1 - m0, Q = (int64_t)N >> kPruneK;
+      ALLOC2(p->fw12, sizeof(double) * STR * (size_t)rows);
+      ALLOC2(p->ghq, sizeof(double2) * N);
+      ALLOC2(p->tw_img12, sizeof(double2) * (SmemTw<kPruneK, kFieldRB>::ENTRIES));
+      ALLOC2(p->mstar, sizeof(int));
+      ALLOC2(p->tmax, sizeof(unsigned long long));
+      // CTAs per spectrum: the grid (ncta x Q) a whole number of SM waves
+      int nc = 1;
+      while (nc < p->sms && (nc * Q) % p->sms != 0) ++nc;
+      p->pr_ncta = (int)std::max<int64_t>(1, std::min<int64_t>(nc, (rows + 1) / 2));
+      ALLOC2(p->pr_cand, sizeof(Cand) * (size_t)Q * p->pr_ncta);
+      const int64_t total = rows * STR;
+      fast_weight_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256>>>(
+          p->radii, p->scales, m0, rows, STR, 1 << (kPruneK - 4), 16, kPruneK - 4, 0, 0, p->fw12);
+      build_tw_image_kernel<kPruneK><<<32, 256>>>(p->tw_img12, p->twct);
+      p->launches += 2;
+      if (cudaGetLastError() != cudaSuccess) return cleanup(fail(AFD_E_CUDA, "pruned tables"));
+      if (cudaFuncSetAttribute(field_kernel<kPruneK, kFieldRB, 2, false, true, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)field_smem<kPruneK>()) != cudaSuccess)
+        return cleanup(fail(AFD_E_CUDA, "pruned field attributes"));
+      p->pruned = true;
+    }
   } else {
     AFD_DISPATCH(K, { rc = setup_kernels<KK>(p); break; });
   }
@@ -1191,6 +1267,12 @@ int afd_plan_destroy(afd_plan* p) {
   cudaFree(p->scratch);
   cudaFree(p->Y);
   cudaFree(p->big_cand);
+  cudaFree(p->fw12);
+  cudaFree(p->ghq);
+  cudaFree(p->tw_img12);
+  cudaFree(p->pr_cand);
+  cudaFree(p->mstar);
+  cudaFree(p->tmax);
   cudaFree(p->big_part);
   cudaFree(p->nodes);
   cudaFree(p->sel);
@@ -1835,6 +1917,29 @@ int afd_time_field(afd_plan* p, const double* ghat, int64_t batch, int reps, dou
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   *avg_ms = ms / reps;
+  return 0;
+}
+
+int afd_field_split(afd_plan* p, int64_t* onchip, int64_t* twopass, void* stream) {
+  if (!p || !onchip || !twopass) return fail(AFD_E_INVALID, "NULL argument");
+  int rc;
+  if ((rc = set_device(p))) return rc;
+  const int64_t rows = p->m1 - p->m0;
+  if (!p->big) {
+    *onchip = rows;
+    *twopass = 0;
+    return 0;
+  }
+  if (!p->pruned) {
+    *onchip = 0;
+    *twopass = rows;
+    return 0;
+  }
+  int ms = 0;
+  CU(cudaMemcpyAsync(&ms, p->mstar, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  CU(cudaStreamSynchronize((cudaStream_t)stream));
+  *onchip = std::max<int64_t>(0, std::min<int64_t>(rows, (int64_t)ms - p->m0));
+  *twopass = rows - *onchip;
   return 0;
 }
 

@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(256 * GROUPS, 1)
 col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __restrict__ twst,
                const double* __restrict__ scales, long long row0, long long row1,
                Cand* __restrict__ cand, const int* __restrict__ stopped,
-               const __grid_constant__ CUtensorMap ymap) {
+               const int* __restrict__ lim, const __grid_constant__ CUtensorMap ymap) {
   using C = ColTma<KC, GROUPS>;
   constexpr int COLS = C::COLS, U = C::U, TILE = C::TILE;
   extern __shared__ __align__(128) double2 csm[];
@@ -104,6 +104,11 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
   // stage's previous tile (a parity wait alone would alias to that phase).
   __shared__ __align__(8) unsigned long long rel[C::STAGES];
   if (stopped && *stopped) return;
+  if (lim != nullptr) {  // pruned field: the rows below *lim were done on chip
+    const long long l = *lim;
+    if (l > row0) row0 = l < row1 ? l : row1;
+    if (row0 >= row1) return;
+  }
   __shared__ uint32_t tm_base_s;
   const long long N = 1LL << K;
   const int rows = (int)(row1 - row0);

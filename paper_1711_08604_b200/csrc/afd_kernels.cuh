@@ -181,6 +181,18 @@ __device__ __forceinline__ unsigned any_gt4(unsigned flag, const double (&m)[4],
   return out;
 }
 
+// Sub-transform mapping of a pruned large-N field (big_pruned_field): the
+// kernel's "signals" are the Q = N_big / N pre-twiddled spectra of one
+// N_big-point row set, so signal q's output p is the big field's position
+// j = q + Q p of row s (flat s N_big + j), and rows at or above *lim (the
+// first row whose weight tail is not negligible, prune_rows_kernel) are
+// left to the two-pass path.  Default: identity (flat s N + j, no limit).
+struct SubMap {
+  long long row_stride;  // flat index row stride (0: N)
+  int q_mul;             // 0: j = p; else j = blockIdx.y + q_mul * p
+  const int* lim;        // device row limit or null
+};
+
 template <int K, int RB, int G, bool MATERIALIZE, bool TM = false, bool FAST = false>
 __global__ void __launch_bounds__(Geo<K, RB>::T * G, (RB <= 3 && Geo<K, RB>::T * G <= 512) ? 2 : 1)
 field_kernel(const double2* __restrict__ ghat,     // [batch][N]
@@ -195,7 +207,8 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
              const double2* __restrict__ tw_img,   // SmemTw<K,RB> image (one bulk copy)
              int pp,                               // 1: offset the row-groups (FieldHook)
              unsigned* __restrict__ row_ctr,       // dynamic rows: [batch][2] counters or null
-             int launch_id) {                      // selects / resets the counter pair
+             int launch_id,                        // selects / resets the counter pair
+             SubMap sub) {                         // pruned large-N mapping (launched without PDL)
   using Gm = Geo<K, RB>;
   constexpr int N = Gm::N, T = Gm::T, P = Gm::P;
   extern __shared__ double2 smem[];
@@ -277,6 +290,10 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
 
   // row counts fit 32 bits (M <= 2^31); 32-bit loop state keeps registers
   // for the butterflies
+  if (sub.lim != nullptr) {
+    const long long l = *sub.lim;
+    if (l < row1) row1 = l > row0 ? l : row0;
+  }
   const int rows = (int)(row1 - row0);
   const int per_round = (int)gridDim.x * Gr;
   // Row-groups of >= 32 threads synchronise on their own named barrier and
@@ -518,8 +535,13 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   __syncthreads();  // all groups done before the block-wide reduction
   Cand best;
   best.mag = best_mag;
-  best.flat = best_sl >= 0 ? (row0 + best_sl) * (long long)N + out_pos<K, RB>(tp, best_i)
-                           : 0x7fffffffffffffffLL;
+  if (best_sl >= 0) {
+    const long long j = out_pos<K, RB>(tp, best_i);
+    best.flat = (row0 + best_sl) * (sub.row_stride ? sub.row_stride : (long long)N) +
+                (sub.q_mul ? (long long)sig + (long long)sub.q_mul * j : j);
+  } else {
+    best.flat = 0x7fffffffffffffffLL;
+  }
   best.re = best_re;
   best.im = best_im;
   // CTA reduction of the candidates (first maximum).

@@ -1,0 +1,116 @@
+// afd_pruned.cuh — the fast large-N field as on-chip 4096-point transforms
+// (AFD_PLAN_FAST, N = 2^K > 8192; BASELINE c2, c4).
+//
+// The field of row s is F_s(j) = scale_s sum_l r_s^l G^_l e^{+2 pi i l j / N}
+// (transform.py:185-201).  Its weights decay geometrically, so for all but
+// the radii closest to 1 the terms l >= L = 4096 are far below the
+// transform's own rounding: with T = max_l |G^_l| and
+// B_s = max_{l < L} r_s^l |G^_l| (the largest kept term),
+//     |sum_{l >= L} r^l G^_l e^{..}| <= T r^L / (1 - r) <= 2^-64 B_s
+// is ~2^-11 of the FP64 rounding error of any N-point transform of the row
+// (>= 2^-53 B_s per stage).  For such a row, split j = q + Q p (Q = N / L):
+//     F_s(q + Q p) = scale_s sum_{l < L} r_s^l (G^_l e^{2 pi i l q / N}) e^{2 pi i l p / L},
+// an L-point inverse transform of the pre-twiddled spectrum
+// g^(q)_l = G^_l e^{2 pi i l q / N}, which does not depend on the row.  So
+// the field over the prunable rows is the N = 4096 field kernel run on a
+// batch of Q spectra g^(q) with the big plan's radii and scales: on chip,
+// no row-batch intermediate in HBM, 12 butterfly stages instead of 20.
+// Rows that fail the test (the last ~1% of r_m = m/M at c4) keep the
+// two-pass path (pass A + TMA column pass), limited on the device to rows
+// at or above the first failing row, so the loop stays free of host syncs
+// and graph-capturable.  The fast engine's contract (identical grid
+// indices, 1e-9 relative) is unchanged; exact mode never prunes.
+#pragma once
+
+#include "afd_big.cuh"
+
+namespace afd {
+
+constexpr int kPruneK = 12;  // on-chip sub-transform length L = 2^kPruneK
+
+// *mstar = m1, *tmax = 0 (the tail maximum is max-reduced on its bits)
+__global__ void prune_init_kernel(int* mstar, long long m1, unsigned long long* tmax) {
+  *mstar = (int)m1;
+  *tmax = 0ull;
+}
+
+// T^2 = max_l |G^_l|^2 over the whole spectrum (an upper bound of the tail's)
+__global__ void prune_tail_kernel(const double2* __restrict__ ghat, long long n,
+                                  unsigned long long* tmax) {
+  double m = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double2 v = __ldg(ghat + i);
+    m = fmax(m, fma(v.x, v.x, v.y * v.y));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  // non-negative doubles order like their bit patterns
+  if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(tmax, (unsigned long long)__double_as_longlong(m));
+}
+
+// G^_l of a large-N plan's field spectrum (pass-A layout, big_pass_col
+// out_mode 4: position rev(l) permuted by perm_of_pos)
+__device__ __forceinline__ double2 spectrum_at(const double2* __restrict__ ghat_perm, int l,
+                                               int K, int ka) {
+  return __ldg(ghat_perm + perm_of_pos(brev_rt(l, K), ka));
+}
+
+// First row s in [m0, m1) whose tail is not negligible:
+//   log2 T + L log2 r - log2(1 - r) > log2 B_s - 64  ->  atomicMin(mstar, s).
+// One warp per row; the CTA stages log2 |G^_l| (l < L, natural order from
+// the bit-reversed spectrum) in shared memory.  A stopped signal pins
+// mstar to m0 (and the field kernels then do nothing).
+__global__ void __launch_bounds__(256) prune_rows_kernel(
+    int K, int ka, const double2* __restrict__ ghat_rev, const double* __restrict__ radii, long long m0,
+    long long m1, const unsigned long long* __restrict__ tmax, const int* __restrict__ stopped,
+    int* mstar) {
+  constexpr int L = 1 << kPruneK;
+  __shared__ double lg[L];
+  if (stopped && *stopped) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicMin(mstar, (int)m0);
+    return;
+  }
+  for (int l = threadIdx.x; l < L; l += blockDim.x) {
+    const double2 v = spectrum_at(ghat_rev, l, K, ka);
+    const double a2 = fma(v.x, v.x, v.y * v.y);
+    lg[l] = a2 > 0.0 ? 0.5 * log2(a2) : -INFINITY;
+  }
+  __syncthreads();
+  const double t2 = __longlong_as_double((long long)*tmax);
+  const double lt = t2 > 0.0 ? 0.5 * log2(t2) : -INFINITY;
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long s = m0 + (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < m1;
+       s += warps) {
+    const double r = radii[s];
+    if (r == 0.0 || lt == -INFINITY) continue;  // no tail at all
+    const double lr = log2(r);
+    double b = -INFINITY;
+    for (int l = lane; l < L; l += 32) b = fmax(b, fma((double)l, lr, lg[l]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+    const double tail = lt + (double)L * lr - log2(1.0 - r);
+    if (lane == 0 && !(tail <= b - 64.0)) atomicMin(mstar, (int)s);
+  }
+}
+
+// g^(q)_l = G^_l e^{+2 pi i l q / N}, q < N / L, l < L (q-major, natural l);
+// the root is the plan's circle table exp(2 pi i m / N) (core.py:87).
+__global__ void pretwiddle_kernel(int K, int ka, const double2* __restrict__ ghat_rev,
+                                  const double2* __restrict__ circle, double2* __restrict__ out,
+                                  const int* __restrict__ stopped) {
+  if (stopped && *stopped) return;
+  constexpr int L = 1 << kPruneK;
+  const long long n = 1LL << K, total = n;  // (N / L) * L entries
+  for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+       x += (long long)gridDim.x * blockDim.x) {
+    const long long q = x >> kPruneK;
+    const int l = (int)(x & (L - 1));
+    const double2 g = spectrum_at(ghat_rev, l, K, ka);
+    const double2 w = __ldg(circle + (((long long)l * q) & (n - 1)));
+    out[x] = make_double2(fma(g.x, w.x, -(g.y * w.y)), fma(g.x, w.y, g.y * w.x));
+  }
+}
+
+}  // namespace afd

@@ -146,6 +146,15 @@ class Plan:
         return int(self.lib.afd_launch_count(self.handle))
 
     @_locked
+    def field_split(self, stream=None):
+        """(on-chip rows, two-pass rows) of the last large-N fast field
+        evaluation (afd_field_split): the pruned 4096-point transforms vs
+        pass A + the column pass."""
+        a, b = C.c_int64(), C.c_int64()
+        _capi.check(self.lib.afd_field_split(self.handle, C.byref(a), C.byref(b),
+                                             _stream(stream)))
+        return a.value, b.value
+
     def time_field(self, ghat, reps=20, stream=None):
         """Mean CUDA-event time (ms) of one fused field+argmax launch."""
         ghat = self._signal(ghat)

@@ -740,10 +740,24 @@ def test_bench_line_contract(afd):
     assert abs(d["value"] - evals / (d["ms_per_step"] * 1e-3)) <= 1e-6 * d["value"]
     assert 0.3 * d["value"] < d["e2e"]["value"] < 1.05 * d["value"]
     r = d["roofline"]
-    assert r["bound"] == "hbm" and r["unit"] == "GB/s"
-    achieved = r["evals_per_launch"] * r["bytes_per_eval"] / (r["launch_ms"] * 1e-3) / 1e9
+    # the binding roofline of the (pruned) fast field: FP64 when most rows
+    # run on chip, HBM when they take the two-pass path
+    if r["bound"] == "hbm":
+        assert r["unit"] == "GB/s"
+        achieved = r["evals_per_launch"] * r["bytes_per_eval"] / (r["launch_ms"] * 1e-3) / 1e9
+    else:
+        assert r["bound"] == "fp64" and r["unit"] == "TFLOP/s"
+        achieved = r["evals_per_launch"] * r["flops_per_eval"] / (r["launch_ms"] * 1e-3) / 1e12
     assert abs(achieved - r["achieved"]) <= 1e-6 * achieved
     assert abs(r["frac"] - r["achieved"] / r["peak"]) <= 1e-9 and 0.0 < r["frac"] < 1.0
+    sp = r.get("split")
+    if sp is not None:
+        rows = d["config"]["m"]
+        assert sp["onchip_rows"] + sp["twopass_rows"] == rows
+        f = (sp["onchip_rows"] * sp["flops_per_eval_onchip"] +
+             sp["twopass_rows"] * sp["flops_per_eval_twopass"]) / rows
+        assert abs(f - r["flops_per_eval"]) <= 1e-9 * f
+        assert abs(r["bytes_per_eval"] - 32.0 * sp["twopass_rows"] / rows) <= 1e-12
     assert r["evals_per_launch"] == d["config"]["n"] * d["config"]["m"]
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
 
