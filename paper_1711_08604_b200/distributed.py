@@ -25,7 +25,8 @@ import numpy as np
 
 from . import _capi
 
-__all__ = ["shard_bounds", "radius_shard_bounds", "live_powers", "decompose_sharded",
+__all__ = ["shard_bounds", "radius_shard_bounds", "live_powers", "expected_twopass",
+           "decompose_sharded",
            "decompose_batch_sharded", "ShardedRunner"]
 
 
@@ -60,22 +61,42 @@ def live_powers(radii, n):
     return live
 
 
+def expected_twopass(radii, n, onchip=4096):
+    """Rows the pruned fast field (csrc/afd_pruned.cuh) is expected to leave
+    to the two-pass path: those whose weight tail r^l, l >= `onchip`,
+    exceeds 2^-64 of the largest kept term even for a flat spectrum,
+    r^L / (1 - r) > 2^-64.  (The device decides per step from the actual
+    spectrum; this is the plan-time estimate used to balance shards.)"""
+    r = np.asarray(radii, dtype=np.float64)
+    with np.errstate(divide="ignore"):
+        lt = onchip * np.log2(np.where(r > 0.0, r, 1.0)) - np.log2(1.0 - r)
+    return (r > 0.0) & (lt > -64.0)
+
+
 def radius_shard_bounds(radii, n, rank, world, exact=True):
     """Contiguous radius block [m0, m1) of `rank` balanced by field cost.
 
-    For the exact large-N field (N > 8192) a row costs its 32 B per eval of
-    row-batch intermediate plus 8 B per live r^l entry (live_powers), so
-    rows with r <= 0.5 are cheaper and equal row counts leave the low-radius
-    ranks idle at the end of every step; blocks are cut at equal cumulative
-    cost instead.  Otherwise (fast mode: r^l formed on chip; on-chip N)
-    every row costs the same and this is shard_bounds.  Blocks stay
-    rank-ordered and non-empty, so the lowest-flat-index tie rule holds."""
+    Large N (> 8192):
+    * exact field: a row costs its 32 B per eval of row-batch intermediate
+      plus 8 B per live r^l entry (live_powers) — rows with r <= 0.5 are
+      cheaper;
+    * fast field: rows whose weight tail is negligible run on chip (the
+      pruned field) and the few radii closest to 1 take the two-pass path,
+      measured 2.2x the cost per row (c4: 123 vs 56 ms per step), so those
+      rows weigh 2.2 (expected_twopass).
+    Blocks are cut at equal cumulative cost, so the high-radius rank does
+    not set the step time.  On-chip N: every row costs the same and this is
+    shard_bounds.  Blocks stay rank-ordered and non-empty, so the
+    lowest-flat-index tie rule holds."""
     m = len(radii)
-    if not exact or n <= 8192 or world == 1:
+    if n <= 8192 or world == 1:
         return shard_bounds(m, rank, world)
     if world < 1 or not 0 <= rank < world:
         raise ValueError("rank %d outside world of %d" % (rank, world))
-    cost = 32.0 + 8.0 * live_powers(radii, n) / float(n)
+    if exact:
+        cost = 32.0 + 8.0 * live_powers(radii, n) / float(n)
+    else:
+        cost = np.where(expected_twopass(radii, n), 2.2, 1.0)
     cum = np.concatenate([[0.0], np.cumsum(cost)])
 
     def cut(p):

@@ -103,7 +103,8 @@ def test_radius_shard_bounds_balance_the_exact_field():
     and balanced in field cost (32 B + 8 B per live r^l entry per eval) to
     within a row; fast mode and on-chip N fall back to row counts."""
     from paper_1711_08604_b200 import workloads as W
-    from paper_1711_08604_b200.distributed import live_powers, radius_shard_bounds, shard_bounds
+    from paper_1711_08604_b200.distributed import (expected_twopass, live_powers,
+                                                   radius_shard_bounds, shard_bounds)
     n, m = 1 << 16, 4096
     radii = W.radii_for(m)
     cost = 32.0 + 8.0 * live_powers(radii, n) / n
@@ -114,8 +115,12 @@ def test_radius_shard_bounds_balance_the_exact_field():
         assert all(h > l for l, h in blocks)
         share = [cost[l:h].sum() for l, h in blocks]
         assert max(share) - min(share) <= 2 * cost.max()
-        assert [radius_shard_bounds(radii, n, r, world, exact=False) for r in range(world)] == \
-            [shard_bounds(m, r, world) for r in range(world)]
+        fast = [radius_shard_bounds(radii, n, r, world, exact=False) for r in range(world)]
+        assert fast[0][0] == 0 and fast[-1][1] == m
+        assert all(a[1] == b[0] for a, b in zip(fast, fast[1:]))
+        w = np.where(expected_twopass(radii, n), 2.2, 1.0)
+        share = [w[l:h].sum() for l, h in fast]
+        assert max(share) - min(share) <= 2 * 2.2
         assert [radius_shard_bounds(radii, 4096, r, world) for r in range(world)] == \
             [shard_bounds(m, r, world) for r in range(world)]
     tiny = (0.1, 0.2, 0.9)
