@@ -964,3 +964,77 @@ def test_c4_exact_all_steps_replayed_by_oracle(afd):
     r = O.replay_check(g, radii, rec[0], w.steps, rows_per_step=3, threads=O.max_threads())
     assert r["ok"], r["why"]
     assert np.array_equal(rem[0], r["remainder"])
+
+
+# ---------------------------------------------------------------------------
+# pruned fast field (csrc/afd_pruned.cuh): rows with a negligible weight tail
+# as on-chip 4096-point transforms of pre-twiddled spectra, the rest through
+# the two-pass path from the first failing row on (decided on the device)
+# ---------------------------------------------------------------------------
+def _first_unprunable(ghat, radii, L=4096):
+    """numpy statement of prune_rows_kernel's test: first row whose tail bound
+    T r^L / (1 - r) exceeds 2^-64 max_{l<L} r^l |G^_l| (log2 domain), with a
+    band of +-1e-6 in the exponent for the device's rounding."""
+    a = np.abs(ghat)
+    lt = np.log2(a.max())
+    lg = np.where(a[:L] > 0, np.log2(np.where(a[:L] > 0, a[:L], 1.0)), -np.inf)
+    lo = hi = len(radii)
+    for s, r in enumerate(radii):
+        if r == 0.0:
+            continue
+        lr = np.log2(r)
+        b = np.max(np.arange(L) * lr + lg)
+        tail = lt + L * lr - np.log2(1.0 - r)
+        if tail > b - 64.0 + 1e-6:
+            hi = min(hi, s)
+        if tail > b - 64.0 - 1e-6:
+            lo = min(lo, s)
+    return lo, hi
+
+
+@pytest.mark.parametrize("radii", [
+    tuple(i / 64 for i in range(64)),                                   # c2-like tail
+    (0.3, 0.999, 0.5, 0.9, 0.99995, 0.1, 0.7, 0.0, 0.95, 0.2),          # unsorted, early long row
+    (0.0, 0.2, 0.4),                                                    # all on chip
+    (0.9999, 0.99999, 0.5),                                             # long rows first
+])
+def test_pruned_field_argmax_and_split(afd, radii):
+    """The pruned field's first maximum is the oracle's (same flat index,
+    |F|^2 within 1e-12), and the device's on-chip / two-pass split is the
+    first row failing the tail test."""
+    core, engine = afd
+    import torch
+    from paper_1711_08604_b200 import workloads as W
+    n = 1 << 16
+    g = W.pole_sum(n, 32, 0.995, 99)
+    ghat = O.dft_forward(g)
+    plan = engine.Plan(radii, n, fast=1)
+    got = np.frombuffer(plan.field_argmax(torch.from_numpy(ghat).cuda()).cpu().numpy().tobytes(),
+                        O.CAND_DTYPE)[0]
+    onchip, twopass = plan.field_split()
+    ref = O.field_argmax(ghat, np.array(radii))
+    assert int(got["flat"]) == int(ref["flat"])
+    assert abs(got["mag"] - ref["mag"]) <= 1e-12 * ref["mag"]
+    lo, hi = _first_unprunable(ghat, radii)
+    assert lo <= onchip <= hi and onchip + twopass == len(radii)
+
+
+def test_pruned_fast_decompose_long_rows_and_threshold(afd):
+    """A fast decomposition whose grid mixes on-chip and two-pass rows (radii
+    up to 0.99999) and stops on the threshold: identical poles and 1e-9
+    against the oracle, and the same number of steps."""
+    core, _ = afd
+    from paper_1711_08604_b200 import workloads as W
+    n = 1 << 16
+    radii = (0.0, 0.2, 0.5, 0.8, 0.9, 0.97, 0.999, 0.99999)
+    g = W.pole_sum(n, 8, 0.999, 123)
+    grid = core.ParameterGrid(radii, n)
+    d = core.decompose(g, grid, max_terms=12, threshold=0.02, engine="fft-fast")
+    o = O.decompose(g, np.array(radii), max_terms=12, threshold=0.02)
+    assert len(d.steps) == len(o.steps)
+    assert [s.point.angle_index for s in d.steps] == list(o.steps["j"])
+    assert [s.point.radius for s in d.steps] == list(o.steps["radius"])
+    oc = o.steps["c_re"] + 1j * o.steps["c_im"]
+    c = np.array([s.coefficient for s in d.steps])
+    assert np.all(np.abs(c - oc) <= FAST_TOL * np.abs(oc))
+    assert np.abs(d.remainder - o.remainder).max() <= FAST_TOL * np.abs(o.remainder).max()
