@@ -144,3 +144,55 @@ def test_two_process_cuda_shards_over_gloo(case, world):
         assert j == list(g["j"]) and radius == list(g["radius"])
         assert coeff == list(g["coeff"]) and resid == list(g["residual"])
         assert np.array_equal(rem, g["remainder"])
+
+
+def _gloo_fast_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1711_08604_b200 import core, distributed, workloads as W
+        n = 1 << 16
+        radii = tuple(i / 48 for i in range(48)) + (0.9995, 0.99995)
+        g = W.pole_sum(n, 16, 0.999, 321)
+        grid = core.ParameterGrid(radii, n)
+        d = distributed.decompose_sharded(g, grid, max_terms=4, engine_name="fft-fast")[0]
+        q.put((rank, [s.point.angle_index for s in d.steps], [s.point.radius for s in d.steps],
+               [s.coefficient for s in d.steps], d.remainder))
+    except Exception as e:  # surfaced by the parent
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_process_cuda_shards_fast_pruned():
+    """Two processes, each driving a real fast CUDA shard plan (N = 2^16: the
+    pruned on-chip field plus two-pass rows for the radii closest to 1, the
+    second rank holding them), exchanging candidates over gloo: identical
+    poles and 1e-9 against the oracle on every rank."""
+    import torch.multiprocessing as mp
+    from paper_1711_08604_b200 import workloads as W
+    import oracle as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_gloo_fast_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+    n = 1 << 16
+    radii = np.array(tuple(i / 48 for i in range(48)) + (0.9995, 0.99995))
+    o = O.decompose(W.pole_sum(n, 16, 0.999, 321), radii, max_terms=4)
+    oc = o.steps["c_re"] + 1j * o.steps["c_im"]
+    for r in res:
+        assert len(r) == 5, r
+        _, j, radius, coeff, rem = r
+        assert j == list(o.steps["j"]) and radius == list(o.steps["radius"])
+        assert np.all(np.abs(np.array(coeff) - oc) <= 1e-9 * np.abs(oc))
+        assert np.abs(rem - o.remainder).max() <= 1e-9 * np.abs(o.remainder).max()
+
