@@ -217,6 +217,18 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   const int tp = threadIdx.x % T;
   const int Gr = blockDim.x / T;  // row-groups actually launched (<= G)
   using TwT = SmemTw<K, RB>;
+  if (sub.lim != nullptr && *sub.lim <= row0) {
+    // pruned launch with no on-chip rows this step (all rows long, or the
+    // signal stopped): a neutral candidate, no TMEM or twiddle setup
+    if (!MATERIALIZE && threadIdx.x == 0) {
+      Cand c;
+      c.mag = -1.0;
+      c.flat = 0x7fffffffffffffffLL;
+      c.re = c.im = 0.0;
+      cand_out[(size_t)sig * gridDim.x + blockIdx.x] = c;
+    }
+    return;
+  }
   FSTAMP(0, 0);
 #ifdef AFD_FIELD_TIMING
   if (tp == 0 && blockIdx.x < 512 && g < 2) {
