@@ -49,12 +49,19 @@ extern "C" {
  * residual = discrete_energy(G_{k+1}).  flags bit 0: the pole's
  * sqrt(1 - abs(a) ** 2) could not be taken from the plan's table of libm
  * pow(h, 2.0) values (never for grid poles: kernel_norm_grid) and the
- * device's h*h is not provably CPython's pow.  72 bytes. */
+ * device's h*h is not provably CPython's pow.  margin (fast engine with
+ * AFD_PLAN_MARGINS): the step's top-2 relative margin (|F|^2_max -
+ * |F|^2_runner-up) / |F|^2_max over the whole grid, the runner-up being the
+ * largest |F|^2 at any other grid point; a fast pick is provably the
+ * reference's when the margin exceeds the fast field's error (~1e-14).  NaN
+ * when not tracked (exact engine, fast plans without AFD_PLAN_MARGINS,
+ * dc_first step, radius-sharded runs).
+ * 72 bytes. */
 typedef struct afd_step {
   int64_t s, j;
   double radius, a_re, a_im, c_re, c_im, residual;
   int32_t flags;
-  int32_t pad;
+  float margin;
 } afd_step;
 
 /* Grid candidate: |F|^2, flat index s*N + j (global s), F.  32 bytes.
@@ -82,6 +89,11 @@ int afd_version(void);
  *   after the argmax (update, energy, forward transform, records) stays
  *   bit-exact arithmetic.  Default (0): bit-identical to the reference. */
 #define AFD_PLAN_FAST 1
+/* AFD_PLAN_MARGINS (with AFD_PLAN_FAST): the field kernels also track each
+ * step's runner-up |F|^2 and the records carry the top-2 margin
+ * (afd_step.margin); costs ~10-15% of the field (every value above a
+ * thread's runner-up takes the slow path of the screened epilogue). */
+#define AFD_PLAN_MARGINS 2
 
 /* Create a plan.  radii_host/scales_host hold all M radii/scales
  * (core.ParameterGrid.radii, core.py:115-145); the plan evaluates global

@@ -25,12 +25,13 @@ AFD_E_NOMEM = -4
 STEP_DTYPE = np.dtype([("s", np.int64), ("j", np.int64), ("radius", np.float64),
                        ("a_re", np.float64), ("a_im", np.float64),
                        ("c_re", np.float64), ("c_im", np.float64),
-                       ("residual", np.float64), ("flags", np.int32), ("pad", np.int32)])
+                       ("residual", np.float64), ("flags", np.int32), ("margin", np.float32)])
 CAND_DTYPE = np.dtype([("mag2", np.float64), ("flat", np.int64),
                        ("re", np.float64), ("im", np.float64)])
 
 STEP_FLAG_POW_AMBIGUOUS = 1
 PLAN_FAST = 1  # AFD_PLAN_FAST
+PLAN_MARGINS = 2  # AFD_PLAN_MARGINS
 
 # (name, restype, argtypes) for every symbol include/afd_capi.h declares
 _VP = C.c_void_p

@@ -22,6 +22,9 @@ the transform engine with the field computed in fast FP64 arithmetic
 (AFD_PLAN_FAST: FMA-fused butterflies, r^l formed on chip): the selected
 poles are identical to the reference's and coefficients, remainders and
 errors agree to ~1e-14 relative (the north-star contract is 1e-9).
+``engine="fft-fast-margins"`` is the same engine with each step's top-2
+relative margin of |F|^2 over the grid recorded in ``Decomposition.margins``
+(~10-15% slower field).
 ``parallel`` is accepted for signature compatibility; the device path is
 always parallel and, like the reference's threaded path, produces
 identical results.
@@ -47,7 +50,8 @@ __all__ = [
 ]
 
 RADIUS_WARN_LIMIT = 0.95  # core.py:59
-ENGINES = ("fft", "direct", "fft-fast")
+ENGINES = ("fft", "direct", "fft-fast", "fft-fast-margins")
+_FAST_LEVEL = {"fft-fast": 1, "fft-fast-margins": 2}  # engine.Plan(fast=...)
 
 
 def _engine():
@@ -173,6 +177,9 @@ class Decomposition:
     # Per-step device flags (bit 0: CPython's pow(|a|, 2) not provably equal
     # to |a|*|a| for this pole, see csrc/afd_common.cuh).  Not in the reference.
     step_flags: tuple = field(default=(), repr=False)
+    # Per-step top-2 relative margin of |F|^2 over the grid (fast engine;
+    # NaN where not tracked), SURVEY.md §7.3(a).  Not in the reference.
+    margins: tuple = field(default=(), repr=False)
 
     def poles(self):
         return np.array([s.point.value for s in self.steps], dtype=np.complex128)
@@ -333,7 +340,8 @@ def _build(grid, n, engine, rec, count, initial, remainder):
         sa(st, "__dict__", {"point": pt, "coefficient": c[k], "residual_energy": res[k]})
         steps.append(st)
     return Decomposition(tuple(steps), grid, n, float(initial), engine, remainder=remainder,
-                         step_flags=tuple(rec["flags"].tolist()))
+                         step_flags=tuple(rec["flags"].tolist()),
+                         margins=tuple(rec["margin"].astype(np.float64).tolist()))
 
 
 def decompose(g, grid, max_terms=10, threshold=None, engine="fft", dc_first=False,
@@ -370,7 +378,7 @@ def decompose_batch(signals, grid, max_terms=10, threshold=None, engine="fft", d
         _check_decompose_args(sig, grid, max_terms, threshold, engine)
     b, n = sig.shape
     plan = _engine().get_plan(grid.radii, n, batch=b, engine=1 if engine == "direct" else 0,
-                              fast=engine == "fft-fast")
+                              fast=_FAST_LEVEL.get(engine, 0))
     rec, counts, initial, rem, _, _ = plan.decompose_host(sig, int(max_terms), threshold,
                                                           dc_first)
     if b == 1:
@@ -396,6 +404,7 @@ def _build_batch(grid, n, engine, rec, counts, initial, rem):
     c = (rec["c_re"] + 1j * rec["c_im"]).tolist()
     res = rec["residual"].tolist()
     flags = rec["flags"].tolist()
+    margins = rec["margin"].astype(np.float64).tolist()
     counts = counts.tolist()
     initial = initial.tolist()
     new, sa = object.__new__, object.__setattr__
@@ -411,7 +420,8 @@ def _build_batch(grid, n, engine, rec, counts, initial, rem):
             sa(st, "__dict__", {"point": pt, "coefficient": ci[k], "residual_energy": si[k]})
             steps.append(st)
         out.append(Decomposition(tuple(steps), grid, n, initial[i], engine, remainder=rem[i],
-                                 step_flags=tuple(flags[i][:count])))
+                                 step_flags=tuple(flags[i][:count]),
+                                 margins=tuple(margins[i][:count])))
     return out
 
 

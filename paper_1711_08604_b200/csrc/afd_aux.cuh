@@ -106,8 +106,11 @@ __global__ void cand_reduce_kernel(const Cand* __restrict__ in, int n_per, Cand*
 // First stage of a large candidate reduction: CTA b reduces in[b*per ..
 // min((b+1)*per, n)) -> out[b] (loads issued 4 at a time; the first-maximum
 // merge is order-free, so any split gives the same result).
+// With runner-up slots (in2/out2 non-null): out2[b] = the largest of the
+// range's runner-ups and of its candidates other than the winner.
 __global__ void cand_partial_kernel(const Cand* __restrict__ in, int n, int per,
-                                    Cand* __restrict__ out) {
+                                    Cand* __restrict__ out, const double* __restrict__ in2 = nullptr,
+                                    double* __restrict__ out2 = nullptr) {
   Cand b = cand_none();
   const int lo = blockIdx.x * per, hi = min(n, lo + per);
   for (int i = lo + threadIdx.x; i < hi; i += 4 * blockDim.x) {
@@ -122,6 +125,16 @@ __global__ void cand_partial_kernel(const Cand* __restrict__ in, int n, int per,
   }
   b = block_argmax(b);
   if (threadIdx.x == 0) out[blockIdx.x] = b;
+  if (in2 != nullptr) {
+    double r = -1.0;
+    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      r = fmax(r, in2[i]);
+      const Cand c = in[i];
+      if (c.flat != b.flat) r = fmax(r, c.mag);
+    }
+    r = block_max(r);
+    if (threadIdx.x == 0) out2[blockIdx.x] = r;
+  }
 }
 
 __global__ void neutral_cand_kernel(Cand* out, int batch) {

@@ -645,11 +645,12 @@ big_pass_col8(int K, int b0, double2* __restrict__ Y, const double2* __restrict_
   }
 }
 
-__global__ void cand_init_kernel(Cand* c, int n) {
+__global__ void cand_init_kernel(Cand* c, int n, double* c2 = nullptr) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     c[i].mag = -1.0;
     c[i].flat = 0x7fffffffffffffffLL;
     c[i].re = c[i].im = 0.0;
+    if (c2 != nullptr) c2[i] = -1.0;
   }
 }
 
@@ -661,7 +662,7 @@ struct BigSel {
   double radius;
   double2 a, coeff;
   int valid;
-  int pad;
+  float margin;  // top-2 relative margin (fast engine) or NaN
 };
 
 // numpy pairwise node sums over aligned kNodeLen slices:
@@ -703,13 +704,14 @@ __global__ void __launch_bounds__(256)
 big_select_kernel(int k, int dc_first, int K, const Cand* __restrict__ cand, int ncand,
                   const double* __restrict__ nodes, int nnodes,
                   const double* __restrict__ radii, const double2* __restrict__ circle,
-                  const State* __restrict__ state, BigSel* __restrict__ sel) {
+                  const State* __restrict__ state, BigSel* __restrict__ sel,
+                  const double* __restrict__ cand2 = nullptr) {
   __shared__ double re[kMaxNodes], im[kMaxNodes];
   if (state->stopped) return;
   const long long N = 1LL << K;
   BigSel out;
   out.valid = 1;
-  out.pad = 0;
+  out.margin = __int_as_float(0x7fc00000);
   if (k == 0 && dc_first) {
     for (int i = threadIdx.x; i < nnodes; i += blockDim.x) {
       re[i] = nodes[2 * i];
@@ -740,6 +742,15 @@ big_select_kernel(int k, int dc_first, int K, const Cand* __restrict__ cand, int
     }
     __syncthreads();
     b = red[0];
+    if (cand2 != nullptr) {  // runner-up of the step (fast engine)
+      double r = -1.0;
+      for (int i = threadIdx.x; i < ncand; i += blockDim.x) {
+        r = fmax(r, cand2[i]);
+        if (cand[i].flat != b.flat) r = fmax(r, cand[i].mag);
+      }
+      r = block_max(r);
+      out.margin = top2_margin(b.mag, r);
+    }
     out.s = b.flat / N;
     out.j = b.flat % N;
     out.radius = radii[out.s];
@@ -828,7 +839,7 @@ big_finalize_kernel(int k, int K, int max_terms, double threshold, const double*
   rec.c_im = s.coeff.y;
   rec.residual = energy;
   rec.flags = *amb ? kStepPowAmbiguous : 0;
-  rec.pad = 0;
+  rec.margin = s.margin;
   steps[k] = rec;
   state->nsteps = k + 1;
   state->flags |= rec.flags;

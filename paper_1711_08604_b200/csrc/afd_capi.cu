@@ -86,6 +86,8 @@ struct afd_plan {
   double2* gin = nullptr;     // [max_batch][N] staged input
   State* state = nullptr;     // [max_batch]
   Cand* cand = nullptr;       // [max_batch][ncand_cap]
+  double* cand2 = nullptr;    // [max_batch][ncand_cap] runner-ups (AFD_PLAN_MARGINS)
+  bool margins = false;
   int ncand_cap = 0;
   Step* steps = nullptr;      // [max_batch][steps_cap]
   int steps_cap = 0;
@@ -111,6 +113,8 @@ struct afd_plan {
   double2* Y = nullptr;        // [big_rows][N]
   Cand* big_cand = nullptr;    // [big_rows][N/16/256]
   Cand* big_part = nullptr;    // [kBigParts] first-stage reduction of big_cand
+  double* big_cand2 = nullptr; // runner-ups of big_cand / big_part (fast engine)
+  double* big_part2 = nullptr;
   unsigned* row_ctr = nullptr; // [max_batch][2] field row counters (dynamic rows)
   int* pw_len = nullptr;       // [m1-m0] first l with r^l == 0 (or N)
   CUtensorMap ymap;            // Y as [big_rows][256][2^ka complex] (8-stage TMA column pass)
@@ -122,6 +126,7 @@ struct afd_plan {
   double2* ghq = nullptr;      // [Q][4096] pre-twiddled spectra
   double2* tw_img12 = nullptr; // SmemTw<12,4> (c, t) image
   Cand* pr_cand = nullptr;     // [Q][pr_ncta]
+  double* pr_cand2 = nullptr;
   int pr_ncta = 0;
   int* mstar = nullptr;        // first row left to the two-pass path
   unsigned long long* tmax = nullptr;
@@ -184,6 +189,13 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 // ---------------------------------------------------------------------------
 // Templated launchers, dispatched on K.
 // ---------------------------------------------------------------------------
+// Runner-up slots (fast engine, on-chip N) beside the plan's own field
+// candidates; null for exact plans, the direct engine and foreign
+// candidate arrays (e.g. all-gathered shards), whose records carry NaN.
+const double* runner_ups_for(const afd_plan* p, const Cand* cand) {
+  return (p->margins && p->engine == 0 && cand != nullptr && cand == p->cand) ? p->cand2 : nullptr;
+}
+
 namespace {
 
 // Field kernel geometry: 8 points per thread (radix-8 register passes,
@@ -262,7 +274,14 @@ int setup_field_kernel(int* occ) {
     CU(cudaFuncSetAttribute(field_kernel<K, kFieldRB, groups_for<K>(), MAT, true, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)field_smem<K>()));
+    if constexpr (!MAT)
+      CU(cudaFuncSetAttribute(field_kernel<K, kFieldRB, groups_for<K>(), MAT, true, true, true>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)field_smem<K>()));
   }
+  if constexpr (!MAT)
+    CU(cudaFuncSetAttribute(field_kernel<K, kFieldRB, groups_for<K>(), MAT, false, true, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem<K>()));
   if (occ) CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, field_block<K>(), field_smem<K>()));
   return 0;
 }
@@ -296,10 +315,17 @@ int setup_kernels(afd_plan* p) {
   if ((rc = setup_field_kernel<K, true>(nullptr))) return rc;
   CU(cudaFuncSetAttribute(step_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)RowSmem<K>::bytes));
+  CU(cudaFuncSetAttribute(step_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)RowSmem<K>::bytes));
   if constexpr (use_cluster_step<K>()) {
     CU(cudaFuncSetAttribute(step_cluster_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)ClusterSmem<K>::bytes));
     CU(cudaFuncSetAttribute(step_cluster_kernel<K>,
+                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CU(cudaFuncSetAttribute(step_cluster_kernel<K, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)ClusterSmem<K>::bytes));
+    CU(cudaFuncSetAttribute(step_cluster_kernel<K, true>,
                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   }
   CU(cudaFuncSetAttribute(fft_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -370,16 +396,20 @@ int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64
                               : field_kernel<K, kFieldRB, G, true>);
     kern<<<grid, block, smem, st>>>(ghat, tab, p->scales, p->twst, r0, r1, p->m0, nullptr,
                                     field_out, nullptr, img, field_pp(), (unsigned*)nullptr, 0,
-                                    SubMap{0, 0, nullptr});
+                                    SubMap{0, 0, nullptr, nullptr});
   } else {
-    auto kern = p->fast ? (tm ? field_kernel<K, kFieldRB, G, false, TMC, true>
-                              : field_kernel<K, kFieldRB, G, false, false, true>)
+    const bool mg = runner_ups_for(p, cand) != nullptr;
+    auto kern = p->fast ? (mg ? (tm ? field_kernel<K, kFieldRB, G, false, TMC, true, true>
+                                    : field_kernel<K, kFieldRB, G, false, false, true, true>)
+                              : (tm ? field_kernel<K, kFieldRB, G, false, TMC, true>
+                                    : field_kernel<K, kFieldRB, G, false, false, true>))
                         : (tm ? field_kernel<K, kFieldRB, G, false, TMC>
                               : field_kernel<K, kFieldRB, G, false>);
     CU(launch_pdl(kern, grid, dim3(block), smem, st, ghat, tab,
                   (const double*)p->scales, (const double2*)p->twst, (long long)r0,
                   (long long)r1, (long long)p->m0, cand, (double2*)nullptr, state,
-                  img, field_pp(), row_ctr, launch_id, SubMap{0, 0, nullptr}));
+                  img, field_pp(), row_ctr, launch_id,
+                  SubMap{0, 0, nullptr, const_cast<double*>(runner_ups_for(p, cand))}));
   }
   p->launches++;
   CU(cudaGetLastError());
@@ -389,17 +419,21 @@ int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64
 template <int K>
 int launch_step(afd_plan* p, int k, int max_terms, double thr, int dc_first, const double2* g0,
                 const Cand* cand, int ncand, int64_t batch, Step* steps, cudaStream_t st) {
+  // the fast field's runner-ups travel beside its own candidates
+  const double* c2 = runner_ups_for(p, cand);
   if constexpr (use_cluster_step<K>()) {
-    CU(launch_pdl_cluster(step_cluster_kernel<K>, dim3((unsigned)(batch * ClusterGeo<K>::C)),
+    CU(launch_pdl_cluster(c2 ? step_cluster_kernel<K, true> : step_cluster_kernel<K, false>,
+                  dim3((unsigned)(batch * ClusterGeo<K>::C)),
                   dim3(ClusterGeo<K>::THREADS), ClusterSmem<K>::bytes, st, ClusterGeo<K>::C, k,
                   max_terms, thr, dc_first, g0, p->rem, p->ghat, cand, ncand,
                   (const double*)p->radii, (int)p->m, (const double2*)p->circle,
-                  (const double2*)p->twst, p->state, steps, (const double*)p->pow2));
+                  (const double2*)p->twst, p->state, steps, (const double*)p->pow2, c2));
   } else {
-    CU(launch_pdl(step_kernel<K>, dim3((unsigned)batch), dim3(row_block<K>()),
+    CU(launch_pdl(c2 ? step_kernel<K, true> : step_kernel<K, false>, dim3((unsigned)batch),
+                  dim3(row_block<K>()),
                   RowSmem<K>::bytes, st, k, max_terms, thr, dc_first, g0, p->rem, p->ghat, cand,
                   ncand, (const double*)p->radii, (const double2*)p->circle,
-                  (const double2*)p->twst, p->state, steps, (const double*)p->pow2));
+                  (const double2*)p->twst, p->state, steps, (const double*)p->pow2, c2));
   }
   p->launches++;
   CU(cudaGetLastError());
@@ -520,9 +554,12 @@ int ensure_cand(afd_plan* p, int64_t batch, int ncta) {
   if (ncta > p->ncand_cap) {
     invalidate_graph(p);
     if (p->cand) cudaFree(p->cand);
+    if (p->cand2) cudaFree(p->cand2);
     p->cand = nullptr;
+    p->cand2 = nullptr;
     p->ncand_cap = 0;
     CU(cudaMalloc(&p->cand, sizeof(Cand) * (size_t)p->max_batch * ncta));
+    if (p->margins) CU(cudaMalloc(&p->cand2, sizeof(double) * (size_t)p->max_batch * ncta));
     p->ncand_cap = ncta;
   }
   (void)batch;
@@ -663,6 +700,10 @@ int big_setup(afd_plan* p) {
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ColTma<4, 2>::SMEM));
     CU(cudaFuncSetAttribute(col_tma_kernel<4, false, 2>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ColTma<4, 2>::SMEM));
+    CU(cudaFuncSetAttribute(col_tma_kernel<8, true, 2, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ColTma<8, 2>::SMEM));
+    CU(cudaFuncSetAttribute(col_tma_kernel<4, true, 2, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ColTma<4, 2>::SMEM));
     return 0;
   });
 }
@@ -744,24 +785,27 @@ int big_launch_cols(afd_plan* p, bool inv, int last_mode, int scale_n, int64_t r
       const int64_t tiles = rows * ((int64_t)1 << b0) / (left == 8 ? 16 : 256);
       const unsigned g = (unsigned)std::min<int64_t>(p->sms, tiles);
       const double2* tws = fastf ? p->twct : p->twst;
-      if (kColGroups == 2) {
-        auto k8 = fastf ? col_tma_kernel<8, true, 2> : col_tma_kernel<8, false, 2>;
-        auto k4 = fastf ? col_tma_kernel<4, true, 2> : col_tma_kernel<4, false, 2>;
+      if (kColGroups == 2 || p->margins) {  // (runner-ups: two-group kernels only)
+        const bool mg = fastf && p->margins;
+        auto k8 = mg ? col_tma_kernel<8, true, 2, true>
+                     : fastf ? col_tma_kernel<8, true, 2> : col_tma_kernel<8, false, 2>;
+        auto k4 = mg ? col_tma_kernel<4, true, 2, true>
+                     : fastf ? col_tma_kernel<4, true, 2> : col_tma_kernel<4, false, 2>;
         if (left == 8)
           k8<<<g, 512, ColTma<8, 2>::SMEM, st>>>(p->K, b0, p->Y, tws, p->scales, r0, r0 + rows,
-                                                 p->big_cand, stopped, lim, p->ymap);
+                                                 p->big_cand, stopped, lim, p->big_cand2, p->ymap);
         else
           k4<<<g, 512, ColTma<4, 2>::SMEM, st>>>(p->K, b0, p->Y, tws, p->scales, r0, r0 + rows,
-                                                 p->big_cand, stopped, lim, p->ymap);
+                                                 p->big_cand, stopped, lim, p->big_cand2, p->ymap);
       } else {
         auto k8 = fastf ? col_tma_kernel<8, true> : col_tma_kernel<8>;
         auto k4 = fastf ? col_tma_kernel<4, true> : col_tma_kernel<4>;
         if (left == 8)
           k8<<<g, 256, ColTma<8>::SMEM, st>>>(p->K, b0, p->Y, tws, p->scales, r0, r0 + rows,
-                                              p->big_cand, stopped, lim, p->ymap);
+                                              p->big_cand, stopped, lim, p->big_cand2, p->ymap);
         else
           k4<<<g, 256, ColTma<4>::SMEM, st>>>(p->K, b0, p->Y, tws, p->scales, r0, r0 + rows,
-                                              p->big_cand, stopped, lim, p->ymap);
+                                              p->big_cand, stopped, lim, p->big_cand2, p->ymap);
       }
       p->launches++;
       CU(cudaGetLastError());
@@ -832,7 +876,8 @@ int big_reduce_cands(afd_plan* p, cudaStream_t st, const Cand** parts, int* npar
   const int n = (int)(p->big_rows * big_col_ctas(p));
   const int np = std::min(kBigParts, (n + 255) / 256);
   const int per = (n + np - 1) / np;
-  cand_partial_kernel<<<np, 256, 0, st>>>(p->big_cand, n, per, p->big_part);
+  cand_partial_kernel<<<np, 256, 0, st>>>(p->big_cand, n, per, p->big_part, p->big_cand2,
+                                          p->big_part2);
   p->launches++;
   CU(cudaGetLastError());
   *parts = p->big_part;
@@ -851,7 +896,7 @@ int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, doub
   int rc;
   if (!fout) {
     const int n = (int)(p->big_rows * big_col_ctas(p));
-    cand_init_kernel<<<(n + 255) / 256, 256, 0, st>>>(p->big_cand, n);
+    cand_init_kernel<<<(n + 255) / 256, 256, 0, st>>>(p->big_cand, n, p->big_cand2);
     p->launches++;
   }
   const int* lim = nullptr;
@@ -867,14 +912,16 @@ int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, doub
                                                   stopped);
     using Gm = Geo<kPruneK, kFieldRB>;
     const size_t smem = field_smem<kPruneK>();
-    field_kernel<kPruneK, kFieldRB, 2, false, true, true>
-        <<<dim3((unsigned)p->pr_ncta, (unsigned)Q), Gm::T * 2, smem, st>>>(
+    auto pk = p->margins ? field_kernel<kPruneK, kFieldRB, 2, false, true, true, true>
+                         : field_kernel<kPruneK, kFieldRB, 2, false, true, true>;
+    pk<<<dim3((unsigned)p->pr_ncta, (unsigned)Q), Gm::T * 2, smem, st>>>(
             p->ghq, p->fw12, p->scales, p->twct, (long long)r0, (long long)r1, (long long)p->m0,
             p->pr_cand, nullptr, nullptr, p->tw_img12, field_pp(), (unsigned*)nullptr, 0,
-            SubMap{(long long)p->n, Q, p->mstar});
+            SubMap{(long long)p->n, Q, p->mstar, p->pr_cand2});
     const int n = Q * p->pr_ncta;
     const int np = std::min(kBigParts, (n + 255) / 256);
-    cand_partial_kernel<<<np, 256, 0, st>>>(p->pr_cand, n, (n + np - 1) / np, p->big_cand);
+    cand_partial_kernel<<<np, 256, 0, st>>>(p->pr_cand, n, (n + np - 1) / np, p->big_cand,
+                                            p->pr_cand2, p->big_cand2);
     p->launches += 6;
     CU(cudaGetLastError());
     lim = p->mstar;
@@ -931,8 +978,10 @@ int big_step(afd_plan* p, int sig, int k, int max_terms, double thr, int dc_firs
       if ((rc = big_field(p, ghat_rev, p->m0, p->m1, nullptr, stopped, st))) return rc;
       if ((rc = big_reduce_cands(p, st, &cands, &ncand))) return rc;
     }
+    // runner-ups only for the plan's own field (not all-gathered shards)
     big_select_kernel<<<1, 256, 0, st>>>(k, dc_first, p->K, cands, ncand, nullptr, 0, p->radii,
-                                         p->circle, state, p->sel);
+                                         p->circle, state, p->sel,
+                                         cands == p->big_part ? p->big_part2 : nullptr);
     p->launches++;
   }
   big_update_kernel<<<nn, 256, 0, st>>>(p->K, p->sel, nullptr, rem, p->circle, state, p->nodes,
@@ -1033,7 +1082,10 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
   if (max_batch < 1) return fail(AFD_E_INVALID, "max_batch must be >= 1");
   if (!radii_host || !scales_host || !twiddle_host || !circle_host)
     return fail(AFD_E_INVALID, "NULL host table");
-  if (flags & ~AFD_PLAN_FAST) return fail(AFD_E_INVALID, "unknown plan flags 0x%x", flags);
+  if (flags & ~(AFD_PLAN_FAST | AFD_PLAN_MARGINS))
+    return fail(AFD_E_INVALID, "unknown plan flags 0x%x", flags);
+  if ((flags & AFD_PLAN_MARGINS) && !(flags & AFD_PLAN_FAST))
+    return fail(AFD_E_INVALID, "AFD_PLAN_MARGINS needs AFD_PLAN_FAST");
   if ((flags & AFD_PLAN_FAST) && K > kMaxOnChipK && K != 16 && K != 20)
     return fail(AFD_E_UNSUPPORTED, "fast mode for N = 2^%d not built (2^3..2^13, 2^16, 2^20)", K);
   for (int64_t i = 0; i < m; ++i) {
@@ -1049,6 +1101,7 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
   p->m1 = m1;
   p->max_batch = max_batch;
   p->fast = (flags & AFD_PLAN_FAST) != 0;
+  p->margins = (flags & AFD_PLAN_MARGINS) != 0;
   auto cleanup = [&](int rc) {
     afd_plan_destroy(p);
     return rc;
@@ -1194,6 +1247,10 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
     ALLOC2(p->Y, sizeof(double2) * N * p->big_rows);
     ALLOC2(p->big_cand, sizeof(Cand) * p->big_rows * big_col_ctas(p));
     ALLOC2(p->big_part, sizeof(Cand) * kBigParts);
+    if (p->margins) {
+      ALLOC2(p->big_cand2, sizeof(double) * p->big_rows * big_col_ctas(p));
+      ALLOC2(p->big_part2, sizeof(double) * kBigParts);
+    }
     ALLOC2(p->nodes, sizeof(double) * 2 * (N / kNodeLen));
     ALLOC2(p->sel, sizeof(BigSel));
     ALLOC2(p->amb, sizeof(int));
@@ -1216,6 +1273,7 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
       while (nc < p->sms && (nc * Q) % p->sms != 0) ++nc;
       p->pr_ncta = (int)std::max<int64_t>(1, std::min<int64_t>(nc, (rows + 1) / 2));
       ALLOC2(p->pr_cand, sizeof(Cand) * (size_t)Q * p->pr_ncta);
+      if (p->margins) ALLOC2(p->pr_cand2, sizeof(double) * (size_t)Q * p->pr_ncta);
       const int64_t total = rows * STR;
       fast_weight_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256>>>(
           p->radii, p->scales, m0, rows, STR, 1 << (kPruneK - 4), 16, kPruneK - 4, 0, 0, p->fw12);
@@ -1223,6 +1281,9 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
       p->launches += 2;
       if (cudaGetLastError() != cudaSuccess) return cleanup(fail(AFD_E_CUDA, "pruned tables"));
       if (cudaFuncSetAttribute(field_kernel<kPruneK, kFieldRB, 2, false, true, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)field_smem<kPruneK>()) != cudaSuccess ||
+          cudaFuncSetAttribute(field_kernel<kPruneK, kFieldRB, 2, false, true, true, true>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)field_smem<kPruneK>()) != cudaSuccess)
         return cleanup(fail(AFD_E_CUDA, "pruned field attributes"));
@@ -1271,6 +1332,10 @@ int afd_plan_destroy(afd_plan* p) {
   cudaFree(p->ghq);
   cudaFree(p->tw_img12);
   cudaFree(p->pr_cand);
+  cudaFree(p->pr_cand2);
+  cudaFree(p->big_cand2);
+  cudaFree(p->big_part2);
+  cudaFree(p->cand2);
   cudaFree(p->mstar);
   cudaFree(p->tmax);
   cudaFree(p->big_part);

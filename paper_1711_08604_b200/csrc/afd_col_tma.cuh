@@ -88,12 +88,13 @@ __device__ __forceinline__ void col_stages4(double2 (&v)[16], uint32_t twm) {
   }
 }
 
-template <int KC, bool FAST = false, int GROUPS = 1>
+template <int KC, bool FAST = false, int GROUPS = 1, bool MARG = false>
 __global__ void __launch_bounds__(256 * GROUPS, 1)
 col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __restrict__ twst,
                const double* __restrict__ scales, long long row0, long long row1,
                Cand* __restrict__ cand, const int* __restrict__ stopped,
-               const int* __restrict__ lim, const __grid_constant__ CUtensorMap ymap) {
+               const int* __restrict__ lim, double* __restrict__ cand2,
+               const __grid_constant__ CUtensorMap ymap) {
   using C = ColTma<KC, GROUPS>;
   constexpr int COLS = C::COLS, U = C::U, TILE = C::TILE;
   extern __shared__ __align__(128) double2 csm[];
@@ -181,6 +182,10 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
   best.mag = -1.0;
   best.flat = 0x7fffffffffffffffLL;
   best.re = best.im = 0.0;
+  // runner-up slots (fast engine): the screen passes every value above the
+  // thread's runner-up, which may become either of its top two
+  constexpr bool track2 = FAST && MARG;
+  [[maybe_unused]] double sec = -1.0;
   int tw_chunk = -1;
   const int c = KC == 8 ? (tid & 15) : tid;
   const int h = KC == 8 ? (tid >> 4) : 0;
@@ -260,7 +265,7 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
         double mg[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) mg[i] = fast_mag2(v[i0 + i]);
-        up = any_ge4(up, mg, best.mag);
+        up = any_ge4(up, mg, track2 ? sec : best.mag);
       }
     }
     if (!FAST || __builtin_expect(up != 0, 0)) {
@@ -271,10 +276,13 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
         const double mg = FAST ? fast_mag2(f) : np_mag2(f);                     // core.py:298
         const long long flat = row * N + j;
         if (mg >= best.mag && cand_better(mg, flat, best.mag, best.flat)) {
+          if constexpr (track2) sec = fmax(sec, best.mag);
           best.mag = mg;
           best.flat = flat;
           best.re = f.x;
           best.im = f.y;
+        } else if constexpr (track2) {
+          sec = fmax(sec, mg);
         }
       }
     }
@@ -288,6 +296,9 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
   // merge this CTA's first maximum into its slot (slots persist over the
   // row batches of one step; the (mag, flat) order makes merging order-free)
   __shared__ Cand red[8 * GROUPS];
+  __shared__ Cand win;
+  [[maybe_unused]] const double own_mag = best.mag;
+  [[maybe_unused]] const long long own_flat = best.flat;
   best = warp_argmax(best);
   const int wid = threadIdx.x >> 5;
   if (lane == 0) red[wid] = best;
@@ -295,12 +306,21 @@ col_tma_kernel(int K, int b0, const double2* __restrict__ Y, const double2* __re
   if (wid == 0) {
     Cand cc = lane < 8 * GROUPS ? red[lane] : best;
     cc = warp_argmax(cc);
-    if (lane == 0) {
-      Cand& slot = cand[blockIdx.x];
-      Cand o = slot;
-      cand_merge(o, cc);
-      slot = o;
-    }
+    if (lane == 0) win = cc;
+  }
+  __syncthreads();
+  [[maybe_unused]] double r2 = -1.0;
+  if constexpr (track2) {
+    __shared__ double red2[8 * GROUPS];
+    r2 = cta_runner_up(sec, own_mag, own_flat, win.flat, red2);
+  }
+  if (threadIdx.x == 0) {
+    const Cand cc = win;
+    Cand& slot = cand[blockIdx.x];
+    Cand o = slot;
+    if constexpr (track2) cand2[blockIdx.x] = runner_merge(cand2[blockIdx.x], o.mag, r2, cc.mag);
+    cand_merge(o, cc);
+    slot = o;
   }
 }
 

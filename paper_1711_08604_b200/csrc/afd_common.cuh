@@ -197,6 +197,35 @@ __device__ __forceinline__ void cand_merge(Cand& a, const Cand& b) {
   if (cand_better(b.mag, b.flat, a.mag, a.flat)) a = b;
 }
 
+// Runner-up bookkeeping (fast engine): a candidate set
+// carries, beside its first maximum, the largest |F|^2 of its other grid
+// points.  Merging two sets, the loser's maximum competes for runner-up.
+__device__ __forceinline__ double runner_merge(double r1, double m1, double r2, double m2) {
+  return fmax(fmax(r1, r2), fmin(m1, m2));
+}
+// Block-wide maximum of a double; result valid in every thread.
+__device__ double block_max(double x) {
+  __shared__ double redm[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) redm[wid] = x;
+  __syncthreads();
+  double y = -1.0;
+  for (int w = 0; w < (int)((blockDim.x + 31) >> 5); ++w) y = fmax(y, redm[w]);
+  __syncthreads();
+  return y;
+}
+
+// |F|^2 of a selected value as the fast epilogues form it
+__device__ __forceinline__ double coeff_mag2(double2 c) { return fma(c.x, c.x, c.y * c.y); }
+// Top-2 relative margin (best - runner-up) / best of the step's |F|^2.
+__device__ __forceinline__ float top2_margin(double best, double runner) {
+  if (!(best > 0.0)) return 0.0f;
+  return (float)((best - fmax(runner, 0.0)) / best);
+}
+
 __device__ __forceinline__ Cand cand_shfl_down(const Cand& c, int off) {
   Cand o;
   o.mag = __shfl_down_sync(0xffffffffu, c.mag, off);

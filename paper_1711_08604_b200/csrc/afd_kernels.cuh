@@ -40,7 +40,7 @@ struct Step {
   long long s, j;
   double radius, a_re, a_im, c_re, c_im, residual;
   int flags;
-  int pad;
+  float margin;  // fast engine: top-2 relative margin of |F|^2; NaN if not tracked
 };
 
 enum : int { kStepPowAmbiguous = 1 };
@@ -181,19 +181,42 @@ __device__ __forceinline__ unsigned any_gt4(unsigned flag, const double (&m)[4],
   return out;
 }
 
-// Sub-transform mapping of a pruned large-N field (big_pruned_field): the
+// Field launch extensions.
+// Sub-transform mapping of a pruned large-N field (afd_pruned.cuh): the
 // kernel's "signals" are the Q = N_big / N pre-twiddled spectra of one
 // N_big-point row set, so signal q's output p is the big field's position
 // j = q + Q p of row s (flat s N_big + j), and rows at or above *lim (the
 // first row whose weight tail is not negligible, prune_rows_kernel) are
 // left to the two-pass path.  Default: identity (flat s N + j, no limit).
+// cand2 (fast mode): per CTA slot, the largest |F|^2 of the CTA's grid
+// points other than its candidate's — the runner-up, from which the step
+// kernels report the step's top-2 relative margin.
 struct SubMap {
   long long row_stride;  // flat index row stride (0: N)
   int q_mul;             // 0: j = p; else j = blockIdx.y + q_mul * p
   const int* lim;        // device row limit or null
+  double* cand2;         // [batch][gridDim.x] runner-up magnitudes or null
 };
 
-template <int K, int RB, int G, bool MATERIALIZE, bool TM = false, bool FAST = false>
+// First maximum of a CTA's candidates and the runner-up: the largest of
+// the threads' runner-ups and of their maxima other than the winner.
+__device__ __forceinline__ double cta_runner_up(double sec, double mag, long long flat,
+                                                long long win_flat, double* red2) {
+  double x = fmax(sec, flat != win_flat ? mag : -1.0);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red2[wid] = x;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  double y = -1.0;
+  for (int w = 0; w < nw; ++w) y = fmax(y, red2[w]);
+  return y;
+}
+
+// MARG (with FAST): track the runner-up into sub.cand2 (AFD_PLAN_MARGINS).
+template <int K, int RB, int G, bool MATERIALIZE, bool TM = false, bool FAST = false,
+          bool MARG = false>
 __global__ void __launch_bounds__(Geo<K, RB>::T * G, (RB <= 3 && Geo<K, RB>::T * G <= 512) ? 2 : 1)
 field_kernel(const double2* __restrict__ ghat,     // [batch][N]
              const double* __restrict__ pw,        // [rows of plan][N], r^l natural l (FAST: fw)
@@ -226,6 +249,7 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
       c.flat = 0x7fffffffffffffffLL;
       c.re = c.im = 0.0;
       cand_out[(size_t)sig * gridDim.x + blockIdx.x] = c;
+      if constexpr (MARG) sub.cand2[(size_t)sig * gridDim.x + blockIdx.x] = -1.0;
     }
     return;
   }
@@ -299,6 +323,10 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   // formed once at the end.
   double best_mag = -1.0, best_re = 0.0, best_im = 0.0;
   int best_sl = -1, best_i = 0;
+  // fast mode with a runner-up slot: the screen lets through every value
+  // above the runner-up (a value above it may become either of the two)
+  constexpr bool track2 = FAST && MARG;
+  [[maybe_unused]] double sec_mag = -1.0;
 
   // row counts fit 32 bits (M <= 2^31); 32-bit loop state keeps registers
   // for the butterflies
@@ -499,7 +527,7 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
           double mg[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) mg[i] = fast_mag2(v[i0 + i]);
-          up = any_gt4(up, mg, best_mag);
+          up = any_gt4(up, mg, track2 ? sec_mag : best_mag);
         }
         if (__builtin_expect(up != 0, 0)) {
 #pragma unroll
@@ -508,7 +536,18 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
             double2 f = v[i];
             asm volatile("" : "+d"(f.x), "+d"(f.y));
             const double mg = fast_mag2(f);
-            if (mg > best_mag) {
+            if constexpr (track2) {
+              if (mg > best_mag) {
+                sec_mag = best_mag;
+                best_mag = mg;
+                best_re = f.x;
+                best_im = f.y;
+                best_sl = sl;
+                best_i = i;
+              } else if (mg > sec_mag) {
+                sec_mag = mg;
+              }
+            } else if (mg > best_mag) {
               best_mag = mg;
               best_re = f.x;
               best_im = f.y;
@@ -556,8 +595,11 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   }
   best.re = best_re;
   best.im = best_im;
+  [[maybe_unused]] const double own_mag = best.mag;
+  [[maybe_unused]] const long long own_flat = best.flat;
   // CTA reduction of the candidates (first maximum).
   __shared__ Cand red[32];
+  __shared__ long long win_flat;
   best = warp_argmax(best);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (lane == 0) red[wid] = best;
@@ -566,7 +608,16 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     const int nw = (blockDim.x + 31) >> 5;
     Cand c = lane < nw ? red[lane] : best;
     c = warp_argmax(c);
-    if (lane == 0) cand_out[(size_t)sig * gridDim.x + blockIdx.x] = c;
+    if (lane == 0) {
+      cand_out[(size_t)sig * gridDim.x + blockIdx.x] = c;
+      if constexpr (track2) win_flat = c.flat;
+    }
+  }
+  if constexpr (track2) {
+    __shared__ double red2[32];
+    __syncthreads();
+    const double r2 = cta_runner_up(sec_mag, own_mag, own_flat, win_flat, red2);
+    if (threadIdx.x == 0) sub.cand2[(size_t)sig * gridDim.x + blockIdx.x] = r2;
   }
 }
 
@@ -646,7 +697,7 @@ struct RowSmem {
 //   k < 0  : initialise (copy g0, initial energy, forward transform)
 //   k >= 0 : select / update / energy / record / stop / forward transform
 // ---------------------------------------------------------------------------
-template <int K>
+template <int K, bool MARG = false>
 __global__ void __launch_bounds__(Geo<K>::T < 64 ? 64 : Geo<K>::T)
 step_kernel(int k, int max_terms, double threshold, int dc_first,
             const double2* __restrict__ g0,       // [batch][N] (init only)
@@ -659,7 +710,8 @@ step_kernel(int k, int max_terms, double threshold, int dc_first,
             const double2* __restrict__ twst,
             State* __restrict__ state,            // [batch]
             Step* __restrict__ steps,             // [batch][max_terms]
-            const double* __restrict__ pow2) {    // [M][kPowRow] (kernel_norm_grid)
+            const double* __restrict__ pow2,      // [M][kPowRow] (kernel_norm_grid)
+            const double* __restrict__ cand2) {   // [batch][ncand] runner-ups or null
   constexpr int N = 1 << K;
   using L = RowSmem<K>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -707,6 +759,7 @@ step_kernel(int k, int max_terms, double threshold, int dc_first,
   long long s = 0, j = 0;
   double radius = 0.0;
   double2 a = make_double2(0.0, 0.0), coeff;
+  double runner = -2.0;  // -2: not tracked
   if (k == 0 && dc_first) {
     // core.py:373-375: a = 0, coeff = complex(np.mean(remainder))
     for (int m = threadIdx.x; m < N; m += blockDim.x) buf[SW(m)] = r[m];
@@ -731,6 +784,15 @@ step_kernel(int k, int max_terms, double threshold, int dc_first,
     }
     __syncthreads();
     b = red[0];
+    if constexpr (MARG) {  // the step's runner-up (AFD_PLAN_MARGINS)
+      double r = -1.0;
+      for (int i = threadIdx.x; i < ncand; i += blockDim.x) {
+        const Cand x = cand[(size_t)sig * ncand + i];
+        r = fmax(r, cand2[(size_t)sig * ncand + i]);
+        if (x.flat != b.flat) r = fmax(r, x.mag);
+      }
+      runner = block_max(r);
+    }
     s = b.flat / N;
     j = b.flat % N;
     radius = radii[s];
@@ -772,7 +834,7 @@ step_kernel(int k, int max_terms, double threshold, int dc_first,
     rec.c_im = coeff.y;
     rec.residual = residual;
     rec.flags = amb ? kStepPowAmbiguous : 0;
-    rec.pad = 0;
+    rec.margin = runner >= -1.0 ? top2_margin(coeff_mag2(coeff), runner) : __int_as_float(0x7fc00000);
     steps[(size_t)sig * max_terms + k] = rec;
     st.nsteps = k + 1;
     st.flags |= rec.flags;

@@ -104,7 +104,7 @@ struct LocalTw {
 };
 
 // Launched with a runtime cluster dimension of ClusterGeo<K>::C.
-template <int K>
+template <int K, bool MARG = false>
 __global__ void __launch_bounds__(256)
 step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
                     const double2* __restrict__ g0, double2* __restrict__ rem,
@@ -112,7 +112,7 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
                     const double* __restrict__ radii, int nrad,
                     const double2* __restrict__ circle, const double2* __restrict__ twst,
                     State* __restrict__ state, Step* __restrict__ steps,
-                    const double* __restrict__ pow2) {
+                    const double* __restrict__ pow2, const double* __restrict__ cand2) {
   using CG = ClusterGeo<K>;
   using L = ClusterSmem<K>;
   using GL = typename CG::GL;
@@ -250,6 +250,7 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
   // ---- select ---------------------------------------------------------------
   long long s = 0, j = 0;
   double radius = 0.0;
+  double runner = -2.0;  // step's runner-up |F|^2 (fast engine, CTA 0 warp 0); -2: none
   double2 a = make_double2(0.0, 0.0), coeff = make_double2(0.0, 0.0);
   if (!(k >= 0 && !(k == 0 && dc_first))) {  // select-free paths
     if (stopped) {
@@ -299,12 +300,17 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
       x.im = hi.y;
       return x;
     };
+    // the record's runner-up (fast engine): warp 0 of CTA 0 loads the
+    // runner-up slots in the same round trip and keeps its candidates
+    const bool want2 = MARG && c == 0 && tid < 32;
+    Cand xs[4];
+    double xs2[4] = {-1.0, -1.0, -1.0, -1.0};
     {
-      Cand xs[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int i = lane + 32 * u;
         if (i < ncand) xs[u] = load_cand(i);
+        if (want2 && i < ncand) xs2[u] = __ldcg(cand2 + (size_t)sig * ncand + i);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -323,6 +329,24 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
     b.flat = __shfl_sync(0xffffffffu, b.flat, 0);
     b.re = __shfl_sync(0xffffffffu, b.re, 0);
     b.im = __shfl_sync(0xffffffffu, b.im, 0);
+    if (MARG && want2) {
+      double r = -1.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (lane + 32 * u < ncand) {
+          r = fmax(r, xs2[u]);
+          if (xs[u].flat != b.flat) r = fmax(r, xs[u].mag);
+        }
+      }
+      for (int i = lane + 128; i < ncand; i += 32) {
+        const Cand x = load_cand(i);
+        r = fmax(r, __ldcg(cand2 + (size_t)sig * ncand + i));
+        if (x.flat != b.flat) r = fmax(r, x.mag);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+      runner = r;
+    }
     STAMP(13);
     s = b.flat / N;
     j = b.flat % N;
@@ -495,7 +519,7 @@ step_cluster_kernel(int k, int max_terms, double threshold, int dc_first,
       rec.c_im = coeff.y;
       rec.residual = energy;
       rec.flags = amb ? kStepPowAmbiguous : 0;
-      rec.pad = 0;
+      rec.margin = runner >= -1.0 ? top2_margin(coeff_mag2(coeff), runner) : __int_as_float(0x7fc00000);
       steps[(size_t)sig * max_terms + k] = rec;
       st.nsteps = k + 1;
       st.flags |= rec.flags;

@@ -126,7 +126,7 @@ def _default_plan(radii, n, batch, m0, m1, device, engine_name="fft"):
     from . import engine
     return engine.get_plan(radii, n, batch=batch, m0=m0, m1=m1, device=device,
                            engine=1 if engine_name == "direct" else 0,
-                           fast=engine_name == "fft-fast")
+                           fast={"fft-fast": 1, "fft-fast-margins": 2}.get(engine_name, 0))
 
 
 _COMMS = {}
@@ -238,7 +238,8 @@ def decompose_sharded(signals, grid, max_terms=10, threshold=None, dc_first=Fals
     m = len(grid.radii)
     if world > m:
         raise ValueError("more ranks (%d) than radii (%d)" % (world, m))
-    m0, m1 = radius_shard_bounds(grid.radii, n, rank, world, exact=engine_name != "fft-fast")
+    m0, m1 = radius_shard_bounds(grid.radii, n, rank, world,
+                                 exact=not engine_name.startswith("fft-fast"))
     if plan_factory is None:
         plan = _default_plan(grid.radii, n, b, m0, m1, device, engine_name)
     else:

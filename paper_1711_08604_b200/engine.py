@@ -91,7 +91,8 @@ class Plan:
     """One afd_plan: device tables for (N, radii, radius shard, batch).
 
     ``fast=1`` builds an AFD_PLAN_FAST plan (FMA-fused field arithmetic, r^l
-    on chip; identical selections, ~1e-14 relative instead of bit-exact).
+    on chip; identical selections, ~1e-14 relative instead of bit-exact);
+    ``fast=2`` also tracks each step's top-2 margin (AFD_PLAN_MARGINS).
     A plan's device buffers are shared by all its entry points, so every
     call holds the plan's lock (concurrent callers serialise instead of
     corrupting each other's state)."""
@@ -105,7 +106,9 @@ class Plan:
         self.m0 = int(m0)
         self.m1 = self.m if m1 is None else int(m1)
         self.max_batch = int(max_batch)
-        self.fast = int(bool(fast))
+        self.fast = int(fast)
+        if self.fast not in (0, 1, 2):
+            raise ValueError("fast must be 0, 1 or 2 (with margins), got %r" % (fast,))
         self.lock = threading.RLock()
         self._last_stream, self._done = None, None
         tw, circle, scales = host_tables(self.radii, self.n)
@@ -115,7 +118,8 @@ class Plan:
             _capi.check(self.lib.afd_plan_create(
                 C.byref(handle), self.device.index, self.n, self.m, self.m0, self.m1,
                 self.max_batch, r.ctypes.data, scales.ctypes.data, tw.ctypes.data,
-                circle.ctypes.data, _capi.PLAN_FAST if self.fast else 0))
+                circle.ctypes.data, (_capi.PLAN_FAST if self.fast else 0) |
+                (_capi.PLAN_MARGINS if self.fast == 2 else 0)))
         self.handle = handle
         self._keep = (tw, circle, scales, r)
         self.engine = int(engine)
@@ -413,7 +417,7 @@ def get_plan(radii, n, batch=1, m0=0, m1=None, device=None, engine=0, fast=0):
     # fast path: the same radii tuple object as the previous call (a grid's
     # radii) skips hashing M floats
     last_key, last_plan = _LAST
-    fast = int(bool(fast))
+    fast = int(fast)
     if (last_key is not None and last_key[0] is radii and last_key[1:] ==
             (n, m0, m1, device, engine, fast) and last_plan.max_batch >= batch and
             last_plan.handle is not None and

@@ -15,7 +15,7 @@ import oracle as O
 CAND = np.dtype([("mag2", "f8"), ("flat", "i8"), ("re", "f8"), ("im", "f8")])
 STEP = np.dtype([("s", "i8"), ("j", "i8"), ("radius", "f8"), ("a_re", "f8"), ("a_im", "f8"),
                  ("c_re", "f8"), ("c_im", "f8"), ("residual", "f8"), ("flags", "i4"),
-                 ("pad", "i4")])
+                 ("margin", "f4")])
 
 
 class OraclePlan:

@@ -1038,3 +1038,67 @@ def test_pruned_fast_decompose_long_rows_and_threshold(afd):
     c = np.array([s.coefficient for s in d.steps])
     assert np.all(np.abs(c - oc) <= FAST_TOL * np.abs(oc))
     assert np.abs(d.remainder - o.remainder).max() <= FAST_TOL * np.abs(o.remainder).max()
+
+
+# ---------------------------------------------------------------------------
+# per-step top-2 margins (fast engine)
+# ---------------------------------------------------------------------------
+def _oracle_margins(g, radii, steps):
+    """The reference's own top-2 relative margin of |F|^2 at every step:
+    replay the oracle's selections, full field each step."""
+    out = []
+    rem = np.ascontiguousarray(g, dtype=np.complex128)
+    for rec in steps:
+        f = O.field(O.dft_forward(rem), np.array(radii))
+        mag = (f.real * f.real + f.imag * f.imag).ravel()
+        top = np.argmax(mag)
+        best = mag[top]
+        mag[top] = -1.0
+        out.append((best - max(mag.max(), 0.0)) / best)
+        rem = O.remainder_update(rem, complex(rec["a_re"], rec["a_im"]),
+                                 complex(rec["c_re"], rec["c_im"]))
+    return np.array(out)
+
+
+@pytest.mark.parametrize("n,m,poles,steps", [(1024, 100, 8, 10), (4096, 96, 16, 6),
+                                             (1 << 16, 12, 16, 3)])
+def test_fast_margins_match_the_reference(afd, n, m, poles, steps):
+    """engine "fft-fast-margins" reports each step's top-2 relative margin;
+    it is the reference's (full-field replay) to 1e-9 absolute (on-chip N,
+    the cluster and one-CTA step kernels, and the pruned + two-pass large-N
+    field).  Exact and plain fast decompositions report NaN."""
+    core, _ = afd
+    from paper_1711_08604_b200 import workloads as W
+    g = W.pole_sum(n, poles, 0.99 if n > 8192 else 0.95, 1000 + n)
+    radii = tuple(0.9995 * i / (m - 1) for i in range(m)) if n > 8192 else \
+        tuple(i / m for i in range(m))
+    grid = core.ParameterGrid(radii, n)
+    d = core.decompose(g, grid, max_terms=steps, engine="fft-fast-margins")
+    o = O.decompose(g, np.array(radii), max_terms=steps)
+    assert [s.point.angle_index for s in d.steps] == list(o.steps["j"])
+    ref = _oracle_margins(g, radii, o.steps)
+    got = np.array(d.margins)
+    assert got.shape == ref.shape and np.all(np.isfinite(got))
+    assert np.all(np.abs(got - ref) <= 1e-9), (got, ref)
+    # the same selections as the margin-free fast engine; exact and plain
+    # fast decompositions report NaN
+    f = core.decompose(g, grid, max_terms=steps, engine="fft-fast")
+    assert [s.point.angle_index for s in f.steps] == [s.point.angle_index for s in d.steps]
+    assert all(np.isnan(x) for x in f.margins)
+    e = core.decompose(g, grid, max_terms=2, engine="fft")
+    assert len(e.margins) == 2 and all(np.isnan(x) for x in e.margins)
+
+
+def test_fast_batch_margins(afd):
+    """decompose_batch with margins: every signal's margins as its own."""
+    core, _ = afd
+    from paper_1711_08604_b200 import workloads as W
+    n, m = 4096, 64
+    radii = tuple(i / m for i in range(m))
+    sig = np.stack([W.pole_sum(n, 16, 0.95, 70 + s) for s in range(3)])
+    grid = core.ParameterGrid(radii, n)
+    ds = core.decompose_batch(sig, grid, max_terms=4, engine="fft-fast-margins")
+    for i in range(3):
+        o = O.decompose(sig[i], np.array(radii), max_terms=4)
+        ref = _oracle_margins(sig[i], radii, o.steps)
+        assert np.all(np.abs(np.array(ds[i].margins) - ref) <= 1e-9)
