@@ -250,6 +250,10 @@ int afd_time_field(afd_plan *plan, const double *ghat, int64_t batch, int reps, 
  * the TMA column pass.  Exact plans and N <= 8192: *onchip = 0 and every
  * row is counted as *twopass (large N) or *onchip = rows (on-chip N). */
 int afd_field_split(afd_plan *plan, int64_t *onchip, int64_t *twopass, void *stream);
+/* afd_field_tiers: the same split by on-chip tier: rows3[0] rows as
+ * 1024-point transforms (tail beyond l = 1024 negligible), rows3[1] as
+ * 4096-point transforms, rows3[2] two-pass (zeros for on-chip N). */
+int afd_field_tiers(afd_plan *plan, int64_t *rows3, void *stream);
 int afd_fp64_peak(int device, double *tflops, void *stream);
 
 #ifdef __cplusplus

@@ -71,6 +71,7 @@ SIGNATURES = [
     ("afd_time_field", _I, [_VP, _VP, _I64, _I, _VP, _VP]),
     ("afd_fp64_peak", _I, [_I, _VP, _VP]),
     ("afd_field_split", _I, [_VP, _VP, _VP, _VP]),
+    ("afd_field_tiers", _I, [_VP, _VP, _VP]),
 ]
 
 _LIB = None

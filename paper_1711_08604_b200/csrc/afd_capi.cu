@@ -120,15 +120,17 @@ struct afd_plan {
   CUtensorMap ymap;            // Y as [big_rows][256][2^ka complex] (8-stage TMA column pass)
   bool ymap_ok = false;
   // pruned fast field (afd_pruned.cuh): rows with a negligible weight tail
-  // as a batch of Q = N / 4096 on-chip 4096-point fields
+  // as batches of Q = N / L on-chip L-point fields, per tier (prune_k)
   bool pruned = false;
-  double* fw12 = nullptr;      // [m1-m0][FastW<12,4>::STRIDE] weights (this plan's scales)
-  double2* ghq = nullptr;      // [Q][4096] pre-twiddled spectra
-  double2* tw_img12 = nullptr; // SmemTw<12,4> (c, t) image
-  Cand* pr_cand = nullptr;     // [Q][pr_ncta]
-  double* pr_cand2 = nullptr;
-  int pr_ncta = 0;
-  int* mstar = nullptr;        // first row left to the two-pass path
+  struct PruneTier {
+    double* fw = nullptr;       // [m1-m0][FastW<k,4>::STRIDE] weights (this plan's scales)
+    double2* ghq = nullptr;     // [Q][L] pre-twiddled spectra
+    double2* tw_img = nullptr;  // SmemTw<k,4> (c, t) image
+    Cand* cand = nullptr;       // [Q][ncta]
+    double* cand2 = nullptr;
+    int ncta = 0;
+  } tier[kPruneTiers];
+  int* mstar = nullptr;        // [kPruneTiers] first row failing each tier's test
   unsigned long long* tmax = nullptr;
   double* nodes = nullptr;     // [2 * N / kNodeLen]
   BigSel* sel = nullptr;
@@ -247,11 +249,22 @@ int row_block() {
   return Geo<K>::T < 64 ? 64 : Geo<K>::T;
 }
 
-// Field launches with two full row-groups at N = 4096 keep their twiddles in
-// TMEM (TmemTw, afd_fft.cuh); AFD_FIELD_TMEM=0 turns it off (experiments).
+// Field launches with two full row-groups at N = 4096 (four at N = 2048)
+// keep their twiddles in TMEM (TmemTw, afd_fft.cuh); AFD_FIELD_TMEM=0 turns
+// it off (experiments).
+#ifndef AFD_FIELD_TMEM11
+#define AFD_FIELD_TMEM11 1
+#endif
+constexpr bool kFieldTmem11 = AFD_FIELD_TMEM11 != 0;
+#ifndef AFD_FIELD_TMEM10
+#define AFD_FIELD_TMEM10 1
+#endif
+constexpr bool kFieldTmem10 = AFD_FIELD_TMEM10 != 0;
 template <int K>
 constexpr bool field_tmem_capable() {
-  return K == 12 && kFieldRB == 4 && groups_for<K>() == 2;
+  return kFieldRB == 4 && ((K == 12 && groups_for<K>() == 2) ||
+                           (K == 11 && groups_for<K>() == 4 && kFieldTmem11) ||
+                           (K == 10 && groups_for<K>() == 8 && kFieldTmem10));
 }
 static bool field_tmem_enabled() {
   static int v = [] {
@@ -895,6 +908,65 @@ int big_reduce_cands(afd_plan* p, cudaStream_t st, const Cand** parts, int* npar
   return 0;
 }
 
+// One tier of the pruned fast field (afd_pruned.cuh): tables at plan time.
+template <int KT>
+int setup_pruned_tier(afd_plan* p, int t) {
+  static_assert(field_tmem_capable<KT>(), "pruned tiers use the TMEM field kernel");
+  constexpr int G = groups_for<KT>();
+  constexpr int STR = FastW<KT, kFieldRB>::STRIDE;
+  const int64_t rows = p->m1 - p->m0, Q = p->n >> KT;
+  auto& T = p->tier[t];
+  CU(cudaMalloc(&T.fw, sizeof(double) * STR * (size_t)rows));
+  CU(cudaMalloc(&T.ghq, sizeof(double2) * (size_t)p->n));
+  CU(cudaMalloc(&T.tw_img, sizeof(double2) * (SmemTw<KT, kFieldRB>::ENTRIES)));
+  // CTAs per spectrum: the grid (ncta x Q) a whole number of SM waves
+  int nc = 1;
+  while (nc < p->sms && (nc * Q) % p->sms != 0) ++nc;
+  T.ncta = (int)std::max<int64_t>(1, std::min<int64_t>(nc, (rows + G - 1) / G));
+  CU(cudaMalloc(&T.cand, sizeof(Cand) * (size_t)Q * T.ncta));
+  if (p->margins) CU(cudaMalloc(&T.cand2, sizeof(double) * (size_t)Q * T.ncta));
+  const int64_t total = rows * STR;
+  fast_weight_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256>>>(
+      p->radii, p->scales, p->m0, rows, STR, 1 << (KT - 4), 16, KT - 4, 0, 0, T.fw);
+  build_tw_image_kernel<KT><<<32, 256>>>(T.tw_img, p->twct);
+  p->launches += 2;
+  CU(cudaGetLastError());
+  CU(cudaFuncSetAttribute(field_kernel<KT, kFieldRB, G, false, true, true>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem<KT>()));
+  CU(cudaFuncSetAttribute(field_kernel<KT, kFieldRB, G, false, true, true, true>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem<KT>()));
+  return 0;
+}
+
+// One tier per step: pre-twiddled spectra, the on-chip field over rows
+// [max(r0, *lo), min(r1, *hi)) (device limits), candidate partials into
+// big_cand slots from *slot on.
+template <int KT>
+int launch_pruned_tier(afd_plan* p, int t, const double2* ghat_rev, int64_t r0, int64_t r1,
+                       const int* lo, const int* hi, const int* stopped, int* slot,
+                       cudaStream_t st) {
+  constexpr int G = groups_for<KT>();
+  const int Q = (int)(p->n >> KT);
+  auto& T = p->tier[t];
+  pretwiddle_kernel<<<4 * p->sms, 256, 0, st>>>(p->K, p->ka, KT, ghat_rev, p->circle, T.ghq,
+                                                stopped);
+  auto pk = p->margins ? field_kernel<KT, kFieldRB, G, false, true, true, true>
+                       : field_kernel<KT, kFieldRB, G, false, true, true>;
+  pk<<<dim3((unsigned)T.ncta, (unsigned)Q), Geo<KT, kFieldRB>::T * G, field_smem<KT>(), st>>>(
+      T.ghq, T.fw, p->scales, p->twct, (long long)r0, (long long)r1, (long long)p->m0, T.cand,
+      nullptr, nullptr, T.tw_img, field_pp(), (unsigned*)nullptr, 0,
+      SubMap{(long long)p->n, Q, hi, T.cand2, lo});
+  const int n = Q * T.ncta;
+  const int slots = (int)(p->big_rows * big_col_ctas(p));
+  const int np = std::max(1, std::min(std::min(kBigParts, (n + 255) / 256), (slots - *slot) / 2));
+  cand_partial_kernel<<<np, 256, 0, st>>>(T.cand, n, (n + np - 1) / np, p->big_cand + *slot,
+                                          T.cand2, p->big_cand2 ? p->big_cand2 + *slot : nullptr);
+  *slot += np;
+  p->launches += 3;
+  CU(cudaGetLastError());
+  return 0;
+}
+
 // Timing experiments only (wrong results): AFD_BIG_SKIP=1 skips pass A of
 // the field, 2 its column pass.
 static const int kBigSkip = getenv("AFD_BIG_SKIP") ? atoi(getenv("AFD_BIG_SKIP")) : 0;
@@ -911,30 +983,23 @@ int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, doub
   }
   const int* lim = nullptr;
   if (!fout && p->pruned) {
-    // rows [r0, mstar) as Q on-chip 4096-point fields; rows [mstar, r1)
-    // through the batches below (their kernels read mstar on the device)
-    const int Q = (int)(p->n >> kPruneK);
+    // tier 0: rows [r0, mstar[0]) as N/1024 1024-point fields, tier 1: rows
+    // [mstar[0], mstar[1]) as N/4096 4096-point fields, rows [mstar[1], r1)
+    // through the batches below (all limits read on the device)
     prune_init_kernel<<<1, 1, 0, st>>>(p->mstar, r1, p->tmax);
     prune_tail_kernel<<<2 * p->sms, 256, 0, st>>>(ghat_rev, p->n, p->tmax);
     prune_rows_kernel<<<2 * p->sms, 256, 0, st>>>(p->K, p->ka, ghat_rev, p->radii, r0, r1,
                                                   p->tmax, stopped, p->mstar);
-    pretwiddle_kernel<<<4 * p->sms, 256, 0, st>>>(p->K, p->ka, ghat_rev, p->circle, p->ghq,
-                                                  stopped);
-    using Gm = Geo<kPruneK, kFieldRB>;
-    const size_t smem = field_smem<kPruneK>();
-    auto pk = p->margins ? field_kernel<kPruneK, kFieldRB, 2, false, true, true, true>
-                         : field_kernel<kPruneK, kFieldRB, 2, false, true, true>;
-    pk<<<dim3((unsigned)p->pr_ncta, (unsigned)Q), Gm::T * 2, smem, st>>>(
-            p->ghq, p->fw12, p->scales, p->twct, (long long)r0, (long long)r1, (long long)p->m0,
-            p->pr_cand, nullptr, nullptr, p->tw_img12, field_pp(), (unsigned*)nullptr, 0,
-            SubMap{(long long)p->n, Q, p->mstar, p->pr_cand2});
-    const int n = Q * p->pr_ncta;
-    const int np = std::min(kBigParts, (n + 255) / 256);
-    cand_partial_kernel<<<np, 256, 0, st>>>(p->pr_cand, n, (n + np - 1) / np, p->big_cand,
-                                            p->pr_cand2, p->big_cand2);
-    p->launches += 6;
+    p->launches += 3;
     CU(cudaGetLastError());
-    lim = p->mstar;
+    int slot = 0, rc2;
+    if ((rc2 = launch_pruned_tier<prune_k(0)>(p, 0, ghat_rev, r0, r1, nullptr, p->mstar, stopped,
+                                               &slot, st)))
+      return rc2;
+    if ((rc2 = launch_pruned_tier<prune_k(1)>(p, 1, ghat_rev, r0, r1, p->mstar, p->mstar + 1,
+                                               stopped, &slot, st)))
+      return rc2;
+    lim = p->mstar + 1;
   }
   for (int64_t b = r0; b < r1; b += p->big_rows) {
     const int64_t rows = std::min<int64_t>(p->big_rows, r1 - b);
@@ -1267,36 +1332,15 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
     ALLOC2(p->tmp, sizeof(double2) * N);
     rc = big_setup(p);
     if (!rc && p->fast && kPrunedEnabled && K > kPruneK && pruned_col_ok(p)) {
-      // pruned fast field: weights {scale r^t, t < 256; r^(256 m), m < 16}
-      // of this plan's radii and N-point scales, the 4096-point (c, t)
-      // twiddle image (the stage tables S_b, b < 12, are the first 4095
-      // entries of the N-point tables), per-CTA candidates
-      constexpr int STR = FastW<kPruneK, kFieldRB>::STRIDE;
-      const int64_t rows = m1 - m0, Q = (int64_t)N >> kPruneK;
-      ALLOC2(p->fw12, sizeof(double) * STR * (size_t)rows);
-      ALLOC2(p->ghq, sizeof(double2) * N);
-      ALLOC2(p->tw_img12, sizeof(double2) * (SmemTw<kPruneK, kFieldRB>::ENTRIES));
-      ALLOC2(p->mstar, sizeof(int));
+      // pruned fast field, per tier: weights {scale r^t, t < L/16;
+      // r^(L/16 m), m < 16} of this plan's radii and N-point scales, the
+      // L-point (c, t) twiddle image (the stage tables S_b, b < log2 L, are
+      // the first L - 1 entries of the N-point tables), per-CTA candidates
+      ALLOC2(p->mstar, sizeof(int) * kPruneTiers);
       ALLOC2(p->tmax, sizeof(unsigned long long));
-      // CTAs per spectrum: the grid (ncta x Q) a whole number of SM waves
-      int nc = 1;
-      while (nc < p->sms && (nc * Q) % p->sms != 0) ++nc;
-      p->pr_ncta = (int)std::max<int64_t>(1, std::min<int64_t>(nc, (rows + 1) / 2));
-      ALLOC2(p->pr_cand, sizeof(Cand) * (size_t)Q * p->pr_ncta);
-      if (p->margins) ALLOC2(p->pr_cand2, sizeof(double) * (size_t)Q * p->pr_ncta);
-      const int64_t total = rows * STR;
-      fast_weight_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256>>>(
-          p->radii, p->scales, m0, rows, STR, 1 << (kPruneK - 4), 16, kPruneK - 4, 0, 0, p->fw12);
-      build_tw_image_kernel<kPruneK><<<32, 256>>>(p->tw_img12, p->twct);
-      p->launches += 2;
-      if (cudaGetLastError() != cudaSuccess) return cleanup(fail(AFD_E_CUDA, "pruned tables"));
-      if (cudaFuncSetAttribute(field_kernel<kPruneK, kFieldRB, 2, false, true, true>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)field_smem<kPruneK>()) != cudaSuccess ||
-          cudaFuncSetAttribute(field_kernel<kPruneK, kFieldRB, 2, false, true, true, true>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)field_smem<kPruneK>()) != cudaSuccess)
-        return cleanup(fail(AFD_E_CUDA, "pruned field attributes"));
+      rc = setup_pruned_tier<prune_k(0)>(p, 0);
+      if (!rc) rc = setup_pruned_tier<prune_k(1)>(p, 1);
+      if (rc) return cleanup(rc);
       p->pruned = true;
     }
   } else {
@@ -1338,11 +1382,13 @@ int afd_plan_destroy(afd_plan* p) {
   cudaFree(p->scratch);
   cudaFree(p->Y);
   cudaFree(p->big_cand);
-  cudaFree(p->fw12);
-  cudaFree(p->ghq);
-  cudaFree(p->tw_img12);
-  cudaFree(p->pr_cand);
-  cudaFree(p->pr_cand2);
+  for (auto& t : p->tier) {
+    cudaFree(t.fw);
+    cudaFree(t.ghq);
+    cudaFree(t.tw_img);
+    cudaFree(t.cand);
+    cudaFree(t.cand2);
+  }
   cudaFree(p->big_cand2);
   cudaFree(p->big_part2);
   cudaFree(p->cand2);
@@ -2010,11 +2056,31 @@ int afd_field_split(afd_plan* p, int64_t* onchip, int64_t* twopass, void* stream
     *twopass = rows;
     return 0;
   }
-  int ms = 0;
-  CU(cudaMemcpyAsync(&ms, p->mstar, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  int64_t tiers[3];
+  int rc2;
+  if ((rc2 = afd_field_tiers(p, tiers, stream))) return rc2;
+  *onchip = tiers[0] + tiers[1];
+  *twopass = tiers[2];
+  return 0;
+}
+
+int afd_field_tiers(afd_plan* p, int64_t* rows3, void* stream) {
+  if (!p || !rows3) return fail(AFD_E_INVALID, "NULL argument");
+  int rc;
+  if ((rc = set_device(p))) return rc;
+  const int64_t rows = p->m1 - p->m0;
+  if (!p->big || !p->pruned) {
+    rows3[0] = rows3[1] = 0;
+    rows3[2] = p->big ? rows : 0;
+    return 0;
+  }
+  int ms[kPruneTiers] = {0, 0};
+  CU(cudaMemcpyAsync(ms, p->mstar, sizeof(ms), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   CU(cudaStreamSynchronize((cudaStream_t)stream));
-  *onchip = std::max<int64_t>(0, std::min<int64_t>(rows, (int64_t)ms - p->m0));
-  *twopass = rows - *onchip;
+  auto clampr = [&](int64_t x) { return std::max<int64_t>(0, std::min<int64_t>(rows, x - p->m0)); };
+  rows3[0] = clampr(ms[0]);
+  rows3[1] = clampr(ms[1]) - rows3[0];
+  rows3[2] = rows - rows3[0] - rows3[1];
   return 0;
 }
 

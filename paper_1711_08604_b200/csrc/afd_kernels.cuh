@@ -194,8 +194,9 @@ __device__ __forceinline__ unsigned any_gt4(unsigned flag, const double (&m)[4],
 struct SubMap {
   long long row_stride;  // flat index row stride (0: N)
   int q_mul;             // 0: j = p; else j = blockIdx.y + q_mul * p
-  const int* lim;        // device row limit or null
+  const int* lim;        // device row limit (rows >= *lim skipped) or null
   double* cand2;         // [batch][gridDim.x] runner-up magnitudes or null
+  const int* lim_lo;     // device lower row limit (rows < *lim_lo skipped) or null
 };
 
 // First maximum of a CTA's candidates and the runner-up: the largest of
@@ -240,6 +241,10 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   const int tp = threadIdx.x % T;
   const int Gr = blockDim.x / T;  // row-groups actually launched (<= G)
   using TwT = SmemTw<K, RB>;
+  if (sub.lim_lo != nullptr) {  // pruned tier: rows below *lim_lo belong to a shorter tier
+    const long long l = *sub.lim_lo;
+    if (l > row0) row0 = l < row1 ? l : row1;
+  }
   if (sub.lim != nullptr && *sub.lim <= row0) {
     // pruned launch with no on-chip rows this step (all rows long, or the
     // signal stopped): a neutral candidate, no TMEM or twiddle setup
@@ -296,10 +301,17 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   using TwSrc = std::conditional_t<TM, std::conditional_t<FAST, TmemTwCT, TmemTw>,
                                    std::conditional_t<FAST, SmemTwCT<K, RB>, TwT>>;
   TwSrc tw;
+  // TMEM lanes follow the warp's quadrant (warp & 3): with T >= 128 every
+  // group's warps cover all four quadrants in thread order, with T = 64 two
+  // groups do, so the first kTmFill groups write the twiddles and spectrum
+  [[maybe_unused]] constexpr int kTmFill = T >= 128 ? 1 : 128 / T;
   if constexpr (TM) {
     const int warp = threadIdx.x >> 5;
+    // lane quadrant of the warp; one column set per 128 threads of a row
+    // (tp >> 7): two sets at N = 4096 (T = 256), one for N = 1024, 2048
+    // (shared by all groups)
     tw.base = tm_base + ((uint32_t)((warp & 3) * 32) << 16) +
-              (uint32_t)(((warp & 7) >> 2) * TmemTw::kSetCols);
+              (uint32_t)((tp >> 7) * TmemTw::kSetCols);
   } else {
     tw.sm = smem;
   }
@@ -314,7 +326,7 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     static_assert(TmemTw::kGhCol + 2 * 4 * P <= 512, "TMEM columns");
     const int warp = threadIdx.x >> 5;
     gh_tm = tm_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)TmemTw::kGhCol +
-            (uint32_t)(((warp & 7) >> 2) * (4 * P));
+            (uint32_t)((tp >> 7) * (4 * P));
   }
 
   // Running first maximum.  Rows are visited in increasing s and, within a
@@ -374,7 +386,7 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     if constexpr (TM) {  // step-independent: fill TMEM before the PDL wait
       mbar_wait(&tw_bar, 0);
       tw_ready = true;
-      if (g == 0) {
+      if (g < kTmFill) {
         tw.template fill<K, RB, !FAST>(tp, TwT{smem});
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
@@ -393,7 +405,7 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
 #pragma unroll
       for (int i = 0; i < P; ++i) v[i] = __ldg(gh + Gm::l0(tp, i));
       if constexpr (TM) {
-        if (g == 0) {
+        if (g < kTmFill) {
 #pragma unroll
           for (int i = 0; i < P; ++i) tm_st4(gh_tm + 4 * i, v[i]);
         }
@@ -407,7 +419,7 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
 #pragma unroll
       for (int i = 0; i < P; ++i) asm volatile("" ::"d"(v[i].x), "d"(v[i].y));  // formed before the test
       if constexpr (TM) {
-        if (g == 0) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        if (g < kTmFill) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
     }
     if (stopped) {
@@ -425,6 +437,14 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     FSTAMP(0, 1);
     // the previous launch is complete: clear the next launch's counter
     if (dyn && threadIdx.x == 0 && blockIdx.x == 0) row_ctr[2 * sig + ((launch_id + 1) & 1)] = 0;
+  }
+  // TMEM variant with more than two groups (N = 2048): no one-pass offset
+  // orders group 0's spectrum store before the others read it at their
+  // second row, so the CTA synchronises once here
+  if constexpr (TM && G > 2) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   }
   // row within [row0, row1); groups that share warps (no kGroupSync) step
   // through `rounds` together with inactive tails masked

@@ -15,6 +15,8 @@
 // the field over the prunable rows is the N = 4096 field kernel run on a
 // batch of Q spectra g^(q) with the big plan's radii and scales: on chip,
 // no row-batch intermediate in HBM, 12 butterfly stages instead of 20.
+// Rows whose tail beyond L = 1024 is already negligible (~96% of r_m = m/M
+// at c4) run as N/1024 1024-point fields instead (prune_k).
 // Rows that fail the test (the last ~1% of r_m = m/M at c4) keep the
 // two-pass path (pass A + TMA column pass), limited on the device to rows
 // at or above the first failing row, so the loop stays free of host syncs
@@ -26,11 +28,19 @@
 
 namespace afd {
 
-constexpr int kPruneK = 12;  // on-chip sub-transform length L = 2^kPruneK
+// On-chip sub-transform tiers: rows whose tail beyond L = 1024 is
+// negligible run as N/1024 1024-point fields (the fastest on-chip field
+// kernel per evaluation: 3.7e11 vs 3.1e11 evals/s at 4096 points), rows
+// that need up to 4096 terms as N/4096 4096-point fields, the rest
+// two-pass.  mstar[t] = first row failing tier t's test; tiers are nested
+// (a row failing L = 4096 fails L = 1024), so mstar[0] <= mstar[1].
+constexpr int kPruneTiers = 2;
+__host__ __device__ constexpr int prune_k(int t) { return t == 0 ? 10 : 12; }
+constexpr int kPruneK = 12;  // the longest tier (the spectrum head staged by prune_rows)
 
-// *mstar = m1, *tmax = 0 (the tail maximum is max-reduced on its bits)
+// mstar[t] = m1, *tmax = 0 (the tail maximum is max-reduced on its bits)
 __global__ void prune_init_kernel(int* mstar, long long m1, unsigned long long* tmax) {
-  *mstar = (int)m1;
+  for (int t = 0; t < kPruneTiers; ++t) mstar[t] = (int)m1;
   *tmax = 0ull;
 }
 
@@ -56,11 +66,12 @@ __device__ __forceinline__ double2 spectrum_at(const double2* __restrict__ ghat_
   return __ldg(ghat_perm + perm_of_pos(brev_rt(l, K), ka));
 }
 
-// First row s in [m0, m1) whose tail is not negligible:
-//   log2 T + L log2 r - log2(1 - r) > log2 B_s - 64  ->  atomicMin(mstar, s).
-// One warp per row; the CTA stages log2 |G^_l| (l < L, natural order from
-// the bit-reversed spectrum) in shared memory.  A stopped signal pins
-// mstar to m0 (and the field kernels then do nothing).
+// First row s in [m0, m1) whose tail is not negligible, per tier t:
+//   log2 T + L_t log2 r - log2(1 - r) > log2 B_s(L_t) - 64 -> atomicMin(mstar[t], s),
+// B_s(L) = max_{l < L} r^l |G^_l|.  One warp per row; the CTA stages
+// log2 |G^_l| (l < 4096, natural order from the permuted spectrum) in
+// shared memory.  A stopped signal pins every mstar[t] to m0 (and the field
+// kernels then do nothing).
 __global__ void __launch_bounds__(256) prune_rows_kernel(
     int K, int ka, const double2* __restrict__ ghat_rev, const double* __restrict__ radii, long long m0,
     long long m1, const unsigned long long* __restrict__ tmax, const int* __restrict__ stopped,
@@ -68,7 +79,7 @@ __global__ void __launch_bounds__(256) prune_rows_kernel(
   constexpr int L = 1 << kPruneK;
   __shared__ double lg[L];
   if (stopped && *stopped) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicMin(mstar, (int)m0);
+    if (blockIdx.x == 0 && threadIdx.x < kPruneTiers) atomicMin(mstar + threadIdx.x, (int)m0);
     return;
   }
   for (int l = threadIdx.x; l < L; l += blockDim.x) {
@@ -85,27 +96,35 @@ __global__ void __launch_bounds__(256) prune_rows_kernel(
        s += warps) {
     const double r = radii[s];
     if (r == 0.0 || lt == -INFINITY) continue;  // no tail at all
-    const double lr = log2(r);
+    const double lr = log2(r), l1r = log2(1.0 - r);
     double b = -INFINITY;
-    for (int l = lane; l < L; l += 32) b = fmax(b, fma((double)l, lr, lg[l]));
+    int lo = 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
-    const double tail = lt + (double)L * lr - log2(1.0 - r);
-    if (lane == 0 && !(tail <= b - 64.0)) atomicMin(mstar, (int)s);
+    for (int t = 0; t < kPruneTiers; ++t) {
+      const int L_t = 1 << prune_k(t);
+      for (int l = lo + lane; l < L_t; l += 32) b = fmax(b, fma((double)l, lr, lg[l]));
+      lo = L_t;
+      double bt = b;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) bt = fmax(bt, __shfl_xor_sync(0xffffffffu, bt, o));
+      const double tail = lt + (double)L_t * lr - l1r;
+      if (lane == 0 && !(tail <= bt - 64.0)) atomicMin(mstar + t, (int)s);
+    }
   }
 }
 
-// g^(q)_l = G^_l e^{+2 pi i l q / N}, q < N / L, l < L (q-major, natural l);
-// the root is the plan's circle table exp(2 pi i m / N) (core.py:87).
-__global__ void pretwiddle_kernel(int K, int ka, const double2* __restrict__ ghat_rev,
+// g^(q)_l = G^_l e^{+2 pi i l q / N}, q < N / L, l < L = 2^kl (q-major,
+// natural l); the root is the plan's circle table exp(2 pi i m / N)
+// (core.py:87).
+__global__ void pretwiddle_kernel(int K, int ka, int kl, const double2* __restrict__ ghat_rev,
                                   const double2* __restrict__ circle, double2* __restrict__ out,
                                   const int* __restrict__ stopped) {
   if (stopped && *stopped) return;
-  constexpr int L = 1 << kPruneK;
+  const int L = 1 << kl;
   const long long n = 1LL << K, total = n;  // (N / L) * L entries
   for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < total;
        x += (long long)gridDim.x * blockDim.x) {
-    const long long q = x >> kPruneK;
+    const long long q = x >> kl;
     const int l = (int)(x & (L - 1));
     const double2 g = spectrum_at(ghat_rev, l, K, ka);
     const double2 w = __ldg(circle + (((long long)l * q) & (n - 1)));

@@ -159,6 +159,13 @@ class Plan:
                                              _stream(stream)))
         return a.value, b.value
 
+    def field_tiers(self, stream=None):
+        """(1024-point rows, 4096-point rows, two-pass rows) of the last
+        large-N fast field evaluation (afd_field_tiers)."""
+        out = (C.c_int64 * 3)()
+        _capi.check(self.lib.afd_field_tiers(self.handle, out, _stream(stream)))
+        return tuple(out)
+
     def time_field(self, ghat, reps=20, stream=None):
         """Mean CUDA-event time (ms) of one fused field+argmax launch."""
         ghat = self._signal(ghat)

@@ -753,9 +753,10 @@ def test_bench_line_contract(afd):
     sp = r.get("split")
     if sp is not None:
         rows = d["config"]["m"]
+        assert sp["rows_1024"] + sp["rows_4096"] == sp["onchip_rows"]
         assert sp["onchip_rows"] + sp["twopass_rows"] == rows
-        f = (sp["onchip_rows"] * sp["flops_per_eval_onchip"] +
-             sp["twopass_rows"] * sp["flops_per_eval_twopass"]) / rows
+        f = (sp["rows_1024"] * sp["flops_per_eval_1024"] + sp["rows_4096"] *
+             sp["flops_per_eval_4096"] + sp["twopass_rows"] * sp["flops_per_eval_twopass"]) / rows
         assert abs(f - r["flops_per_eval"]) <= 1e-9 * f
         assert abs(r["bytes_per_eval"] - 32.0 * sp["twopass_rows"] / rows) <= 1e-12
     assert r["evals_per_launch"] == d["config"]["n"] * d["config"]["m"]
@@ -1012,11 +1013,14 @@ def test_pruned_field_argmax_and_split(afd, radii):
     got = np.frombuffer(plan.field_argmax(torch.from_numpy(ghat).cuda()).cpu().numpy().tobytes(),
                         O.CAND_DTYPE)[0]
     onchip, twopass = plan.field_split()
+    n1k, n4k, n2p = plan.field_tiers()
     ref = O.field_argmax(ghat, np.array(radii))
     assert int(got["flat"]) == int(ref["flat"])
     assert abs(got["mag"] - ref["mag"]) <= 1e-12 * ref["mag"]
     lo, hi = _first_unprunable(ghat, radii)
     assert lo <= onchip <= hi and onchip + twopass == len(radii)
+    lo1, hi1 = _first_unprunable(ghat, radii, L=1024)
+    assert lo1 <= n1k <= hi1 and n1k + n4k == onchip and n2p == twopass
 
 
 def test_pruned_fast_decompose_long_rows_and_threshold(afd):
@@ -1102,3 +1106,32 @@ def test_fast_batch_margins(afd):
         o = O.decompose(sig[i], np.array(radii), max_terms=4)
         ref = _oracle_margins(sig[i], radii, o.steps)
         assert np.all(np.abs(np.array(ds[i].margins) - ref) <= 1e-9)
+
+
+@pytest.mark.parametrize("n", [1024, 2048, 4096])
+@pytest.mark.parametrize("fast", [0, 1])
+def test_tmem_field_variants_full_groups(afd, n, fast):
+    """The TMEM field kernel at N = 1024 (eight row-groups of 64 threads: two
+    groups fill the four lane quadrants), 2048 (four groups) and 4096 (two),
+    launched with every group busy: materialised rows bitwise (exact) or to
+    1e-12 of the row's largest value (fast) against the oracle, and the
+    first maximum."""
+    core, engine = afd
+    import torch
+    from paper_1711_08604_b200 import workloads as W
+    m = 512
+    radii = tuple(0.99 * i / m for i in range(m))
+    g = W.pole_sum(n, 16, 0.95, 7 + n)
+    ghat = O.dft_forward(g)
+    plan = engine.Plan(radii, n, fast=fast)
+    got = plan.field(torch.from_numpy(ghat).cuda()).cpu().numpy()
+    ref = O.field(ghat, np.array(radii))
+    if fast:
+        scale = np.abs(ref).max(axis=1, keepdims=True)
+        assert np.all(np.abs(got - ref) <= 1e-12 * scale)
+    else:
+        assert np.array_equal(got, ref)
+    c = np.frombuffer(plan.field_argmax(torch.from_numpy(ghat).cuda()).cpu().numpy().tobytes(),
+                      O.CAND_DTYPE)[0]
+    r = O.field_argmax(ghat, np.array(radii))
+    assert int(c["flat"]) == int(r["flat"])
