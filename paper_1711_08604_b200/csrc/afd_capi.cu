@@ -260,11 +260,16 @@ constexpr bool kFieldTmem11 = AFD_FIELD_TMEM11 != 0;
 #define AFD_FIELD_TMEM10 1
 #endif
 constexpr bool kFieldTmem10 = AFD_FIELD_TMEM10 != 0;
+#ifndef AFD_FIELD_TMEM9
+#define AFD_FIELD_TMEM9 0
+#endif
+constexpr bool kFieldTmem9 = AFD_FIELD_TMEM9 != 0;
 template <int K>
 constexpr bool field_tmem_capable() {
   return kFieldRB == 4 && ((K == 12 && groups_for<K>() == 2) ||
                            (K == 11 && groups_for<K>() == 4 && kFieldTmem11) ||
-                           (K == 10 && groups_for<K>() == 8 && kFieldTmem10));
+                           (K == 10 && groups_for<K>() == 8 && kFieldTmem10) ||
+                           (K == 9 && groups_for<K>() == 16 && kFieldTmem9));
 }
 static bool field_tmem_enabled() {
   static int v = [] {

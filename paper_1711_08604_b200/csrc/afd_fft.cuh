@@ -546,6 +546,11 @@ struct GroupSync {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
   }
 };
+// A group that is exactly one warp (N = 512: sixteen 32-thread groups, more
+// than the 15 named barriers 1..15 a CTA has) synchronises as a warp.
+struct WarpSync {
+  __device__ __forceinline__ void operator()() const { __syncwarp(); }
+};
 
 // Optional per-pass hook: before(PASS) / after(PASS) around a pass's
 // butterflies, exch(PASS) after the exchange that follows it (timing

@@ -353,6 +353,7 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   // of phase (one group's loads overlap another's FP64 passes); smaller
   // groups share warps and step together with the whole block.
   constexpr bool kGroupSync = (T % 32 == 0) && G > 1;
+  static_assert(!kGroupSync || T == 32 || G <= 15, "named barriers 1 + g must be < 16");
   const int rounds = kGroupSync ? (rows - ((int)blockIdx.x * Gr + g) + per_round - 1) / per_round
                                 : (rows + per_round - 1) / per_round;
   // phase offset of group 1 (FieldHook): only when both groups have rows
@@ -521,7 +522,10 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
       }
       const FieldHook hook{offset && rd == 0 && g == 0, 2 * T, st, TM,
                            (dyn && tp == 0) ? &next_sl[g][rd & 1] : nullptr, &claim, per_round};
-      fft_passes<K, true, RB>(v, tp, active, sm, tw, GroupSync{1 + g, T}, hook);
+      if constexpr (T == 32)
+        fft_passes<K, true, RB>(v, tp, active, sm, tw, WarpSync{}, hook);
+      else
+        fft_passes<K, true, RB>(v, tp, active, sm, tw, GroupSync{1 + g, T}, hook);
     } else {
       fft_passes<K, true, RB>(v, tp, active, sm, tw);
     }

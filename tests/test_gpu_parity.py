@@ -1135,3 +1135,25 @@ def test_tmem_field_variants_full_groups(afd, n, fast):
                       O.CAND_DTYPE)[0]
     r = O.field_argmax(ghat, np.array(radii))
     assert int(c["flat"]) == int(r["flat"])
+
+
+@pytest.mark.parametrize("fast", [0, 1])
+def test_field_n512_many_signals(afd, fast):
+    """N = 512 with enough signals that every CTA runs all sixteen one-warp
+    row-groups (a regression: named barriers 1..16 overflowed the 16 a CTA
+    has); argmax per signal against the oracle."""
+    core, engine = afd
+    import torch
+    from paper_1711_08604_b200 import workloads as W
+    n, m, b = 512, 256, 32
+    radii = tuple(i / m for i in range(m))
+    sig = np.stack([W.pole_sum(n, 8, 0.95, 300 + i) for i in range(b)])
+    ghat = np.stack([O.dft_forward(x) for x in sig])
+    plan = engine.Plan(radii, n, max_batch=b, fast=fast)
+    got = np.frombuffer(plan.field_argmax(torch.from_numpy(ghat).cuda()).cpu().numpy().tobytes(),
+                        O.CAND_DTYPE)
+    for i in range(b):
+        r = O.field_argmax(ghat[i], np.array(radii))
+        assert int(got[i]["flat"]) == int(r["flat"]), i
+        if not fast:
+            assert got[i]["mag"] == r["mag"]
