@@ -20,6 +20,7 @@
 #include "afd_step_cluster.cuh"
 #include "afd_big.cuh"
 #include "afd_pruned.cuh"
+#include "afd_field_warp.cuh"
 #include "afd_direct.cuh"
 
 using namespace afd;
@@ -129,6 +130,7 @@ struct afd_plan {
     Cand* cand = nullptr;       // [Q][ncta]
     double* cand2 = nullptr;
     int ncta = 0;
+    bool warp = false;          // tier 0: one warp per 1024-point row (afd_field_warp.cuh)
   } tier[kPruneTiers];
   int* mstar = nullptr;        // [kPruneTiers] first row failing each tier's test
   unsigned long long* tmax = nullptr;
@@ -913,26 +915,36 @@ int big_reduce_cands(afd_plan* p, cudaStream_t st, const Cand** parts, int* npar
   return 0;
 }
 
+// AFD_WARP_FIELD=0: the 1024-point tier on field_kernel<10> (16 points per
+// thread, two exchanges) instead of the warp-per-row kernel (A/B switch).
+static const int kWarpField = getenv("AFD_WARP_FIELD") ? atoi(getenv("AFD_WARP_FIELD")) : 1;
+
 // One tier of the pruned fast field (afd_pruned.cuh): tables at plan time.
 template <int KT>
 int setup_pruned_tier(afd_plan* p, int t) {
   static_assert(field_tmem_capable<KT>(), "pruned tiers use the TMEM field kernel");
   constexpr int G = groups_for<KT>();
-  constexpr int STR = FastW<KT, kFieldRB>::STRIDE;
-  const int64_t rows = p->m1 - p->m0, Q = p->n >> KT;
   auto& T = p->tier[t];
+  T.warp = KT == kFwK && kWarpField;
+  const int STR = T.warp ? kFwStride : FastW<KT, kFieldRB>::STRIDE;
+  const int rows_per_cta = T.warp ? kFwWarps : G;
+  const int64_t rows = p->m1 - p->m0, Q = p->n >> KT;
   CU(cudaMalloc(&T.fw, sizeof(double) * STR * (size_t)rows));
   CU(cudaMalloc(&T.ghq, sizeof(double2) * (size_t)p->n));
   CU(cudaMalloc(&T.tw_img, sizeof(double2) * (SmemTw<KT, kFieldRB>::ENTRIES)));
   // CTAs per spectrum: the grid (ncta x Q) a whole number of SM waves
   int nc = 1;
   while (nc < p->sms && (nc * Q) % p->sms != 0) ++nc;
-  T.ncta = (int)std::max<int64_t>(1, std::min<int64_t>(nc, (rows + G - 1) / G));
+  T.ncta = (int)std::max<int64_t>(1, std::min<int64_t>(nc, (rows + rows_per_cta - 1) / rows_per_cta));
   CU(cudaMalloc(&T.cand, sizeof(Cand) * (size_t)Q * T.ncta));
   if (p->margins) CU(cudaMalloc(&T.cand2, sizeof(double) * (size_t)Q * T.ncta));
   const int64_t total = rows * STR;
-  fast_weight_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256>>>(
-      p->radii, p->scales, p->m0, rows, STR, 1 << (KT - 4), 16, KT - 4, 0, 0, T.fw);
+  if (T.warp)  // scale r^t (t < 32), r^(32 m) (m < 32): afd_field_warp.cuh
+    fast_weight_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256>>>(
+        p->radii, p->scales, p->m0, rows, STR, 32, 32, 5, 0, 0, T.fw);
+  else
+    fast_weight_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256>>>(
+        p->radii, p->scales, p->m0, rows, STR, 1 << (KT - 4), 16, KT - 4, 0, 0, T.fw);
   build_tw_image_kernel<KT><<<32, 256>>>(T.tw_img, p->twct);
   p->launches += 2;
   CU(cudaGetLastError());
@@ -940,6 +952,12 @@ int setup_pruned_tier(afd_plan* p, int t) {
                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem<KT>()));
   CU(cudaFuncSetAttribute(field_kernel<KT, kFieldRB, G, false, true, true, true>,
                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem<KT>()));
+  if (T.warp) {
+    CU(cudaFuncSetAttribute(field_warp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kFwSmem));
+    CU(cudaFuncSetAttribute(field_warp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kFwSmem));
+  }
   return 0;
 }
 
@@ -955,12 +973,19 @@ int launch_pruned_tier(afd_plan* p, int t, const double2* ghat_rev, int64_t r0, 
   auto& T = p->tier[t];
   pretwiddle_kernel<<<4 * p->sms, 256, 0, st>>>(p->K, p->ka, KT, ghat_rev, p->circle, T.ghq,
                                                 stopped);
-  auto pk = p->margins ? field_kernel<KT, kFieldRB, G, false, true, true, true>
-                       : field_kernel<KT, kFieldRB, G, false, true, true>;
-  pk<<<dim3((unsigned)T.ncta, (unsigned)Q), Geo<KT, kFieldRB>::T * G, field_smem<KT>(), st>>>(
-      T.ghq, T.fw, p->scales, p->twct, (long long)r0, (long long)r1, (long long)p->m0, T.cand,
-      nullptr, nullptr, T.tw_img, field_pp(), (unsigned*)nullptr, 0,
-      SubMap{(long long)p->n, Q, hi, T.cand2, lo});
+  if (T.warp) {  // 1024-point rows, one warp per row (afd_field_warp.cuh)
+    auto wk = p->margins ? field_warp_kernel<true> : field_warp_kernel<false>;
+    wk<<<dim3((unsigned)T.ncta, (unsigned)Q), 32 * kFwWarps, kFwSmem, st>>>(
+        T.ghq, T.fw, p->twct, (long long)r0, (long long)r1, (long long)p->m0, T.cand,
+        SubMap{(long long)p->n, Q, hi, T.cand2, lo});
+  } else {
+    auto pk = p->margins ? field_kernel<KT, kFieldRB, G, false, true, true, true>
+                         : field_kernel<KT, kFieldRB, G, false, true, true>;
+    pk<<<dim3((unsigned)T.ncta, (unsigned)Q), Geo<KT, kFieldRB>::T * G, field_smem<KT>(), st>>>(
+        T.ghq, T.fw, p->scales, p->twct, (long long)r0, (long long)r1, (long long)p->m0, T.cand,
+        nullptr, nullptr, T.tw_img, field_pp(), (unsigned*)nullptr, 0,
+        SubMap{(long long)p->n, Q, hi, T.cand2, lo});
+  }
   const int n = Q * T.ncta;
   const int slots = (int)(p->big_rows * big_col_ctas(p));
   const int np = std::max(1, std::min(std::min(kBigParts, (n + 255) / 256), (slots - *slot) / 2));

@@ -40,7 +40,7 @@ void run(int warps_per_sm, double* out) {
 }
 int main() {
   double* out; cudaMalloc(&out, 8);
-  for (int w : {4, 8, 16, 32, 64}) { run<1, 0>(w, out); run<2, 0>(w, out); run<4, 0>(w, out); run<8, 0>(w, out); }
+  for (int w : {4, 8, 16, 32, 64}) { run<1, 0>(w, out); run<2, 0>(w, out); run<4, 0>(w, out); run<6, 0>(w, out); run<8, 0>(w, out); run<12, 0>(w, out); run<16, 0>(w, out); }
   run<8, 1>(32, out); run<8, 2>(32, out); run<8, 1>(64, out); run<8, 2>(64, out);
   return 0;
 }
