@@ -21,6 +21,7 @@
 #include "afd_big.cuh"
 #include "afd_pruned.cuh"
 #include "afd_field_warp.cuh"
+#include "afd_field_reg.cuh"
 #include "afd_direct.cuh"
 
 using namespace afd;
@@ -130,8 +131,11 @@ struct afd_plan {
     Cand* cand = nullptr;       // [Q][ncta]
     double* cand2 = nullptr;
     int ncta = 0;
-    bool warp = false;          // tier 0: one warp per 1024-point row (afd_field_warp.cuh)
+    bool warp = false;          // 1024-point tier: one warp per row (afd_field_warp.cuh)
+    int qblocks = 0;            // register tiers: CTAs along q' (afd_field_reg.cuh)
   } tier[kPruneTiers];
+  int first_tier = 0;          // tiers below are switched off (AFD_REG_TIERS=0: kRegTiers)
+  unsigned long long* hint = nullptr;  // screening hint of the register tiers
   int* mstar = nullptr;        // [kPruneTiers] first row failing each tier's test
   unsigned long long* tmax = nullptr;
   double* nodes = nullptr;     // [2 * N / kNodeLen]
@@ -961,6 +965,58 @@ int setup_pruned_tier(afd_plan* p, int t) {
   return 0;
 }
 
+// AFD_REG_TIERS=0: no register tiers (rows of r <= 0.5 stay on the 1024-point
+// tier; A/B switch).
+static const int kRegTiersOn = getenv("AFD_REG_TIERS") ? atoi(getenv("AFD_REG_TIERS")) : 1;
+
+// A register tier (afd_field_reg.cuh, D = t + 1 blocks of 32 terms): the
+// factor rows {scale r^t, t < 32; r^(32 m), m < 32} (tier 0's are shared),
+// the [32 D][N / 32] pre-twiddled spectra, per-CTA candidates.
+int setup_reg_tier(afd_plan* p, int t) {
+  auto& T = p->tier[t];
+  const int D = t + 1;
+  const int64_t rows = p->m1 - p->m0, Qp = p->n >> 5;
+  T.qblocks = (int)(Qp / kFrThreads);
+  if (t == 0) {
+    CU(cudaMalloc(&T.fw, sizeof(double) * kFwStride * (size_t)rows));
+    const int64_t total = rows * kFwStride;
+    fast_weight_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256>>>(
+        p->radii, p->scales, p->m0, rows, kFwStride, 32, 32, 5, 0, 0, T.fw);
+    p->launches++;
+    CU(cudaGetLastError());
+  }
+  CU(cudaMalloc(&T.ghq, sizeof(double2) * (size_t)p->n * D));
+  // row splits: the grid (ncta x qblocks) a whole number of SM waves
+  int nc = 1;
+  while (nc < p->sms && (nc * T.qblocks) % p->sms != 0) ++nc;
+  T.ncta = (int)std::max<int64_t>(1, std::min<int64_t>(nc, rows));
+  CU(cudaMalloc(&T.cand, sizeof(Cand) * (size_t)T.qblocks * T.ncta));
+  if (p->margins) CU(cudaMalloc(&T.cand2, sizeof(double) * (size_t)T.qblocks * T.ncta));
+  return 0;
+}
+
+template <int D>
+int launch_reg_tier(afd_plan* p, int t, const double2* ghat_rev, int64_t r0, int64_t r1,
+                    const int* lo, const int* hi, const int* stopped, int* slot, cudaStream_t st) {
+  auto& T = p->tier[t];
+  pretwiddle_reg_kernel<<<4 * p->sms, 256, 0, st>>>(p->K, p->ka, D, ghat_rev, p->circle, T.ghq,
+                                                    stopped);
+  auto rk = p->margins ? field_reg_kernel<D, true> : field_reg_kernel<D, false>;
+  rk<<<dim3((unsigned)T.ncta, (unsigned)T.qblocks), kFrThreads, 0, st>>>(
+      T.ghq, p->tier[0].fw, (long long)r0, (long long)r1, (long long)p->m0,
+      (long long)(p->n >> 5), T.cand, p->hint,
+      SubMap{(long long)p->n, 0, hi, T.cand2, lo, nullptr});
+  const int n = T.qblocks * T.ncta;
+  const int slots = (int)(p->big_rows * big_col_ctas(p));
+  const int np = std::max(1, std::min(std::min(kBigParts, (n + 255) / 256), (slots - *slot) / 2));
+  cand_partial_kernel<<<np, 256, 0, st>>>(T.cand, n, (n + np - 1) / np, p->big_cand + *slot,
+                                          T.cand2, p->big_cand2 ? p->big_cand2 + *slot : nullptr);
+  *slot += np;
+  p->launches += 3;
+  CU(cudaGetLastError());
+  return 0;
+}
+
 // One tier per step: pre-twiddled spectra, the on-chip field over rows
 // [max(r0, *lo), min(r1, *hi)) (device limits), candidate partials into
 // big_cand slots from *slot on.
@@ -977,7 +1033,7 @@ int launch_pruned_tier(afd_plan* p, int t, const double2* ghat_rev, int64_t r0, 
     auto wk = p->margins ? field_warp_kernel<true> : field_warp_kernel<false>;
     wk<<<dim3((unsigned)T.ncta, (unsigned)Q), 32 * kFwWarps, kFwSmem, st>>>(
         T.ghq, T.fw, p->twct, (long long)r0, (long long)r1, (long long)p->m0, T.cand,
-        SubMap{(long long)p->n, Q, hi, T.cand2, lo});
+        SubMap{(long long)p->n, Q, hi, T.cand2, lo, p->hint});
   } else {
     auto pk = p->margins ? field_kernel<KT, kFieldRB, G, false, true, true, true>
                          : field_kernel<KT, kFieldRB, G, false, true, true>;
@@ -1013,23 +1069,32 @@ int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, doub
   }
   const int* lim = nullptr;
   if (!fout && p->pruned) {
-    // tier 0: rows [r0, mstar[0]) as N/1024 1024-point fields, tier 1: rows
-    // [mstar[0], mstar[1]) as N/4096 4096-point fields, rows [mstar[1], r1)
-    // through the batches below (all limits read on the device)
-    prune_init_kernel<<<1, 1, 0, st>>>(p->mstar, r1, p->tmax);
+    // tier t takes rows [mstar[t-1], mstar[t]): tiers 0, 1 in registers (32
+    // and 64 terms), tier 2 as N/1024 1024-point fields, tier 3 as N/4096
+    // 4096-point fields, rows [mstar[3], r1) through the batches below (all
+    // limits read on the device).  The 1024-point tier runs first: its
+    // maxima start the register tiers' screens (hint).
+    prune_init_kernel<<<1, 1, 0, st>>>(p->mstar, r0, r1, p->first_tier, p->tmax, p->hint);
     prune_tail_kernel<<<2 * p->sms, 256, 0, st>>>(ghat_rev, p->n, p->tmax);
     prune_rows_kernel<<<2 * p->sms, 256, 0, st>>>(p->K, p->ka, ghat_rev, p->radii, r0, r1,
                                                   p->tmax, stopped, p->mstar);
     p->launches += 3;
     CU(cudaGetLastError());
     int slot = 0, rc2;
-    if ((rc2 = launch_pruned_tier<prune_k(0)>(p, 0, ghat_rev, r0, r1, nullptr, p->mstar, stopped,
-                                               &slot, st)))
-      return rc2;
-    if ((rc2 = launch_pruned_tier<prune_k(1)>(p, 1, ghat_rev, r0, r1, p->mstar, p->mstar + 1,
+    if ((rc2 = launch_pruned_tier<prune_k(2)>(p, 2, ghat_rev, r0, r1, p->mstar + 1, p->mstar + 2,
                                                stopped, &slot, st)))
       return rc2;
-    lim = p->mstar + 1;
+    if ((rc2 = launch_pruned_tier<prune_k(3)>(p, 3, ghat_rev, r0, r1, p->mstar + 2, p->mstar + 3,
+                                               stopped, &slot, st)))
+      return rc2;
+    if (p->first_tier == 0) {
+      if ((rc2 = launch_reg_tier<1>(p, 0, ghat_rev, r0, r1, nullptr, p->mstar, stopped, &slot, st)))
+        return rc2;
+      if ((rc2 = launch_reg_tier<2>(p, 1, ghat_rev, r0, r1, p->mstar, p->mstar + 1, stopped, &slot,
+                                    st)))
+        return rc2;
+    }
+    lim = p->mstar + kPruneTiers - 1;
   }
   for (int64_t b = r0; b < r1; b += p->big_rows) {
     const int64_t rows = std::min<int64_t>(p->big_rows, r1 - b);
@@ -1368,8 +1433,12 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
       // the first L - 1 entries of the N-point tables), per-CTA candidates
       ALLOC2(p->mstar, sizeof(int) * kPruneTiers);
       ALLOC2(p->tmax, sizeof(unsigned long long));
-      rc = setup_pruned_tier<prune_k(0)>(p, 0);
-      if (!rc) rc = setup_pruned_tier<prune_k(1)>(p, 1);
+      ALLOC2(p->hint, sizeof(unsigned long long));
+      p->first_tier = kRegTiersOn ? 0 : kRegTiers;
+      rc = setup_pruned_tier<prune_k(2)>(p, 2);
+      if (!rc) rc = setup_pruned_tier<prune_k(3)>(p, 3);
+      if (!rc && p->first_tier == 0) rc = setup_reg_tier(p, 0);
+      if (!rc && p->first_tier == 0) rc = setup_reg_tier(p, 1);
       if (rc) return cleanup(rc);
       p->pruned = true;
     }
@@ -1424,6 +1493,7 @@ int afd_plan_destroy(afd_plan* p) {
   cudaFree(p->cand2);
   cudaFree(p->mstar);
   cudaFree(p->tmax);
+  cudaFree(p->hint);
   cudaFree(p->big_part);
   cudaFree(p->nodes);
   cudaFree(p->sel);
@@ -2094,23 +2164,38 @@ int afd_field_split(afd_plan* p, int64_t* onchip, int64_t* twopass, void* stream
   return 0;
 }
 
-int afd_field_tiers(afd_plan* p, int64_t* rows3, void* stream) {
-  if (!p || !rows3) return fail(AFD_E_INVALID, "NULL argument");
+int afd_field_tiers5(afd_plan* p, int64_t* rows5, void* stream) {
+  if (!p || !rows5) return fail(AFD_E_INVALID, "NULL argument");
   int rc;
   if ((rc = set_device(p))) return rc;
   const int64_t rows = p->m1 - p->m0;
+  for (int t = 0; t <= kPruneTiers; ++t) rows5[t] = 0;
   if (!p->big || !p->pruned) {
-    rows3[0] = rows3[1] = 0;
-    rows3[2] = p->big ? rows : 0;
+    rows5[kPruneTiers] = p->big ? rows : 0;
     return 0;
   }
-  int ms[kPruneTiers] = {0, 0};
+  int ms[kPruneTiers] = {};
   CU(cudaMemcpyAsync(ms, p->mstar, sizeof(ms), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   CU(cudaStreamSynchronize((cudaStream_t)stream));
   auto clampr = [&](int64_t x) { return std::max<int64_t>(0, std::min<int64_t>(rows, x - p->m0)); };
-  rows3[0] = clampr(ms[0]);
-  rows3[1] = clampr(ms[1]) - rows3[0];
-  rows3[2] = rows - rows3[0] - rows3[1];
+  int64_t prev = 0;
+  for (int t = 0; t < kPruneTiers; ++t) {
+    const int64_t e = std::max(prev, clampr(ms[t]));
+    rows5[t] = e - prev;
+    prev = e;
+  }
+  rows5[kPruneTiers] = rows - prev;
+  return 0;
+}
+
+int afd_field_tiers(afd_plan* p, int64_t* rows3, void* stream) {
+  if (!rows3) return fail(AFD_E_INVALID, "NULL argument");
+  int64_t r5[kPruneTiers + 1];
+  int rc;
+  if ((rc = afd_field_tiers5(p, r5, stream))) return rc;
+  rows3[0] = r5[0] + r5[1] + r5[2];
+  rows3[1] = r5[3];
+  rows3[2] = r5[4];
   return 0;
 }
 

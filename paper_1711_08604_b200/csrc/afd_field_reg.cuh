@@ -1,0 +1,244 @@
+// afd_field_reg.cuh — fast-engine field + argmax for rows that need at most
+// L = 32 D spectrum terms (D = 1, 2), entirely in registers: one thread per
+// 32 outputs, no exchange, no barriers (weighted_inverse_grid +
+// maximal_selection, transform.py:185-201, core.py:285-300; the arithmetic
+// of the fast engine, afd_fft.cuh "Fast mode").
+//
+// Row s of the field is F_s(j) = sum_l w_l G^_l e^{2 pi i l j / N} with
+// w_l = scale_s r_s^l.  When the terms l >= 32 D are negligible
+// (prune_rows_kernel: below 2^-64 of a kept term, r <= 0.25 for D = 1,
+// r <= 0.5 for D = 2 — half of r_m = m/M), split j = q' + Q' i with
+// Q' = N / 32 and l = l0 + 32 m:
+//   F_s(q' + Q' i) = sum_{l0 < 32} e^{2 pi i l0 i / 32} w_{l0} sum_{m < D} rho^m h^(q')_{l0, m},
+//   h^(q')_{l0, m} = G^_{l0 + 32 m} e^{2 pi i (l0 + 32 m) q' / N},  rho = r_s^32,
+// a 32-point inverse transform (five register stages with compile-time
+// 32nd roots of unity: warp_pass0_stage) of a polynomial in rho of degree
+// D - 1.  Thread q' keeps its 32 D pre-twiddled values h (row-independent,
+// pretwiddle_reg_kernel) in tensor memory and walks the rows: per grid
+// evaluation 2 (D - 1) DFMA for the polynomial, 3 for the weights fused with
+// stage 0, ~10 for stages 1-4, 3 for |F|^2 and the screen: ~16-18 FP64
+// instructions against ~33 for the 1024-point warp kernel, and no shared
+// memory traffic beyond the row's 32 weights (a broadcast line per warp).
+//
+// Rows are visited in decreasing order (|F|^2 grows with r at small radii, so
+// the first rows set the maximum and the rest only pass the screen), and the
+// screen starts from `hint`: the largest |F|^2 (margins: runner-up) the
+// tiers launched before have already found — a lower bound of the step's
+// maximum, so no candidate is lost; ties (>=) still reach the update path.
+#pragma once
+
+#include "afd_field_warp.cuh"
+
+namespace afd {
+
+constexpr int kFrWarps = 8;
+constexpr int kFrThreads = 32 * kFrWarps;
+
+template <int D, bool MARG>
+__global__ void __launch_bounds__(kFrThreads, 1)
+field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled spectra
+                 const double* __restrict__ fw,      // [rows of plan][64] factor rows (kFwStride)
+                 long long row0, long long row1,     // global rows to evaluate
+                 long long pw_row0,                  // global row of fw[0]
+                 long long qp_total,                 // Q' = N / 32
+                 Cand* __restrict__ cand_out,        // [gridDim.y][gridDim.x]
+                 const unsigned long long* __restrict__ hint, SubMap sub) {
+  static_assert(D == 1 || D == 2, "TMEM holds 128 D columns for each of two warps per quadrant");
+  constexpr int GI = 8 / D;          // registers i per 32-word TMEM load
+  constexpr int NCH = 32 / GI;       // loads per row
+  constexpr int kCols = 128 * D;     // columns per warp
+  constexpr int kTmCols = 2 * kCols;
+  __shared__ uint32_t tm_base;
+  __shared__ __align__(16) double wsm[kFrWarps][2][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = blockIdx.y * gridDim.x + blockIdx.x;
+  if (sub.lim_lo != nullptr) {
+    const long long l = *sub.lim_lo;
+    if (l > row0) row0 = l < row1 ? l : row1;
+  }
+  if (sub.lim != nullptr) {
+    const long long l = *sub.lim;
+    if (l < row1) row1 = l > row0 ? l : row0;
+  }
+  const int rows = (int)(row1 - row0);
+  if (rows <= (int)blockIdx.x) {  // no rows for this CTA this step: a neutral candidate
+    if (threadIdx.x == 0) {
+      Cand c;
+      c.mag = -1.0;
+      c.flat = 0x7fffffffffffffffLL;
+      c.re = c.im = 0.0;
+      cand_out[slot] = c;
+      if constexpr (MARG) sub.cand2[slot] = -1.0;
+    }
+    return;
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&tm_base)),
+                 "n"(kTmCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // the warp's lane quadrant; warps w and w + 4 share it, side by side
+  const uint32_t tmw = tm_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * kCols);
+  const long long qp = (long long)blockIdx.y * kFrThreads + threadIdx.x;
+  // chunk c holds registers i = GI c .. GI c + GI - 1, block m at word 4 GI m
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    double2 g[8];
+#pragma unroll
+    for (int m = 0; m < D; ++m)
+#pragma unroll
+      for (int u = 0; u < GI; ++u)
+        g[m * GI + u] = __ldg(h + (size_t)(m * 32 + c * GI + u) * (size_t)qp_total + qp);
+#pragma unroll
+    for (int x = 0; x < 8; ++x) tm_st4(tmw + 32 * c + 4 * x, g[x]);
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+
+  double best_mag = -1.0, best_re = 0.0, best_im = 0.0;
+  int best_sl = 0x7fffffff, best_i = 0;
+  [[maybe_unused]] double sec_mag = -1.0;
+  double thr = hint ? __longlong_as_double((long long)*hint) : 0.0;
+  if (!(thr > 0.0)) thr = -1.0;
+
+  // rows sl = blockIdx.x + k gridDim.x, k = nk - 1 .. 0
+  const int nk = (rows - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const double* __restrict__ fr0 = fw + (size_t)(row0 + blockIdx.x - pw_row0) * kFwStride;
+  const size_t fstep = (size_t)gridDim.x * kFwStride;
+  double a_nx = __ldg(fr0 + (size_t)(nk - 1) * fstep + lane);
+  [[maybe_unused]] double rho_nx = D > 1 ? __ldg(fr0 + (size_t)(nk - 1) * fstep + 33) : 0.0;
+  const int wpos = brev_bits(lane, 5);  // weight of l0 = lane sits at register index rev5(l0)
+  for (int k = nk - 1; k >= 0; --k) {
+    const int sl = (int)blockIdx.x + k * (int)gridDim.x;
+    double* wrow = wsm[warp][k & 1];
+    wrow[wpos] = a_nx;
+    [[maybe_unused]] const double rho = rho_nx;
+    __syncwarp();
+    if (k > 0) {  // next row's factors, one row ahead
+      a_nx = __ldg(fr0 + (size_t)(k - 1) * fstep + lane);
+      if constexpr (D > 1) rho_nx = __ldg(fr0 + (size_t)(k - 1) * fstep + 33);
+    }
+    double2 v[32];
+    {
+      // y_i = w_l0 sum_m rho^m h_(l0, m) and the stage-0 butterflies (register
+      // pairs 2 u, 2 u + 1), GI registers per TMEM load, the next load in flight
+      uint32_t r[2][32];
+      tm_ld<32>(tmw, r[0]);
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        tm_wait_ld();
+        tm_dep(r[c & 1]);
+        if (c + 1 < NCH) tm_ld<32>(tmw + 32 * (c + 1), r[(c + 1) & 1]);
+        const uint32_t* rc = r[c & 1];
+#pragma unroll
+        for (int u = 0; u < GI; u += 2) {
+          const int i0 = GI * c + u, i1 = i0 + 1;
+          const double2 w = *reinterpret_cast<const double2*>(wrow + i0);
+          double2 x0 = make_double2(tm_dbl(rc + 4 * ((D - 1) * GI + u)),
+                                    tm_dbl(rc + 4 * ((D - 1) * GI + u) + 2));
+          double2 x1 = make_double2(tm_dbl(rc + 4 * ((D - 1) * GI + u + 1)),
+                                    tm_dbl(rc + 4 * ((D - 1) * GI + u + 1) + 2));
+#pragma unroll
+          for (int m = D - 2; m >= 0; --m) {
+            x0.x = fma(rho, x0.x, tm_dbl(rc + 4 * (m * GI + u)));
+            x0.y = fma(rho, x0.y, tm_dbl(rc + 4 * (m * GI + u) + 2));
+            x1.x = fma(rho, x1.x, tm_dbl(rc + 4 * (m * GI + u + 1)));
+            x1.y = fma(rho, x1.y, tm_dbl(rc + 4 * (m * GI + u + 1) + 2));
+          }
+          const double zr = w.y * x1.x, zi = w.y * x1.y;
+          v[i0] = make_double2(fma(w.x, x0.x, zr), fma(w.x, x0.y, zi));
+          v[i1] = make_double2(fma(w.x, x0.x, -zr), fma(w.x, x0.y, -zi));
+        }
+      }
+    }
+    warp_pass0_stage<1>(v);
+    warp_pass0_stage<2>(v);
+    warp_pass0_stage<3>(v);
+    warp_pass0_stage<4>(v);
+
+    // the screen: one predicate-accumulating compare per point
+    unsigned up = 0;
+#pragma unroll
+    for (int i0 = 0; i0 < 32; i0 += 4) {
+      double mg[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) mg[i] = fast_mag2(v[i0 + i]);
+      up = any_ge4(up, mg, thr);
+    }
+    if (__builtin_expect(__any_sync(0xffffffffu, up != 0), 0)) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        double2 f = v[i];
+        asm volatile("" : "+d"(f.x), "+d"(f.y));
+        const double mg = fast_mag2(f);
+        // rows descend: an equal magnitude in a lower row wins; within a row
+        // j = q' + Q' i increases with i
+        const bool better = mg > best_mag || (mg == best_mag && sl < best_sl);
+        if (better) {
+          if constexpr (MARG) sec_mag = best_mag;
+          best_mag = mg;
+          best_re = f.x;
+          best_im = f.y;
+          best_sl = sl;
+          best_i = i;
+        } else if constexpr (MARG) {
+          if (mg > sec_mag) sec_mag = mg;
+        }
+      }
+      double m = best_mag;
+      [[maybe_unused]] double r = sec_mag;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        if constexpr (MARG) {
+          const double r2 = __shfl_xor_sync(0xffffffffu, r, o);
+          r = runner_merge(r, m, r2, m2);
+        }
+        m = fmax(m, m2);
+      }
+      thr = fmax(thr, MARG ? r : m);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_base),
+                 "n"(kTmCols)
+                 : "memory");
+  Cand best;
+  best.mag = best_mag;
+  if (best_mag >= 0.0) {
+    best.flat = (row0 + best_sl) * sub.row_stride + qp + qp_total * (long long)best_i;
+  } else {
+    best.flat = 0x7fffffffffffffffLL;
+  }
+  best.re = best_re;
+  best.im = best_im;
+  [[maybe_unused]] const double own_mag = best.mag;
+  [[maybe_unused]] const long long own_flat = best.flat;
+  __shared__ Cand red[kFrWarps];
+  __shared__ long long win_flat;
+  best = warp_argmax(best);
+  if (lane == 0) red[warp] = best;
+  __syncthreads();
+  if (warp == 0) {
+    Cand c = lane < kFrWarps ? red[lane] : best;
+    c = warp_argmax(c);
+    if (lane == 0) {
+      cand_out[slot] = c;
+      if constexpr (MARG) win_flat = c.flat;
+    }
+  }
+  if constexpr (MARG) {
+    __shared__ double red2[32];
+    __syncthreads();
+    const double r2 = cta_runner_up(sec_mag, own_mag, own_flat, win_flat, red2);
+    if (threadIdx.x == 0) sub.cand2[slot] = r2;
+  }
+}
+
+}  // namespace afd

@@ -388,13 +388,19 @@ field_warp_kernel(const double2* __restrict__ ghat,   // [batch][1024]
     if (lane == 0) {
       cand_out[(size_t)sig * gridDim.x + blockIdx.x] = c;
       if constexpr (MARG) win_flat = c.flat;
+      // non-negative doubles order like their bit patterns
+      if (!MARG && sub.hint && c.mag > 0.0)
+        atomicMax(sub.hint, (unsigned long long)__double_as_longlong(c.mag));
     }
   }
   if constexpr (MARG) {
     __shared__ double red2[32];
     __syncthreads();
     const double r2 = cta_runner_up(sec_mag, own_mag, own_flat, win_flat, red2);
-    if (threadIdx.x == 0) sub.cand2[(size_t)sig * gridDim.x + blockIdx.x] = r2;
+    if (threadIdx.x == 0) {
+      sub.cand2[(size_t)sig * gridDim.x + blockIdx.x] = r2;
+      if (sub.hint && r2 > 0.0) atomicMax(sub.hint, (unsigned long long)__double_as_longlong(r2));
+    }
   }
 }
 

@@ -197,6 +197,8 @@ struct SubMap {
   const int* lim;        // device row limit (rows >= *lim skipped) or null
   double* cand2;         // [batch][gridDim.x] runner-up magnitudes or null
   const int* lim_lo;     // device lower row limit (rows < *lim_lo skipped) or null
+  unsigned long long* hint;  // max-reduced bits of the launch's largest |F|^2 (margins: runner-up)
+                             // for the screens of later tiers (afd_field_reg.cuh), or null
 };
 
 // First maximum of a CTA's candidates and the runner-up: the largest of

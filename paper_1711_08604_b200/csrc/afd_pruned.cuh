@@ -28,20 +28,27 @@
 
 namespace afd {
 
-// On-chip sub-transform tiers: rows whose tail beyond L = 1024 is
-// negligible run as N/1024 1024-point fields (the fastest on-chip field
-// kernel per evaluation: 3.7e11 vs 3.1e11 evals/s at 4096 points), rows
-// that need up to 4096 terms as N/4096 4096-point fields, the rest
+// On-chip sub-transform tiers, by the number of spectrum terms L a row needs
+// (its tail beyond l = L negligible): L = 32 and L = 64 run in registers,
+// one thread per 32 outputs and no exchange at all (afd_field_reg.cuh: half
+// of r_m = m/M), L = 1024 as N/1024 1024-point fields (one warp per row,
+// afd_field_warp.cuh), L = 4096 as N/4096 4096-point fields, the rest
 // two-pass.  mstar[t] = first row failing tier t's test; tiers are nested
-// (a row failing L = 4096 fails L = 1024), so mstar[0] <= mstar[1].
-constexpr int kPruneTiers = 2;
-__host__ __device__ constexpr int prune_k(int t) { return t == 0 ? 10 : 12; }
+// (a row failing a longer tier fails every shorter one), so mstar[] is
+// non-decreasing and tier t takes rows [mstar[t-1], mstar[t]).
+constexpr int kPruneTiers = 4;
+constexpr int kRegTiers = 2;  // tiers 0, 1: the register kernels (D = 1, 2 blocks of 32 terms)
+__host__ __device__ constexpr int prune_k(int t) { return t == 0 ? 5 : t == 1 ? 6 : t == 2 ? 10 : 12; }
 constexpr int kPruneK = 12;  // the longest tier (the spectrum head staged by prune_rows)
 
-// mstar[t] = m1, *tmax = 0 (the tail maximum is max-reduced on its bits)
-__global__ void prune_init_kernel(int* mstar, long long m1, unsigned long long* tmax) {
-  for (int t = 0; t < kPruneTiers; ++t) mstar[t] = (int)m1;
+// mstar[t] = m1 (tiers below `first`: m0, switched off), *tmax = 0 (the tail
+// maximum is max-reduced on its bits), *hint = 0 (the screening hint of the
+// register tiers, afd_field_reg.cuh)
+__global__ void prune_init_kernel(int* mstar, long long m0, long long m1, int first,
+                                  unsigned long long* tmax, unsigned long long* hint) {
+  for (int t = 0; t < kPruneTiers; ++t) mstar[t] = (int)(t < first ? m0 : m1);
   *tmax = 0ull;
+  *hint = 0ull;
 }
 
 // T^2 = max_l |G^_l|^2 over the whole spectrum (an upper bound of the tail's)
@@ -126,6 +133,27 @@ __global__ void pretwiddle_kernel(int K, int ka, int kl, const double2* __restri
        x += (long long)gridDim.x * blockDim.x) {
     const long long q = x >> kl;
     const int l = (int)(x & (L - 1));
+    const double2 g = spectrum_at(ghat_rev, l, K, ka);
+    const double2 w = __ldg(circle + (((long long)l * q) & (n - 1)));
+    out[x] = make_double2(fma(g.x, w.x, -(g.y * w.y)), fma(g.x, w.y, g.y * w.x));
+  }
+}
+
+// The register tiers' spectra (afd_field_reg.cuh): for q' < Q' = N / 32,
+// register i < 32 and block m < D,
+//   h[(m 32 + i) Q' + q'] = G^_l e^{+2 pi i l q' / N},  l = rev5(i) + 32 m
+// (q' fastest: thread q' of the field kernel reads its 32 D values coalesced).
+__global__ void pretwiddle_reg_kernel(int K, int ka, int D, const double2* __restrict__ ghat_rev,
+                                      const double2* __restrict__ circle,
+                                      double2* __restrict__ out, const int* __restrict__ stopped) {
+  if (stopped && *stopped) return;
+  const int kq = K - 5;
+  const long long n = 1LL << K, qmask = (1LL << kq) - 1, total = (long long)D << K;
+  for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+       x += (long long)gridDim.x * blockDim.x) {
+    const long long q = x & qmask;
+    const int im = (int)(x >> kq);
+    const int l = (int)(__brev((unsigned)(im & 31)) >> 27) + 32 * (im >> 5);
     const double2 g = spectrum_at(ghat_rev, l, K, ka);
     const double2 w = __ldg(circle + (((long long)l * q) & (n - 1)));
     out[x] = make_double2(fma(g.x, w.x, -(g.y * w.y)), fma(g.x, w.y, g.y * w.x));

@@ -160,10 +160,18 @@ class Plan:
         return a.value, b.value
 
     def field_tiers(self, stream=None):
-        """(1024-point rows, 4096-point rows, two-pass rows) of the last
+        """(rows of at most 1024 points, 4096-point rows, two-pass rows) of the last
         large-N fast field evaluation (afd_field_tiers)."""
         out = (C.c_int64 * 3)()
         _capi.check(self.lib.afd_field_tiers(self.handle, out, _stream(stream)))
+        return tuple(out)
+
+    def field_tiers5(self, stream=None):
+        """(32-term rows, 64-term rows, 1024-point rows, 4096-point rows,
+        two-pass rows) of the last large-N fast field evaluation
+        (afd_field_tiers5)."""
+        out = (C.c_int64 * 5)()
+        _capi.check(self.lib.afd_field_tiers5(self.handle, out, _stream(stream)))
         return tuple(out)
 
     def time_field(self, ghat, reps=20, stream=None):

@@ -1021,6 +1021,99 @@ def test_pruned_field_argmax_and_split(afd, radii):
     assert lo <= onchip <= hi and onchip + twopass == len(radii)
     lo1, hi1 = _first_unprunable(ghat, radii, L=1024)
     assert lo1 <= n1k <= hi1 and n1k + n4k == onchip and n2p == twopass
+    # the register tiers (32 and 64 spectrum terms) inside the <= 1024 rows
+    t5 = plan.field_tiers5()
+    assert sum(t5) == len(radii) and t5[0] + t5[1] + t5[2] == n1k and t5[3] == n4k
+    lo32, hi32 = _first_unprunable(ghat, radii, L=32)
+    lo64, hi64 = _first_unprunable(ghat, radii, L=64)
+    assert lo32 <= t5[0] <= hi32 and lo64 <= t5[0] + t5[1] <= hi64
+
+
+# ---------------------------------------------------------------------------
+# register tiers of the pruned field (csrc/afd_field_reg.cuh): rows that need
+# at most 32 or 64 spectrum terms, one thread per 32 outputs
+# ---------------------------------------------------------------------------
+def _cand(plan, ghat):
+    import torch
+    return np.frombuffer(plan.field_argmax(torch.from_numpy(ghat).cuda()).cpu().numpy().tobytes(),
+                         O.CAND_DTYPE)[0]
+
+
+@pytest.mark.parametrize("k", [16, 20])
+def test_reg_tier_rows_one_by_one(afd, k):
+    """Single-row fields at radii across both register tiers (and just
+    beyond): each row's first maximum is the oracle's (flat index; value and
+    magnitude to 1e-12), and the row went to the expected tier."""
+    core, engine = afd
+    from paper_1711_08604_b200 import workloads as W
+    n = 1 << k
+    g = W.pole_sum(n, 24, 0.9, 4242 + k)
+    ghat = O.dft_forward(g)
+    rs = (0.0, 0.03, 0.11, 0.2, 0.249, 0.27, 0.33, 0.41, 0.499, 0.52, 0.61) if k == 16 else \
+        (0.17, 0.38)
+    for r in rs:
+        plan = engine.Plan((r,), n, fast=1)
+        got = _cand(plan, ghat)
+        t5 = plan.field_tiers5()
+        del plan
+        ref = O.field_argmax(ghat, np.array([r]))
+        assert int(got["flat"]) == int(ref["flat"]), r
+        assert abs(got["mag"] - ref["mag"]) <= 1e-12 * ref["mag"], r
+        assert abs(complex(got["re"], got["im"]) - complex(ref["re"], ref["im"])) \
+            <= 1e-12 * np.sqrt(ref["mag"]), r
+        lo32, _ = _first_unprunable(ghat, (r,), L=32)
+        lo64, _ = _first_unprunable(ghat, (r,), L=64)
+        want = 0 if lo32 == 1 else 1 if lo64 == 1 else 2
+        assert t5[want] == 1, (r, t5)
+
+
+@pytest.mark.parametrize("engine_name", ["fft-fast", "fft-fast-margins"])
+def test_reg_tier_low_radius_grid_decomposes_like_the_oracle(afd, engine_name):
+    """Every radius <= 0.5: the whole field runs in the register tiers, so
+    every selection comes from them (many rows per CTA, several CTAs per
+    row block, descending row order): identical poles, 1e-9 values, and the
+    reference's margins."""
+    core, _ = afd
+    from paper_1711_08604_b200 import workloads as W
+    n, m = 1 << 16, 300
+    radii = tuple(0.5 * i / (m - 1) for i in range(m))
+    g = W.pole_sum(n, 16, 0.6, 777)
+    grid = core.ParameterGrid(radii, n)
+    d = core.decompose(g, grid, max_terms=4, engine=engine_name)
+    o = O.decompose(g, np.array(radii), max_terms=4)
+    assert [s.point.angle_index for s in d.steps] == list(o.steps["j"])
+    assert [s.point.radius for s in d.steps] == list(o.steps["radius"])
+    oc = o.steps["c_re"] + 1j * o.steps["c_im"]
+    c = np.array([s.coefficient for s in d.steps])
+    assert np.all(np.abs(c - oc) <= FAST_TOL * np.abs(oc))
+    assert np.abs(d.remainder - o.remainder).max() <= FAST_TOL * np.abs(o.remainder).max()
+    if engine_name.endswith("margins"):
+        ref = _oracle_margins(g, radii, o.steps)
+        assert np.all(np.abs(np.array(d.margins) - ref) <= 1e-9)
+
+
+def test_reg_tier_ties_take_the_lowest_flat_index(afd):
+    """Exact ties inside the register tiers: a constant signal (every point
+    of a row equal, the r = 0 row the largest) and duplicated radii (equal
+    rows): the first maximum in flat order wins although rows are visited in
+    decreasing order and every thread holds an equal candidate."""
+    core, engine = afd
+    n = 1 << 16
+    ghat = O.dft_forward(np.full(n, 0.75 - 0.25j))
+    plan = engine.Plan((0.0, 0.1, 0.2), n, fast=1)
+    got = _cand(plan, ghat)
+    assert plan.field_tiers5()[0] == 3
+    del plan
+    assert int(got["flat"]) == 0 == int(O.field_argmax(ghat, np.array([0.0, 0.1, 0.2]))["flat"])
+    from paper_1711_08604_b200 import workloads as W
+    ghat = O.dft_forward(W.pole_sum(n, 8, 0.8, 5))
+    radii = (0.1, 0.3, 0.2, 0.3, 0.3, 0.05)
+    plan = engine.Plan(radii, n, fast=1)
+    got = _cand(plan, ghat)
+    del plan
+    ref = O.field_argmax(ghat, np.array(radii))
+    assert int(got["flat"]) == int(ref["flat"])
+    assert int(ref["flat"]) // n == 1
 
 
 def test_pruned_fast_decompose_long_rows_and_threshold(afd):
