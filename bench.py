@@ -394,22 +394,21 @@ def field_roofline(plan, w, radii_rows, ghat, exact, local):
         # 4096-point transforms of pre-twiddled spectra (F(L) flops, no HBM
         # bytes: the spectra and the weight tables are L2-resident), the
         # rest the two-pass path (F(N) flops, 32 B per eval)
-        n32, n64, n1k, n4k, twopass = plan.field_tiers5()
-        f32, f64, f1k, f4k = (flops_per_eval(32), flops_per_eval(64), flops_per_eval(1024),
-                              flops_per_eval(4096))
-        fpe = (n32 * f32 + n64 * f64 + n1k * f1k + n4k * f4k + twopass * fpe) / float(rows)
+        tiers = plan.field_tier_rows()
+        twopass = tiers.pop(w.n, 0)
+        fpe = (sum(r * flops_per_eval(t) for t, r in tiers.items()) + twopass * fpe) / float(rows)
         bpe = 32.0 * twopass / float(rows)
-        split = {"rows_32": n32, "rows_64": n64, "rows_1024": n1k, "rows_4096": n4k,
-                 "onchip_rows": n32 + n64 + n1k + n4k, "twopass_rows": twopass,
-                 "flops_per_eval_32": f32, "flops_per_eval_64": f64,
-                 "flops_per_eval_1024": f1k, "flops_per_eval_4096": f4k,
-                 "flops_per_eval_twopass": flops_per_eval(w.n),
+        split = {"rows_%d" % t: r for t, r in tiers.items()}
+        split.update({"flops_per_eval_%d" % t: flops_per_eval(t) for t in tiers})
+        split.update({"onchip_rows": sum(tiers.values()), "twopass_rows": twopass,
+                      "flops_per_eval_twopass": flops_per_eval(w.n)})
+        split.update({
                  "bytes_per_eval_twopass": 32.0,
                  "note": "rows whose weight tail beyond l = L is below 2^-64 of the largest "
                          "kept term are evaluated from their first L spectrum terms: L = 32, "
-                         "64 in registers (one thread per 32 outputs), L = 1024, 4096 as N/L "
-                         "on-chip L-point fields; credited F(L) = 5 log2 L + 7 flops per "
-                         "eval (DESIGN.md §4)"}
+                         "64, 128 in registers (one thread per 32 outputs), L = 1024, 4096 as "
+                         "N/L on-chip L-point fields; credited F(L) = 5 log2 L + 7 flops per "
+                         "eval (DESIGN.md §4)"})
     achieved = launch_evals * fpe / (field_ms * 1e-3) / 1e12
     peak = engine.fp64_peak_tflops(local)
     hbm_peak, hbm_src = hbm_peak_gbs()
@@ -439,7 +438,7 @@ def field_roofline(plan, w, radii_rows, ghat, exact, local):
                    if w.n <= 8192 else
                    "large-N field: pass A (big_field_a) + TMA column pass (col_tma_kernel)"
                    if split is None else
-                   "pruned large-N field: register tiers (field_reg_kernel<1>, <2>), on-chip "
+                   "pruned large-N field: register tiers (field_reg_kernel<1>, <2>, <4>), on-chip "
                    "1024- and 4096-point fields (field_warp_kernel, field_kernel<12>) + "
                    "two-pass rows (big_field_a + col_tma_kernel)"),
         "flops_per_eval": fpe, "evals_per_launch": launch_evals, "launch_ms": field_ms})

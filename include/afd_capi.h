@@ -254,11 +254,14 @@ int afd_field_split(afd_plan *plan, int64_t *onchip, int64_t *twopass, void *str
  * at most 1024-point transforms (tail beyond l = 1024 negligible), rows3[1] as
  * 4096-point transforms, rows3[2] two-pass (zeros for on-chip N). */
 int afd_field_tiers(afd_plan *plan, int64_t *rows3, void *stream);
-/* afd_field_tiers5: the split by every tier: rows5[0], rows5[1] rows in
- * registers (32 and 64 spectrum terms, one thread per 32 outputs), rows5[2]
- * as 1024-point transforms, rows5[3] as 4096-point transforms, rows5[4]
- * two-pass.  afd_field_tiers' rows3[0] = rows5[0] + rows5[1] + rows5[2]. */
-int afd_field_tiers5(afd_plan *plan, int64_t *rows5, void *stream);
+/* afd_field_tier_rows: the split by every tier, in row order: terms[t] =
+ * spectrum terms a row of tier t is evaluated from (32, 64, 128: in
+ * registers, one thread per 32 outputs; 1024, 4096: on-chip transforms; N:
+ * two-pass, the last entry), rows[t] = its rows in the last evaluation.
+ * Writes *count <= cap entries (cap >= 8 always suffices; one entry
+ * {N, all rows} for unpruned plans). */
+int afd_field_tier_rows(afd_plan *plan, int64_t *terms, int64_t *rows, int cap, int *count,
+                        void *stream);
 int afd_fp64_peak(int device, double *tflops, void *stream);
 
 #ifdef __cplusplus

@@ -72,7 +72,7 @@ SIGNATURES = [
     ("afd_fp64_peak", _I, [_I, _VP, _VP]),
     ("afd_field_split", _I, [_VP, _VP, _VP, _VP]),
     ("afd_field_tiers", _I, [_VP, _VP, _VP]),
-    ("afd_field_tiers5", _I, [_VP, _VP, _VP]),
+    ("afd_field_tier_rows", _I, [_VP, _VP, _VP, _I, _VP, _VP]),
 ]
 
 _LIB = None

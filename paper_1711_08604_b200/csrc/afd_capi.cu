@@ -969,14 +969,14 @@ int setup_pruned_tier(afd_plan* p, int t) {
 // tier; A/B switch).
 static const int kRegTiersOn = getenv("AFD_REG_TIERS") ? atoi(getenv("AFD_REG_TIERS")) : 1;
 
-// A register tier (afd_field_reg.cuh, D = t + 1 blocks of 32 terms): the
+// A register tier (afd_field_reg.cuh, D = 2^t blocks of 32 terms): the
 // factor rows {scale r^t, t < 32; r^(32 m), m < 32} (tier 0's are shared),
 // the [32 D][N / 32] pre-twiddled spectra, per-CTA candidates.
 int setup_reg_tier(afd_plan* p, int t) {
   auto& T = p->tier[t];
-  const int D = t + 1;
+  const int D = 1 << t;
   const int64_t rows = p->m1 - p->m0, Qp = p->n >> 5;
-  T.qblocks = (int)(Qp / kFrThreads);
+  T.qblocks = (int)((Qp + fr_threads(D) - 1) / fr_threads(D));
   if (t == 0) {
     CU(cudaMalloc(&T.fw, sizeof(double) * kFwStride * (size_t)rows));
     const int64_t total = rows * kFwStride;
@@ -1002,7 +1002,7 @@ int launch_reg_tier(afd_plan* p, int t, const double2* ghat_rev, int64_t r0, int
   pretwiddle_reg_kernel<<<4 * p->sms, 256, 0, st>>>(p->K, p->ka, D, ghat_rev, p->circle, T.ghq,
                                                     stopped);
   auto rk = p->margins ? field_reg_kernel<D, true> : field_reg_kernel<D, false>;
-  rk<<<dim3((unsigned)T.ncta, (unsigned)T.qblocks), kFrThreads, 0, st>>>(
+  rk<<<dim3((unsigned)T.ncta, (unsigned)T.qblocks), fr_threads(D), 0, st>>>(
       T.ghq, p->tier[0].fw, (long long)r0, (long long)r1, (long long)p->m0,
       (long long)(p->n >> 5), T.cand, p->hint,
       SubMap{(long long)p->n, 0, hi, T.cand2, lo, nullptr});
@@ -1069,9 +1069,9 @@ int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, doub
   }
   const int* lim = nullptr;
   if (!fout && p->pruned) {
-    // tier t takes rows [mstar[t-1], mstar[t]): tiers 0, 1 in registers (32
-    // and 64 terms), tier 2 as N/1024 1024-point fields, tier 3 as N/4096
-    // 4096-point fields, rows [mstar[3], r1) through the batches below (all
+    // tier t takes rows [mstar[t-1], mstar[t]): tiers 0..2 in registers (32,
+    // 64 and 128 terms), tier 3 as N/1024 1024-point fields, tier 4 as N/4096
+    // 4096-point fields, rows [mstar[4], r1) through the batches below (all
     // limits read on the device).  The 1024-point tier runs first: its
     // maxima start the register tiers' screens (hint).
     prune_init_kernel<<<1, 1, 0, st>>>(p->mstar, r0, r1, p->first_tier, p->tmax, p->hint);
@@ -1081,17 +1081,21 @@ int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, doub
     p->launches += 3;
     CU(cudaGetLastError());
     int slot = 0, rc2;
-    if ((rc2 = launch_pruned_tier<prune_k(2)>(p, 2, ghat_rev, r0, r1, p->mstar + 1, p->mstar + 2,
-                                               stopped, &slot, st)))
+    constexpr int t1k = kRegTiers, t4k = kRegTiers + 1;
+    if ((rc2 = launch_pruned_tier<prune_k(t1k)>(p, t1k, ghat_rev, r0, r1, p->mstar + t1k - 1,
+                                                 p->mstar + t1k, stopped, &slot, st)))
       return rc2;
-    if ((rc2 = launch_pruned_tier<prune_k(3)>(p, 3, ghat_rev, r0, r1, p->mstar + 2, p->mstar + 3,
-                                               stopped, &slot, st)))
+    if ((rc2 = launch_pruned_tier<prune_k(t4k)>(p, t4k, ghat_rev, r0, r1, p->mstar + t4k - 1,
+                                                 p->mstar + t4k, stopped, &slot, st)))
       return rc2;
     if (p->first_tier == 0) {
       if ((rc2 = launch_reg_tier<1>(p, 0, ghat_rev, r0, r1, nullptr, p->mstar, stopped, &slot, st)))
         return rc2;
       if ((rc2 = launch_reg_tier<2>(p, 1, ghat_rev, r0, r1, p->mstar, p->mstar + 1, stopped, &slot,
                                     st)))
+        return rc2;
+      if ((rc2 = launch_reg_tier<4>(p, 2, ghat_rev, r0, r1, p->mstar + 1, p->mstar + 2, stopped,
+                                    &slot, st)))
         return rc2;
     }
     lim = p->mstar + kPruneTiers - 1;
@@ -1435,10 +1439,9 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
       ALLOC2(p->tmax, sizeof(unsigned long long));
       ALLOC2(p->hint, sizeof(unsigned long long));
       p->first_tier = kRegTiersOn ? 0 : kRegTiers;
-      rc = setup_pruned_tier<prune_k(2)>(p, 2);
-      if (!rc) rc = setup_pruned_tier<prune_k(3)>(p, 3);
-      if (!rc && p->first_tier == 0) rc = setup_reg_tier(p, 0);
-      if (!rc && p->first_tier == 0) rc = setup_reg_tier(p, 1);
+      rc = setup_pruned_tier<prune_k(kRegTiers)>(p, kRegTiers);
+      if (!rc) rc = setup_pruned_tier<prune_k(kRegTiers + 1)>(p, kRegTiers + 1);
+      for (int t = 0; t < kRegTiers && !rc && p->first_tier == 0; ++t) rc = setup_reg_tier(p, t);
       if (rc) return cleanup(rc);
       p->pruned = true;
     }
@@ -2164,16 +2167,21 @@ int afd_field_split(afd_plan* p, int64_t* onchip, int64_t* twopass, void* stream
   return 0;
 }
 
-int afd_field_tiers5(afd_plan* p, int64_t* rows5, void* stream) {
-  if (!p || !rows5) return fail(AFD_E_INVALID, "NULL argument");
+int afd_field_tier_rows(afd_plan* p, int64_t* terms, int64_t* rows_out, int cap, int* count,
+                        void* stream) {
+  if (!p || !terms || !rows_out || !count) return fail(AFD_E_INVALID, "NULL argument");
   int rc;
   if ((rc = set_device(p))) return rc;
   const int64_t rows = p->m1 - p->m0;
-  for (int t = 0; t <= kPruneTiers; ++t) rows5[t] = 0;
   if (!p->big || !p->pruned) {
-    rows5[kPruneTiers] = p->big ? rows : 0;
+    if (cap < 1) return fail(AFD_E_INVALID, "afd_field_tier_rows: cap %d < 1", cap);
+    terms[0] = p->n;
+    rows_out[0] = rows;
+    *count = 1;
     return 0;
   }
+  if (cap < kPruneTiers + 1)
+    return fail(AFD_E_INVALID, "afd_field_tier_rows: cap %d < %d", cap, kPruneTiers + 1);
   int ms[kPruneTiers] = {};
   CU(cudaMemcpyAsync(ms, p->mstar, sizeof(ms), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   CU(cudaStreamSynchronize((cudaStream_t)stream));
@@ -2181,21 +2189,24 @@ int afd_field_tiers5(afd_plan* p, int64_t* rows5, void* stream) {
   int64_t prev = 0;
   for (int t = 0; t < kPruneTiers; ++t) {
     const int64_t e = std::max(prev, clampr(ms[t]));
-    rows5[t] = e - prev;
+    terms[t] = 1LL << prune_k(t);
+    rows_out[t] = e - prev;
     prev = e;
   }
-  rows5[kPruneTiers] = rows - prev;
+  terms[kPruneTiers] = p->n;
+  rows_out[kPruneTiers] = rows - prev;
+  *count = kPruneTiers + 1;
   return 0;
 }
 
 int afd_field_tiers(afd_plan* p, int64_t* rows3, void* stream) {
-  if (!rows3) return fail(AFD_E_INVALID, "NULL argument");
-  int64_t r5[kPruneTiers + 1];
-  int rc;
-  if ((rc = afd_field_tiers5(p, r5, stream))) return rc;
-  rows3[0] = r5[0] + r5[1] + r5[2];
-  rows3[1] = r5[3];
-  rows3[2] = r5[4];
+  if (!p || !rows3) return fail(AFD_E_INVALID, "NULL argument");
+  rows3[0] = rows3[1] = rows3[2] = 0;
+  if (!p->big) return 0;
+  int64_t terms[kPruneTiers + 1], r[kPruneTiers + 1];
+  int rc, cnt = 0;
+  if ((rc = afd_field_tier_rows(p, terms, r, kPruneTiers + 1, &cnt, stream))) return rc;
+  for (int t = 0; t < cnt; ++t) rows3[t == cnt - 1 ? 2 : terms[t] <= 1024 ? 0 : 1] += r[t];
   return 0;
 }
 

@@ -1,5 +1,5 @@
 // afd_field_reg.cuh — fast-engine field + argmax for rows that need at most
-// L = 32 D spectrum terms (D = 1, 2), entirely in registers: one thread per
+// L = 32 D spectrum terms (D = 1, 2, 4), entirely in registers: one thread per
 // 32 outputs, no exchange, no barriers (weighted_inverse_grid +
 // maximal_selection, transform.py:185-201, core.py:285-300; the arithmetic
 // of the fast engine, afd_fft.cuh "Fast mode").
@@ -7,7 +7,7 @@
 // Row s of the field is F_s(j) = sum_l w_l G^_l e^{2 pi i l j / N} with
 // w_l = scale_s r_s^l.  When the terms l >= 32 D are negligible
 // (prune_rows_kernel: below 2^-64 of a kept term, r <= 0.25 for D = 1,
-// r <= 0.5 for D = 2 — half of r_m = m/M), split j = q' + Q' i with
+// r <= 0.5 for D = 2, r <= 0.7 for D = 4), split j = q' + Q' i with
 // Q' = N / 32 and l = l0 + 32 m:
 //   F_s(q' + Q' i) = sum_{l0 < 32} e^{2 pi i l0 i / 32} w_{l0} sum_{m < D} rho^m h^(q')_{l0, m},
 //   h^(q')_{l0, m} = G^_{l0 + 32 m} e^{2 pi i (l0 + 32 m) q' / N},  rho = r_s^32,
@@ -16,7 +16,7 @@
 // D - 1.  Thread q' keeps its 32 D pre-twiddled values h (row-independent,
 // pretwiddle_reg_kernel) in tensor memory and walks the rows: per grid
 // evaluation 2 (D - 1) DFMA for the polynomial, 3 for the weights fused with
-// stage 0, ~10 for stages 1-4, 3 for |F|^2 and the screen: ~16-18 FP64
+// stage 0, ~10 for stages 1-4, 3 for |F|^2 and the screen: ~16-22 FP64
 // instructions against ~33 for the 1024-point warp kernel, and no shared
 // memory traffic beyond the row's 32 weights (a broadcast line per warp).
 //
@@ -31,11 +31,17 @@
 
 namespace afd {
 
-constexpr int kFrWarps = 8;
-constexpr int kFrThreads = 32 * kFrWarps;
+// Warps per CTA (one CTA per SM): tensor memory has room for 512 / (128 D)
+// warps per lane quadrant (D = 4: one, four warps per SM), registers for 8
+// warps at 255 or 12 at 168.
+#ifndef AFD_FR_WARPS1
+#define AFD_FR_WARPS1 8
+#endif
+__host__ __device__ constexpr int fr_warps(int D) { return D == 1 ? AFD_FR_WARPS1 : D == 2 ? 8 : 4; }
+__host__ __device__ constexpr int fr_threads(int D) { return 32 * fr_warps(D); }
 
 template <int D, bool MARG>
-__global__ void __launch_bounds__(kFrThreads, 1)
+__global__ void __launch_bounds__(fr_threads(D), 1)
 field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled spectra
                  const double* __restrict__ fw,      // [rows of plan][64] factor rows (kFwStride)
                  long long row0, long long row1,     // global rows to evaluate
@@ -43,11 +49,13 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
                  long long qp_total,                 // Q' = N / 32
                  Cand* __restrict__ cand_out,        // [gridDim.y][gridDim.x]
                  const unsigned long long* __restrict__ hint, SubMap sub) {
-  static_assert(D == 1 || D == 2, "TMEM holds 128 D columns for each of two warps per quadrant");
+  static_assert(D == 1 || D == 2 || D == 4, "chunks of 8 / D registers per 32-word TMEM load");
   constexpr int GI = 8 / D;          // registers i per 32-word TMEM load
   constexpr int NCH = 32 / GI;       // loads per row
+  constexpr int kFrWarps = fr_warps(D), kFrThreads = fr_threads(D);
   constexpr int kCols = 128 * D;     // columns per warp
-  constexpr int kTmCols = 2 * kCols;
+  constexpr int kTmCols = kCols * (kFrWarps / 4) <= 256 ? 256 : 512;
+  static_assert(kFrWarps % 4 == 0 && kCols * (kFrWarps / 4) <= 512, "TMEM columns");
   __shared__ uint32_t tm_base;
   __shared__ __align__(16) double wsm[kFrWarps][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -85,9 +93,10 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
   // the warp's lane quadrant; warps w and w + 4 share it, side by side
   const uint32_t tmw = tm_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * kCols);
   const long long qp = (long long)blockIdx.y * kFrThreads + threadIdx.x;
+  const bool active = qp < qp_total;  // warp-uniform (Q' is a multiple of 32)
   // chunk c holds registers i = GI c .. GI c + GI - 1, block m at word 4 GI m
 #pragma unroll
-  for (int c = 0; c < NCH; ++c) {
+  for (int c = 0; c < NCH && active; ++c) {
     double2 g[8];
 #pragma unroll
     for (int m = 0; m < D; ++m)
@@ -106,11 +115,11 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
   if (!(thr > 0.0)) thr = -1.0;
 
   // rows sl = blockIdx.x + k gridDim.x, k = nk - 1 .. 0
-  const int nk = (rows - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int nk = active ? (rows - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
   const double* __restrict__ fr0 = fw + (size_t)(row0 + blockIdx.x - pw_row0) * kFwStride;
   const size_t fstep = (size_t)gridDim.x * kFwStride;
-  double a_nx = __ldg(fr0 + (size_t)(nk - 1) * fstep + lane);
-  [[maybe_unused]] double rho_nx = D > 1 ? __ldg(fr0 + (size_t)(nk - 1) * fstep + 33) : 0.0;
+  double a_nx = nk > 0 ? __ldg(fr0 + (size_t)(nk - 1) * fstep + lane) : 0.0;
+  [[maybe_unused]] double rho_nx = D > 1 && nk > 0 ? __ldg(fr0 + (size_t)(nk - 1) * fstep + 33) : 0.0;
   const int wpos = brev_bits(lane, 5);  // weight of l0 = lane sits at register index rev5(l0)
   for (int k = nk - 1; k >= 0; --k) {
     const int sl = (int)blockIdx.x + k * (int)gridDim.x;

@@ -29,16 +29,18 @@
 namespace afd {
 
 // On-chip sub-transform tiers, by the number of spectrum terms L a row needs
-// (its tail beyond l = L negligible): L = 32 and L = 64 run in registers,
-// one thread per 32 outputs and no exchange at all (afd_field_reg.cuh: half
+// (its tail beyond l = L negligible): L = 32, 64 and 128 run in registers,
+// one thread per 32 outputs and no exchange at all (afd_field_reg.cuh: 70%
 // of r_m = m/M), L = 1024 as N/1024 1024-point fields (one warp per row,
 // afd_field_warp.cuh), L = 4096 as N/4096 4096-point fields, the rest
 // two-pass.  mstar[t] = first row failing tier t's test; tiers are nested
 // (a row failing a longer tier fails every shorter one), so mstar[] is
 // non-decreasing and tier t takes rows [mstar[t-1], mstar[t]).
-constexpr int kPruneTiers = 4;
-constexpr int kRegTiers = 2;  // tiers 0, 1: the register kernels (D = 1, 2 blocks of 32 terms)
-__host__ __device__ constexpr int prune_k(int t) { return t == 0 ? 5 : t == 1 ? 6 : t == 2 ? 10 : 12; }
+constexpr int kPruneTiers = 5;
+constexpr int kRegTiers = 3;  // tiers 0..2: the register kernels (D = 1, 2, 4 blocks of 32 terms)
+__host__ __device__ constexpr int prune_k(int t) {
+  return t == 0 ? 5 : t == 1 ? 6 : t == 2 ? 7 : t == 3 ? 10 : 12;
+}
 constexpr int kPruneK = 12;  // the longest tier (the spectrum head staged by prune_rows)
 
 // mstar[t] = m1 (tiers below `first`: m0, switched off), *tmax = 0 (the tail

@@ -166,13 +166,14 @@ class Plan:
         _capi.check(self.lib.afd_field_tiers(self.handle, out, _stream(stream)))
         return tuple(out)
 
-    def field_tiers5(self, stream=None):
-        """(32-term rows, 64-term rows, 1024-point rows, 4096-point rows,
-        two-pass rows) of the last large-N fast field evaluation
-        (afd_field_tiers5)."""
-        out = (C.c_int64 * 5)()
-        _capi.check(self.lib.afd_field_tiers5(self.handle, out, _stream(stream)))
-        return tuple(out)
+    def field_tier_rows(self, stream=None):
+        """{spectrum terms: rows} of the last large-N fast field evaluation by
+        tier, in row order (afd_field_tier_rows): 32, 64, 128 (register
+        tiers), 1024, 4096 (on-chip transforms), N (two-pass)."""
+        terms, rows, cnt = (C.c_int64 * 8)(), (C.c_int64 * 8)(), C.c_int()
+        _capi.check(self.lib.afd_field_tier_rows(self.handle, terms, rows, 8, C.byref(cnt),
+                                                 _stream(stream)))
+        return {int(terms[t]): int(rows[t]) for t in range(cnt.value)}
 
     def time_field(self, ghat, reps=20, stream=None):
         """Mean CUDA-event time (ms) of one fused field+argmax launch."""

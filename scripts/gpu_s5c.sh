@@ -1,0 +1,24 @@
+#!/bin/bash
+# round 2, session 5 (c): third register tier (128 terms, four warps per SM): tests, c4 / c2 bench, per-kernel times
+cd $GRAFT_REPO_ROOT
+O=gpurun_out/s5c
+mkdir -p $O
+timeout 1500 python -m pytest tests -m gpu -x -q -k "reg_tier or pruned or margins or fast" > $O/tests.log 2>&1; echo "tests rc=$?"; tail -4 $O/tests.log
+timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_c4.json 2> $O/bench_c4.err; echo "c4 rc=$?"
+timeout 600 python bench.py --config c2 --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_c2.json 2> $O/bench_c2.err; echo "c2 rc=$?"
+python - <<'PY'
+import json
+for f in ("c4","c2"):
+    try:
+        d=json.loads(open("gpurun_out/s5c/bench_%s.json"%f).read())
+        print(f, "%.4e"%d["value"], "e2e %.4e"%d["e2e"]["value"], d["roofline"]["frac"], d["roofline"]["launch_ms"], d.get("parity_vs_oracle"), d["clocks"], {k:v for k,v in d["roofline"].get("split",{}).items() if k.startswith("rows")})
+    except Exception as e: print(f, "ERR", e)
+PY
+cmd="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-parity"
+timeout 900 ncu --metrics gpu__time_duration.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_elapsed --clock-control none -k regex:"field_reg_kernel|field_warp_kernel|field_kernel" -s 12 -c 10 --csv \
+   --log-file $O/tier_kernels.csv $cmd > $O/ncu2.log 2>&1; echo "ncu rc=$?"
+grep -v "^==" $O/tier_kernels.csv | python -c "
+import csv,sys
+for r in csv.DictReader(sys.stdin):
+    print(r['Kernel Name'][:40], r['Metric Name'], r['Metric Value'])
+"

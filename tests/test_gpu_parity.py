@@ -1021,17 +1021,21 @@ def test_pruned_field_argmax_and_split(afd, radii):
     assert lo <= onchip <= hi and onchip + twopass == len(radii)
     lo1, hi1 = _first_unprunable(ghat, radii, L=1024)
     assert lo1 <= n1k <= hi1 and n1k + n4k == onchip and n2p == twopass
-    # the register tiers (32 and 64 spectrum terms) inside the <= 1024 rows
-    t5 = plan.field_tiers5()
-    assert sum(t5) == len(radii) and t5[0] + t5[1] + t5[2] == n1k and t5[3] == n4k
-    lo32, hi32 = _first_unprunable(ghat, radii, L=32)
-    lo64, hi64 = _first_unprunable(ghat, radii, L=64)
-    assert lo32 <= t5[0] <= hi32 and lo64 <= t5[0] + t5[1] <= hi64
+    # the register tiers (32, 64, 128 spectrum terms) inside the <= 1024 rows
+    tr = plan.field_tier_rows()
+    assert list(tr) == [32, 64, 128, 1024, 4096, n]
+    assert sum(tr.values()) == len(radii) and tr[4096] == n4k and tr[n] == n2p
+    assert tr[32] + tr[64] + tr[128] + tr[1024] == n1k
+    upto = 0
+    for L in (32, 64, 128):
+        lo_l, hi_l = _first_unprunable(ghat, radii, L=L)
+        upto += tr[L]
+        assert lo_l <= upto <= hi_l, L
 
 
 # ---------------------------------------------------------------------------
 # register tiers of the pruned field (csrc/afd_field_reg.cuh): rows that need
-# at most 32 or 64 spectrum terms, one thread per 32 outputs
+# at most 32, 64 or 128 spectrum terms, one thread per 32 outputs
 # ---------------------------------------------------------------------------
 def _cand(plan, ghat):
     import torch
@@ -1041,7 +1045,7 @@ def _cand(plan, ghat):
 
 @pytest.mark.parametrize("k", [16, 20])
 def test_reg_tier_rows_one_by_one(afd, k):
-    """Single-row fields at radii across both register tiers (and just
+    """Single-row fields at radii across the register tiers (and just
     beyond): each row's first maximum is the oracle's (flat index; value and
     magnitude to 1e-12), and the row went to the expected tier."""
     core, engine = afd
@@ -1049,35 +1053,34 @@ def test_reg_tier_rows_one_by_one(afd, k):
     n = 1 << k
     g = W.pole_sum(n, 24, 0.9, 4242 + k)
     ghat = O.dft_forward(g)
-    rs = (0.0, 0.03, 0.11, 0.2, 0.249, 0.27, 0.33, 0.41, 0.499, 0.52, 0.61) if k == 16 else \
-        (0.17, 0.38)
+    rs = (0.0, 0.03, 0.11, 0.2, 0.249, 0.27, 0.33, 0.41, 0.499, 0.52, 0.61, 0.68, 0.73) \
+        if k == 16 else (0.17, 0.38, 0.6)
     for r in rs:
         plan = engine.Plan((r,), n, fast=1)
         got = _cand(plan, ghat)
-        t5 = plan.field_tiers5()
+        tr = plan.field_tier_rows()
         del plan
         ref = O.field_argmax(ghat, np.array([r]))
         assert int(got["flat"]) == int(ref["flat"]), r
         assert abs(got["mag"] - ref["mag"]) <= 1e-12 * ref["mag"], r
         assert abs(complex(got["re"], got["im"]) - complex(ref["re"], ref["im"])) \
             <= 1e-12 * np.sqrt(ref["mag"]), r
-        lo32, _ = _first_unprunable(ghat, (r,), L=32)
-        lo64, _ = _first_unprunable(ghat, (r,), L=64)
-        want = 0 if lo32 == 1 else 1 if lo64 == 1 else 2
-        assert t5[want] == 1, (r, t5)
+        want = next((L for L in (32, 64, 128) if _first_unprunable(ghat, (r,), L=L)[0] == 1),
+                    1024)
+        assert tr[want] == 1, (r, tr)
 
 
 @pytest.mark.parametrize("engine_name", ["fft-fast", "fft-fast-margins"])
 def test_reg_tier_low_radius_grid_decomposes_like_the_oracle(afd, engine_name):
-    """Every radius <= 0.5: the whole field runs in the register tiers, so
+    """Every radius <= 0.69: the whole field runs in the register tiers, so
     every selection comes from them (many rows per CTA, several CTAs per
     row block, descending row order): identical poles, 1e-9 values, and the
     reference's margins."""
     core, _ = afd
     from paper_1711_08604_b200 import workloads as W
     n, m = 1 << 16, 300
-    radii = tuple(0.5 * i / (m - 1) for i in range(m))
-    g = W.pole_sum(n, 16, 0.6, 777)
+    radii = tuple(0.69 * i / (m - 1) for i in range(m))
+    g = W.pole_sum(n, 16, 0.75, 777)
     grid = core.ParameterGrid(radii, n)
     d = core.decompose(g, grid, max_terms=4, engine=engine_name)
     o = O.decompose(g, np.array(radii), max_terms=4)
@@ -1102,7 +1105,7 @@ def test_reg_tier_ties_take_the_lowest_flat_index(afd):
     ghat = O.dft_forward(np.full(n, 0.75 - 0.25j))
     plan = engine.Plan((0.0, 0.1, 0.2), n, fast=1)
     got = _cand(plan, ghat)
-    assert plan.field_tiers5()[0] == 3
+    assert plan.field_tier_rows()[32] == 3
     del plan
     assert int(got["flat"]) == 0 == int(O.field_argmax(ghat, np.array([0.0, 0.1, 0.2]))["flat"])
     from paper_1711_08604_b200 import workloads as W
