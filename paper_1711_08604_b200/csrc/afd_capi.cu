@@ -134,6 +134,7 @@ struct afd_plan {
     bool warp = false;          // 1024-point tier: one warp per row (afd_field_warp.cuh)
     int qblocks = 0;            // register tiers: CTAs along q' (afd_field_reg.cuh)
   } tier[kPruneTiers];
+  int64_t est_rows[kPruneTiers] = {};  // rows per tier expected from the radii alone
   int first_tier = 0;          // tiers below are switched off (AFD_REG_TIERS=0: kRegTiers)
   unsigned long long* hint = nullptr;  // screening hint of the register tiers
   int* mstar = nullptr;        // [kPruneTiers] first row failing each tier's test
@@ -923,6 +924,47 @@ int big_reduce_cands(afd_plan* p, cudaStream_t st, const Cand** parts, int* npar
 // thread, two exchanges) instead of the warp-per-row kernel (A/B switch).
 static const int kWarpField = getenv("AFD_WARP_FIELD") ? atoi(getenv("AFD_WARP_FIELD")) : 1;
 
+// AFD_TIER_NCTA=n: row splits of every on-chip tier (default: tier_ncta).
+static const int kTierNcta = getenv("AFD_TIER_NCTA") ? atoi(getenv("AFD_TIER_NCTA")) : 0;
+
+// Rows per tier from the radii alone (a flat spectrum: T = B_s): the tier of
+// r is the first L with r^L / (1 - r) <= 2^-64.  The device decides per step
+// (prune_rows_kernel); this only sizes the grids.
+void estimate_tier_rows(afd_plan* p, const double* radii_host) {
+  for (auto& e : p->est_rows) e = 0;
+  for (int64_t s = p->m0; s < p->m1; ++s) {
+    const double r = radii_host[s];
+    int t = 0;
+    if (r > 0.0)
+      while (t < kPruneTiers &&
+             (double)(1 << prune_k(t)) * std::log2(r) - std::log2(1.0 - r) > -64.0)
+        ++t;
+    if (t < p->first_tier) t = p->first_tier;
+    if (t < kPruneTiers) p->est_rows[t]++;
+  }
+}
+
+// Row splits of a tier's grid (nc x q CTAs, one CTA per SM at a time, each
+// running its share of the tier's rows `rpc` at a time after a prologue
+// worth `prologue` row-times: TMEM allocation, twiddles, the spectrum): the
+// nc that minimises waves x (prologue + row rounds) for the expected rows.
+int tier_ncta(const afd_plan* p, int64_t q, int64_t est, int rpc, double prologue) {
+  if (kTierNcta > 0) return kTierNcta;
+  est = std::max<int64_t>(est, rpc);
+  int best = 1;
+  double best_cost = 1e300;
+  for (int nc = 1; nc <= p->sms; ++nc) {
+    const double waves = std::ceil((double)nc * q / p->sms);
+    const double rounds = std::ceil((double)est / ((double)nc * rpc));
+    const double cost = waves * (prologue + rounds);
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = nc;
+    }
+  }
+  return best;
+}
+
 // One tier of the pruned fast field (afd_pruned.cuh): tables at plan time.
 template <int KT>
 int setup_pruned_tier(afd_plan* p, int t) {
@@ -936,9 +978,8 @@ int setup_pruned_tier(afd_plan* p, int t) {
   CU(cudaMalloc(&T.fw, sizeof(double) * STR * (size_t)rows));
   CU(cudaMalloc(&T.ghq, sizeof(double2) * (size_t)p->n));
   CU(cudaMalloc(&T.tw_img, sizeof(double2) * (SmemTw<KT, kFieldRB>::ENTRIES)));
-  // CTAs per spectrum: the grid (ncta x Q) a whole number of SM waves
-  int nc = 1;
-  while (nc < p->sms && (nc * Q) % p->sms != 0) ++nc;
+  // row splits of the grid (ncta x Q): tier_ncta
+  const int nc = tier_ncta(p, Q, p->est_rows[t], rows_per_cta, 1.6);
   T.ncta = (int)std::max<int64_t>(1, std::min<int64_t>(nc, (rows + rows_per_cta - 1) / rows_per_cta));
   CU(cudaMalloc(&T.cand, sizeof(Cand) * (size_t)Q * T.ncta));
   if (p->margins) CU(cudaMalloc(&T.cand2, sizeof(double) * (size_t)Q * T.ncta));
@@ -986,9 +1027,7 @@ int setup_reg_tier(afd_plan* p, int t) {
     CU(cudaGetLastError());
   }
   CU(cudaMalloc(&T.ghq, sizeof(double2) * (size_t)p->n * D));
-  // row splits: the grid (ncta x qblocks) a whole number of SM waves
-  int nc = 1;
-  while (nc < p->sms && (nc * T.qblocks) % p->sms != 0) ++nc;
+  const int nc = tier_ncta(p, T.qblocks, p->est_rows[t], 1, 1.0);
   T.ncta = (int)std::max<int64_t>(1, std::min<int64_t>(nc, rows));
   CU(cudaMalloc(&T.cand, sizeof(Cand) * (size_t)T.qblocks * T.ncta));
   if (p->margins) CU(cudaMalloc(&T.cand2, sizeof(double) * (size_t)T.qblocks * T.ncta));
@@ -1040,7 +1079,7 @@ int launch_pruned_tier(afd_plan* p, int t, const double2* ghat_rev, int64_t r0, 
     pk<<<dim3((unsigned)T.ncta, (unsigned)Q), Geo<KT, kFieldRB>::T * G, field_smem<KT>(), st>>>(
         T.ghq, T.fw, p->scales, p->twct, (long long)r0, (long long)r1, (long long)p->m0, T.cand,
         nullptr, nullptr, T.tw_img, field_pp(), (unsigned*)nullptr, 0,
-        SubMap{(long long)p->n, Q, hi, T.cand2, lo});
+        SubMap{(long long)p->n, Q, hi, T.cand2, lo, p->hint});
   }
   const int n = Q * T.ncta;
   const int slots = (int)(p->big_rows * big_col_ctas(p));
@@ -1072,8 +1111,9 @@ int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, doub
     // tier t takes rows [mstar[t-1], mstar[t]): tiers 0..2 in registers (32,
     // 64 and 128 terms), tier 3 as N/1024 1024-point fields, tier 4 as N/4096
     // 4096-point fields, rows [mstar[4], r1) through the batches below (all
-    // limits read on the device).  The 1024-point tier runs first: its
-    // maxima start the register tiers' screens (hint).
+    // limits read on the device).  Longest tiers first (the largest |F|^2
+    // sit at the radii closest to the poles): each tier's maxima start the
+    // next tiers' screens (hint).
     prune_init_kernel<<<1, 1, 0, st>>>(p->mstar, r0, r1, p->first_tier, p->tmax, p->hint);
     prune_tail_kernel<<<2 * p->sms, 256, 0, st>>>(ghat_rev, p->n, p->tmax);
     prune_rows_kernel<<<2 * p->sms, 256, 0, st>>>(p->K, p->ka, ghat_rev, p->radii, r0, r1,
@@ -1082,11 +1122,11 @@ int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, doub
     CU(cudaGetLastError());
     int slot = 0, rc2;
     constexpr int t1k = kRegTiers, t4k = kRegTiers + 1;
-    if ((rc2 = launch_pruned_tier<prune_k(t1k)>(p, t1k, ghat_rev, r0, r1, p->mstar + t1k - 1,
-                                                 p->mstar + t1k, stopped, &slot, st)))
-      return rc2;
     if ((rc2 = launch_pruned_tier<prune_k(t4k)>(p, t4k, ghat_rev, r0, r1, p->mstar + t4k - 1,
                                                  p->mstar + t4k, stopped, &slot, st)))
+      return rc2;
+    if ((rc2 = launch_pruned_tier<prune_k(t1k)>(p, t1k, ghat_rev, r0, r1, p->mstar + t1k - 1,
+                                                 p->mstar + t1k, stopped, &slot, st)))
       return rc2;
     if (p->first_tier == 0) {
       if ((rc2 = launch_reg_tier<1>(p, 0, ghat_rev, r0, r1, nullptr, p->mstar, stopped, &slot, st)))
@@ -1439,6 +1479,7 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
       ALLOC2(p->tmax, sizeof(unsigned long long));
       ALLOC2(p->hint, sizeof(unsigned long long));
       p->first_tier = kRegTiersOn ? 0 : kRegTiers;
+      estimate_tier_rows(p, radii_host);
       rc = setup_pruned_tier<prune_k(kRegTiers)>(p, kRegTiers);
       if (!rc) rc = setup_pruned_tier<prune_k(kRegTiers + 1)>(p, kRegTiers + 1);
       for (int t = 0; t < kRegTiers && !rc && p->first_tier == 0; ++t) rc = setup_reg_tier(p, t);

@@ -215,7 +215,10 @@ field_warp_kernel(const double2* __restrict__ ghat,   // [batch][1024]
   double best_mag = -1.0, best_re = 0.0, best_im = 0.0;
   int best_sl = -1, best_i = 0;
   [[maybe_unused]] double sec_mag = -1.0;
-  double thr = -1.0;
+  // the screen starts from the largest |F|^2 (margins: runner-up) of the
+  // tiers launched before (a lower bound of the step's; afd_field_reg.cuh)
+  double thr = sub.hint ? __longlong_as_double((long long)*(volatile unsigned long long*)sub.hint) : 0.0;
+  if (!(thr > 0.0)) thr = -1.0;
 
   const int sl0 = (int)blockIdx.x * kFwWarps + warp;
   const int nk = sl0 < rows ? (rows - sl0 + per_round - 1) / per_round : 0;
@@ -355,7 +358,7 @@ field_warp_kernel(const double2* __restrict__ ghat,   // [batch][1024]
         }
         m = fmax(m, m2);
       }
-      thr = MARG ? r : m;
+      thr = fmax(thr, MARG ? r : m);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

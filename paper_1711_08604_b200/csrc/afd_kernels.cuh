@@ -637,13 +637,19 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     if (lane == 0) {
       cand_out[(size_t)sig * gridDim.x + blockIdx.x] = c;
       if constexpr (track2) win_flat = c.flat;
+      // non-negative doubles order like their bit patterns
+      if (!track2 && sub.hint && c.mag > 0.0)
+        atomicMax(sub.hint, (unsigned long long)__double_as_longlong(c.mag));
     }
   }
   if constexpr (track2) {
     __shared__ double red2[32];
     __syncthreads();
     const double r2 = cta_runner_up(sec_mag, own_mag, own_flat, win_flat, red2);
-    if (threadIdx.x == 0) sub.cand2[(size_t)sig * gridDim.x + blockIdx.x] = r2;
+    if (threadIdx.x == 0) {
+      sub.cand2[(size_t)sig * gridDim.x + blockIdx.x] = r2;
+      if (sub.hint && r2 > 0.0) atomicMax(sub.hint, (unsigned long long)__double_as_longlong(r2));
+    }
   }
 }
 
