@@ -137,6 +137,14 @@ struct afd_plan {
   int64_t est_rows[kPruneTiers] = {};  // rows per tier expected from the radii alone
   int first_tier = 0;          // tiers below are switched off (AFD_REG_TIERS=0: kRegTiers)
   unsigned long long* hint = nullptr;  // screening hint of the register tiers
+  // register tiers for batches of on-chip fields (pruned_small: fast engine,
+  // 1024 <= N <= 8192, many signals; afd_field_reg.cuh BATCH)
+  bool sp = false;
+  double* sp_fw = nullptr;               // [m1-m0][kFwStride] factor rows
+  int* sp_mstar = nullptr;               // [max_batch][kRegTiers] tier limits per signal
+  unsigned long long* sp_hint = nullptr; // [max_batch]
+  double2* sp_h = nullptr;               // [max_batch][128 N/32] pre-twiddled spectra
+  int64_t sp_last_batch = 0;
   int* mstar = nullptr;        // [kPruneTiers] first row failing each tier's test
   unsigned long long* tmax = nullptr;
   double* nodes = nullptr;     // [2 * N / kNodeLen]
@@ -399,7 +407,7 @@ int groups_eff(const afd_plan* p, int64_t rows, int64_t batch) {
 template <int K>
 int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64_t batch,
                  Cand* cand, int ncta, double2* field_out, const State* state, cudaStream_t st,
-                 unsigned* row_ctr = nullptr, int launch_id = 0) {
+                 unsigned* row_ctr = nullptr, int launch_id = 0, const SubMap* subp = nullptr) {
   constexpr int G = groups_for<K>();
   const int ge = groups_eff<K>(p, r1 - r0, batch);  // ncta from field_ctas_for
   dim3 grid(ncta, (unsigned)batch);
@@ -430,6 +438,12 @@ int launch_field(afd_plan* p, const double2* ghat, int64_t r0, int64_t r1, int64
                                     : field_kernel<K, kFieldRB, G, false, false, true>))
                         : (tm ? field_kernel<K, kFieldRB, G, false, TMC>
                               : field_kernel<K, kFieldRB, G, false>);
+    if (subp)  // pruned_small: the launch reads its row limits at its top, so no PDL
+      kern<<<grid, block, smem, st>>>(ghat, tab, (const double*)p->scales,
+                                      (const double2*)p->twst, (long long)r0, (long long)r1,
+                                      (long long)p->m0, cand, (double2*)nullptr, state, img,
+                                      field_pp(), row_ctr, launch_id, *subp);
+    else
     CU(launch_pdl(kern, grid, dim3(block), smem, st, ghat, tab,
                   (const double*)p->scales, (const double2*)p->twst, (long long)r0,
                   (long long)r1, (long long)p->m0, cand, (double2*)nullptr, state,
@@ -636,6 +650,81 @@ int set_device(const afd_plan* p) {
   return 0;
 }
 
+// Batches of on-chip fields with the register tiers (pruned_small).  Per
+// step: prune_small_kernel (per-signal tier limits, hints, pre-twiddled
+// spectra), the N-point field kernel over each signal's rows from its last
+// limit on (it publishes the signal's hint), then the register kernels over
+// the rows below — all into one candidate row per signal: [ncta N-point
+// slots | per tier nc[t] * Q'/32 warp slots].
+static const bool kSmallPrunedOn = !(getenv("AFD_SMALL_PRUNED") && atoi(getenv("AFD_SMALL_PRUNED")) == 0);
+constexpr int64_t kSmallPrunedMinEvals = 1LL << 28;  // per field launch (c3: 2^32)
+
+int tier_ncta(const afd_plan* p, int64_t q, int64_t est, int rpc, double prologue);
+
+struct SmallGrid {
+  bool pruned;
+  int ncta;            // CTAs per signal of the N-point field
+  int nc[kRegTiers];   // row splits per register tier
+  int off[kRegTiers];  // first candidate slot per tier
+  int ncand;           // candidates per signal
+};
+
+SmallGrid small_grid(const afd_plan* p, int64_t batch, int ncta) {
+  SmallGrid g{};
+  g.ncta = ncta;
+  g.ncand = ncta;
+  const int64_t rows = p->m1 - p->m0;
+  g.pruned = p->sp && batch >= 8 && batch * rows * p->n >= kSmallPrunedMinEvals;
+  if (!g.pruned) return g;
+  const int64_t qn = p->n >> 5;
+  for (int t = 0; t < kRegTiers; ++t) {
+    const int threads = fr_threads(1 << t);
+    const int64_t yb = (batch * qn + threads - 1) / threads;
+    g.nc[t] = (int)std::min<int64_t>(tier_ncta(p, yb, p->est_rows[t], 1, 1.0), rows);
+    g.off[t] = g.ncand;
+    g.ncand += g.nc[t] * (int)(qn >> 5);
+  }
+  return g;
+}
+
+template <int D>
+int launch_reg_small(afd_plan* p, int t, int64_t batch, Cand* cand, const SmallGrid& sg,
+                     cudaStream_t st) {
+  const int64_t qn = p->n >> 5;
+  const int threads = fr_threads(D);
+  const unsigned yb = (unsigned)((batch * qn + threads - 1) / threads);
+  double* c2 = const_cast<double*>(runner_ups_for(p, cand));
+  auto rk = c2 ? field_reg_kernel<D, true, true> : field_reg_kernel<D, false, true>;
+  rk<<<dim3((unsigned)sg.nc[t], yb), threads, 0, st>>>(
+      p->sp_h, p->sp_fw, (long long)p->m0, (long long)p->m1, (long long)p->m0, (long long)qn, cand,
+      p->sp_hint,
+      SubMap{(long long)p->n, 0, p->sp_mstar + t, c2, t ? p->sp_mstar + t - 1 : nullptr, nullptr,
+             kRegTiers, sg.ncand},
+      RegBatch{p->K - 5, batch * qn, sg.off[t]});
+  p->launches++;
+  CU(cudaGetLastError());
+  return 0;
+}
+
+template <int K>
+int launch_field_small_pruned(afd_plan* p, const double2* ghat, int64_t batch, Cand* cand,
+                              const SmallGrid& sg, const State* state, cudaStream_t st) {
+  int rc;
+  prune_small_kernel<<<(unsigned)batch, 256, 0, st>>>(K, ghat, p->radii, p->m0, p->m1, p->circle,
+                                                      state, p->sp_mstar, p->sp_hint, p->sp_h);
+  p->launches++;
+  CU(cudaGetLastError());
+  p->sp_last_batch = batch;
+  const SubMap sub{0, 0, nullptr, const_cast<double*>(runner_ups_for(p, cand)),
+                   p->sp_mstar + kRegTiers - 1, p->sp_hint, kRegTiers, sg.ncand};
+  if ((rc = launch_field<K>(p, ghat, p->m0, p->m1, batch, cand, sg.ncta, nullptr, state, st,
+                            nullptr, 0, &sub)))
+    return rc;
+  if ((rc = launch_reg_small<1>(p, 0, batch, cand, sg, st))) return rc;
+  if ((rc = launch_reg_small<2>(p, 1, batch, cand, sg, st))) return rc;
+  return launch_reg_small<4>(p, 2, batch, cand, sg, st);
+}
+
 // Enqueue the whole decomposition (init + max_terms steps) on `st`.
 int enqueue_decompose(afd_plan* p, int64_t batch, int max_terms, double thr, int dc_first,
                       cudaStream_t st) {
@@ -643,8 +732,9 @@ int enqueue_decompose(afd_plan* p, int64_t batch, int max_terms, double thr, int
   const int G = groups_of(p->K);
   const int ncta = decomp_field_ctas(p, batch);
   const bool dyn = field_dyn_ctas(p, rows, batch) > 0;
+  const SmallGrid sg = small_grid(p, batch, ncta);
   int rc;
-  if ((rc = ensure_cand(p, batch, ncta))) return rc;
+  if ((rc = ensure_cand(p, batch, sg.ncand))) return rc;
   if (dyn) CU(cudaMemsetAsync(p->row_ctr, 0, sizeof(unsigned) * 2 * (size_t)batch, st));
   AFD_DISPATCH(p->K, {
     if ((rc = launch_step<KK>(p, -1, max_terms, thr, dc_first, p->gin, nullptr, 0, batch,
@@ -654,12 +744,14 @@ int enqueue_decompose(afd_plan* p, int64_t batch, int max_terms, double thr, int
       if (!(k == 0 && dc_first)) {
         if (p->engine == 1)
           rc = launch_direct(p, p->rem, p->m0, p->m1, batch, p->cand, nullptr, p->state, st);
+        else if (sg.pruned)
+          rc = launch_field_small_pruned<KK>(p, p->ghat, batch, p->cand, sg, p->state, st);
         else
           rc = launch_field<KK>(p, p->ghat, p->m0, p->m1, batch, p->cand, ncta, nullptr,
                                 p->state, st, dyn ? p->row_ctr : nullptr, k);
         if (rc) return rc;
       }
-      if ((rc = launch_step<KK>(p, k, max_terms, thr, dc_first, nullptr, p->cand, ncta, batch,
+      if ((rc = launch_step<KK>(p, k, max_terms, thr, dc_first, nullptr, p->cand, sg.ncand, batch,
                                 p->steps, st)))
         return rc;
     }
@@ -1044,7 +1136,7 @@ int launch_reg_tier(afd_plan* p, int t, const double2* ghat_rev, int64_t r0, int
   rk<<<dim3((unsigned)T.ncta, (unsigned)T.qblocks), fr_threads(D), 0, st>>>(
       T.ghq, p->tier[0].fw, (long long)r0, (long long)r1, (long long)p->m0,
       (long long)(p->n >> 5), T.cand, p->hint,
-      SubMap{(long long)p->n, 0, hi, T.cand2, lo, nullptr});
+      SubMap{(long long)p->n, 0, hi, T.cand2, lo, nullptr}, RegBatch{});
   const int n = T.qblocks * T.ncta;
   const int slots = (int)(p->big_rows * big_col_ctas(p));
   const int np = std::max(1, std::min(std::min(kBigParts, (n + 255) / 256), (slots - *slot) / 2));
@@ -1488,6 +1580,22 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
     }
   } else {
     AFD_DISPATCH(K, { rc = setup_kernels<KK>(p); break; });
+    const int64_t rows = m1 - m0;
+    if (!rc && p->fast && p->engine == 0 && kSmallPrunedOn && K >= 10 && max_batch >= 8 &&
+        max_batch * rows * N >= (size_t)kSmallPrunedMinEvals) {
+      // register tiers for batches (pruned_small)
+      ALLOC2(p->sp_fw, sizeof(double) * kFwStride * (size_t)rows);
+      ALLOC2(p->sp_mstar, sizeof(int) * kRegTiers * (size_t)max_batch);
+      ALLOC2(p->sp_hint, sizeof(unsigned long long) * (size_t)max_batch);
+      ALLOC2(p->sp_h, sizeof(double2) * 128 * (N >> 5) * (size_t)max_batch);
+      const int64_t total = rows * kFwStride;
+      fast_weight_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256>>>(
+          p->radii, p->scales, p->m0, rows, kFwStride, 32, 32, 5, 0, 0, p->sp_fw);
+      p->launches++;
+      p->first_tier = 0;
+      estimate_tier_rows(p, radii_host);
+      p->sp = true;
+    }
   }
   if (rc) return cleanup(rc);
   if (cudaDeviceSynchronize() != cudaSuccess) return cleanup(fail(AFD_E_CUDA, "plan init: %s",
@@ -1538,6 +1646,10 @@ int afd_plan_destroy(afd_plan* p) {
   cudaFree(p->mstar);
   cudaFree(p->tmax);
   cudaFree(p->hint);
+  cudaFree(p->sp_fw);
+  cudaFree(p->sp_mstar);
+  cudaFree(p->sp_hint);
+  cudaFree(p->sp_h);
   cudaFree(p->big_part);
   cudaFree(p->nodes);
   cudaFree(p->sel);
@@ -1652,14 +1764,18 @@ int afd_field_argmax(afd_plan* p, const double* ghat, afd_candidate* out, int64_
     return 0;
   }
   const int ncta = field_ctas_for(p, p->m1 - p->m0, batch);
-  if ((rc = ensure_cand(p, batch, ncta))) return rc;
+  const SmallGrid sg = small_grid(p, batch, ncta);
+  if ((rc = ensure_cand(p, batch, sg.ncand))) return rc;
   AFD_DISPATCH(p->K, {
-    if ((rc = launch_field<KK>(p, (const double2*)ghat, p->m0, p->m1, batch, p->cand, ncta,
-                               nullptr, nullptr, st)))
-      return rc;
+    if (sg.pruned)
+      rc = launch_field_small_pruned<KK>(p, (const double2*)ghat, batch, p->cand, sg, nullptr, st);
+    else
+      rc = launch_field<KK>(p, (const double2*)ghat, p->m0, p->m1, batch, p->cand, ncta, nullptr,
+                            nullptr, st);
+    if (rc) return rc;
     break;
   });
-  cand_reduce_kernel<<<(unsigned)batch, 128, 0, st>>>(p->cand, ncta, (Cand*)out);
+  cand_reduce_kernel<<<(unsigned)batch, 128, 0, st>>>(p->cand, sg.ncand, (Cand*)out);
   p->launches++;
   CU(cudaGetLastError());
   return 0;
@@ -1757,7 +1873,7 @@ int afd_decompose(afd_plan* p, const double* g0, int64_t batch, int max_terms, d
   if (!reuse) {
     invalidate_graph(p);
     // make sure buffers exist before capture (allocation is not capturable)
-    const int ncta = decomp_field_ctas(p, batch);
+    const int ncta = small_grid(p, batch, decomp_field_ctas(p, batch)).ncand;
     if ((rc = ensure_cand(p, batch, ncta))) return rc;
     cudaStream_t cap;
     CU(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
@@ -2158,11 +2274,15 @@ int afd_time_field(afd_plan* p, const double* ghat, int64_t batch, int reps, dou
   // (the decomposition's launch configuration, dynamic rows included)
   const int ncta = decomp_field_ctas(p, batch);
   const bool dyn = field_dyn_ctas(p, p->m1 - p->m0, batch) > 0;
-  if ((rc = ensure_cand(p, batch, ncta))) return rc;
+  const SmallGrid sg = small_grid(p, batch, ncta);
+  if ((rc = ensure_cand(p, batch, sg.ncand))) return rc;
   if (dyn) CU(cudaMemsetAsync(p->row_ctr, 0, sizeof(unsigned) * 2 * (size_t)batch, st));
   int launch_id = 0;
   auto one = [&]() -> int {
     AFD_DISPATCH(p->K, {
+      if (sg.pruned)
+        return launch_field_small_pruned<KK>(p, (const double2*)ghat, batch, p->cand, sg, nullptr,
+                                             st);
       return launch_field<KK>(p, (const double2*)ghat, p->m0, p->m1, batch, p->cand, ncta,
                               nullptr, nullptr, st, dyn ? p->row_ctr : nullptr, launch_id++);
     });
@@ -2214,6 +2334,32 @@ int afd_field_tier_rows(afd_plan* p, int64_t* terms, int64_t* rows_out, int cap,
   int rc;
   if ((rc = set_device(p))) return rc;
   const int64_t rows = p->m1 - p->m0;
+  if (!p->big && p->sp && p->sp_last_batch > 0) {
+    // batches of on-chip fields with register tiers: rows summed over the
+    // signals of the last evaluation
+    if (cap < kRegTiers + 1)
+      return fail(AFD_E_INVALID, "afd_field_tier_rows: cap %d < %d", cap, kRegTiers + 1);
+    std::vector<int> ms((size_t)p->sp_last_batch * kRegTiers);
+    CU(cudaMemcpyAsync(ms.data(), p->sp_mstar, sizeof(int) * ms.size(), cudaMemcpyDeviceToHost,
+                       (cudaStream_t)stream));
+    CU(cudaStreamSynchronize((cudaStream_t)stream));
+    for (int t = 0; t <= kRegTiers; ++t) {
+      terms[t] = t < kRegTiers ? 1LL << prune_k(t) : p->n;
+      rows_out[t] = 0;
+    }
+    for (int64_t b = 0; b < p->sp_last_batch; ++b) {
+      int64_t prev = 0;
+      for (int t = 0; t < kRegTiers; ++t) {
+        const int64_t e = std::max(
+            prev, std::max<int64_t>(0, std::min<int64_t>(rows, ms[b * kRegTiers + t] - p->m0)));
+        rows_out[t] += e - prev;
+        prev = e;
+      }
+      rows_out[kRegTiers] += rows - prev;
+    }
+    *count = kRegTiers + 1;
+    return 0;
+  }
   if (!p->big || !p->pruned) {
     if (cap < 1) return fail(AFD_E_INVALID, "afd_field_tier_rows: cap %d < 1", cap);
     terms[0] = p->n;

@@ -40,7 +40,19 @@ namespace afd {
 __host__ __device__ constexpr int fr_warps(int D) { return D == 1 ? AFD_FR_WARPS1 : D == 2 ? 8 : 4; }
 __host__ __device__ constexpr int fr_threads(int D) { return 32 * fr_warps(D); }
 
-template <int D, bool MARG>
+// BATCH: many signals of an on-chip N (afd_capi.cu pruned_small, BASELINE
+// c3): thread g of the launch serves signal g >> kq and q' = g mod Q' (a warp
+// never straddles signals: Q' >= 32), its spectra at h + sig * 128 Q' (four
+// blocks per signal whatever D), its row limits and hint are the signal's
+// (sub.lim_stride), and every warp writes its own candidate to the signal's
+// candidate row: slot cand_off + blockIdx.x * (Q' / 32) + (q' >> 5).
+struct RegBatch {
+  int kq;                   // log2 Q'
+  long long threads_total;  // batch * Q'
+  int cand_off;             // first slot of this tier in a signal's candidate row
+};
+
+template <int D, bool MARG, bool BATCH = false>
 __global__ void __launch_bounds__(fr_threads(D), 1)
 field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled spectra
                  const double* __restrict__ fw,      // [rows of plan][64] factor rows (kFwStride)
@@ -48,7 +60,7 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
                  long long pw_row0,                  // global row of fw[0]
                  long long qp_total,                 // Q' = N / 32
                  Cand* __restrict__ cand_out,        // [gridDim.y][gridDim.x]
-                 const unsigned long long* __restrict__ hint, SubMap sub) {
+                 const unsigned long long* __restrict__ hint, SubMap sub, RegBatch rb) {
   static_assert(D == 1 || D == 2 || D == 4, "chunks of 8 / D registers per 32-word TMEM load");
   constexpr int GI = 8 / D;          // registers i per 32-word TMEM load
   constexpr int NCH = 32 / GI;       // loads per row
@@ -60,16 +72,25 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
   __shared__ __align__(16) double wsm[kFrWarps][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = blockIdx.y * gridDim.x + blockIdx.x;
+  const long long gthread = (long long)blockIdx.y * kFrThreads + threadIdx.x;
+  // warp-uniform (Q' is a multiple of 32)
+  const bool active = gthread < (BATCH ? rb.threads_total : qp_total);
+  const int sig = BATCH && active ? (int)(gthread >> rb.kq) : 0;
+  const long long qp = BATCH ? gthread & (qp_total - 1) : gthread;
+  if constexpr (BATCH) {
+    h += (size_t)sig * 128 * (size_t)qp_total;
+    if (hint) hint += sig;
+  }
   if (sub.lim_lo != nullptr) {
-    const long long l = *sub.lim_lo;
+    const long long l = sub.lim_lo[(size_t)sig * sub.lim_stride];
     if (l > row0) row0 = l < row1 ? l : row1;
   }
   if (sub.lim != nullptr) {
-    const long long l = *sub.lim;
+    const long long l = sub.lim[(size_t)sig * sub.lim_stride];
     if (l < row1) row1 = l > row0 ? l : row0;
   }
   const int rows = (int)(row1 - row0);
-  if (rows <= (int)blockIdx.x) {  // no rows for this CTA this step: a neutral candidate
+  if (!BATCH && rows <= (int)blockIdx.x) {  // no rows for this CTA this step: a neutral candidate
     if (threadIdx.x == 0) {
       Cand c;
       c.mag = -1.0;
@@ -92,8 +113,6 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // the warp's lane quadrant; warps w and w + 4 share it, side by side
   const uint32_t tmw = tm_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * kCols);
-  const long long qp = (long long)blockIdx.y * kFrThreads + threadIdx.x;
-  const bool active = qp < qp_total;  // warp-uniform (Q' is a multiple of 32)
   // chunk c holds registers i = GI c .. GI c + GI - 1, block m at word 4 GI m
 #pragma unroll
   for (int c = 0; c < NCH && active; ++c) {
@@ -115,7 +134,9 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
   if (!(thr > 0.0)) thr = -1.0;
 
   // rows sl = blockIdx.x + k gridDim.x, k = nk - 1 .. 0
-  const int nk = active ? (rows - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  const int nk = active && rows > (int)blockIdx.x
+                     ? (rows - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x
+                     : 0;
   const double* __restrict__ fr0 = fw + (size_t)(row0 + blockIdx.x - pw_row0) * kFwStride;
   const size_t fstep = (size_t)gridDim.x * kFwStride;
   double a_nx = nk > 0 ? __ldg(fr0 + (size_t)(nk - 1) * fstep + lane) : 0.0;
@@ -229,6 +250,20 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
   best.im = best_im;
   [[maybe_unused]] const double own_mag = best.mag;
   [[maybe_unused]] const long long own_flat = best.flat;
+  if constexpr (BATCH) {  // one candidate per warp, in the signal's candidate row
+    best = warp_argmax(best);
+    const size_t ws = (size_t)sig * sub.cand_stride + rb.cand_off +
+                      (size_t)blockIdx.x * (size_t)(qp_total >> 5) + (size_t)(qp >> 5);
+    if (active && lane == 0) cand_out[ws] = best;
+    if constexpr (MARG) {
+      const long long wf = __shfl_sync(0xffffffffu, best.flat, 0);
+      double x = fmax(sec_mag, own_flat != wf ? own_mag : -1.0);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+      if (active && lane == 0) sub.cand2[ws] = x;
+    }
+    return;
+  }
   __shared__ Cand red[kFrWarps];
   __shared__ long long win_flat;
   best = warp_argmax(best);

@@ -199,7 +199,15 @@ struct SubMap {
   const int* lim_lo;     // device lower row limit (rows < *lim_lo skipped) or null
   unsigned long long* hint;  // max-reduced bits of the launch's largest |F|^2 (margins: runner-up)
                              // for the screens of later tiers (afd_field_reg.cuh), or null
+  // batches of on-chip fields with register tiers (pruned_small): the limits
+  // and the hint are per signal (lim[sig * lim_stride], hint[sig]) and the
+  // candidates of signal `sig` go to cand_out[sig * cand_stride + slot]
+  int lim_stride;            // 0: one limit / hint for the launch
+  int cand_stride;           // 0: gridDim.x
 };
+__device__ __forceinline__ size_t cand_slot(const SubMap& sub, int sig) {
+  return (size_t)sig * (sub.cand_stride ? (unsigned)sub.cand_stride : gridDim.x) + blockIdx.x;
+}
 
 // First maximum of a CTA's candidates and the runner-up: the largest of
 // the threads' runner-ups and of their maxima other than the winner.
@@ -244,10 +252,10 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   const int Gr = blockDim.x / T;  // row-groups actually launched (<= G)
   using TwT = SmemTw<K, RB>;
   if (sub.lim_lo != nullptr) {  // pruned tier: rows below *lim_lo belong to a shorter tier
-    const long long l = *sub.lim_lo;
+    const long long l = sub.lim_lo[(size_t)sig * sub.lim_stride];
     if (l > row0) row0 = l < row1 ? l : row1;
   }
-  if (sub.lim != nullptr && *sub.lim <= row0) {
+  if (sub.lim != nullptr && sub.lim[(size_t)sig * sub.lim_stride] <= row0) {
     // pruned launch with no on-chip rows this step (all rows long, or the
     // signal stopped): a neutral candidate, no TMEM or twiddle setup
     if (!MATERIALIZE && threadIdx.x == 0) {
@@ -255,8 +263,8 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
       c.mag = -1.0;
       c.flat = 0x7fffffffffffffffLL;
       c.re = c.im = 0.0;
-      cand_out[(size_t)sig * gridDim.x + blockIdx.x] = c;
-      if constexpr (MARG) sub.cand2[(size_t)sig * gridDim.x + blockIdx.x] = -1.0;
+      cand_out[cand_slot(sub, sig)] = c;
+      if constexpr (MARG) sub.cand2[cand_slot(sub, sig)] = -1.0;
     }
     return;
   }
@@ -345,7 +353,7 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
   // row counts fit 32 bits (M <= 2^31); 32-bit loop state keeps registers
   // for the butterflies
   if (sub.lim != nullptr) {
-    const long long l = *sub.lim;
+    const long long l = sub.lim[(size_t)sig * sub.lim_stride];
     if (l < row1) row1 = l > row0 ? l : row0;
   }
   const int rows = (int)(row1 - row0);
@@ -635,11 +643,12 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     Cand c = lane < nw ? red[lane] : best;
     c = warp_argmax(c);
     if (lane == 0) {
-      cand_out[(size_t)sig * gridDim.x + blockIdx.x] = c;
+      cand_out[cand_slot(sub, sig)] = c;
       if constexpr (track2) win_flat = c.flat;
       // non-negative doubles order like their bit patterns
       if (!track2 && sub.hint && c.mag > 0.0)
-        atomicMax(sub.hint, (unsigned long long)__double_as_longlong(c.mag));
+        atomicMax(sub.hint + (sub.lim_stride ? sig : 0),
+                  (unsigned long long)__double_as_longlong(c.mag));
     }
   }
   if constexpr (track2) {
@@ -647,8 +656,10 @@ field_kernel(const double2* __restrict__ ghat,     // [batch][N]
     __syncthreads();
     const double r2 = cta_runner_up(sec_mag, own_mag, own_flat, win_flat, red2);
     if (threadIdx.x == 0) {
-      sub.cand2[(size_t)sig * gridDim.x + blockIdx.x] = r2;
-      if (sub.hint && r2 > 0.0) atomicMax(sub.hint, (unsigned long long)__double_as_longlong(r2));
+      sub.cand2[cand_slot(sub, sig)] = r2;
+      if (sub.hint && r2 > 0.0)
+        atomicMax(sub.hint + (sub.lim_stride ? sig : 0),
+                  (unsigned long long)__double_as_longlong(r2));
     }
   }
 }

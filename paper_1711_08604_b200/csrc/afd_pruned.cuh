@@ -162,4 +162,74 @@ __global__ void pretwiddle_reg_kernel(int K, int ka, int D, const double2* __res
   }
 }
 
+// Batches of on-chip fields (N <= 8192, many signals: BASELINE c3) with the
+// register tiers: one CTA per signal decides the signal's tier limits
+// mstar[sig][t], t < kRegTiers (the same tail test as prune_rows_kernel; a
+// stopped signal: every limit m0, and the field kernels then do nothing),
+// clears its hint and writes its pre-twiddled spectra
+//   h[sig][(m 32 + i) Q' + q'] = G^_l e^{+2 pi i l q' / N},  l = rev5(i) + 32 m,  m < 4
+// (natural-order spectrum, [batch][N]).  Rows from mstar[sig][kRegTiers-1]
+// on stay with the N-point field kernel (SubMap::lim_lo).
+__global__ void __launch_bounds__(256) prune_small_kernel(
+    int K, const double2* __restrict__ ghat, const double* __restrict__ radii, long long m0,
+    long long m1, const double2* __restrict__ circle, const State* __restrict__ state,
+    int* __restrict__ mstar, unsigned long long* __restrict__ hint, double2* __restrict__ h) {
+  constexpr int L = 128;  // terms of the longest register tier
+  __shared__ double lg[L];
+  __shared__ double wmax[8];
+  __shared__ int ms[kRegTiers];
+  const int sig = blockIdx.x;
+  const int n = 1 << K, kq = K - 5, qn = 1 << kq;
+  const double2* __restrict__ gh = ghat + (size_t)sig * n;
+  if (threadIdx.x == 0) hint[sig] = 0ull;
+  if (state && state[sig].stopped) {
+    if (threadIdx.x < kRegTiers) mstar[sig * kRegTiers + threadIdx.x] = (int)m0;
+    return;
+  }
+  if (threadIdx.x < kRegTiers) ms[threadIdx.x] = (int)m1;
+  double m = 0.0;
+  for (int l = threadIdx.x; l < n; l += blockDim.x) {
+    const double2 v = __ldg(gh + l);
+    const double a2 = fma(v.x, v.x, v.y * v.y);
+    m = fmax(m, a2);
+    if (l < L) lg[l] = a2 > 0.0 ? 0.5 * log2(a2) : -INFINITY;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) wmax[warp] = m;
+  __syncthreads();
+  double t2 = 0.0;
+  for (int w = 0; w < 8; ++w) t2 = fmax(t2, wmax[w]);
+  const double lt = t2 > 0.0 ? 0.5 * log2(t2) : -INFINITY;
+  for (long long s = m0 + warp; s < m1; s += 8) {
+    const double r = radii[s];
+    if (r == 0.0 || lt == -INFINITY) continue;  // no tail at all
+    const double lr = log2(r), l1r = log2(1.0 - r);
+    double b = -INFINITY;
+    int lo = 0;
+#pragma unroll
+    for (int t = 0; t < kRegTiers; ++t) {
+      const int L_t = 1 << prune_k(t);
+      for (int l = lo + lane; l < L_t; l += 32) b = fmax(b, fma((double)l, lr, lg[l]));
+      lo = L_t;
+      double bt = b;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) bt = fmax(bt, __shfl_xor_sync(0xffffffffu, bt, o));
+      const double tail = lt + (double)L_t * lr - l1r;
+      if (lane == 0 && !(tail <= bt - 64.0)) atomicMin(ms + t, (int)s);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < kRegTiers) mstar[sig * kRegTiers + threadIdx.x] = ms[threadIdx.x];
+  double2* __restrict__ out = h + (size_t)sig * L * qn;
+  for (int x = threadIdx.x; x < L * qn; x += blockDim.x) {
+    const int q = x & (qn - 1), im = x >> kq;
+    const int l = (int)(__brev((unsigned)(im & 31)) >> 27) + 32 * (im >> 5);
+    const double2 g = __ldg(gh + l);
+    const double2 w = __ldg(circle + ((l * q) & (n - 1)));
+    out[x] = make_double2(fma(g.x, w.x, -(g.y * w.y)), fma(g.x, w.y, g.y * w.x));
+  }
+}
+
 }  // namespace afd

@@ -26,7 +26,7 @@ import numpy as np
 from . import _capi
 
 __all__ = ["shard_bounds", "radius_shard_bounds", "live_powers", "expected_twopass",
-           "decompose_sharded",
+           "expected_tier", "FAST_TIER_COST", "decompose_sharded",
            "decompose_batch_sharded", "ShardedRunner"]
 
 
@@ -73,6 +73,30 @@ def expected_twopass(radii, n, onchip=4096):
     return (r > 0.0) & (lt > -64.0)
 
 
+# Spectrum terms per tier of the pruned fast field (csrc/afd_pruned.cuh: 32,
+# 64, 128 in registers, 1024 and 4096 as on-chip transforms) and the measured
+# cost of one row relative to a 1024-point row (c4, N = 2^20, one B200:
+# 1.02, 1.18, 1.71, 2.40, 3.41 us per row; two-pass 7.5 us;
+# profiles/r02/tier_kernels_c4_v9.txt).
+FAST_TIERS = (32, 64, 128, 1024, 4096)
+FAST_TIER_COST = {32: 0.43, 64: 0.49, 128: 0.71, 1024: 1.0, 4096: 1.42, None: 3.1}
+
+
+def expected_tier(radii, n):
+    """Per radius, the spectrum terms L of the tier the pruned fast field is
+    expected to evaluate the row from — the first L in FAST_TIERS with
+    r^L / (1 - r) <= 2^-64 (a flat spectrum) — or `n` for the two-pass rows
+    (estimate_tier_rows in csrc/afd_capi.cu; the device decides per step
+    from the actual spectrum)."""
+    r = np.asarray(radii, dtype=np.float64)
+    out = np.full(r.shape, int(n), dtype=np.int64)
+    with np.errstate(divide="ignore"):
+        lr, l1r = np.log2(np.where(r > 0.0, r, 1.0)), np.log2(1.0 - r)
+    for L in reversed(FAST_TIERS):
+        out[(r == 0.0) | (L * lr - l1r <= -64.0)] = L
+    return out
+
+
 def radius_shard_bounds(radii, n, rank, world, exact=True):
     """Contiguous radius block [m0, m1) of `rank` balanced by field cost.
 
@@ -80,10 +104,11 @@ def radius_shard_bounds(radii, n, rank, world, exact=True):
     * exact field: a row costs its 32 B per eval of row-batch intermediate
       plus 8 B per live r^l entry (live_powers) — rows with r <= 0.5 are
       cheaper;
-    * fast field: rows whose weight tail is negligible run on chip (the
-      pruned field) and the few radii closest to 1 take the two-pass path,
-      measured 2.2x the cost per row (c4: 123 vs 56 ms per step), so those
-      rows weigh 2.2 (expected_twopass).
+    * fast field: a row is evaluated from as many spectrum terms as its
+      weight tail needs (the pruned field's tiers) and costs accordingly —
+      the register tiers (r <= 0.7) under half a 1024-point row, the few
+      radii closest to 1 (two-pass) three times as much: rows weigh
+      FAST_TIER_COST[expected_tier].
     Blocks are cut at equal cumulative cost, so the high-radius rank does
     not set the step time.  On-chip N: every row costs the same and this is
     shard_bounds.  Blocks stay rank-ordered and non-empty, so the
@@ -96,7 +121,10 @@ def radius_shard_bounds(radii, n, rank, world, exact=True):
     if exact:
         cost = 32.0 + 8.0 * live_powers(radii, n) / float(n)
     else:
-        cost = np.where(expected_twopass(radii, n), 2.2, 1.0)
+        tier = expected_tier(radii, n)
+        cost = np.full(m, FAST_TIER_COST[None])
+        for L in FAST_TIERS:
+            cost[tier == L] = FAST_TIER_COST[L]
     cum = np.concatenate([[0.0], np.cumsum(cost)])
 
     def cut(p):

@@ -753,10 +753,12 @@ def test_bench_line_contract(afd):
     sp = r.get("split")
     if sp is not None:
         rows = d["config"]["m"]
-        assert sp["rows_1024"] + sp["rows_4096"] == sp["onchip_rows"]
+        tiers = (32, 64, 128, 1024, 4096)
+        assert sum(sp["rows_%d" % t] for t in tiers) == sp["onchip_rows"]
         assert sp["onchip_rows"] + sp["twopass_rows"] == rows
-        f = (sp["rows_1024"] * sp["flops_per_eval_1024"] + sp["rows_4096"] *
-             sp["flops_per_eval_4096"] + sp["twopass_rows"] * sp["flops_per_eval_twopass"]) / rows
+        assert all(sp["flops_per_eval_%d" % t] == 5 * (t.bit_length() - 1) + 7 for t in tiers)
+        f = (sum(sp["rows_%d" % t] * sp["flops_per_eval_%d" % t] for t in tiers) +
+             sp["twopass_rows"] * sp["flops_per_eval_twopass"]) / rows
         assert abs(f - r["flops_per_eval"]) <= 1e-9 * f
         assert abs(r["bytes_per_eval"] - 32.0 * sp["twopass_rows"] / rows) <= 1e-12
     assert r["evals_per_launch"] == d["config"]["n"] * d["config"]["m"]
@@ -1138,6 +1140,77 @@ def test_pruned_fast_decompose_long_rows_and_threshold(afd):
     c = np.array([s.coefficient for s in d.steps])
     assert np.all(np.abs(c - oc) <= FAST_TOL * np.abs(oc))
     assert np.abs(d.remainder - o.remainder).max() <= FAST_TOL * np.abs(o.remainder).max()
+
+
+# ---------------------------------------------------------------------------
+# register tiers for batches of on-chip fields (pruned_small in afd_capi.cu,
+# BASELINE c3's regime): per-signal tier limits, hints and candidate rows
+# ---------------------------------------------------------------------------
+def _batch_cands(plan, ghat):
+    import torch
+    raw = plan.field_argmax(torch.from_numpy(ghat).cuda()).cpu().numpy().tobytes()
+    return np.frombuffer(raw, O.CAND_DTYPE)
+
+
+@pytest.mark.parametrize("n,m,b", [(4096, 1024, 64), (1024, 1024, 256), (8192, 512, 64)])
+def test_small_pruned_batch_field_argmax(afd, n, m, b):
+    """A batch large enough for the register tiers (batch x rows x N >= 2^28):
+    every signal's first maximum is the oracle's — signals whose poles sit at
+    small radii (maximum inside a register tier), at large radii (N-point
+    rows), a constant (exact ties, flat index 0) — and the tier rows add up."""
+    core, engine = afd
+    from paper_1711_08604_b200 import workloads as W
+    radii = tuple(i / m for i in range(m))
+    rmax = (0.2, 0.45, 0.65, 0.9, 0.97)
+    sig = np.stack([W.pole_sum(n, 6, rmax[i % 5], 9000 + i) for i in range(b)])
+    sig[3] = 0.5 - 0.125j
+    ghat = np.stack([O.dft_forward(x) for x in sig])
+    plan = engine.Plan(radii, n, max_batch=b, fast=1)
+    got = _batch_cands(plan, ghat)
+    tr = plan.field_tier_rows()
+    del plan
+    assert list(tr) == [32, 64, 128, n] and sum(tr.values()) == b * m
+    assert tr[32] > 0 and tr[64] > 0 and tr[128] > 0 and tr[n] > 0
+    tiers_hit = set()
+    for i in list(range(0, b, 7)) + [3]:
+        ref = O.field_argmax(ghat[i], np.array(radii), threads=O.max_threads())
+        assert int(got[i]["flat"]) == int(ref["flat"]), i
+        assert abs(got[i]["mag"] - ref["mag"]) <= 1e-12 * ref["mag"], i
+        tiers_hit.add(min(3, int(radii[int(ref["flat"]) // n] * 4)))
+    assert int(got[3]["flat"]) == 0
+    assert len(tiers_hit) >= 2
+
+
+@pytest.mark.parametrize("engine_name", ["fft-fast", "fft-fast-margins"])
+def test_small_pruned_batch_decompose(afd, engine_name):
+    """decompose_batch through the register tiers (64 signals of N = 4096 on
+    1024 radii), some signals stopping on the threshold: identical poles,
+    1e-9 values and the reference's margins for a sample of the signals."""
+    core, _ = afd
+    from paper_1711_08604_b200 import workloads as W
+    n, m, b, steps = 4096, 1024, 64, 4
+    radii = tuple(i / m for i in range(m))
+    rmax = (0.3, 0.6, 0.95)
+    sig = np.stack([W.pole_sum(n, 2 if i % 4 == 1 else 12, rmax[i % 3], 500 + i)
+                    for i in range(b)])
+    grid = core.ParameterGrid(radii, n)
+    ds = core.decompose_batch(sig, grid, max_terms=steps, threshold=1e-3, engine=engine_name)
+    stopped = 0
+    for i in (0, 1, 2, 5, 13, 30, 63):
+        o = O.decompose(sig[i], np.array(radii), max_terms=steps, threshold=1e-3)
+        stopped += len(o.steps) < steps
+        assert len(ds[i].steps) == len(o.steps), i
+        assert [s.point.angle_index for s in ds[i].steps] == list(o.steps["j"]), i
+        assert [s.point.radius for s in ds[i].steps] == list(o.steps["radius"]), i
+        c = np.array([s.coefficient for s in ds[i].steps])
+        oc = o.steps["c_re"] + 1j * o.steps["c_im"]
+        assert np.all(np.abs(c - oc) <= FAST_TOL * np.abs(oc)), i
+        scale = np.abs(o.remainder).max() + 1e-300
+        assert np.abs(ds[i].remainder - o.remainder).max() <= FAST_TOL * scale, i
+        if engine_name.endswith("margins") and i in (0, 2):
+            ref = _oracle_margins(sig[i], radii, o.steps)
+            assert np.all(np.abs(np.array(ds[i].margins) - ref) <= 1e-9), i
+    assert stopped >= 1
 
 
 # ---------------------------------------------------------------------------

@@ -101,9 +101,11 @@ def test_live_powers_match_the_cumprod_fold():
 def test_radius_shard_bounds_balance_the_exact_field():
     """Exact large-N shards: contiguous, rank-ordered, non-empty, covering,
     and balanced in field cost (32 B + 8 B per live r^l entry per eval) to
-    within a row; fast mode and on-chip N fall back to row counts."""
+    within a row; fast mode balances the pruned field's per-tier row costs;
+    on-chip N falls back to row counts."""
     from paper_1711_08604_b200 import workloads as W
-    from paper_1711_08604_b200.distributed import (expected_twopass, live_powers,
+    from paper_1711_08604_b200.distributed import (FAST_TIER_COST, expected_tier,
+                                                   expected_twopass, live_powers,
                                                    radius_shard_bounds, shard_bounds)
     n, m = 1 << 16, 4096
     radii = W.radii_for(m)
@@ -118,11 +120,17 @@ def test_radius_shard_bounds_balance_the_exact_field():
         fast = [radius_shard_bounds(radii, n, r, world, exact=False) for r in range(world)]
         assert fast[0][0] == 0 and fast[-1][1] == m
         assert all(a[1] == b[0] for a, b in zip(fast, fast[1:]))
-        w = np.where(expected_twopass(radii, n), 2.2, 1.0)
+        tier = expected_tier(radii, n)
+        assert np.array_equal(tier == n, expected_twopass(radii, n))
+        w = np.array([FAST_TIER_COST[None if t == n else int(t)] for t in tier])
         share = [w[l:h].sum() for l, h in fast]
-        assert max(share) - min(share) <= 2 * 2.2
+        assert max(share) - min(share) <= 2 * w.max()
         assert [radius_shard_bounds(radii, 4096, r, world) for r in range(world)] == \
             [shard_bounds(m, r, world) for r in range(world)]
+    # tiers by radius: r^L / (1 - r) <= 2^-64 at L = 32, 64, 128, 1024, 4096
+    assert list(expected_tier((0.0, 0.2, 0.25, 0.3, 0.49, 0.55, 0.69, 0.75, 0.95, 0.97, 0.985,
+                               0.99), n)) == [32, 32, 64, 64, 64, 128, 128, 1024, 1024, 4096,
+                                              4096, n]
     tiny = (0.1, 0.2, 0.9)
     assert [radius_shard_bounds(tiny, n, r, 3) for r in range(3)] == [(0, 1), (1, 2), (2, 3)]
 
