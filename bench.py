@@ -389,26 +389,34 @@ def field_roofline(plan, w, radii_rows, ghat, exact, local):
     launch_evals = batch * rows * w.n
     bpe = bytes_per_eval(w.n, radii_rows) if exact else (32.0 if w.n > 8192 else 0.0)
     split = None
-    if not exact and w.n > 8192:
-        # pruned fast field (afd_pruned.cuh): on-chip rows are 1024- or
-        # 4096-point transforms of pre-twiddled spectra (F(L) flops, no HBM
-        # bytes: the spectra and the weight tables are L2-resident), the
-        # rest the two-pass path (F(N) flops, 32 B per eval)
-        tiers = plan.field_tier_rows()
-        twopass = tiers.pop(w.n, 0)
-        fpe = (sum(r * flops_per_eval(t) for t, r in tiers.items()) + twopass * fpe) / float(rows)
-        bpe = 32.0 * twopass / float(rows)
+    tiers = plan.field_tier_rows() if not exact else {}
+    if len(tiers) > 1:
+        # pruned fast field (afd_pruned.cuh): a row whose weight tail beyond
+        # l = L is negligible is evaluated from its first L spectrum terms —
+        # in registers (L = 32, 64, 128) or as on-chip L-point transforms of
+        # pre-twiddled spectra (L = 1024, 4096): F(L) flops, no HBM bytes (the
+        # spectra and the weight tables are L2-resident).  The rest: large N
+        # the two-pass path (F(N) flops, 32 B per eval); on-chip N (batches,
+        # rows summed over the signals) the N-point field kernel, F(N) flops.
+        big = w.n > 8192
+        full = tiers.pop(w.n, 0)
+        total = float(sum(tiers.values()) + full)
+        fpe = (sum(r * flops_per_eval(t) for t, r in tiers.items()) + full * fpe) / total
+        bpe = 32.0 * full / total if big else 0.0
         split = {"rows_%d" % t: r for t, r in tiers.items()}
         split.update({"flops_per_eval_%d" % t: flops_per_eval(t) for t in tiers})
-        split.update({"onchip_rows": sum(tiers.values()), "twopass_rows": twopass,
-                      "flops_per_eval_twopass": flops_per_eval(w.n)})
-        split.update({
-                 "bytes_per_eval_twopass": 32.0,
-                 "note": "rows whose weight tail beyond l = L is below 2^-64 of the largest "
-                         "kept term are evaluated from their first L spectrum terms: L = 32, "
-                         "64, 128 in registers (one thread per 32 outputs), L = 1024, 4096 as "
-                         "N/L on-chip L-point fields; credited F(L) = 5 log2 L + 7 flops per "
-                         "eval (DESIGN.md §4)"})
+        if big:
+            split.update({"onchip_rows": sum(tiers.values()), "twopass_rows": full,
+                          "flops_per_eval_twopass": flops_per_eval(w.n),
+                          "bytes_per_eval_twopass": 32.0})
+        else:
+            split.update({"rows_%d" % w.n: full, "flops_per_eval_%d" % w.n: flops_per_eval(w.n),
+                          "rows_are": "summed over the batch's signals"})
+        split["note"] = ("rows whose weight tail beyond l = L is below 2^-64 of the largest kept "
+                         "term are evaluated from their first L spectrum terms: L = 32, 64, 128 "
+                         "in registers (one thread per 32 outputs), L = 1024, 4096 as N/L "
+                         "on-chip L-point fields; credited F(L) = 5 log2 L + 7 flops per eval "
+                         "(DESIGN.md §4)")
     achieved = launch_evals * fpe / (field_ms * 1e-3) / 1e12
     peak = engine.fp64_peak_tflops(local)
     hbm_peak, hbm_src = hbm_peak_gbs()
@@ -435,7 +443,9 @@ def field_roofline(plan, w, radii_rows, ghat, exact, local):
             roof["frac_ceiling_at_this_instruction_mix"] = fpe / (2.0 * instr)
     roof.update({
         "kernel": ("field_kernel (fused prologue + inverse DIT + scale + |.|^2 + argmax)"
-                   if w.n <= 8192 else
+                   if w.n <= 8192 and split is None else
+                   "batched pruned field: register tiers (field_reg_kernel<1>, <2>, <4>, BATCH) + "
+                   "N-point rows (field_kernel)" if w.n <= 8192 else
                    "large-N field: pass A (big_field_a) + TMA column pass (col_tma_kernel)"
                    if split is None else
                    "pruned large-N field: register tiers (field_reg_kernel<1>, <2>, <4>), on-chip "

@@ -144,6 +144,7 @@ struct afd_plan {
   int* sp_mstar = nullptr;               // [max_batch][kRegTiers] tier limits per signal
   unsigned long long* sp_hint = nullptr; // [max_batch]
   double2* sp_h = nullptr;               // [max_batch][128 N/32] pre-twiddled spectra
+  double2* sp_rlog = nullptr;            // [m1-m0] {log2 r, log2(1 - r)}
   int64_t sp_last_batch = 0;
   int* mstar = nullptr;        // [kPruneTiers] first row failing each tier's test
   unsigned long long* tmax = nullptr;
@@ -661,6 +662,22 @@ constexpr int64_t kSmallPrunedMinEvals = 1LL << 28;  // per field launch (c3: 2^
 
 int tier_ncta(const afd_plan* p, int64_t q, int64_t est, int rpc, double prologue);
 
+// the register kernels whose extra warps keep their spectra in shared memory
+int reg_kernel_attrs() {
+  if (fr_smem_bytes(4) > 0) {
+    const int b = (int)fr_smem_bytes(4);
+    CU(cudaFuncSetAttribute(field_reg_kernel<4, false, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CU(cudaFuncSetAttribute(field_reg_kernel<4, true, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CU(cudaFuncSetAttribute(field_reg_kernel<4, false, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+    CU(cudaFuncSetAttribute(field_reg_kernel<4, true, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+  }
+  return 0;
+}
+
 struct SmallGrid {
   bool pruned;
   int ncta;            // CTAs per signal of the N-point field
@@ -695,7 +712,7 @@ int launch_reg_small(afd_plan* p, int t, int64_t batch, Cand* cand, const SmallG
   const unsigned yb = (unsigned)((batch * qn + threads - 1) / threads);
   double* c2 = const_cast<double*>(runner_ups_for(p, cand));
   auto rk = c2 ? field_reg_kernel<D, true, true> : field_reg_kernel<D, false, true>;
-  rk<<<dim3((unsigned)sg.nc[t], yb), threads, 0, st>>>(
+  rk<<<dim3((unsigned)sg.nc[t], yb), threads, fr_smem_bytes(D), st>>>(
       p->sp_h, p->sp_fw, (long long)p->m0, (long long)p->m1, (long long)p->m0, (long long)qn, cand,
       p->sp_hint,
       SubMap{(long long)p->n, 0, p->sp_mstar + t, c2, t ? p->sp_mstar + t - 1 : nullptr, nullptr,
@@ -710,7 +727,7 @@ template <int K>
 int launch_field_small_pruned(afd_plan* p, const double2* ghat, int64_t batch, Cand* cand,
                               const SmallGrid& sg, const State* state, cudaStream_t st) {
   int rc;
-  prune_small_kernel<<<(unsigned)batch, 256, 0, st>>>(K, ghat, p->radii, p->m0, p->m1, p->circle,
+  prune_small_kernel<<<(unsigned)batch, 256, 0, st>>>(K, ghat, p->sp_rlog, p->m0, p->m1, p->circle,
                                                       state, p->sp_mstar, p->sp_hint, p->sp_h);
   p->launches++;
   CU(cudaGetLastError());
@@ -1133,7 +1150,7 @@ int launch_reg_tier(afd_plan* p, int t, const double2* ghat_rev, int64_t r0, int
   pretwiddle_reg_kernel<<<4 * p->sms, 256, 0, st>>>(p->K, p->ka, D, ghat_rev, p->circle, T.ghq,
                                                     stopped);
   auto rk = p->margins ? field_reg_kernel<D, true> : field_reg_kernel<D, false>;
-  rk<<<dim3((unsigned)T.ncta, (unsigned)T.qblocks), fr_threads(D), 0, st>>>(
+  rk<<<dim3((unsigned)T.ncta, (unsigned)T.qblocks), fr_threads(D), fr_smem_bytes(D), st>>>(
       T.ghq, p->tier[0].fw, (long long)r0, (long long)r1, (long long)p->m0,
       (long long)(p->n >> 5), T.cand, p->hint,
       SubMap{(long long)p->n, 0, hi, T.cand2, lo, nullptr}, RegBatch{});
@@ -1575,6 +1592,7 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
       rc = setup_pruned_tier<prune_k(kRegTiers)>(p, kRegTiers);
       if (!rc) rc = setup_pruned_tier<prune_k(kRegTiers + 1)>(p, kRegTiers + 1);
       for (int t = 0; t < kRegTiers && !rc && p->first_tier == 0; ++t) rc = setup_reg_tier(p, t);
+      if (!rc) rc = reg_kernel_attrs();
       if (rc) return cleanup(rc);
       p->pruned = true;
     }
@@ -1588,12 +1606,24 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
       ALLOC2(p->sp_mstar, sizeof(int) * kRegTiers * (size_t)max_batch);
       ALLOC2(p->sp_hint, sizeof(unsigned long long) * (size_t)max_batch);
       ALLOC2(p->sp_h, sizeof(double2) * 128 * (N >> 5) * (size_t)max_batch);
+      ALLOC2(p->sp_rlog, sizeof(double2) * (size_t)rows);
+      {
+        std::vector<double2> rl((size_t)rows);
+        for (int64_t s = 0; s < rows; ++s) {
+          const double r = radii_host[m0 + s];
+          rl[s] = make_double2(r > 0.0 ? std::log2(r) : -INFINITY, std::log2(1.0 - r));
+        }
+        if (cudaMemcpy(p->sp_rlog, rl.data(), sizeof(double2) * rl.size(),
+                       cudaMemcpyHostToDevice) != cudaSuccess)
+          return cleanup(fail(AFD_E_CUDA, "plan init: rlog upload"));
+      }
       const int64_t total = rows * kFwStride;
       fast_weight_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256>>>(
           p->radii, p->scales, p->m0, rows, kFwStride, 32, 32, 5, 0, 0, p->sp_fw);
       p->launches++;
       p->first_tier = 0;
       estimate_tier_rows(p, radii_host);
+      if ((rc = reg_kernel_attrs())) return cleanup(rc);
       p->sp = true;
     }
   }
@@ -1650,6 +1680,7 @@ int afd_plan_destroy(afd_plan* p) {
   cudaFree(p->sp_mstar);
   cudaFree(p->sp_hint);
   cudaFree(p->sp_h);
+  cudaFree(p->sp_rlog);
   cudaFree(p->big_part);
   cudaFree(p->nodes);
   cudaFree(p->sel);

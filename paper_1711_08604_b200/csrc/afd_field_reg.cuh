@@ -32,13 +32,26 @@
 namespace afd {
 
 // Warps per CTA (one CTA per SM): tensor memory has room for 512 / (128 D)
-// warps per lane quadrant (D = 4: one, four warps per SM), registers for 8
-// warps at 255 or 12 at 168.
+// warps per lane quadrant, registers for 8 warps at 255.  D = 4 fills tensor
+// memory with four warps (one per scheduler: FP64 pipe 73% busy).
+// -DAFD_FR_SMWARPS4=3 adds three warps that keep their spectra in shared
+// memory instead (64 KiB each, [value][lane]: conflict-free 16-byte loads,
+// a chunk ahead) — measured slower (c4 5.95e11 -> 5.70e11 evals/s, c3
+// 5.10e11 -> 4.92e11), so it is off.
 #ifndef AFD_FR_WARPS1
 #define AFD_FR_WARPS1 8
 #endif
-__host__ __device__ constexpr int fr_warps(int D) { return D == 1 ? AFD_FR_WARPS1 : D == 2 ? 8 : 4; }
+#ifndef AFD_FR_SMWARPS4
+#define AFD_FR_SMWARPS4 0
+#endif
+__host__ __device__ constexpr int fr_smem_warps(int D) { return D == 4 ? AFD_FR_SMWARPS4 : 0; }
+__host__ __device__ constexpr int fr_warps(int D) {
+  return D == 1 ? AFD_FR_WARPS1 : D == 2 ? 8 : 4 + fr_smem_warps(D);
+}
 __host__ __device__ constexpr int fr_threads(int D) { return 32 * fr_warps(D); }
+__host__ __device__ constexpr size_t fr_smem_bytes(int D) {
+  return sizeof(double2) * 32 * D * 32 * fr_smem_warps(D);
+}
 
 // BATCH: many signals of an on-chip N (afd_capi.cu pruned_small, BASELINE
 // c3): thread g of the launch serves signal g >> kq and q' = g mod Q' (a warp
@@ -66,8 +79,10 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
   constexpr int NCH = 32 / GI;       // loads per row
   constexpr int kFrWarps = fr_warps(D), kFrThreads = fr_threads(D);
   constexpr int kCols = 128 * D;     // columns per warp
-  constexpr int kTmCols = kCols * (kFrWarps / 4) <= 256 ? 256 : 512;
-  static_assert(kFrWarps % 4 == 0 && kCols * (kFrWarps / 4) <= 512, "TMEM columns");
+  constexpr int kSmWarps = fr_smem_warps(D), kTmWarps = kFrWarps - kSmWarps;
+  constexpr int kTmCols = kCols * (kTmWarps / 4) <= 256 ? 256 : 512;
+  static_assert(kTmWarps % 4 == 0 && kCols * (kTmWarps / 4) <= 512, "TMEM columns");
+  extern __shared__ double2 hs_all[];  // [kSmWarps][32 D][32 lanes]
   __shared__ uint32_t tm_base;
   __shared__ __align__(16) double wsm[kFrWarps][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -113,6 +128,8 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // the warp's lane quadrant; warps w and w + 4 share it, side by side
   const uint32_t tmw = tm_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * kCols);
+  const bool smem_fed = kSmWarps > 0 && warp >= kTmWarps;  // warp-uniform
+  double2* __restrict__ hs = hs_all + (size_t)(smem_fed ? warp - kTmWarps : 0) * (32 * D * 32) + lane;
   // chunk c holds registers i = GI c .. GI c + GI - 1, block m at word 4 GI m
 #pragma unroll
   for (int c = 0; c < NCH && active; ++c) {
@@ -122,8 +139,13 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
 #pragma unroll
       for (int u = 0; u < GI; ++u)
         g[m * GI + u] = __ldg(h + (size_t)(m * 32 + c * GI + u) * (size_t)qp_total + qp);
+    if (smem_fed) {
 #pragma unroll
-    for (int x = 0; x < 8; ++x) tm_st4(tmw + 32 * c + 4 * x, g[x]);
+      for (int x = 0; x < 8; ++x) hs[(8 * c + x) * 32] = g[x];
+    } else {
+#pragma unroll
+      for (int x = 0; x < 8; ++x) tm_st4(tmw + 32 * c + 4 * x, g[x]);
+    }
   }
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 
@@ -156,13 +178,28 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
     {
       // y_i = w_l0 sum_m rho^m h_(l0, m) and the stage-0 butterflies (register
       // pairs 2 u, 2 u + 1), GI registers per TMEM load, the next load in flight
+      // (shared-memory warps: the same 32-word chunks by eight 16-byte loads)
       uint32_t r[2][32];
-      tm_ld<32>(tmw, r[0]);
+      auto fetch = [&](int c, uint32_t (&buf)[32]) {
+        if (smem_fed) {
+#pragma unroll
+          for (int x = 0; x < 8; ++x) {
+            const uint4 t = *reinterpret_cast<const uint4*>(hs + (8 * c + x) * 32);
+            buf[4 * x] = t.x;
+            buf[4 * x + 1] = t.y;
+            buf[4 * x + 2] = t.z;
+            buf[4 * x + 3] = t.w;
+          }
+        } else {
+          tm_ld<32>(tmw + 32 * c, buf);
+        }
+      };
+      fetch(0, r[0]);
 #pragma unroll
       for (int c = 0; c < NCH; ++c) {
-        tm_wait_ld();
+        if (!smem_fed) tm_wait_ld();
         tm_dep(r[c & 1]);
-        if (c + 1 < NCH) tm_ld<32>(tmw + 32 * (c + 1), r[(c + 1) & 1]);
+        if (c + 1 < NCH) fetch(c + 1, r[(c + 1) & 1]);
         const uint32_t* rc = r[c & 1];
 #pragma unroll
         for (int u = 0; u < GI; u += 2) {

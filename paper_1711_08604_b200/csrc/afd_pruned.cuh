@@ -169,9 +169,11 @@ __global__ void pretwiddle_reg_kernel(int K, int ka, int D, const double2* __res
 // clears its hint and writes its pre-twiddled spectra
 //   h[sig][(m 32 + i) Q' + q'] = G^_l e^{+2 pi i l q' / N},  l = rev5(i) + 32 m,  m < 4
 // (natural-order spectrum, [batch][N]).  Rows from mstar[sig][kRegTiers-1]
-// on stay with the N-point field kernel (SubMap::lim_lo).
+// on stay with the N-point field kernel (SubMap::lim_lo).  One thread per
+// row; rlog[2 (s - m0)] = {log2 r_s, log2(1 - r_s)} is tabulated at plan
+// time (-inf for r = 0: no tail at all).
 __global__ void __launch_bounds__(256) prune_small_kernel(
-    int K, const double2* __restrict__ ghat, const double* __restrict__ radii, long long m0,
+    int K, const double2* __restrict__ ghat, const double2* __restrict__ rlog, long long m0,
     long long m1, const double2* __restrict__ circle, const State* __restrict__ state,
     int* __restrict__ mstar, unsigned long long* __restrict__ hint, double2* __restrict__ h) {
   constexpr int L = 128;  // terms of the longest register tier
@@ -202,22 +204,18 @@ __global__ void __launch_bounds__(256) prune_small_kernel(
   double t2 = 0.0;
   for (int w = 0; w < 8; ++w) t2 = fmax(t2, wmax[w]);
   const double lt = t2 > 0.0 ? 0.5 * log2(t2) : -INFINITY;
-  for (long long s = m0 + warp; s < m1; s += 8) {
-    const double r = radii[s];
-    if (r == 0.0 || lt == -INFINITY) continue;  // no tail at all
-    const double lr = log2(r), l1r = log2(1.0 - r);
+  for (long long s = m0 + threadIdx.x; s < m1 && lt != -INFINITY; s += blockDim.x) {
+    const double2 rl = __ldg(rlog + (s - m0));
+    if (rl.x == -INFINITY) continue;  // r = 0: no tail at all
     double b = -INFINITY;
     int lo = 0;
 #pragma unroll
     for (int t = 0; t < kRegTiers; ++t) {
       const int L_t = 1 << prune_k(t);
-      for (int l = lo + lane; l < L_t; l += 32) b = fmax(b, fma((double)l, lr, lg[l]));
+      for (int l = lo; l < L_t; ++l) b = fmax(b, fma((double)l, rl.x, lg[l]));
       lo = L_t;
-      double bt = b;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) bt = fmax(bt, __shfl_xor_sync(0xffffffffu, bt, o));
-      const double tail = lt + (double)L_t * lr - l1r;
-      if (lane == 0 && !(tail <= bt - 64.0)) atomicMin(ms + t, (int)s);
+      const double tail = lt + (double)L_t * rl.x - rl.y;
+      if (!(tail <= b - 64.0)) atomicMin(ms + t, (int)s);
     }
   }
   __syncthreads();
