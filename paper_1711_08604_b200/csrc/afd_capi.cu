@@ -141,7 +141,8 @@ struct afd_plan {
   // 1024 <= N <= 8192, many signals; afd_field_reg.cuh BATCH)
   bool sp = false;
   double* sp_fw = nullptr;               // [m1-m0][kFwStride] factor rows
-  int* sp_mstar = nullptr;               // [max_batch][kRegTiers] tier limits per signal
+  int* sp_mstar = nullptr;               // [max_batch][kSmallTiers] tier limits per signal
+  double2* sp_g1k = nullptr;             // [max_batch][N/1024][1024] spectra of the warp tier (N >= 4096)
   unsigned long long* sp_hint = nullptr; // [max_batch]
   double2* sp_h = nullptr;               // [max_batch][128 N/32] pre-twiddled spectra
   double2* sp_rlog = nullptr;            // [m1-m0] {log2 r, log2(1 - r)}
@@ -658,6 +659,8 @@ int set_device(const afd_plan* p) {
 // the rows below — all into one candidate row per signal: [ncta N-point
 // slots | per tier nc[t] * Q'/32 warp slots].
 static const bool kSmallPrunedOn = !(getenv("AFD_SMALL_PRUNED") && atoi(getenv("AFD_SMALL_PRUNED")) == 0);
+// AFD_SMALL_WARP_TIER=0: no 1024-point warp tier in batches (A/B switch)
+static const bool kSmallWarpTier = !(getenv("AFD_SMALL_WARP_TIER") && atoi(getenv("AFD_SMALL_WARP_TIER")) == 0);
 constexpr int64_t kSmallPrunedMinEvals = 1LL << 28;  // per field launch (c3: 2^32)
 
 int tier_ncta(const afd_plan* p, int64_t q, int64_t est, int rpc, double prologue);
@@ -683,6 +686,7 @@ struct SmallGrid {
   int ncta;            // CTAs per signal of the N-point field
   int nc[kRegTiers];   // row splits per register tier
   int off[kRegTiers];  // first candidate slot per tier
+  int nc1k, off1k;     // the 1024-point warp tier (N >= 4096; nc1k = 0: none)
   int ncand;           // candidates per signal
 };
 
@@ -701,6 +705,14 @@ SmallGrid small_grid(const afd_plan* p, int64_t batch, int ncta) {
     g.off[t] = g.ncand;
     g.ncand += g.nc[t] * (int)(qn >> 5);
   }
+  if (p->sp_g1k) {
+    const int64_t q1k = p->n >> kFwK;
+    g.nc1k = (int)std::max<int64_t>(
+        1, std::min<int64_t>(tier_ncta(p, batch * q1k, p->est_rows[kRegTiers], kFwWarps, 1.6),
+                             (rows + kFwWarps - 1) / kFwWarps));
+    g.off1k = g.ncand;
+    g.ncand += g.nc1k * (int)q1k;
+  }
   return g;
 }
 
@@ -716,7 +728,7 @@ int launch_reg_small(afd_plan* p, int t, int64_t batch, Cand* cand, const SmallG
       p->sp_h, p->sp_fw, (long long)p->m0, (long long)p->m1, (long long)p->m0, (long long)qn, cand,
       p->sp_hint,
       SubMap{(long long)p->n, 0, p->sp_mstar + t, c2, t ? p->sp_mstar + t - 1 : nullptr, nullptr,
-             kRegTiers, sg.ncand},
+             kSmallTiers, sg.ncand, 0},
       RegBatch{p->K - 5, batch * qn, sg.off[t]});
   p->launches++;
   CU(cudaGetLastError());
@@ -728,15 +740,27 @@ int launch_field_small_pruned(afd_plan* p, const double2* ghat, int64_t batch, C
                               const SmallGrid& sg, const State* state, cudaStream_t st) {
   int rc;
   prune_small_kernel<<<(unsigned)batch, 256, 0, st>>>(K, ghat, p->sp_rlog, p->m0, p->m1, p->circle,
-                                                      state, p->sp_mstar, p->sp_hint, p->sp_h);
+                                                      state, p->sp_mstar, p->sp_hint, p->sp_h,
+                                                      p->sp_g1k);
   p->launches++;
   CU(cudaGetLastError());
   p->sp_last_batch = batch;
-  const SubMap sub{0, 0, nullptr, const_cast<double*>(runner_ups_for(p, cand)),
-                   p->sp_mstar + kRegTiers - 1, p->sp_hint, kRegTiers, sg.ncand};
+  double* c2 = const_cast<double*>(runner_ups_for(p, cand));
+  const SubMap sub{0, 0, nullptr, c2, p->sp_mstar + kSmallTiers - 1, p->sp_hint, kSmallTiers,
+                   sg.ncand, 0};
   if ((rc = launch_field<K>(p, ghat, p->m0, p->m1, batch, cand, sg.ncta, nullptr, state, st,
                             nullptr, 0, &sub)))
     return rc;
+  if (sg.nc1k > 0) {  // rows [limit 2, limit 3) as N / 1024 1024-point fields, one warp per row
+    const int q1k = (int)(p->n >> kFwK);
+    auto wk = c2 ? field_warp_kernel<true, true> : field_warp_kernel<false, true>;
+    wk<<<dim3((unsigned)sg.nc1k, (unsigned)(batch * q1k)), 32 * kFwWarps, kFwSmem, st>>>(
+        p->sp_g1k, p->sp_fw, p->twct, (long long)p->m0, (long long)p->m1, (long long)p->m0, cand,
+        SubMap{(long long)p->n, q1k, p->sp_mstar + kSmallTiers - 1, c2,
+               p->sp_mstar + kSmallTiers - 2, p->sp_hint, kSmallTiers, sg.ncand, sg.off1k});
+    p->launches++;
+    CU(cudaGetLastError());
+  }
   if ((rc = launch_reg_small<1>(p, 0, batch, cand, sg, st))) return rc;
   if ((rc = launch_reg_small<2>(p, 1, batch, cand, sg, st))) return rc;
   return launch_reg_small<4>(p, 2, batch, cand, sg, st);
@@ -1603,7 +1627,14 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
         max_batch * rows * N >= (size_t)kSmallPrunedMinEvals) {
       // register tiers for batches (pruned_small)
       ALLOC2(p->sp_fw, sizeof(double) * kFwStride * (size_t)rows);
-      ALLOC2(p->sp_mstar, sizeof(int) * kRegTiers * (size_t)max_batch);
+      ALLOC2(p->sp_mstar, sizeof(int) * kSmallTiers * (size_t)max_batch);
+      if (K >= 12 && kSmallWarpTier) {
+        ALLOC2(p->sp_g1k, sizeof(double2) * N * (size_t)max_batch);
+        CU(cudaFuncSetAttribute(field_warp_kernel<false, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwSmem));
+        CU(cudaFuncSetAttribute(field_warp_kernel<true, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwSmem));
+      }
       ALLOC2(p->sp_hint, sizeof(unsigned long long) * (size_t)max_batch);
       ALLOC2(p->sp_h, sizeof(double2) * 128 * (N >> 5) * (size_t)max_batch);
       ALLOC2(p->sp_rlog, sizeof(double2) * (size_t)rows);
@@ -1681,6 +1712,7 @@ int afd_plan_destroy(afd_plan* p) {
   cudaFree(p->sp_hint);
   cudaFree(p->sp_h);
   cudaFree(p->sp_rlog);
+  cudaFree(p->sp_g1k);
   cudaFree(p->big_part);
   cudaFree(p->nodes);
   cudaFree(p->sel);
@@ -2368,27 +2400,28 @@ int afd_field_tier_rows(afd_plan* p, int64_t* terms, int64_t* rows_out, int cap,
   if (!p->big && p->sp && p->sp_last_batch > 0) {
     // batches of on-chip fields with register tiers: rows summed over the
     // signals of the last evaluation
-    if (cap < kRegTiers + 1)
-      return fail(AFD_E_INVALID, "afd_field_tier_rows: cap %d < %d", cap, kRegTiers + 1);
-    std::vector<int> ms((size_t)p->sp_last_batch * kRegTiers);
+    const int nt = p->sp_g1k ? kSmallTiers : kRegTiers;
+    if (cap < nt + 1)
+      return fail(AFD_E_INVALID, "afd_field_tier_rows: cap %d < %d", cap, nt + 1);
+    std::vector<int> ms((size_t)p->sp_last_batch * kSmallTiers);
     CU(cudaMemcpyAsync(ms.data(), p->sp_mstar, sizeof(int) * ms.size(), cudaMemcpyDeviceToHost,
                        (cudaStream_t)stream));
     CU(cudaStreamSynchronize((cudaStream_t)stream));
-    for (int t = 0; t <= kRegTiers; ++t) {
-      terms[t] = t < kRegTiers ? 1LL << prune_k(t) : p->n;
+    for (int t = 0; t <= nt; ++t) {
+      terms[t] = t < nt ? 1LL << prune_k(t) : p->n;
       rows_out[t] = 0;
     }
     for (int64_t b = 0; b < p->sp_last_batch; ++b) {
       int64_t prev = 0;
-      for (int t = 0; t < kRegTiers; ++t) {
+      for (int t = 0; t < nt; ++t) {
         const int64_t e = std::max(
-            prev, std::max<int64_t>(0, std::min<int64_t>(rows, ms[b * kRegTiers + t] - p->m0)));
+            prev, std::max<int64_t>(0, std::min<int64_t>(rows, ms[b * kSmallTiers + t] - p->m0)));
         rows_out[t] += e - prev;
         prev = e;
       }
-      rows_out[kRegTiers] += rows - prev;
+      rows_out[nt] += rows - prev;
     }
-    *count = kRegTiers + 1;
+    *count = nt + 1;
     return 0;
   }
   if (!p->big || !p->pruned) {

@@ -125,7 +125,11 @@ __device__ __forceinline__ void warp_pass1_stage(double2 (&v)[32], const uint32_
   }
 }
 
-template <bool MARG>
+// BATCH (batches of on-chip fields, afd_capi.cu pruned_small): blockIdx.y =
+// sig * Q + q over the signals' Q = N / 1024 pre-twiddled spectra; limits,
+// hint and candidate row are the signal's (SubMap lim_stride / cand_stride /
+// cand_off: slot cand_off + q * gridDim.x + blockIdx.x).
+template <bool MARG, bool BATCH = false>
 __global__ void __launch_bounds__(32 * kFwWarps, 1)
 field_warp_kernel(const double2* __restrict__ ghat,   // [batch][1024]
                   const double* __restrict__ fw,      // [rows of plan][64] factor rows
@@ -138,14 +142,22 @@ field_warp_kernel(const double2* __restrict__ ghat,   // [batch][1024]
   extern __shared__ double2 smem[];
   __shared__ uint32_t tm_base;
   __shared__ double wsm[kFwWarps][32];
-  const int sig = blockIdx.y;
+  const int sig = blockIdx.y;  // spectrum of the launch
+  const int sig_b = BATCH ? (int)blockIdx.y / sub.q_mul : 0;  // signal of the batch
+  const int q_b = BATCH ? (int)blockIdx.y % sub.q_mul : (int)blockIdx.y;
+  const size_t slot = BATCH ? (size_t)sig_b * sub.cand_stride + sub.cand_off +
+                                  (size_t)q_b * gridDim.x + blockIdx.x
+                            : (size_t)sig * gridDim.x + blockIdx.x;
+  if constexpr (BATCH) {
+    if (sub.hint) sub.hint += sig_b;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (sub.lim_lo != nullptr) {
-    const long long l = *sub.lim_lo;
+    const long long l = sub.lim_lo[(size_t)sig_b * sub.lim_stride];
     if (l > row0) row0 = l < row1 ? l : row1;
   }
   if (sub.lim != nullptr) {
-    const long long l = *sub.lim;
+    const long long l = sub.lim[(size_t)sig_b * sub.lim_stride];
     if (l < row1) row1 = l > row0 ? l : row0;
   }
   if (row1 <= row0) {  // no rows for this kernel this step: a neutral candidate
@@ -154,8 +166,8 @@ field_warp_kernel(const double2* __restrict__ ghat,   // [batch][1024]
       c.mag = -1.0;
       c.flat = 0x7fffffffffffffffLL;
       c.re = c.im = 0.0;
-      cand_out[(size_t)sig * gridDim.x + blockIdx.x] = c;
-      if constexpr (MARG) sub.cand2[(size_t)sig * gridDim.x + blockIdx.x] = -1.0;
+      cand_out[slot] = c;
+      if constexpr (MARG) sub.cand2[slot] = -1.0;
     }
     return;
   }
@@ -372,7 +384,7 @@ field_warp_kernel(const double2* __restrict__ ghat,   // [batch][1024]
   if (best_sl >= 0) {
     const long long j = (long long)(lane | (best_i << 5));
     best.flat = (row0 + best_sl) * (sub.row_stride ? sub.row_stride : (long long)N) +
-                (sub.q_mul ? (long long)sig + (long long)sub.q_mul * j : j);
+                (sub.q_mul ? (long long)q_b + (long long)sub.q_mul * j : j);
   } else {
     best.flat = 0x7fffffffffffffffLL;
   }
@@ -389,7 +401,7 @@ field_warp_kernel(const double2* __restrict__ ghat,   // [batch][1024]
     Cand c = lane < kFwWarps ? red[lane] : best;
     c = warp_argmax(c);
     if (lane == 0) {
-      cand_out[(size_t)sig * gridDim.x + blockIdx.x] = c;
+      cand_out[slot] = c;
       if constexpr (MARG) win_flat = c.flat;
       // non-negative doubles order like their bit patterns
       if (!MARG && sub.hint && c.mag > 0.0)
@@ -401,7 +413,7 @@ field_warp_kernel(const double2* __restrict__ ghat,   // [batch][1024]
     __syncthreads();
     const double r2 = cta_runner_up(sec_mag, own_mag, own_flat, win_flat, red2);
     if (threadIdx.x == 0) {
-      sub.cand2[(size_t)sig * gridDim.x + blockIdx.x] = r2;
+      sub.cand2[slot] = r2;
       if (sub.hint && r2 > 0.0) atomicMax(sub.hint, (unsigned long long)__double_as_longlong(r2));
     }
   }

@@ -204,6 +204,7 @@ struct SubMap {
   // candidates of signal `sig` go to cand_out[sig * cand_stride + slot]
   int lim_stride;            // 0: one limit / hint for the launch
   int cand_stride;           // 0: gridDim.x
+  int cand_off;              // first slot of the launch in a signal's candidate row
 };
 __device__ __forceinline__ size_t cand_slot(const SubMap& sub, int sig) {
   return (size_t)sig * (sub.cand_stride ? (unsigned)sub.cand_stride : gridDim.x) + blockIdx.x;

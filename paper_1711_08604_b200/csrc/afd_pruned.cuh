@@ -163,38 +163,46 @@ __global__ void pretwiddle_reg_kernel(int K, int ka, int D, const double2* __res
 }
 
 // Batches of on-chip fields (N <= 8192, many signals: BASELINE c3) with the
-// register tiers: one CTA per signal decides the signal's tier limits
-// mstar[sig][t], t < kRegTiers (the same tail test as prune_rows_kernel; a
-// stopped signal: every limit m0, and the field kernels then do nothing),
-// clears its hint and writes its pre-twiddled spectra
-//   h[sig][(m 32 + i) Q' + q'] = G^_l e^{+2 pi i l q' / N},  l = rev5(i) + 32 m,  m < 4
-// (natural-order spectrum, [batch][N]).  Rows from mstar[sig][kRegTiers-1]
-// on stay with the N-point field kernel (SubMap::lim_lo).  One thread per
-// row; rlog[2 (s - m0)] = {log2 r_s, log2(1 - r_s)} is tabulated at plan
-// time (-inf for r = 0: no tail at all).
+// register tiers and (N >= 4096: g1k != null) the 1024-point warp tier: one
+// CTA per signal decides the signal's tier limits mstar[sig][t],
+// t < kSmallTiers = kRegTiers + 1 (the same tail test as prune_rows_kernel;
+// without the warp tier the last limit repeats the one before; a stopped
+// signal: every limit m0, and the field kernels then do nothing), clears its
+// hint and writes its pre-twiddled spectra
+//   h[sig][(m 32 + i) Q' + q'] = G^_l e^{+2 pi i l q' / N},  l = rev5(i) + 32 m,  m < 4,
+//   g1k[sig][q][l] = G^_l e^{+2 pi i l q / N},  q < N / 1024,  l < 1024
+// (natural-order spectrum, [batch][N]).  Rows from the last limit on stay
+// with the N-point field kernel (SubMap::lim_lo).  One thread per row;
+// rlog[s - m0] = {log2 r_s, log2(1 - r_s)} is tabulated at plan time (-inf
+// for r = 0: no tail at all).
+constexpr int kSmallTiers = kRegTiers + 1;
 __global__ void __launch_bounds__(256) prune_small_kernel(
     int K, const double2* __restrict__ ghat, const double2* __restrict__ rlog, long long m0,
     long long m1, const double2* __restrict__ circle, const State* __restrict__ state,
-    int* __restrict__ mstar, unsigned long long* __restrict__ hint, double2* __restrict__ h) {
+    int* __restrict__ mstar, unsigned long long* __restrict__ hint, double2* __restrict__ h,
+    double2* __restrict__ g1k) {
   constexpr int L = 128;  // terms of the longest register tier
-  __shared__ double lg[L];
+  constexpr int LG = 1 << prune_k(kRegTiers);  // 1024: the warp tier
+  static_assert(LG == 1024, "tier after the register tiers");
+  __shared__ double lg[LG];
   __shared__ double wmax[8];
-  __shared__ int ms[kRegTiers];
+  __shared__ int ms[kSmallTiers];
+  const int ntier = g1k ? kSmallTiers : kRegTiers;
   const int sig = blockIdx.x;
   const int n = 1 << K, kq = K - 5, qn = 1 << kq;
   const double2* __restrict__ gh = ghat + (size_t)sig * n;
   if (threadIdx.x == 0) hint[sig] = 0ull;
   if (state && state[sig].stopped) {
-    if (threadIdx.x < kRegTiers) mstar[sig * kRegTiers + threadIdx.x] = (int)m0;
+    if (threadIdx.x < kSmallTiers) mstar[sig * kSmallTiers + threadIdx.x] = (int)m0;
     return;
   }
-  if (threadIdx.x < kRegTiers) ms[threadIdx.x] = (int)m1;
+  if (threadIdx.x < kSmallTiers) ms[threadIdx.x] = (int)m1;
   double m = 0.0;
   for (int l = threadIdx.x; l < n; l += blockDim.x) {
     const double2 v = __ldg(gh + l);
     const double a2 = fma(v.x, v.x, v.y * v.y);
     m = fmax(m, a2);
-    if (l < L) lg[l] = a2 > 0.0 ? 0.5 * log2(a2) : -INFINITY;
+    if (l < LG) lg[l] = a2 > 0.0 ? 0.5 * log2(a2) : -INFINITY;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -209,17 +217,30 @@ __global__ void __launch_bounds__(256) prune_small_kernel(
     if (rl.x == -INFINITY) continue;  // r = 0: no tail at all
     double b = -INFINITY;
     int lo = 0;
-#pragma unroll
-    for (int t = 0; t < kRegTiers; ++t) {
+    for (int t = 0; t < ntier; ++t) {
       const int L_t = 1 << prune_k(t);
-      for (int l = lo; l < L_t; ++l) b = fmax(b, fma((double)l, rl.x, lg[l]));
+      // four independent maxima (the loop is a latency chain otherwise)
+      double b0 = b, b1 = b, b2 = b, b3 = b;
+      for (int l = lo; l < L_t; l += 4) {
+        b0 = fmax(b0, fma((double)l, rl.x, lg[l]));
+        b1 = fmax(b1, fma((double)(l + 1), rl.x, lg[l + 1]));
+        b2 = fmax(b2, fma((double)(l + 2), rl.x, lg[l + 2]));
+        b3 = fmax(b3, fma((double)(l + 3), rl.x, lg[l + 3]));
+      }
+      b = fmax(fmax(b0, b1), fmax(b2, b3));
       lo = L_t;
       const double tail = lt + (double)L_t * rl.x - rl.y;
-      if (!(tail <= b - 64.0)) atomicMin(ms + t, (int)s);
+      if (tail <= b - 64.0) break;  // passes: it passes every longer tier as well
+      atomicMin(ms + t, (int)s);
     }
   }
   __syncthreads();
-  if (threadIdx.x < kRegTiers) mstar[sig * kRegTiers + threadIdx.x] = ms[threadIdx.x];
+  if (threadIdx.x < kSmallTiers) {
+    // a row failing tier t fails every shorter one: limits are non-decreasing
+    int v = ms[threadIdx.x < ntier ? threadIdx.x : ntier - 1];
+    for (int t = threadIdx.x + 1; t < ntier; ++t) v = min(v, ms[t]);
+    mstar[sig * kSmallTiers + threadIdx.x] = v;
+  }
   double2* __restrict__ out = h + (size_t)sig * L * qn;
   for (int x = threadIdx.x; x < L * qn; x += blockDim.x) {
     const int q = x & (qn - 1), im = x >> kq;
@@ -227,6 +248,15 @@ __global__ void __launch_bounds__(256) prune_small_kernel(
     const double2 g = __ldg(gh + l);
     const double2 w = __ldg(circle + ((l * q) & (n - 1)));
     out[x] = make_double2(fma(g.x, w.x, -(g.y * w.y)), fma(g.x, w.y, g.y * w.x));
+  }
+  if (g1k) {
+    double2* __restrict__ o1 = g1k + (size_t)sig * n;
+    for (int x = threadIdx.x; x < n; x += blockDim.x) {
+      const int q = x >> 10, l = x & 1023;
+      const double2 g = __ldg(gh + l);
+      const double2 w = __ldg(circle + ((l * q) & (n - 1)));
+      o1[x] = make_double2(fma(g.x, w.x, -(g.y * w.y)), fma(g.x, w.y, g.y * w.x));
+    }
   }
 }
 

@@ -1,8 +1,8 @@
 #!/bin/bash
-# round 2, session 5 (f): full GPU suite on the five-tier pruned field, bench lines for every
-# config/engine (v9), reference arm, launch list of the default bench, ncu of the tier kernels
+# round 2, session 5 (j): full GPU suite on the five-tier pruned field, bench lines for every
+# config/engine (v10), reference arm, launch list of the default bench, ncu of the tier kernels
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/s5f
+O=gpurun_out/s5j
 mkdir -p $O
 timeout 1800 python -m pytest tests -m gpu -x -q > $O/gpu_tests.log 2>&1; echo "gpu tests rc=$?"
 tail -3 $O/gpu_tests.log
@@ -18,11 +18,11 @@ done; done
 cmd="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-parity"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 4000 --csv \
    --log-file $O/launches_c4.csv $cmd > $O/ncu1.log 2>&1; echo "ncu list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'field_warp_kernel|field_reg_kernel<4' -s 4 -c 2 \
-   -o $O/field_warp_reg4_c4 $cmd > $O/ncu2.log 2>&1; echo "ncu warp/reg4 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'field_reg_kernel<4' -s 1 -c 1 \
+   -o $O/field_reg4_c4 $cmd > $O/ncu2.log 2>&1; echo "ncu warp/reg4 rc=$?"
 python - <<'PY'
 import json,glob
-for f in sorted(glob.glob("gpurun_out/s5f/bench_*.json")):
+for f in sorted(glob.glob("gpurun_out/s5j/bench_*.json")):
     try:
         d=json.loads(open(f).read())
         print(f.split("/")[-1], "%.4e"%d["value"], "e2e %.4e"%d["e2e"]["value"], d["roofline"]["bound"], "%.3f"%d["roofline"]["frac"], d["roofline"].get("launch_ms"), d.get("parity_vs_oracle"), d.get("clocks"))
