@@ -699,11 +699,11 @@ SmallGrid small_grid(const afd_plan* p, int64_t batch, int ncta) {
   if (!g.pruned) return g;
   const int64_t qn = p->n >> 5;
   for (int t = 0; t < kRegTiers; ++t) {
-    const int threads = fr_threads(1 << t);
-    const int64_t yb = (batch * qn + threads - 1) / threads;
-    g.nc[t] = (int)std::min<int64_t>(tier_ncta(p, yb, p->est_rows[t], 1, 1.0), rows);
+    const int qt = fr_qthreads(1 << t), share = fr_share(1 << t);
+    const int64_t yb = (batch * qn + qt - 1) / qt;
+    g.nc[t] = (int)std::min<int64_t>(tier_ncta(p, yb, p->est_rows[t], share, 1.0), rows);
     g.off[t] = g.ncand;
-    g.ncand += g.nc[t] * (int)(qn >> 5);
+    g.ncand += g.nc[t] * share * (int)(qn >> 5);
   }
   if (p->sp_g1k) {
     const int64_t q1k = p->n >> kFwK;
@@ -721,7 +721,7 @@ int launch_reg_small(afd_plan* p, int t, int64_t batch, Cand* cand, const SmallG
                      cudaStream_t st) {
   const int64_t qn = p->n >> 5;
   const int threads = fr_threads(D);
-  const unsigned yb = (unsigned)((batch * qn + threads - 1) / threads);
+  const unsigned yb = (unsigned)((batch * qn + fr_qthreads(D) - 1) / fr_qthreads(D));
   double* c2 = const_cast<double*>(runner_ups_for(p, cand));
   auto rk = c2 ? field_reg_kernel<D, true, true> : field_reg_kernel<D, false, true>;
   rk<<<dim3((unsigned)sg.nc[t], yb), threads, fr_smem_bytes(D), st>>>(
@@ -1150,7 +1150,7 @@ int setup_reg_tier(afd_plan* p, int t) {
   auto& T = p->tier[t];
   const int D = 1 << t;
   const int64_t rows = p->m1 - p->m0, Qp = p->n >> 5;
-  T.qblocks = (int)((Qp + fr_threads(D) - 1) / fr_threads(D));
+  T.qblocks = (int)((Qp + fr_qthreads(D) - 1) / fr_qthreads(D));
   if (t == 0) {
     CU(cudaMalloc(&T.fw, sizeof(double) * kFwStride * (size_t)rows));
     const int64_t total = rows * kFwStride;
@@ -1160,7 +1160,7 @@ int setup_reg_tier(afd_plan* p, int t) {
     CU(cudaGetLastError());
   }
   CU(cudaMalloc(&T.ghq, sizeof(double2) * (size_t)p->n * D));
-  const int nc = tier_ncta(p, T.qblocks, p->est_rows[t], 1, 1.0);
+  const int nc = tier_ncta(p, T.qblocks, p->est_rows[t], fr_share(D), 1.0);
   T.ncta = (int)std::max<int64_t>(1, std::min<int64_t>(nc, rows));
   CU(cudaMalloc(&T.cand, sizeof(Cand) * (size_t)T.qblocks * T.ncta));
   if (p->margins) CU(cudaMalloc(&T.cand2, sizeof(double) * (size_t)T.qblocks * T.ncta));

@@ -44,11 +44,24 @@ namespace afd {
 #ifndef AFD_FR_SMWARPS4
 #define AFD_FR_SMWARPS4 0
 #endif
+// D = 4: tensor memory holds the spectra of only 128 values of q' per SM (four
+// warps, one per scheduler: FP64 pipe 73% busy).  Warps w and w + 4 read the
+// same lane quadrant, so a second set of four warps serves the SAME 128 q'
+// from the same columns and takes every other row of the CTA's rows
+// (AFD_FR_SHARE4 = 2 row sets): eight warps per SM without more storage.
+#ifndef AFD_FR_SHARE4
+#define AFD_FR_SHARE4 2
+#endif
 __host__ __device__ constexpr int fr_smem_warps(int D) { return D == 4 ? AFD_FR_SMWARPS4 : 0; }
+__host__ __device__ constexpr int fr_share(int D) {
+  return D == 4 && AFD_FR_SMWARPS4 == 0 ? AFD_FR_SHARE4 : 1;
+}
 __host__ __device__ constexpr int fr_warps(int D) {
-  return D == 1 ? AFD_FR_WARPS1 : D == 2 ? 8 : 4 + fr_smem_warps(D);
+  return D == 1 ? AFD_FR_WARPS1 : D == 2 ? 8 : 4 * fr_share(D) + fr_smem_warps(D);
 }
 __host__ __device__ constexpr int fr_threads(int D) { return 32 * fr_warps(D); }
+// threads of a CTA that serve distinct q' (the CTA's extent along q')
+__host__ __device__ constexpr int fr_qthreads(int D) { return fr_threads(D) / fr_share(D); }
 __host__ __device__ constexpr size_t fr_smem_bytes(int D) {
   return sizeof(double2) * 32 * D * 32 * fr_smem_warps(D);
 }
@@ -58,7 +71,8 @@ __host__ __device__ constexpr size_t fr_smem_bytes(int D) {
 // never straddles signals: Q' >= 32), its spectra at h + sig * 128 Q' (four
 // blocks per signal whatever D), its row limits and hint are the signal's
 // (sub.lim_stride), and every warp writes its own candidate to the signal's
-// candidate row: slot cand_off + blockIdx.x * (Q' / 32) + (q' >> 5).
+// candidate row: slot cand_off + (blockIdx.x * fr_share(D) + row set) * (Q' / 32)
+// + (q' >> 5).
 struct RegBatch {
   int kq;                   // log2 Q'
   long long threads_total;  // batch * Q'
@@ -75,11 +89,19 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
                  Cand* __restrict__ cand_out,        // [gridDim.y][gridDim.x]
                  const unsigned long long* __restrict__ hint, SubMap sub, RegBatch rb) {
   static_assert(D == 1 || D == 2 || D == 4, "chunks of 8 / D registers per 32-word TMEM load");
-  constexpr int GI = 8 / D;          // registers i per 32-word TMEM load
+#ifndef AFD_FR_LDW4
+#define AFD_FR_LDW4 32
+#endif
+  // words per TMEM load (-DAFD_FR_LDW4=64: twice as long for D = 4; measured
+  // 1% slower)
+  constexpr int W = D == 4 ? AFD_FR_LDW4 : 32;
+  constexpr int CV = W / 4;          // complex values per load
+  constexpr int GI = CV / D;         // registers i per load
   constexpr int NCH = 32 / GI;       // loads per row
   constexpr int kFrWarps = fr_warps(D), kFrThreads = fr_threads(D);
   constexpr int kCols = 128 * D;     // columns per warp
-  constexpr int kSmWarps = fr_smem_warps(D), kTmWarps = kFrWarps - kSmWarps;
+  constexpr int kShare = fr_share(D), kQThreads = fr_qthreads(D);
+  constexpr int kSmWarps = fr_smem_warps(D), kTmWarps = (kFrWarps - kSmWarps) / kShare;
   constexpr int kTmCols = kCols * (kTmWarps / 4) <= 256 ? 256 : 512;
   static_assert(kTmWarps % 4 == 0 && kCols * (kTmWarps / 4) <= 512, "TMEM columns");
   extern __shared__ double2 hs_all[];  // [kSmWarps][32 D][32 lanes]
@@ -87,7 +109,8 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
   __shared__ __align__(16) double wsm[kFrWarps][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = blockIdx.y * gridDim.x + blockIdx.x;
-  const long long gthread = (long long)blockIdx.y * kFrThreads + threadIdx.x;
+  const int rset = (int)threadIdx.x / kQThreads;  // row set of the thread (kShare > 1)
+  const long long gthread = (long long)blockIdx.y * kQThreads + (int)threadIdx.x % kQThreads;
   // warp-uniform (Q' is a multiple of 32)
   const bool active = gthread < (BATCH ? rb.threads_total : qp_total);
   const int sig = BATCH && active ? (int)(gthread >> rb.kq) : 0;
@@ -127,13 +150,14 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // the warp's lane quadrant; warps w and w + 4 share it, side by side
-  const uint32_t tmw = tm_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * kCols);
+  const int tw = kShare > 1 ? warp % kTmWarps : warp;  // the warp whose columns this one reads
+  const uint32_t tmw = tm_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((tw >> 2) * kCols);
   const bool smem_fed = kSmWarps > 0 && warp >= kTmWarps;  // warp-uniform
   double2* __restrict__ hs = hs_all + (size_t)(smem_fed ? warp - kTmWarps : 0) * (32 * D * 32) + lane;
   // chunk c holds registers i = GI c .. GI c + GI - 1, block m at word 4 GI m
 #pragma unroll
-  for (int c = 0; c < NCH && active; ++c) {
-    double2 g[8];
+  for (int c = 0; c < NCH && active && rset == 0; ++c) {
+    double2 g[CV];
 #pragma unroll
     for (int m = 0; m < D; ++m)
 #pragma unroll
@@ -141,13 +165,18 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
         g[m * GI + u] = __ldg(h + (size_t)(m * 32 + c * GI + u) * (size_t)qp_total + qp);
     if (smem_fed) {
 #pragma unroll
-      for (int x = 0; x < 8; ++x) hs[(8 * c + x) * 32] = g[x];
+      for (int x = 0; x < CV; ++x) hs[(CV * c + x) * 32] = g[x];
     } else {
 #pragma unroll
-      for (int x = 0; x < 8; ++x) tm_st4(tmw + 32 * c + 4 * x, g[x]);
+      for (int x = 0; x < CV; ++x) tm_st4(tmw + W * c + 4 * x, g[x]);
     }
   }
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  if constexpr (kShare > 1) {  // the other row sets read what row set 0 stored
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
 
   double best_mag = -1.0, best_re = 0.0, best_im = 0.0;
   int best_sl = 0x7fffffff, best_i = 0;
@@ -155,43 +184,46 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
   double thr = hint ? __longlong_as_double((long long)*hint) : 0.0;
   if (!(thr > 0.0)) thr = -1.0;
 
-  // rows sl = blockIdx.x + k gridDim.x, k = nk - 1 .. 0
+  // rows sl = blockIdx.x + k gridDim.x, k = nk - 1 .. 0 (row set s: every
+  // kShare-th of them from nk - 1 - s down)
   const int nk = active && rows > (int)blockIdx.x
                      ? (rows - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x
                      : 0;
   const double* __restrict__ fr0 = fw + (size_t)(row0 + blockIdx.x - pw_row0) * kFwStride;
   const size_t fstep = (size_t)gridDim.x * kFwStride;
-  double a_nx = nk > 0 ? __ldg(fr0 + (size_t)(nk - 1) * fstep + lane) : 0.0;
-  [[maybe_unused]] double rho_nx = D > 1 && nk > 0 ? __ldg(fr0 + (size_t)(nk - 1) * fstep + 33) : 0.0;
+  const int k0 = nk - 1 - rset;
+  double a_nx = k0 >= 0 ? __ldg(fr0 + (size_t)k0 * fstep + lane) : 0.0;
+  [[maybe_unused]] double rho_nx = D > 1 && k0 >= 0 ? __ldg(fr0 + (size_t)k0 * fstep + 33) : 0.0;
   const int wpos = brev_bits(lane, 5);  // weight of l0 = lane sits at register index rev5(l0)
-  for (int k = nk - 1; k >= 0; --k) {
+  int it = 0;
+  for (int k = k0; k >= 0; k -= kShare, ++it) {
     const int sl = (int)blockIdx.x + k * (int)gridDim.x;
-    double* wrow = wsm[warp][k & 1];
+    double* wrow = wsm[warp][it & 1];
     wrow[wpos] = a_nx;
     [[maybe_unused]] const double rho = rho_nx;
     __syncwarp();
-    if (k > 0) {  // next row's factors, one row ahead
-      a_nx = __ldg(fr0 + (size_t)(k - 1) * fstep + lane);
-      if constexpr (D > 1) rho_nx = __ldg(fr0 + (size_t)(k - 1) * fstep + 33);
+    if (k >= kShare) {  // next row's factors, one row ahead
+      a_nx = __ldg(fr0 + (size_t)(k - kShare) * fstep + lane);
+      if constexpr (D > 1) rho_nx = __ldg(fr0 + (size_t)(k - kShare) * fstep + 33);
     }
     double2 v[32];
     {
       // y_i = w_l0 sum_m rho^m h_(l0, m) and the stage-0 butterflies (register
       // pairs 2 u, 2 u + 1), GI registers per TMEM load, the next load in flight
       // (shared-memory warps: the same 32-word chunks by eight 16-byte loads)
-      uint32_t r[2][32];
-      auto fetch = [&](int c, uint32_t (&buf)[32]) {
+      uint32_t r[2][W];
+      auto fetch = [&](int c, uint32_t (&buf)[W]) {
         if (smem_fed) {
 #pragma unroll
-          for (int x = 0; x < 8; ++x) {
-            const uint4 t = *reinterpret_cast<const uint4*>(hs + (8 * c + x) * 32);
+          for (int x = 0; x < CV; ++x) {
+            const uint4 t = *reinterpret_cast<const uint4*>(hs + (CV * c + x) * 32);
             buf[4 * x] = t.x;
             buf[4 * x + 1] = t.y;
             buf[4 * x + 2] = t.z;
             buf[4 * x + 3] = t.w;
           }
         } else {
-          tm_ld<32>(tmw + 32 * c, buf);
+          tm_ld<W>(tmw + W * c, buf);
         }
       };
       fetch(0, r[0]);
@@ -290,7 +322,8 @@ field_reg_kernel(const double2* __restrict__ h,      // [32 D][Q'] pre-twiddled 
   if constexpr (BATCH) {  // one candidate per warp, in the signal's candidate row
     best = warp_argmax(best);
     const size_t ws = (size_t)sig * sub.cand_stride + rb.cand_off +
-                      (size_t)blockIdx.x * (size_t)(qp_total >> 5) + (size_t)(qp >> 5);
+                      ((size_t)blockIdx.x * kShare + rset) * (size_t)(qp_total >> 5) +
+                      (size_t)(qp >> 5);
     if (active && lane == 0) cand_out[ws] = best;
     if constexpr (MARG) {
       const long long wf = __shfl_sync(0xffffffffu, best.flat, 0);
