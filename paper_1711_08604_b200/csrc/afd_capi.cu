@@ -22,6 +22,7 @@
 #include "afd_pruned.cuh"
 #include "afd_field_warp.cuh"
 #include "afd_field_reg.cuh"
+#include "afd_field_sub.cuh"
 #include "afd_direct.cuh"
 
 using namespace afd;
@@ -136,6 +137,7 @@ struct afd_plan {
   } tier[kPruneTiers];
   int64_t est_rows[kPruneTiers] = {};  // rows per tier expected from the radii alone
   int first_tier = 0;          // tiers below are switched off (AFD_REG_TIERS=0: kRegTiers)
+  bool tier_on[kPruneTiers] = {};  // tiers in use: an unused tier's rows go to the next one
   unsigned long long* hint = nullptr;  // screening hint of the register tiers
   // register tiers for batches of on-chip fields (pruned_small: fast engine,
   // 1024 <= N <= 8192, many signals; afd_field_reg.cuh BATCH)
@@ -143,6 +145,8 @@ struct afd_plan {
   double* sp_fw = nullptr;               // [m1-m0][kFwStride] factor rows
   int* sp_mstar = nullptr;               // [max_batch][kSmallTiers] tier limits per signal
   double2* sp_g1k = nullptr;             // [max_batch][N/1024][1024] spectra of the warp tier (N >= 4096)
+  double2* sp_gsub[2] = {nullptr, nullptr};  // [max_batch][N/L][L], L = 256, 512 (N >= 4096)
+  double* sp_fwsub[2] = {nullptr, nullptr};  // [m1-m0][L/32 + 32] factor rows of the sub tiers
   unsigned long long* sp_hint = nullptr; // [max_batch]
   double2* sp_h = nullptr;               // [max_batch][128 N/32] pre-twiddled spectra
   double2* sp_rlog = nullptr;            // [m1-m0] {log2 r, log2(1 - r)}
@@ -687,6 +691,7 @@ struct SmallGrid {
   int nc[kRegTiers];   // row splits per register tier
   int off[kRegTiers];  // first candidate slot per tier
   int nc1k, off1k;     // the 1024-point warp tier (N >= 4096; nc1k = 0: none)
+  int ncs[2], offs[2]; // the 256- and 512-point tiers (ncs = 0: none)
   int ncand;           // candidates per signal
 };
 
@@ -713,7 +718,24 @@ SmallGrid small_grid(const afd_plan* p, int64_t batch, int ncta) {
     g.off1k = g.ncand;
     g.ncand += g.nc1k * (int)q1k;
   }
+  for (int u = 0; u < 2; ++u) {
+    if (!p->sp_gsub[u]) continue;
+    const int kl = 8 + u, S = 32 >> (kl - 5);
+    const int64_t qb = (p->n >> kl) / S;  // CTAs along y per signal
+    g.ncs[u] = (int)std::max<int64_t>(
+        1, std::min<int64_t>(tier_ncta(p, batch * qb, p->est_rows[kTierSub + u], kFwWarps, 1.6),
+                             (rows + kFwWarps - 1) / kFwWarps));
+    g.offs[u] = g.ncand;
+    g.ncand += g.ncs[u] * (int)qb;
+  }
   return g;
+}
+
+// lower limit of tier t: the limit of the last tier in use below it
+const int* tier_lo(const afd_plan* p, const int* mstar, int t) {
+  for (int u = t - 1; u >= 0; --u)
+    if (p->tier_on[u]) return mstar + u;
+  return nullptr;
 }
 
 template <int D>
@@ -727,9 +749,27 @@ int launch_reg_small(afd_plan* p, int t, int64_t batch, Cand* cand, const SmallG
   rk<<<dim3((unsigned)sg.nc[t], yb), threads, fr_smem_bytes(D), st>>>(
       p->sp_h, p->sp_fw, (long long)p->m0, (long long)p->m1, (long long)p->m0, (long long)qn, cand,
       p->sp_hint,
-      SubMap{(long long)p->n, 0, p->sp_mstar + t, c2, t ? p->sp_mstar + t - 1 : nullptr, nullptr,
+      SubMap{(long long)p->n, 0, p->sp_mstar + t, c2, tier_lo(p, p->sp_mstar, t), nullptr,
              kSmallTiers, sg.ncand, 0},
       RegBatch{p->K - 5, batch * qn, sg.off[t]});
+  p->launches++;
+  CU(cudaGetLastError());
+  return 0;
+}
+
+template <int KL>
+int launch_sub_small(afd_plan* p, int u, int64_t batch, Cand* cand, const SmallGrid& sg,
+                     cudaStream_t st) {
+  using SG = SubGeo<KL>;
+  const int ql = (int)(p->n >> KL);
+  double* c2 = const_cast<double*>(runner_ups_for(p, cand));
+  auto sk = c2 ? field_sub_kernel<KL, true, true> : field_sub_kernel<KL, false, true>;
+  sk<<<dim3((unsigned)sg.ncs[u], (unsigned)(batch * (ql / SG::S))), 32 * kFwWarps, SG::kSmem, st>>>(
+      p->sp_gsub[u], p->sp_fwsub[u], p->twct, (long long)p->m0, (long long)p->m1, (long long)p->m0,
+      cand,
+      SubMap{(long long)p->n, ql, p->sp_mstar + kTierSub + u, c2,
+             tier_lo(p, p->sp_mstar, kTierSub + u), p->sp_hint, kSmallTiers, sg.ncand,
+             sg.offs[u]});
   p->launches++;
   CU(cudaGetLastError());
   return 0;
@@ -741,26 +781,30 @@ int launch_field_small_pruned(afd_plan* p, const double2* ghat, int64_t batch, C
   int rc;
   prune_small_kernel<<<(unsigned)batch, 256, 0, st>>>(K, ghat, p->sp_rlog, p->m0, p->m1, p->circle,
                                                       state, p->sp_mstar, p->sp_hint, p->sp_h,
-                                                      p->sp_g1k);
+                                                      SmallSpectra{{p->sp_gsub[0], p->sp_gsub[1],
+                                                                    p->sp_g1k}});
   p->launches++;
   CU(cudaGetLastError());
   p->sp_last_batch = batch;
   double* c2 = const_cast<double*>(runner_ups_for(p, cand));
+  // (without the longer tiers their limits repeat the last register tier's)
   const SubMap sub{0, 0, nullptr, c2, p->sp_mstar + kSmallTiers - 1, p->sp_hint, kSmallTiers,
                    sg.ncand, 0};
   if ((rc = launch_field<K>(p, ghat, p->m0, p->m1, batch, cand, sg.ncta, nullptr, state, st,
                             nullptr, 0, &sub)))
     return rc;
-  if (sg.nc1k > 0) {  // rows [limit 2, limit 3) as N / 1024 1024-point fields, one warp per row
+  if (sg.nc1k > 0) {  // rows up to the 1024-term limit as N / 1024 1024-point fields, one warp per row
     const int q1k = (int)(p->n >> kFwK);
     auto wk = c2 ? field_warp_kernel<true, true> : field_warp_kernel<false, true>;
     wk<<<dim3((unsigned)sg.nc1k, (unsigned)(batch * q1k)), 32 * kFwWarps, kFwSmem, st>>>(
         p->sp_g1k, p->sp_fw, p->twct, (long long)p->m0, (long long)p->m1, (long long)p->m0, cand,
-        SubMap{(long long)p->n, q1k, p->sp_mstar + kSmallTiers - 1, c2,
-               p->sp_mstar + kSmallTiers - 2, p->sp_hint, kSmallTiers, sg.ncand, sg.off1k});
+        SubMap{(long long)p->n, q1k, p->sp_mstar + kTier1k, c2, tier_lo(p, p->sp_mstar, kTier1k),
+               p->sp_hint, kSmallTiers, sg.ncand, sg.off1k});
     p->launches++;
     CU(cudaGetLastError());
   }
+  if (sg.ncs[1] > 0 && (rc = launch_sub_small<9>(p, 1, batch, cand, sg, st))) return rc;
+  if (sg.ncs[0] > 0 && (rc = launch_sub_small<8>(p, 0, batch, cand, sg, st))) return rc;
   if ((rc = launch_reg_small<1>(p, 0, batch, cand, sg, st))) return rc;
   if ((rc = launch_reg_small<2>(p, 1, batch, cand, sg, st))) return rc;
   return launch_reg_small<4>(p, 2, batch, cand, sg, st);
@@ -1072,7 +1116,7 @@ void estimate_tier_rows(afd_plan* p, const double* radii_host) {
       while (t < kPruneTiers &&
              (double)(1 << prune_k(t)) * std::log2(r) - std::log2(1.0 - r) > -64.0)
         ++t;
-    if (t < p->first_tier) t = p->first_tier;
+    while (t < kPruneTiers && !p->tier_on[t]) ++t;
     if (t < kPruneTiers) p->est_rows[t]++;
   }
 }
@@ -1136,6 +1180,79 @@ int setup_pruned_tier(afd_plan* p, int t) {
     CU(cudaFuncSetAttribute(field_warp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kFwSmem));
   }
+  return 0;
+}
+
+// AFD_SUB_TIERS=0: no 256- / 512-point tiers (their rows stay on the
+// 1024-point tier; A/B switch).  A sub tier is used when the rows the radii
+// predict for it make at least AFD_SUB_MIN_EVALS grid evaluations per field
+// (default 2^30: c4 — field 28.0 -> 26.7 ms; below that the extra launches and
+// CTA prologues cost what the shorter transforms save: c2 +2%, c3 +0.3%
+// slower when forced on).  The GPU tests run with AFD_SUB_MIN_EVALS=0.
+static const int kSubTiersOn = getenv("AFD_SUB_TIERS") ? atoi(getenv("AFD_SUB_TIERS")) : 1;
+static const double kSubMinEvals =
+    getenv("AFD_SUB_MIN_EVALS") ? atof(getenv("AFD_SUB_MIN_EVALS")) : (double)(1LL << 30);
+void estimate_tier_rows(afd_plan* p, const double* radii_host);
+// tier_on[] of the sub tiers (the others set by the caller) and est_rows[]
+void choose_sub_tiers(afd_plan* p, const double* radii_host, int64_t fields) {
+  for (int t = kTierSub; t < kTier1k; ++t) p->tier_on[t] = kSubTiersOn != 0 && p->tier_on[kTier1k];
+  estimate_tier_rows(p, radii_host);
+  bool changed = false;
+  for (int t = kTierSub; t < kTier1k; ++t)
+    if (p->tier_on[t] && (double)p->est_rows[t] * (double)p->n * (double)fields < kSubMinEvals) {
+      p->tier_on[t] = false;
+      changed = true;
+    }
+  if (changed) estimate_tier_rows(p, radii_host);
+}
+
+// A sub-warp tier (afd_field_sub.cuh, L = 2^KL = 256 or 512): factor rows
+// {scale r^t, t < L/32; r^(L/32 m), m < 32}, the N/L pre-twiddled spectra,
+// per-CTA candidates.
+template <int KL>
+int setup_sub_tier(afd_plan* p, int t) {
+  using SG = SubGeo<KL>;
+  auto& T = p->tier[t];
+  const int64_t rows = p->m1 - p->m0, Q = p->n >> KL;
+  CU(cudaMalloc(&T.fw, sizeof(double) * SG::kStride * (size_t)rows));
+  CU(cudaMalloc(&T.ghq, sizeof(double2) * (size_t)p->n));
+  T.qblocks = (int)(Q / SG::S);
+  const int nc = tier_ncta(p, T.qblocks, p->est_rows[t], kFwWarps, 1.6);
+  T.ncta = (int)std::max<int64_t>(1, std::min<int64_t>(nc, (rows + kFwWarps - 1) / kFwWarps));
+  CU(cudaMalloc(&T.cand, sizeof(Cand) * (size_t)T.qblocks * T.ncta));
+  if (p->margins) CU(cudaMalloc(&T.cand2, sizeof(double) * (size_t)T.qblocks * T.ncta));
+  const int64_t total = rows * SG::kStride;
+  fast_weight_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256>>>(
+      p->radii, p->scales, p->m0, rows, SG::kStride, SG::T, 32, SG::C, 0, 0, T.fw);
+  p->launches++;
+  CU(cudaGetLastError());
+  CU(cudaFuncSetAttribute(field_sub_kernel<KL, false, false>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SG::kSmem));
+  CU(cudaFuncSetAttribute(field_sub_kernel<KL, true, false>,
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SG::kSmem));
+  return 0;
+}
+
+template <int KL>
+int launch_sub_tier(afd_plan* p, int t, const double2* ghat_rev, int64_t r0, int64_t r1,
+                    const int* lo, const int* hi, const int* stopped, int* slot, cudaStream_t st) {
+  using SG = SubGeo<KL>;
+  auto& T = p->tier[t];
+  const int Q = (int)(p->n >> KL);
+  pretwiddle_kernel<<<4 * p->sms, 256, 0, st>>>(p->K, p->ka, KL, ghat_rev, p->circle, T.ghq,
+                                                stopped);
+  auto sk = p->margins ? field_sub_kernel<KL, true> : field_sub_kernel<KL, false>;
+  sk<<<dim3((unsigned)T.ncta, (unsigned)T.qblocks), 32 * kFwWarps, SG::kSmem, st>>>(
+      T.ghq, T.fw, p->twct, (long long)r0, (long long)r1, (long long)p->m0, T.cand,
+      SubMap{(long long)p->n, Q, hi, T.cand2, lo, p->hint});
+  const int n = T.qblocks * T.ncta;
+  const int slots = (int)(p->big_rows * big_col_ctas(p));
+  const int np = std::max(1, std::min(std::min(kBigParts, (n + 255) / 256), (slots - *slot) / 2));
+  cand_partial_kernel<<<np, 256, 0, st>>>(T.cand, n, (n + np - 1) / np, p->big_cand + *slot,
+                                          T.cand2, p->big_cand2 ? p->big_cand2 + *slot : nullptr);
+  *slot += np;
+  p->launches += 3;
+  CU(cudaGetLastError());
   return 0;
 }
 
@@ -1241,10 +1358,11 @@ int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, doub
   }
   const int* lim = nullptr;
   if (!fout && p->pruned) {
-    // tier t takes rows [mstar[t-1], mstar[t]): tiers 0..2 in registers (32,
-    // 64 and 128 terms), tier 3 as N/1024 1024-point fields, tier 4 as N/4096
-    // 4096-point fields, rows [mstar[4], r1) through the batches below (all
-    // limits read on the device).  Longest tiers first (the largest |F|^2
+    // tier t takes rows [mstar[t-1], mstar[t]) (of the tiers in use): tiers
+    // 0..2 in registers (32, 64 and 128 terms), 3 and 4 as N/256 256-point and
+    // N/512 512-point fields on 8 / 16 threads each, 5 as N/1024 1024-point
+    // fields, 6 as N/4096 4096-point fields, rows [mstar[6], r1) through the
+    // batches below (all limits read on the device).  Longest tiers first (the largest |F|^2
     // sit at the radii closest to the poles): each tier's maxima start the
     // next tiers' screens (hint).
     prune_init_kernel<<<1, 1, 0, st>>>(p->mstar, r0, r1, p->first_tier, p->tmax, p->hint);
@@ -1254,21 +1372,28 @@ int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, doub
     p->launches += 3;
     CU(cudaGetLastError());
     int slot = 0, rc2;
-    constexpr int t1k = kRegTiers, t4k = kRegTiers + 1;
-    if ((rc2 = launch_pruned_tier<prune_k(t4k)>(p, t4k, ghat_rev, r0, r1, p->mstar + t4k - 1,
-                                                 p->mstar + t4k, stopped, &slot, st)))
+    constexpr int t1k = kTier1k, t4k = kTier4k;
+    const int* ms = p->mstar;
+    if ((rc2 = launch_pruned_tier<prune_k(t4k)>(p, t4k, ghat_rev, r0, r1, tier_lo(p, ms, t4k),
+                                                 ms + t4k, stopped, &slot, st)))
       return rc2;
-    if ((rc2 = launch_pruned_tier<prune_k(t1k)>(p, t1k, ghat_rev, r0, r1, p->mstar + t1k - 1,
-                                                 p->mstar + t1k, stopped, &slot, st)))
+    if ((rc2 = launch_pruned_tier<prune_k(t1k)>(p, t1k, ghat_rev, r0, r1, tier_lo(p, ms, t1k),
+                                                 ms + t1k, stopped, &slot, st)))
       return rc2;
-    if (p->first_tier == 0) {
-      if ((rc2 = launch_reg_tier<1>(p, 0, ghat_rev, r0, r1, nullptr, p->mstar, stopped, &slot, st)))
+    if (p->tier_on[kTierSub + 1] &&
+        (rc2 = launch_sub_tier<9>(p, kTierSub + 1, ghat_rev, r0, r1, tier_lo(p, ms, kTierSub + 1),
+                                  ms + kTierSub + 1, stopped, &slot, st)))
+      return rc2;
+    if (p->tier_on[kTierSub] &&
+        (rc2 = launch_sub_tier<8>(p, kTierSub, ghat_rev, r0, r1, tier_lo(p, ms, kTierSub),
+                                  ms + kTierSub, stopped, &slot, st)))
+      return rc2;
+    if (p->tier_on[0]) {
+      if ((rc2 = launch_reg_tier<1>(p, 0, ghat_rev, r0, r1, nullptr, ms, stopped, &slot, st)))
         return rc2;
-      if ((rc2 = launch_reg_tier<2>(p, 1, ghat_rev, r0, r1, p->mstar, p->mstar + 1, stopped, &slot,
-                                    st)))
+      if ((rc2 = launch_reg_tier<2>(p, 1, ghat_rev, r0, r1, ms, ms + 1, stopped, &slot, st)))
         return rc2;
-      if ((rc2 = launch_reg_tier<4>(p, 2, ghat_rev, r0, r1, p->mstar + 1, p->mstar + 2, stopped,
-                                    &slot, st)))
+      if ((rc2 = launch_reg_tier<4>(p, 2, ghat_rev, r0, r1, ms + 1, ms + 2, stopped, &slot, st)))
         return rc2;
     }
     lim = p->mstar + kPruneTiers - 1;
@@ -1611,11 +1736,15 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
       ALLOC2(p->mstar, sizeof(int) * kPruneTiers);
       ALLOC2(p->tmax, sizeof(unsigned long long));
       ALLOC2(p->hint, sizeof(unsigned long long));
-      p->first_tier = kRegTiersOn ? 0 : kRegTiers;
-      estimate_tier_rows(p, radii_host);
-      rc = setup_pruned_tier<prune_k(kRegTiers)>(p, kRegTiers);
-      if (!rc) rc = setup_pruned_tier<prune_k(kRegTiers + 1)>(p, kRegTiers + 1);
-      for (int t = 0; t < kRegTiers && !rc && p->first_tier == 0; ++t) rc = setup_reg_tier(p, t);
+      for (int t = 0; t < kPruneTiers; ++t) p->tier_on[t] = t < kRegTiers ? kRegTiersOn != 0 : true;
+      choose_sub_tiers(p, radii_host, 1);
+      p->first_tier = 0;
+      while (!p->tier_on[p->first_tier]) ++p->first_tier;
+      rc = setup_pruned_tier<prune_k(kTier1k)>(p, kTier1k);
+      if (!rc) rc = setup_pruned_tier<prune_k(kTier4k)>(p, kTier4k);
+      if (!rc && p->tier_on[kTierSub]) rc = setup_sub_tier<8>(p, kTierSub);
+      if (!rc && p->tier_on[kTierSub + 1]) rc = setup_sub_tier<9>(p, kTierSub + 1);
+      for (int t = 0; t < kRegTiers && !rc && p->tier_on[t]; ++t) rc = setup_reg_tier(p, t);
       if (!rc) rc = reg_kernel_attrs();
       if (rc) return cleanup(rc);
       p->pruned = true;
@@ -1628,6 +1757,29 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
       // register tiers for batches (pruned_small)
       ALLOC2(p->sp_fw, sizeof(double) * kFwStride * (size_t)rows);
       ALLOC2(p->sp_mstar, sizeof(int) * kSmallTiers * (size_t)max_batch);
+      for (int t = 0; t < kPruneTiers; ++t)
+        p->tier_on[t] = t < kRegTiers || (K >= 12 && kSmallWarpTier && t == kTier1k);
+      choose_sub_tiers(p, radii_host, max_batch);
+      {
+        for (int u = 0; u < 2; ++u) {
+          if (!p->tier_on[kTierSub + u]) continue;
+          const int T = 8 << u, stride = T + 32;
+          ALLOC2(p->sp_gsub[u], sizeof(double2) * N * (size_t)max_batch);
+          ALLOC2(p->sp_fwsub[u], sizeof(double) * stride * (size_t)rows);
+          const int64_t tot = rows * stride;
+          fast_weight_kernel<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 65535), 256>>>(
+              p->radii, p->scales, p->m0, rows, stride, T, 32, 3 + u, 0, 0, p->sp_fwsub[u]);
+          p->launches++;
+        }
+        CU(cudaFuncSetAttribute(field_sub_kernel<8, false, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SubGeo<8>::kSmem));
+        CU(cudaFuncSetAttribute(field_sub_kernel<8, true, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SubGeo<8>::kSmem));
+        CU(cudaFuncSetAttribute(field_sub_kernel<9, false, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SubGeo<9>::kSmem));
+        CU(cudaFuncSetAttribute(field_sub_kernel<9, true, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SubGeo<9>::kSmem));
+      }
       if (K >= 12 && kSmallWarpTier) {
         ALLOC2(p->sp_g1k, sizeof(double2) * N * (size_t)max_batch);
         CU(cudaFuncSetAttribute(field_warp_kernel<false, true>,
@@ -1653,7 +1805,6 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
           p->radii, p->scales, p->m0, rows, kFwStride, 32, 32, 5, 0, 0, p->sp_fw);
       p->launches++;
       p->first_tier = 0;
-      estimate_tier_rows(p, radii_host);
       if ((rc = reg_kernel_attrs())) return cleanup(rc);
       p->sp = true;
     }
@@ -1713,6 +1864,10 @@ int afd_plan_destroy(afd_plan* p) {
   cudaFree(p->sp_h);
   cudaFree(p->sp_rlog);
   cudaFree(p->sp_g1k);
+  for (int u = 0; u < 2; ++u) {
+    cudaFree(p->sp_gsub[u]);
+    cudaFree(p->sp_fwsub[u]);
+  }
   cudaFree(p->big_part);
   cudaFree(p->nodes);
   cudaFree(p->sel);
@@ -2397,31 +2552,35 @@ int afd_field_tier_rows(afd_plan* p, int64_t* terms, int64_t* rows_out, int cap,
   int rc;
   if ((rc = set_device(p))) return rc;
   const int64_t rows = p->m1 - p->m0;
+  // tiers in use, in row order; an unused tier's rows belong to the next one
+  int act[kPruneTiers], na = 0;
+  const int tmax = p->big ? kPruneTiers : kSmallTiers;
+  for (int t = 0; t < tmax; ++t)
+    if (p->tier_on[t]) act[na++] = t;
+  auto clampr = [&](int64_t x) { return std::max<int64_t>(0, std::min<int64_t>(rows, x - p->m0)); };
   if (!p->big && p->sp && p->sp_last_batch > 0) {
     // batches of on-chip fields with register tiers: rows summed over the
     // signals of the last evaluation
-    const int nt = p->sp_g1k ? kSmallTiers : kRegTiers;
-    if (cap < nt + 1)
-      return fail(AFD_E_INVALID, "afd_field_tier_rows: cap %d < %d", cap, nt + 1);
+    if (cap < na + 1)
+      return fail(AFD_E_INVALID, "afd_field_tier_rows: cap %d < %d", cap, na + 1);
     std::vector<int> ms((size_t)p->sp_last_batch * kSmallTiers);
     CU(cudaMemcpyAsync(ms.data(), p->sp_mstar, sizeof(int) * ms.size(), cudaMemcpyDeviceToHost,
                        (cudaStream_t)stream));
     CU(cudaStreamSynchronize((cudaStream_t)stream));
-    for (int t = 0; t <= nt; ++t) {
-      terms[t] = t < nt ? 1LL << prune_k(t) : p->n;
-      rows_out[t] = 0;
+    for (int a = 0; a <= na; ++a) {
+      terms[a] = a < na ? 1LL << prune_k(act[a]) : p->n;
+      rows_out[a] = 0;
     }
     for (int64_t b = 0; b < p->sp_last_batch; ++b) {
       int64_t prev = 0;
-      for (int t = 0; t < nt; ++t) {
-        const int64_t e = std::max(
-            prev, std::max<int64_t>(0, std::min<int64_t>(rows, ms[b * kSmallTiers + t] - p->m0)));
-        rows_out[t] += e - prev;
+      for (int a = 0; a < na; ++a) {
+        const int64_t e = std::max(prev, clampr(ms[b * kSmallTiers + act[a]]));
+        rows_out[a] += e - prev;
         prev = e;
       }
-      rows_out[nt] += rows - prev;
+      rows_out[na] += rows - prev;
     }
-    *count = nt + 1;
+    *count = na + 1;
     return 0;
   }
   if (!p->big || !p->pruned) {
@@ -2431,22 +2590,21 @@ int afd_field_tier_rows(afd_plan* p, int64_t* terms, int64_t* rows_out, int cap,
     *count = 1;
     return 0;
   }
-  if (cap < kPruneTiers + 1)
-    return fail(AFD_E_INVALID, "afd_field_tier_rows: cap %d < %d", cap, kPruneTiers + 1);
+  if (cap < na + 1)
+    return fail(AFD_E_INVALID, "afd_field_tier_rows: cap %d < %d", cap, na + 1);
   int ms[kPruneTiers] = {};
   CU(cudaMemcpyAsync(ms, p->mstar, sizeof(ms), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   CU(cudaStreamSynchronize((cudaStream_t)stream));
-  auto clampr = [&](int64_t x) { return std::max<int64_t>(0, std::min<int64_t>(rows, x - p->m0)); };
   int64_t prev = 0;
-  for (int t = 0; t < kPruneTiers; ++t) {
-    const int64_t e = std::max(prev, clampr(ms[t]));
-    terms[t] = 1LL << prune_k(t);
-    rows_out[t] = e - prev;
+  for (int a = 0; a < na; ++a) {
+    const int64_t e = std::max(prev, clampr(ms[act[a]]));
+    terms[a] = 1LL << prune_k(act[a]);
+    rows_out[a] = e - prev;
     prev = e;
   }
-  terms[kPruneTiers] = p->n;
-  rows_out[kPruneTiers] = rows - prev;
-  *count = kPruneTiers + 1;
+  terms[na] = p->n;
+  rows_out[na] = rows - prev;
+  *count = na + 1;
   return 0;
 }
 

@@ -31,15 +31,18 @@ namespace afd {
 // On-chip sub-transform tiers, by the number of spectrum terms L a row needs
 // (its tail beyond l = L negligible): L = 32, 64 and 128 run in registers,
 // one thread per 32 outputs and no exchange at all (afd_field_reg.cuh: 70%
-// of r_m = m/M), L = 1024 as N/1024 1024-point fields (one warp per row,
-// afd_field_warp.cuh), L = 4096 as N/4096 4096-point fields, the rest
-// two-pass.  mstar[t] = first row failing tier t's test; tiers are nested
+// of r_m = m/M), L = 256 and 512 as N/L L-point fields on 8 or 16 threads
+// each (afd_field_sub.cuh), L = 1024 as N/1024 1024-point fields (one warp
+// per row, afd_field_warp.cuh), L = 4096 as N/4096 4096-point fields, the
+// rest two-pass.  mstar[t] = first row failing tier t's test; tiers are nested
 // (a row failing a longer tier fails every shorter one), so mstar[] is
 // non-decreasing and tier t takes rows [mstar[t-1], mstar[t]).
-constexpr int kPruneTiers = 5;
+constexpr int kPruneTiers = 7;
 constexpr int kRegTiers = 3;  // tiers 0..2: the register kernels (D = 1, 2, 4 blocks of 32 terms)
+constexpr int kTierSub = 3;   // tiers 3, 4: 256- and 512-point sub-warp fields
+constexpr int kTier1k = 5, kTier4k = 6;
 __host__ __device__ constexpr int prune_k(int t) {
-  return t == 0 ? 5 : t == 1 ? 6 : t == 2 ? 7 : t == 3 ? 10 : 12;
+  return t < kRegTiers ? 5 + t : t == 3 ? 8 : t == 4 ? 9 : t == kTier1k ? 10 : 12;
 }
 constexpr int kPruneK = 12;  // the longest tier (the spectrum head staged by prune_rows)
 
@@ -163,31 +166,34 @@ __global__ void pretwiddle_reg_kernel(int K, int ka, int D, const double2* __res
 }
 
 // Batches of on-chip fields (N <= 8192, many signals: BASELINE c3) with the
-// register tiers and (N >= 4096: g1k != null) the 1024-point warp tier: one
-// CTA per signal decides the signal's tier limits mstar[sig][t],
-// t < kSmallTiers = kRegTiers + 1 (the same tail test as prune_rows_kernel;
-// without the warp tier the last limit repeats the one before; a stopped
-// signal: every limit m0, and the field kernels then do nothing), clears its
-// hint and writes its pre-twiddled spectra
+// register tiers and (N >= 4096: gl.g[] != null) the 256-, 512- and
+// 1024-point tiers: one CTA per signal decides the signal's tier limits
+// mstar[sig][t], t < kSmallTiers (the same tail test as prune_rows_kernel;
+// without the longer tiers their limits repeat the last register tier's; a
+// stopped signal: every limit m0, and the field kernels then do nothing),
+// clears its hint and writes its pre-twiddled spectra
 //   h[sig][(m 32 + i) Q' + q'] = G^_l e^{+2 pi i l q' / N},  l = rev5(i) + 32 m,  m < 4,
-//   g1k[sig][q][l] = G^_l e^{+2 pi i l q / N},  q < N / 1024,  l < 1024
+//   gl.g[u][sig][q][l] = G^_l e^{+2 pi i l q / N},  q < N / L_u,  l < L_u = 256 << u
 // (natural-order spectrum, [batch][N]).  Rows from the last limit on stay
 // with the N-point field kernel (SubMap::lim_lo).  One thread per row;
 // rlog[s - m0] = {log2 r_s, log2(1 - r_s)} is tabulated at plan time (-inf
 // for r = 0: no tail at all).
-constexpr int kSmallTiers = kRegTiers + 1;
+constexpr int kSmallTiers = kTier1k + 1;  // limits per signal: tiers 0 .. kTier1k
+struct SmallSpectra {
+  double2* g[3];  // L = 256, 512, 1024 (null: tier not used)
+};
 __global__ void __launch_bounds__(256) prune_small_kernel(
     int K, const double2* __restrict__ ghat, const double2* __restrict__ rlog, long long m0,
     long long m1, const double2* __restrict__ circle, const State* __restrict__ state,
     int* __restrict__ mstar, unsigned long long* __restrict__ hint, double2* __restrict__ h,
-    double2* __restrict__ g1k) {
+    SmallSpectra gl) {
   constexpr int L = 128;  // terms of the longest register tier
-  constexpr int LG = 1 << prune_k(kRegTiers);  // 1024: the warp tier
-  static_assert(LG == 1024, "tier after the register tiers");
+  constexpr int LG = 1 << prune_k(kTier1k);  // 1024: the longest tier tested here
+  static_assert(LG == 1024 && kTier1k == kRegTiers + 2, "tiers 256, 512, 1024 follow the register tiers");
   __shared__ double lg[LG];
   __shared__ double wmax[8];
   __shared__ int ms[kSmallTiers];
-  const int ntier = g1k ? kSmallTiers : kRegTiers;
+  const int ntier = gl.g[2] ? kSmallTiers : kRegTiers;
   const int sig = blockIdx.x;
   const int n = 1 << K, kq = K - 5, qn = 1 << kq;
   const double2* __restrict__ gh = ghat + (size_t)sig * n;
@@ -249,10 +255,13 @@ __global__ void __launch_bounds__(256) prune_small_kernel(
     const double2 w = __ldg(circle + ((l * q) & (n - 1)));
     out[x] = make_double2(fma(g.x, w.x, -(g.y * w.y)), fma(g.x, w.y, g.y * w.x));
   }
-  if (g1k) {
-    double2* __restrict__ o1 = g1k + (size_t)sig * n;
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    if (!gl.g[u]) continue;
+    const int kl = 8 + u;
+    double2* __restrict__ o1 = gl.g[u] + (size_t)sig * n;
     for (int x = threadIdx.x; x < n; x += blockDim.x) {
-      const int q = x >> 10, l = x & 1023;
+      const int q = x >> kl, l = x & ((1 << kl) - 1);
       const double2 g = __ldg(gh + l);
       const double2 w = __ldg(circle + ((l * q) & (n - 1)));
       o1[x] = make_double2(fma(g.x, w.x, -(g.y * w.y)), fma(g.x, w.y, g.y * w.x));

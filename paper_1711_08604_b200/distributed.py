@@ -78,8 +78,9 @@ def expected_twopass(radii, n, onchip=4096):
 # cost of one row relative to a 1024-point row (c4, N = 2^20, one B200:
 # 1.02, 1.18, 1.71, 2.40, 3.41 us per row; two-pass 7.5 us;
 # profiles/r02/tier_kernels_c4_v9.txt).
-FAST_TIERS = (32, 64, 128, 1024, 4096)
-FAST_TIER_COST = {32: 0.43, 64: 0.49, 128: 0.71, 1024: 1.0, 4096: 1.42, None: 3.1}
+FAST_TIERS = (32, 64, 128, 256, 512, 1024, 4096)
+FAST_TIER_COST = {32: 0.43, 64: 0.49, 128: 0.62, 256: 0.8, 512: 0.9, 1024: 1.0, 4096: 1.42,
+                  None: 3.1}
 
 
 def expected_tier(radii, n):

@@ -16,6 +16,13 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
+# The 256- / 512-point tiers of the pruned fast field are used only when they
+# carry enough work (csrc/afd_capi.cu: AFD_SUB_MIN_EVALS, default 2^30 grid
+# evaluations per field: BASELINE c4).  The GPU tests force them on at every
+# size so the small cases exercise those kernels too (read when the library
+# loads; test_default_tier_choice checks the default in a fresh process).
+os.environ.setdefault("AFD_SUB_MIN_EVALS", "0")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")

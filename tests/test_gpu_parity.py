@@ -7,13 +7,14 @@ package's public API.
 """
 
 import json
+import os
 import warnings
 
 import numpy as np
 import pytest
 
 import oracle as O
-from conftest import DECOMP_CASES, load_golden
+from conftest import DECOMP_CASES, ROOT, load_golden
 
 pytestmark = pytest.mark.gpu
 
@@ -753,7 +754,7 @@ def test_bench_line_contract(afd):
     sp = r.get("split")
     if sp is not None:
         rows = d["config"]["m"]
-        tiers = (32, 64, 128, 1024, 4096)
+        tiers = (32, 64, 128, 256, 512, 1024, 4096)
         assert sum(sp["rows_%d" % t] for t in tiers) == sp["onchip_rows"]
         assert sp["onchip_rows"] + sp["twopass_rows"] == rows
         assert all(sp["flops_per_eval_%d" % t] == 5 * (t.bit_length() - 1) + 7 for t in tiers)
@@ -1025,11 +1026,11 @@ def test_pruned_field_argmax_and_split(afd, radii):
     assert lo1 <= n1k <= hi1 and n1k + n4k == onchip and n2p == twopass
     # the register tiers (32, 64, 128 spectrum terms) inside the <= 1024 rows
     tr = plan.field_tier_rows()
-    assert list(tr) == [32, 64, 128, 1024, 4096, n]
+    assert list(tr) == [32, 64, 128, 256, 512, 1024, 4096, n]
     assert sum(tr.values()) == len(radii) and tr[4096] == n4k and tr[n] == n2p
-    assert tr[32] + tr[64] + tr[128] + tr[1024] == n1k
+    assert sum(tr[L] for L in (32, 64, 128, 256, 512, 1024)) == n1k
     upto = 0
-    for L in (32, 64, 128):
+    for L in (32, 64, 128, 256, 512):
         lo_l, hi_l = _first_unprunable(ghat, radii, L=L)
         upto += tr[L]
         assert lo_l <= upto <= hi_l, L
@@ -1047,16 +1048,16 @@ def _cand(plan, ghat):
 
 @pytest.mark.parametrize("k", [16, 20])
 def test_reg_tier_rows_one_by_one(afd, k):
-    """Single-row fields at radii across the register tiers (and just
-    beyond): each row's first maximum is the oracle's (flat index; value and
+    """Single-row fields at radii across the register and sub-warp tiers (and
+    just beyond): each row's first maximum is the oracle's (flat index; value and
     magnitude to 1e-12), and the row went to the expected tier."""
     core, engine = afd
     from paper_1711_08604_b200 import workloads as W
     n = 1 << k
     g = W.pole_sum(n, 24, 0.9, 4242 + k)
     ghat = O.dft_forward(g)
-    rs = (0.0, 0.03, 0.11, 0.2, 0.249, 0.27, 0.33, 0.41, 0.499, 0.52, 0.61, 0.68, 0.73) \
-        if k == 16 else (0.17, 0.38, 0.6)
+    rs = (0.0, 0.03, 0.11, 0.2, 0.249, 0.27, 0.33, 0.41, 0.499, 0.52, 0.61, 0.68, 0.73, 0.8,
+          0.83, 0.86, 0.9, 0.93) if k == 16 else (0.17, 0.38, 0.6, 0.78, 0.89)
     for r in rs:
         plan = engine.Plan((r,), n, fast=1)
         got = _cand(plan, ghat)
@@ -1067,9 +1068,43 @@ def test_reg_tier_rows_one_by_one(afd, k):
         assert abs(got["mag"] - ref["mag"]) <= 1e-12 * ref["mag"], r
         assert abs(complex(got["re"], got["im"]) - complex(ref["re"], ref["im"])) \
             <= 1e-12 * np.sqrt(ref["mag"]), r
-        want = next((L for L in (32, 64, 128) if _first_unprunable(ghat, (r,), L=L)[0] == 1),
-                    1024)
+        want = next((L for L in (32, 64, 128, 256, 512)
+                     if _first_unprunable(ghat, (r,), L=L)[0] == 1), 1024)
         assert tr[want] == 1, (r, tr)
+
+
+def test_default_tier_choice(afd):
+    """Without AFD_SUB_MIN_EVALS (the tests force the 256- / 512-point tiers
+    on) a mid-size plan leaves their rows on the 1024-point tier, a c4-size
+    radius grid uses them; the first maximum is the oracle's either way."""
+    import subprocess
+    import sys
+    code = r'''
+import json, sys, numpy as np, torch
+sys.path.insert(0, %r)
+import oracle as O
+from paper_1711_08604_b200 import engine, workloads as W
+out = {}
+for name, n, m in (("mid", 1 << 16, 96), ("big", 1 << 20, 16384)):
+    radii = tuple(0.97 * i / m for i in range(m))
+    plan = engine.Plan(radii, n, fast=1)
+    ghat = O.dft_forward(W.pole_sum(n, 12, 0.9, 31))
+    got = np.frombuffer(plan.field_argmax(torch.from_numpy(ghat).cuda()).cpu().numpy().tobytes(),
+                        O.CAND_DTYPE)[0]
+    out[name] = {"tiers": [int(k) for k in plan.field_tier_rows()], "flat": int(got["flat"])}
+    if name == "mid":
+        out[name]["ref"] = int(O.field_argmax(ghat, np.array(radii))["flat"])
+    del plan
+print(json.dumps(out))
+''' % ROOT
+    env = {k: v for k, v in os.environ.items() if k != "AFD_SUB_MIN_EVALS"}
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    out = json.loads(res.stdout.strip().splitlines()[-1])
+    assert out["mid"]["tiers"] == [32, 64, 128, 1024, 4096, 1 << 16]
+    assert out["mid"]["flat"] == out["mid"]["ref"]
+    assert out["big"]["tiers"] == [32, 64, 128, 256, 512, 1024, 4096, 1 << 20]
 
 
 @pytest.mark.parametrize("engine_name", ["fft-fast", "fft-fast-margins"])
@@ -1170,7 +1205,7 @@ def test_small_pruned_batch_field_argmax(afd, n, m, b):
     tr = plan.field_tier_rows()
     del plan
     # N >= 4096: rows that need up to 1024 terms run as N / 1024 warp-per-row fields
-    assert list(tr) == ([32, 64, 128, 1024, n] if n >= 4096 else [32, 64, 128, n])
+    assert list(tr) == ([32, 64, 128, 256, 512, 1024, n] if n >= 4096 else [32, 64, 128, n])
     assert sum(tr.values()) == b * m and all(v > 0 for v in tr.values())
     tiers_hit = set()
     for i in list(range(0, b, 7)) + [3]:

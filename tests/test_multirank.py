@@ -127,10 +127,10 @@ def test_radius_shard_bounds_balance_the_exact_field():
         assert max(share) - min(share) <= 2 * w.max()
         assert [radius_shard_bounds(radii, 4096, r, world) for r in range(world)] == \
             [shard_bounds(m, r, world) for r in range(world)]
-    # tiers by radius: r^L / (1 - r) <= 2^-64 at L = 32, 64, 128, 1024, 4096
-    assert list(expected_tier((0.0, 0.2, 0.25, 0.3, 0.49, 0.55, 0.69, 0.75, 0.95, 0.97, 0.985,
-                               0.99), n)) == [32, 32, 64, 64, 64, 128, 128, 1024, 1024, 4096,
-                                              4096, n]
+    # tiers by radius: r^L / (1 - r) <= 2^-64 at L = 32, 64, 128, 256, 512, 1024, 4096
+    assert list(expected_tier((0.0, 0.2, 0.25, 0.3, 0.49, 0.55, 0.69, 0.75, 0.83, 0.9, 0.95, 0.97,
+                               0.985, 0.99), n)) == [32, 32, 64, 64, 64, 128, 128, 256, 256, 512,
+                                                     1024, 4096, 4096, n]
     tiny = (0.1, 0.2, 0.9)
     assert [radius_shard_bounds(tiny, n, r, 3) for r in range(3)] == [(0, 1), (1, 2), (2, 3)]
 
