@@ -1276,7 +1276,10 @@ int setup_reg_tier(afd_plan* p, int t) {
     p->launches++;
     CU(cudaGetLastError());
   }
-  CU(cudaMalloc(&T.ghq, sizeof(double2) * (size_t)p->n * D));
+  // one buffer of pre-twiddled spectra for the three tiers: block m of
+  // register i sits at row m 32 + i whatever D, so the D = 4 layout holds the
+  // other two as prefixes (tier[kRegTiers - 1].ghq, one pretwiddle launch)
+  if (t == kRegTiers - 1) CU(cudaMalloc(&T.ghq, sizeof(double2) * (size_t)p->n * D));
   const int nc = tier_ncta(p, T.qblocks, p->est_rows[t], fr_share(D), 1.0);
   T.ncta = (int)std::max<int64_t>(1, std::min<int64_t>(nc, rows));
   CU(cudaMalloc(&T.cand, sizeof(Cand) * (size_t)T.qblocks * T.ncta));
@@ -1288,11 +1291,15 @@ template <int D>
 int launch_reg_tier(afd_plan* p, int t, const double2* ghat_rev, int64_t r0, int64_t r1,
                     const int* lo, const int* hi, const int* stopped, int* slot, cudaStream_t st) {
   auto& T = p->tier[t];
-  pretwiddle_reg_kernel<<<4 * p->sms, 256, 0, st>>>(p->K, p->ka, D, ghat_rev, p->circle, T.ghq,
-                                                    stopped);
+  double2* hq = p->tier[kRegTiers - 1].ghq;
+  if (t == 0) {  // the register tiers launch in order 0, 1, 2: one pre-twiddle for all
+    pretwiddle_reg_kernel<<<4 * p->sms, 256, 0, st>>>(p->K, p->ka, 1 << (kRegTiers - 1), ghat_rev,
+                                                      p->circle, hq, stopped);
+    p->launches++;
+  }
   auto rk = p->margins ? field_reg_kernel<D, true> : field_reg_kernel<D, false>;
   rk<<<dim3((unsigned)T.ncta, (unsigned)T.qblocks), fr_threads(D), fr_smem_bytes(D), st>>>(
-      T.ghq, p->tier[0].fw, (long long)r0, (long long)r1, (long long)p->m0,
+      hq, p->tier[0].fw, (long long)r0, (long long)r1, (long long)p->m0,
       (long long)(p->n >> 5), T.cand, p->hint,
       SubMap{(long long)p->n, 0, hi, T.cand2, lo, nullptr}, RegBatch{});
   const int n = T.qblocks * T.ncta;
@@ -1301,7 +1308,7 @@ int launch_reg_tier(afd_plan* p, int t, const double2* ghat_rev, int64_t r0, int
   cand_partial_kernel<<<np, 256, 0, st>>>(T.cand, n, (n + np - 1) / np, p->big_cand + *slot,
                                           T.cand2, p->big_cand2 ? p->big_cand2 + *slot : nullptr);
   *slot += np;
-  p->launches += 3;
+  p->launches += 2;
   CU(cudaGetLastError());
   return 0;
 }

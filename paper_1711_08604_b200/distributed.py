@@ -74,13 +74,13 @@ def expected_twopass(radii, n, onchip=4096):
 
 
 # Spectrum terms per tier of the pruned fast field (csrc/afd_pruned.cuh: 32,
-# 64, 128 in registers, 1024 and 4096 as on-chip transforms) and the measured
+# 64, 128 in registers, 256 ... 4096 as on-chip transforms) and the measured
 # cost of one row relative to a 1024-point row (c4, N = 2^20, one B200:
-# 1.02, 1.18, 1.71, 2.40, 3.41 us per row; two-pass 7.5 us;
-# profiles/r02/tier_kernels_c4_v9.txt).
+# 1.03, 1.18, 1.53, 1.98, 2.25, 2.55, 3.47 us per row; two-pass 7.5 us;
+# profiles/r02/tier_kernels_c4_v13.txt).
 FAST_TIERS = (32, 64, 128, 256, 512, 1024, 4096)
-FAST_TIER_COST = {32: 0.43, 64: 0.49, 128: 0.62, 256: 0.8, 512: 0.9, 1024: 1.0, 4096: 1.42,
-                  None: 3.1}
+FAST_TIER_COST = {32: 0.40, 64: 0.46, 128: 0.60, 256: 0.78, 512: 0.88, 1024: 1.0, 4096: 1.36,
+                  None: 2.9}
 
 
 def expected_tier(radii, n):
