@@ -120,7 +120,10 @@ __global__ void __launch_bounds__(256) prune_rows_kernel(
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) bt = fmax(bt, __shfl_xor_sync(0xffffffffu, bt, o));
       const double tail = lt + (double)L_t * lr - l1r;
-      if (lane == 0 && !(tail <= bt - 64.0)) atomicMin(mstar + t, (int)s);
+      // (warp-uniform) a row that passes a tier passes every longer one: the
+      // tail bound falls and the kept maximum grows with L
+      if (tail <= bt - 64.0) break;
+      if (lane == 0) atomicMin(mstar + t, (int)s);
     }
   }
 }
