@@ -449,8 +449,8 @@ def field_roofline(plan, w, radii_rows, ghat, exact, local):
                    "large-N field: pass A (big_field_a) + TMA column pass (col_tma_kernel)"
                    if split is None else
                    "pruned large-N field: register tiers (field_reg_kernel<1>, <2>, <4>), on-chip "
-                   "1024- and 4096-point fields (field_warp_kernel, field_kernel<12>) + "
-                   "two-pass rows (big_field_a + col_tma_kernel)"),
+                   "256- ... 4096-point fields (field_sub_kernel<8>, <9>, field_warp_kernel, "
+                   "field_kernel<12>) + two-pass rows (big_field_a + col_tma_kernel)"),
         "flops_per_eval": fpe, "evals_per_launch": launch_evals, "launch_ms": field_ms})
     if split is not None:
         roof["split"] = split
