@@ -153,6 +153,11 @@ struct afd_plan {
   int64_t sp_last_batch = 0;
   int* mstar = nullptr;        // [kPruneTiers] first row failing each tier's test
   unsigned long long* tmax = nullptr;
+  // the step's two-pass limit read back by the host (one pinned int, an event
+  // right after the pruning test) so that the row batches wholly below it —
+  // 63 of 64 at c4 — are not launched at all; not under stream capture
+  int* lim_host = nullptr;
+  cudaEvent_t lim_ev = nullptr;
   double* nodes = nullptr;     // [2 * N / kNodeLen]
   BigSel* sel = nullptr;
   int* amb = nullptr;
@@ -1183,6 +1188,10 @@ int setup_pruned_tier(afd_plan* p, int t) {
   return 0;
 }
 
+// AFD_LIM_READBACK=0: launch every two-pass row batch (they exit on the
+// device limit) instead of reading the limit back (A/B switch).
+static const int kLimReadback = getenv("AFD_LIM_READBACK") ? atoi(getenv("AFD_LIM_READBACK")) : 1;
+
 // AFD_SUB_TIERS=0: no 256- / 512-point tiers (their rows stay on the
 // 1024-point tier; A/B switch).  A sub tier is used when the rows the radii
 // predict for it make at least AFD_SUB_MIN_EVALS grid evaluations per field
@@ -1364,6 +1373,7 @@ int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, doub
     p->launches++;
   }
   const int* lim = nullptr;
+  bool read_lim = false;
   if (!fout && p->pruned) {
     // tier t takes rows [mstar[t-1], mstar[t]) (of the tiers in use): tiers
     // 0..2 in registers (32, 64 and 128 terms), 3 and 4 as N/256 256-point and
@@ -1378,6 +1388,17 @@ int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, doub
                                                   p->tmax, stopped, p->mstar);
     p->launches += 3;
     CU(cudaGetLastError());
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CU(cudaStreamIsCapturing(st, &cap));
+    // (worth a host wait only when there are several batches to skip: c2's
+    // rows fit one batch and the wait cost it 1.5%)
+    read_lim = kLimReadback && p->lim_host && cap == cudaStreamCaptureStatusNone &&
+               (r1 - r0 + p->big_rows - 1) / p->big_rows >= 4;
+    if (read_lim) {
+      CU(cudaMemcpyAsync(p->lim_host, p->mstar + kPruneTiers - 1, sizeof(int),
+                         cudaMemcpyDeviceToHost, st));
+      CU(cudaEventRecord(p->lim_ev, st));
+    }
     int slot = 0, rc2;
     constexpr int t1k = kTier1k, t4k = kTier4k;
     const int* ms = p->mstar;
@@ -1405,8 +1426,16 @@ int big_field(afd_plan* p, const double2* ghat_rev, int64_t r0, int64_t r1, doub
     }
     lim = p->mstar + kPruneTiers - 1;
   }
+  int64_t first_row = r0;
+  if (read_lim) {
+    // the tier kernels are already queued: the device stays busy while the
+    // host waits for the pruning test only
+    CU(cudaEventSynchronize(p->lim_ev));
+    first_row = std::max<int64_t>(r0, std::min<int64_t>(r1, *p->lim_host));
+  }
   for (int64_t b = r0; b < r1; b += p->big_rows) {
     const int64_t rows = std::min<int64_t>(p->big_rows, r1 - b);
+    if (b + rows <= first_row) continue;  // every row of the batch is on chip
     if (!(kBigSkip & 1) &&
         (rc = big_launch_a(p, true, 0, ghat_rev, nullptr, b, rows, stopped, st, lim)))
       return rc;
@@ -1742,6 +1771,9 @@ int afd_plan_create(afd_plan** out, int device, int64_t n, int64_t m, int64_t m0
       // the first L - 1 entries of the N-point tables), per-CTA candidates
       ALLOC2(p->mstar, sizeof(int) * kPruneTiers);
       ALLOC2(p->tmax, sizeof(unsigned long long));
+      if (cudaHostAlloc(&p->lim_host, sizeof(int), cudaHostAllocDefault) != cudaSuccess ||
+          cudaEventCreateWithFlags(&p->lim_ev, cudaEventDisableTiming) != cudaSuccess)
+        return cleanup(fail(AFD_E_CUDA, "plan init: limit readback"));
       ALLOC2(p->hint, sizeof(unsigned long long));
       for (int t = 0; t < kPruneTiers; ++t) p->tier_on[t] = t < kRegTiers ? kRegTiersOn != 0 : true;
       choose_sub_tiers(p, radii_host, 1);
@@ -1864,6 +1896,8 @@ int afd_plan_destroy(afd_plan* p) {
   cudaFree(p->cand2);
   cudaFree(p->mstar);
   cudaFree(p->tmax);
+  if (p->lim_host) cudaFreeHost(p->lim_host);
+  if (p->lim_ev) cudaEventDestroy(p->lim_ev);
   cudaFree(p->hint);
   cudaFree(p->sp_fw);
   cudaFree(p->sp_mstar);
