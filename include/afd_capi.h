@@ -256,8 +256,10 @@ int afd_field_split(afd_plan *plan, int64_t *onchip, int64_t *twopass, void *str
 int afd_field_tiers(afd_plan *plan, int64_t *rows3, void *stream);
 /* afd_field_tier_rows: the split by every tier, in row order: terms[t] =
  * spectrum terms a row of tier t is evaluated from (32, 64, 128: in
- * registers, one thread per 32 outputs; 1024, 4096: on-chip transforms; N:
- * two-pass, the last entry), rows[t] = its rows in the last evaluation.
+ * registers, one thread per 32 outputs; 256, 512 (when in use), 1024, 4096:
+ * on-chip transforms; N: two-pass — for batches of on-chip N: the N-point
+ * field kernel, rows summed over the signals — the last entry), rows[t] =
+ * its rows in the last evaluation.
  * Writes *count <= cap entries (cap >= 8 always suffices; one entry
  * {N, all rows} for unpruned plans). */
 int afd_field_tier_rows(afd_plan *plan, int64_t *terms, int64_t *rows, int cap, int *count,

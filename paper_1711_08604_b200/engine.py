@@ -169,7 +169,9 @@ class Plan:
     def field_tier_rows(self, stream=None):
         """{spectrum terms: rows} of the last large-N fast field evaluation by
         tier, in row order (afd_field_tier_rows): 32, 64, 128 (register
-        tiers), 1024, 4096 (on-chip transforms), N (two-pass)."""
+        tiers), 256, 512 (when in use), 1024, 4096 (on-chip transforms), N
+        (two-pass; batches of on-chip N: the N-point field kernel, rows
+        summed over the signals)."""
         terms, rows, cnt = (C.c_int64 * 8)(), (C.c_int64 * 8)(), C.c_int()
         _capi.check(self.lib.afd_field_tier_rows(self.handle, terms, rows, 8, C.byref(cnt),
                                                  _stream(stream)))
